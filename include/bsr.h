@@ -1,0 +1,160 @@
+/*
+ * bsr.h -- C-ABI of the B200-native tile rasterizer ("Beta-splat renderer", libbsr.so).
+ *
+ * Drop-in boundary for the hot path of /root/reference (betasplat, arXiv 2501.18630):
+ *
+ *   reference (pkg/src/betasplat/...)                     this ABI
+ *   ---------------------------------------------------   ------------------------------
+ *   rasterizer.render_tiled        rasterizer.py:194-211   bsr_forward
+ *   rasterizer.render_backward     rasterizer.py:230-321   bsr_backward
+ *     (_view_setup :88-103, project_arrays primitive.py:221-277, sh_basis
+ *      appearance.py:235-261, _depth_order :83-85, tile_bins :161-191,
+ *      project_backward primitive.py:302-367, _sh_basis_grad appearance.py:264-300)
+ *   core.forward_tiled             _raster.pyx:130-155     bsr_core_forward_tiled
+ *   core.backward                  _raster.pyx:244-287     bsr_core_backward
+ *   training.loss / ssim           training.py:51-131      bsr_loss_l1_dssim
+ *   training.adam_step             training.py:258-273     bsr_adam_step
+ *
+ * Conventions
+ *   - Every pointer is DEVICE memory owned by the caller unless stated; the library
+ *     allocates nothing.  Scratch/state lives in a caller-provided "frame" buffer sized
+ *     by bsr_frame_bytes(); forward writes the saved state backward reads (the
+ *     reference recomputes projection/sort/binning in backward, rasterizer.py:243-251).
+ *   - Every call is stream-ordered on the given cudaStream_t (passed as void*), reentrant
+ *     per stream, no global mutable state, no host synchronisation except
+ *     bsr_frame_status() (which synchronises the stream to read counters).
+ *   - Every function returns an int status (BSR_OK = 0).  No C++ exception crosses the ABI.
+ *   - Layouts follow PrimitiveSet / Camera (primitive.py:83-137, 387-426), fp32 on device:
+ *       positions (N,3), rotations (N,4) wxyz unnormalised, log_scales (N,3),
+ *       opacity_raw (N,) pre-sigmoid, shapes (N,) Beta shape b, sh (N,K,3) DC first.
+ *     Images are (H,W,3) / (H,W) row-major, pixel (row i, col j) at (x=j, y=i).
+ */
+#ifndef BSR_H_
+#define BSR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum bsr_status {
+    BSR_OK = 0,
+    BSR_ERR_BAD_ARG = 1,          /* ValueError in the reference (shape/dtype/size)        */
+    BSR_ERR_CAPACITY = 2,         /* tile-entry capacity exceeded: retry with entries_needed */
+    BSR_ERR_CUDA = 3,             /* a CUDA runtime error (launch / async fault)            */
+    BSR_ERR_DEGENERATE_QUAT = 4,  /* DegenerateQuaternionError (primitive.py:44-56)         */
+    BSR_ERR_FRAME_TOO_SMALL = 5,  /* frame buffer smaller than bsr_frame_bytes()            */
+};
+
+/* Pinhole camera (primitive.py:83-137); world_to_camera row-major 4x4. */
+typedef struct bsr_camera {
+    double world_to_camera[16];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} bsr_camera;
+
+/* Primitive parameters, device fp32 SoA (PrimitiveSet layout + SH). */
+typedef struct bsr_scene {
+    const float *positions, *rotations, *log_scales, *opacity_raw, *shapes, *sh;
+    int64_t n;
+    int32_t sh_coeffs; /* K = (degree+1)^2, degree <= 3 */
+} bsr_scene;
+
+/* Per-parameter gradient buffers (device fp32, same shapes); bsr_backward ADDS into them. */
+typedef struct bsr_grads {
+    float *positions, *rotations, *log_scales, *opacity_raw, *shapes, *sh;
+} bsr_grads;
+
+/* Forward outputs (device; any pointer may be NULL to skip that output). */
+typedef struct bsr_outputs {
+    float *color;          /* (H,W,3) max(raw, 0)                          rasterizer.py:136 */
+    float *raw;            /* (H,W,3) composite incl. background             _raster.pyx:124  */
+    float *alpha;          /* (H,W)   1 - T                                                  */
+    float *transmittance;  /* (H,W)   final T                                                */
+    float *depth;          /* (H,W)   sum_k w_k z_k (extension, no background term)          */
+    int32_t *pixel_count;  /* (H,W)   contributors per pixel (extension)                     */
+    int32_t *contributions;/* (N,)    pixels each primitive contributed to, ADDED into       */
+} bsr_outputs;
+
+typedef struct bsr_frame_info {
+    int64_t visible;         /* V: primitives kept by projection                           */
+    int64_t entries;         /* E: (tile, primitive) entries                               */
+    int64_t entries_needed;  /* E required (== entries unless capacity was exceeded)       */
+    int64_t flagged_pixels;  /* pixels re-composited in fp64 (near a decision threshold)   */
+    int32_t status;          /* first error raised on the device side (bsr_status)         */
+    int32_t reserved;
+} bsr_frame_info;
+
+/* ---- version / capability -------------------------------------------------------- */
+int bsr_version(int32_t *major, int32_t *minor);
+const char *bsr_status_string(int32_t status);
+
+/* ---- frame (state + scratch) sizing ------------------------------------------------- */
+int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_cap,
+                    uint64_t *bytes);
+
+/* ---- full pipeline (render_tiled / render_backward) -------------------------------- */
+int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                void *frame, uint64_t frame_bytes, int64_t entry_cap, const bsr_outputs *out,
+                void *stream);
+/* Synchronises `stream`, then reports counters / device-side errors of the last forward. */
+int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream);
+/* d_color: (H,W,3) dL/d color (clamped image); d_depth: (H,W) or NULL. */
+int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                 void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
+                 const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
+                 void *stream);
+
+/* ---- core seam (backend.get_core(): forward_tiled / backward on depth-sorted input) -- */
+/* Inputs are DEVICE fp64 arrays exactly as the reference core receives them
+ * (_raster.pyx:130-134): means (V,2), conics (V,3), opac (V,), betas (V,), colors (V,3),
+ * bounds (V,4) int32 [x0,x1,y0,y1], offsets (T+1,) int64, lists (E,) int64. */
+int bsr_core_scratch_bytes(int64_t v, int32_t width, int32_t height, int64_t n_entries,
+                           uint64_t *bytes);
+int bsr_core_forward_tiled(int64_t v, const double *means, const double *conics,
+                           const double *opac, const double *betas, const double *colors,
+                           const int32_t *bounds, int32_t height, int32_t width,
+                           const double background[3], int32_t tile_size, const int64_t *offsets,
+                           const int64_t *lists, int64_t n_entries, double alpha_min,
+                           double t_stop, float *raw, float *transmittance,
+                           int32_t *contrib, int32_t *pixel_count, void *scratch,
+                           uint64_t scratch_bytes, int64_t *flagged_out, void *stream);
+int bsr_core_backward(int64_t v, const double *means, const double *conics, const double *opac,
+                      const double *betas, const double *colors, const int32_t *bounds,
+                      int32_t height, int32_t width, const double background[3],
+                      const float *d_raw, int32_t tile_size, const int64_t *offsets,
+                      const int64_t *lists, int64_t n_entries, double alpha_min, double t_stop,
+                      float *d_means, float *d_conics, float *d_opac, float *d_betas,
+                      float *d_colors, void *scratch, uint64_t scratch_bytes, void *stream);
+
+/* ---- loss (training.loss with lambda_opacity = lambda_scale = 0) ------------------- */
+/* rendered/target (H,W,3); raw (H,W,3) or NULL: when given, the clamp chain
+ * d_raw = d_image * [raw >= 0] (rasterizer.py:253) is fused into the output.
+ * loss_out: device double[3] = {loss, l1, ssim}.  scratch: bsr_loss_scratch_bytes(). */
+int bsr_loss_scratch_bytes(int32_t width, int32_t height, uint64_t *bytes);
+int bsr_loss_l1_dssim(const float *rendered, const float *target, const float *raw,
+                      int32_t width, int32_t height, double lambda_ssim, double *loss_out,
+                      float *d_image, void *scratch, uint64_t scratch_bytes, void *stream);
+
+/* ---- Adam (training.adam_step), flat parameter buffer with per-group lr ----------- */
+/* Groups are contiguous ranges [group_end[g-1], group_end[g]) of the flat buffers. */
+int bsr_adam_step(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
+                  int64_t count, int32_t n_groups, const int64_t *group_end /* host */,
+                  const float *group_lr /* host */, int64_t step, double beta1, double beta2,
+                  double eps, void *stream);
+
+/* ---- parity / debug: export the binning of the last forward (synchronises) ---------- */
+/* order (V): compact index per depth rank (== np.argsort(depths, kind="stable"),
+ * rasterizer.py:83-85, over the visible subset in source order); src_index (V): source
+ * index of each compact primitive (batch.indices); bounds (V,4) compact order; lists (E):
+ * compact index per tile entry (tile_bins, rasterizer.py:161-191); ranges (T,2): per-tile
+ * [start, end).  Any pointer may be NULL. */
+int bsr_debug_export(const void *frame, int64_t n, int32_t width, int32_t height,
+                     int64_t entry_cap, int32_t *order, int32_t *src_index, int32_t *bounds,
+                     int32_t *lists, int32_t *ranges, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSR_H_ */

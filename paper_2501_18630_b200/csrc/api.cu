@@ -1,0 +1,358 @@
+// C-ABI entry points of libbsr.so (declared in include/bsr.h): stream-ordered
+// orchestration of the kernels.  No allocation, no host sync except bsr_frame_status.
+#include <math.h>
+#include <string.h>
+
+#include "frame.cuh"
+
+namespace bsr {
+// kernel launchers (one per translation unit)
+int launch_preprocess(const bsr_scene &, const KCam &, const FrameView &, cudaStream_t);
+int launch_depth_sort(const FrameView &, cudaStream_t);
+int launch_emit(const FrameView &, cudaStream_t);
+int launch_tile_sort(const FrameView &, cudaStream_t);
+int launch_tile_ranges(const FrameView &, cudaStream_t);
+int launch_raster_fwd(const FrameView &, const bsr_outputs &, const float bg[3], float, float,
+                      const uint32_t *, const uint2 *, const Record *, cudaStream_t);
+int launch_raster_bwd(const FrameView &, const float *, bool, const float *, const float bg[3],
+                      float, const uint32_t *, const uint2 *, const Record *, cudaStream_t);
+int launch_replay_scene(bool, const FrameView &, const bsr_scene &, const KCam &, const bsr_outputs &,
+                        const double bg[3], double, double, const float *, const float *,
+                        cudaStream_t);
+int launch_replay_arrays(bool, const FrameView &, const double *, const double *, const double *,
+                         const double *, const double *, const int32_t *, const uint32_t *,
+                         const uint2 *, const bsr_outputs &, const double bg[3], double, double,
+                         const float *, cudaStream_t);
+int launch_preprocess_bwd(const bsr_scene &, const KCam &, const FrameView &, const bsr_grads &,
+                          float *, cudaStream_t);
+
+constexpr double kAlphaMin = 1.0 / 255.0;  // rasterizer.py:28
+constexpr double kTStop = 1e-4;            // rasterizer.py:29
+
+__global__ void zero_acc_kernel(FrameView f) {
+    const uint32_t V = f.ctr->visible;
+    const int64_t n4 = (int64_t)V * kGradStride / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<float4 *>(f.grad_acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// ---- core seam helpers ------------------------------------------------------------
+struct CoreView {
+    FrameView f;
+    uint32_t *lists;
+    uint2 *ranges;
+    uint64_t bytes;
+};
+
+inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
+    // reuse the frame layout for the per-pixel state + records, add lists/ranges
+    CoreView c;
+    c.f = carve_frame(base, v, W, H, 0);
+    uint64_t off = c.f.total_bytes;
+    char *b = static_cast<char *>(base);
+    c.lists = b ? (uint32_t *)(b + off) : nullptr;
+    off = align_up(off + 4ull * (e > 0 ? e : 1), 256);
+    c.ranges = b ? (uint2 *)(b + off) : nullptr;
+    off = align_up(off + 8ull * c.f.n_tiles, 256);
+    c.bytes = off;
+    return c;
+}
+
+__global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
+                                 const double *opac, const double *betas, const double *colors,
+                                 const int32_t *bounds, Record *rec) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= v) return;
+    const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
+    Record r;
+    r.a = make_float4((float)(means[2 * k] - x0), (float)(means[2 * k + 1] - y0), (float)conics[3 * k],
+                      (float)conics[3 * k + 1]);
+    r.b = make_float4((float)conics[3 * k + 2], (float)opac[k], (float)betas[k], 0.f);
+    r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
+                      __int_as_float((int)k));
+    r.d = make_int4(x0, x1, y0, y1);
+    rec[k] = r;
+}
+
+__global__ void core_lists_kernel(const int64_t *offsets, const int64_t *lists, int64_t e,
+                                  int n_tiles, uint32_t *lists32, uint2 *ranges) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < e) lists32[i] = (uint32_t)lists[i];
+    if (i < n_tiles) ranges[i] = make_uint2((uint32_t)offsets[i], (uint32_t)offsets[i + 1]);
+}
+
+__global__ void core_unpack_kernel(int64_t v, const float *acc, float *d_means, float *d_conics,
+                                   float *d_opac, float *d_betas, float *d_colors) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= v) return;
+    const float *g = acc + k * kGradStride;
+    d_means[2 * k] = g[0];
+    d_means[2 * k + 1] = g[1];
+    d_conics[3 * k] = g[2];
+    d_conics[3 * k + 1] = g[3];
+    d_conics[3 * k + 2] = g[4];
+    d_opac[k] = g[5];
+    d_betas[k] = g[6];
+    d_colors[3 * k] = g[7];
+    d_colors[3 * k + 1] = g[8];
+    d_colors[3 * k + 2] = g[9];
+}
+
+__global__ void set_visible_kernel(FrameView f, uint32_t v) { f.ctr->visible = v; }
+
+}  // namespace bsr
+
+using namespace bsr;
+
+static bool bad_camera(const bsr_camera *c) {
+    return !c || c->width < 1 || c->height < 1 || !(c->fx > 0) || !(c->fy > 0);
+}
+
+static bool bad_scene(const bsr_scene *s) {
+    if (!s || s->n < 0 || s->n >= (1ll << 31)) return true;
+    if (!(s->sh_coeffs == 1 || s->sh_coeffs == 4 || s->sh_coeffs == 9 || s->sh_coeffs == 16)) return true;
+    if (s->n > 0 && (!s->positions || !s->rotations || !s->log_scales || !s->opacity_raw || !s->shapes ||
+                     !s->sh))
+        return true;
+    return false;
+}
+
+extern "C" int bsr_version(int32_t *major, int32_t *minor) {
+    if (major) *major = 0;
+    if (minor) *minor = 1;
+    return BSR_OK;
+}
+
+extern "C" const char *bsr_status_string(int32_t s) {
+    switch (s) {
+        case BSR_OK: return "ok";
+        case BSR_ERR_BAD_ARG: return "bad argument (shape / dtype / size)";
+        case BSR_ERR_CAPACITY: return "tile-entry capacity exceeded";
+        case BSR_ERR_CUDA: return "CUDA error";
+        case BSR_ERR_DEGENERATE_QUAT: return "quaternion norm below 1e-12";
+        case BSR_ERR_FRAME_TOO_SMALL: return "frame buffer too small";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_cap,
+                               uint64_t *bytes) {
+    if (!bytes || n < 0 || width < 1 || height < 1 || entry_cap < 0 || entry_cap >= (1ll << 31))
+        return BSR_ERR_BAD_ARG;
+    *bytes = carve_frame(nullptr, n, width, height, entry_cap).total_bytes;
+    return BSR_OK;
+}
+
+extern "C" int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                           void *frame, uint64_t frame_bytes, int64_t entry_cap,
+                           const bsr_outputs *out, void *stream) {
+    if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !out ||
+        entry_cap < 0 || entry_cap >= (1ll << 31))
+        return BSR_ERR_BAD_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
+    if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
+    const KCam cam = make_kcam(*camera);
+    BSR_CUDA_TRY(cudaMemsetAsync(frame, 0, f.zero_bytes, st));
+    int rc;
+    if ((rc = launch_preprocess(*scene, cam, f, st))) return rc;
+    if ((rc = launch_depth_sort(f, st))) return rc;
+    if ((rc = launch_emit(f, st))) return rc;
+    if ((rc = launch_tile_sort(f, st))) return rc;
+    if ((rc = launch_tile_ranges(f, st))) return rc;
+    if ((rc = launch_raster_fwd(f, *out, background, (float)kAlphaMin, (float)kTStop, nullptr, nullptr,
+                                nullptr, st)))
+        return rc;
+    const double bg64[3] = {background[0], background[1], background[2]};
+    return launch_replay_scene(true, f, *scene, cam, *out, bg64, kAlphaMin, kTStop, nullptr, nullptr, st);
+}
+
+extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream) {
+    if (!frame || !info) return BSR_ERR_BAD_ARG;
+    Counters c;
+    BSR_CUDA_TRY(cudaMemcpyAsync(&c, frame, sizeof(Counters), cudaMemcpyDeviceToHost,
+                                 (cudaStream_t)stream));
+    BSR_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    info->visible = c.visible;
+    info->entries = c.entries;
+    info->entries_needed = (int64_t)c.entries_needed;
+    info->flagged_pixels = c.flagged;
+    info->status = c.status;
+    info->reserved = 0;
+    return c.status;
+}
+
+extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
+                            const float background[3], void *frame, uint64_t frame_bytes,
+                            int64_t entry_cap, const float *d_color, const float *d_depth,
+                            const bsr_grads *grads, float *screen_grad_norm, void *stream) {
+    if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || !grads)
+        return BSR_ERR_BAD_ARG;
+    if (scene->n > 0 && (!grads->positions || !grads->rotations || !grads->log_scales ||
+                         !grads->opacity_raw || !grads->shapes || !grads->sh))
+        return BSR_ERR_BAD_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
+    if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
+    if (scene->n == 0) return BSR_OK;
+    const KCam cam = make_kcam(*camera);
+    zero_acc_kernel<<<(unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8), BSR_BLOCK,
+                      0, st>>>(f);
+    BSR_LAUNCH_CHECK();
+    int rc;
+    if ((rc = launch_raster_bwd(f, d_color, true, d_depth, background, (float)kAlphaMin, nullptr, nullptr,
+                                nullptr, st)))
+        return rc;
+    bsr_outputs none;
+    memset(&none, 0, sizeof(none));
+    const double bg64[3] = {background[0], background[1], background[2]};
+    if ((rc = launch_replay_scene(false, f, *scene, cam, none, bg64, kAlphaMin, kTStop, d_color, d_depth, st)))
+        return rc;
+    return launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, st);
+}
+
+// ---- core seam ---------------------------------------------------------------------
+extern "C" int bsr_core_scratch_bytes(int64_t v, int32_t width, int32_t height, int64_t n_entries,
+                                      uint64_t *bytes) {
+    if (!bytes || v < 0 || width < 1 || height < 1 || n_entries < 0) return BSR_ERR_BAD_ARG;
+    *bytes = carve_core(nullptr, v, width, height, n_entries).bytes;
+    return BSR_OK;
+}
+
+static int core_prepare(const CoreView &c, int64_t v, const double *means, const double *conics,
+                        const double *opac, const double *betas, const double *colors,
+                        const int32_t *bounds, const int64_t *offsets, const int64_t *lists,
+                        int64_t n_entries, cudaStream_t st) {
+    BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
+    if (v > 0)
+        core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
+                                                                               colors, bounds, c.f.rec);
+    const int64_t m = imax64(n_entries, c.f.n_tiles);
+    core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
+        offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);
+    set_visible_kernel<<<1, 1, 0, st>>>(c.f, (uint32_t)v);
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+extern "C" int bsr_core_forward_tiled(int64_t v, const double *means, const double *conics,
+                                      const double *opac, const double *betas, const double *colors,
+                                      const int32_t *bounds, int32_t height, int32_t width,
+                                      const double background[3], int32_t tile_size,
+                                      const int64_t *offsets, const int64_t *lists, int64_t n_entries,
+                                      double alpha_min, double t_stop, float *raw, float *transmittance,
+                                      int32_t *contrib, int32_t *pixel_count, void *scratch,
+                                      uint64_t scratch_bytes, int64_t *flagged_out, void *stream) {
+    if (tile_size != BSR_TILE || v < 0 || v >= (1ll << 31) || height < 1 || width < 1 || !background ||
+        !offsets || (n_entries > 0 && !lists) || !scratch)
+        return BSR_ERR_BAD_ARG;
+    const CoreView c = carve_core(scratch, v, width, height, n_entries);
+    if (scratch_bytes < c.bytes) return BSR_ERR_FRAME_TOO_SMALL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if ((rc = core_prepare(c, v, means, conics, opac, betas, colors, bounds, offsets, lists, n_entries, st)))
+        return rc;
+    bsr_outputs out;
+    memset(&out, 0, sizeof(out));
+    out.raw = raw;
+    out.transmittance = transmittance;
+    out.contributions = contrib;
+    out.pixel_count = pixel_count;
+    const float bg[3] = {(float)background[0], (float)background[1], (float)background[2]};
+    if ((rc = launch_raster_fwd(c.f, out, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, st)))
+        return rc;
+    if ((rc = launch_replay_arrays(true, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
+                                   out, background, alpha_min, t_stop, nullptr, st)))
+        return rc;
+    if (flagged_out) {
+        Counters h;
+        BSR_CUDA_TRY(cudaMemcpyAsync(&h, c.f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        BSR_CUDA_TRY(cudaStreamSynchronize(st));
+        *flagged_out = h.flagged;
+    }
+    return BSR_OK;
+}
+
+extern "C" int bsr_core_backward(int64_t v, const double *means, const double *conics, const double *opac,
+                                 const double *betas, const double *colors, const int32_t *bounds,
+                                 int32_t height, int32_t width, const double background[3],
+                                 const float *d_raw, int32_t tile_size, const int64_t *offsets,
+                                 const int64_t *lists, int64_t n_entries, double alpha_min, double t_stop,
+                                 float *d_means, float *d_conics, float *d_opac, float *d_betas,
+                                 float *d_colors, void *scratch, uint64_t scratch_bytes, void *stream) {
+    if (tile_size != BSR_TILE || v < 0 || v >= (1ll << 31) || height < 1 || width < 1 || !background ||
+        !offsets || (n_entries > 0 && !lists) || !scratch || !d_raw)
+        return BSR_ERR_BAD_ARG;
+    const CoreView c = carve_core(scratch, v, width, height, n_entries);
+    if (scratch_bytes < c.bytes) return BSR_ERR_FRAME_TOO_SMALL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if ((rc = core_prepare(c, v, means, conics, opac, betas, colors, bounds, offsets, lists, n_entries, st)))
+        return rc;
+    // replay the forward to recover the saved per-pixel state (the reference core
+    // recomputes the forward inside backward too, _raster.pyx:191-241)
+    bsr_outputs none;
+    memset(&none, 0, sizeof(none));
+    const float bg[3] = {(float)background[0], (float)background[1], (float)background[2]};
+    if ((rc = launch_raster_fwd(c.f, none, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, st)))
+        return rc;
+    if ((rc = launch_replay_arrays(true, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
+                                   none, background, alpha_min, t_stop, nullptr, st)))
+        return rc;
+    if (v > 0)
+        BSR_CUDA_TRY(cudaMemsetAsync(c.f.grad_acc, 0, 4ull * kGradStride * v, st));
+    if ((rc = launch_raster_bwd(c.f, d_raw, false, nullptr, bg, (float)alpha_min, c.lists, c.ranges, c.f.rec,
+                                st)))
+        return rc;
+    if ((rc = launch_replay_arrays(false, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
+                                   none, background, alpha_min, t_stop, d_raw, st)))
+        return rc;
+    if (v > 0)
+        core_unpack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, c.f.grad_acc, d_means,
+                                                                                 d_conics, d_opac, d_betas,
+                                                                                 d_colors);
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+// ---- debug / parity export -----------------------------------------------------------
+namespace bsr {
+__global__ void export_records_kernel(FrameView f, int32_t *src, int32_t *bounds) {
+    const uint32_t V = f.ctr->visible;
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= V) return;
+    const Record r = f.rec[c];
+    if (src) src[c] = __float_as_int(r.c.w);
+    if (bounds) {
+        bounds[4 * c] = r.d.x;
+        bounds[4 * c + 1] = r.d.y;
+        bounds[4 * c + 2] = r.d.z;
+        bounds[4 * c + 3] = r.d.w;
+    }
+}
+}  // namespace bsr
+
+extern "C" int bsr_debug_export(const void *frame, int64_t n, int32_t width, int32_t height,
+                                int64_t entry_cap, int32_t *order, int32_t *src_index,
+                                int32_t *bounds, int32_t *lists, int32_t *ranges, void *stream) {
+    if (!frame || n < 0 || width < 1 || height < 1) return BSR_ERR_BAD_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const FrameView f = carve_frame(const_cast<void *>(frame), n, width, height, entry_cap);
+    Counters c;
+    BSR_CUDA_TRY(cudaMemcpyAsync(&c, f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    BSR_CUDA_TRY(cudaStreamSynchronize(st));
+    if (order && c.visible)
+        BSR_CUDA_TRY(cudaMemcpyAsync(order, f.dvals[c.depth_plan[kDepthPasses] & 1u], 4ull * c.visible,
+                                     cudaMemcpyDeviceToDevice, st));
+    if (lists && c.entries)
+        BSR_CUDA_TRY(cudaMemcpyAsync(lists, f.tvals[c.tile_plan[f.tile_passes] & 1u], 4ull * c.entries,
+                                     cudaMemcpyDeviceToDevice, st));
+    if (ranges)
+        BSR_CUDA_TRY(cudaMemcpyAsync(ranges, f.tile_ranges, 8ull * f.n_tiles, cudaMemcpyDeviceToDevice, st));
+    if ((src_index || bounds) && c.visible)
+        export_records_kernel<<<(unsigned)div_up(c.visible, BSR_BLOCK), BSR_BLOCK, 0, st>>>(f, src_index, bounds);
+    BSR_LAUNCH_CHECK();
+    BSR_CUDA_TRY(cudaStreamSynchronize(st));
+    return BSR_OK;
+}

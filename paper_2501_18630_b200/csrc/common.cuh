@@ -1,0 +1,120 @@
+// Internal definitions shared by the libbsr kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bsr.h"
+
+#define BSR_TILE 16
+#define BSR_BLOCK 256
+
+namespace bsr {
+
+// Constants of the reference contract (rasterizer.py:28-30, primitive.py:22-25,
+// kernel.py:24-28).
+constexpr double kNearPlane = 0.01;
+constexpr double kCovConditioning = 0.3;
+constexpr int kBoundsGuard = 1;
+constexpr double kShapeClamp = 10.0;
+constexpr double kBaseExponent = 4.0;
+constexpr float kEdgeGradClamp = 1e7f;
+
+// Device-side error word values (bsr_status); first error wins (atomicCAS from 0).
+__device__ __forceinline__ void raise_status(int32_t *status, int32_t code) {
+    atomicCAS(reinterpret_cast<int *>(status), 0, code);
+}
+
+// ----------------------------------------------------------------------------------
+// Camera as seen by kernels.
+struct KCam {
+    double R[9];  // world->camera rotation, row-major
+    double t[3];
+    double center[3];  // -R^T t
+    double fx, fy, cx, cy;
+    int W, H, tiles_x, tiles_y;
+};
+
+inline KCam make_kcam(const bsr_camera &c) {
+    KCam k;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) k.R[3 * i + j] = c.world_to_camera[4 * i + j];
+        k.t[i] = c.world_to_camera[4 * i + 3];
+    }
+    for (int j = 0; j < 3; ++j)
+        k.center[j] = -(k.R[0 + j] * k.t[0] + k.R[3 + j] * k.t[1] + k.R[6 + j] * k.t[2]);
+    k.fx = c.fx;
+    k.fy = c.fy;
+    k.cx = c.cx;
+    k.cy = c.cy;
+    k.W = c.width;
+    k.H = c.height;
+    k.tiles_x = (c.width + BSR_TILE - 1) / BSR_TILE;
+    k.tiles_y = (c.height + BSR_TILE - 1) / BSR_TILE;
+    return k;
+}
+
+// ----------------------------------------------------------------------------------
+// Raster record: one per visible primitive, compact (source) order, 64 B.
+//   A: mean_x - x0, mean_y - y0, conic a, conic b      (mean stored relative to its
+//      bounds corner so dx = (px - x0) - rel loses no bits at large pixel coordinates)
+//   B: conic c, opacity, beta, depth z
+//   C: r, g, b, source index (bit-cast)
+//   D: x0, x1, y0, y1 (inclusive pixel bounds, primitive.py:252-262)
+struct __align__(16) Record {
+    float4 a, b, c;
+    int4 d;
+};
+static_assert(sizeof(Record) == 64, "record must be 64 B");
+
+// fp64 projected primitive (primitive.py:221-277), the single source of truth used by
+// preprocess AND by the fp64 replay of flagged pixels (same code => same bits).
+struct Proj64 {
+    double mx, my;       // mean2d
+    double c00, c01, c11;  // conditioned cov2d
+    double ca, cb, cc;   // conic
+    double tx, ty, tz;   // camera-space point
+    int x0, x1, y0, y1;  // bounds (inclusive)
+    bool visible;
+    bool degenerate;
+};
+
+// Lookback status word: [31:30] flag (0 none, 1 aggregate, 2 inclusive prefix), [29:0] value.
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagPrefix = 2u << 30;
+constexpr uint32_t kValueMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
+    return *reinterpret_cast<const volatile uint32_t *>(p);
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+    __threadfence();
+    *reinterpret_cast<volatile uint32_t *>(p) = v;
+}
+
+// Exclusive prefix over predecessors [0, part) via decoupled look-back on `status`.
+__device__ __forceinline__ uint32_t lookback_exclusive(const uint32_t *status, int part) {
+    uint32_t excl = 0;
+    for (int j = part - 1; j >= 0;) {
+        uint32_t s = ld_volatile(status + j);
+        if ((s & ~kValueMask) == 0) continue;  // spin until published
+        excl += s & kValueMask;
+        if (s & kFlagPrefix) break;
+        --j;
+    }
+    return excl;
+}
+
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline uint64_t align_up(uint64_t a, uint64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace bsr
+
+#define BSR_CUDA_TRY(expr)                                      \
+    do {                                                        \
+        cudaError_t _e = (expr);                                \
+        if (_e != cudaSuccess) return BSR_ERR_CUDA;             \
+    } while (0)
+#define BSR_LAUNCH_CHECK() BSR_CUDA_TRY(cudaGetLastError())

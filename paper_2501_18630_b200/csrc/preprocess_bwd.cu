@@ -1,0 +1,255 @@
+// K6 preprocess_bwd: per visible primitive, chain the raster gradients (grad_acc) back to
+// the unconstrained parameters -- the tail of render_backward (rasterizer.py:262-320):
+//   opacity sigmoid chain (:292-293), Beta exponent chain (:296-299),
+//   conic -> conditioned covariance  dSigma' = -Inv G Inv  (:302-312),
+//   project_backward + _rotation_grad_to_quat (primitive.py:302-367),
+//   SH colour chain (appearance.py:264-318, the SH adapter of SURVEY 8(c)) and the
+//   view-direction -> position chain (rasterizer.py:287-289),
+//   plus the depth extension  z = R[2].p + t[2].
+// Gradients are ADDED into the caller's per-parameter buffers (multi-view accumulation).
+// HBM roofline: V * (48 B grad_acc + 240 B params read + 240 B grads RMW) at SH-3.
+#include "frame.cuh"
+
+namespace bsr {
+
+struct PreBwdArgs {
+    bsr_scene sc;
+    KCam cam;
+    FrameView f;
+    bsr_grads g;
+    float *screen_grad_norm;
+};
+
+template <int K>
+__device__ __forceinline__ void sh_basis_and_grad(float x, float y, float z, float *b, float (*db)[3]) {
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    b[0] = C0;
+    db[0][0] = db[0][1] = db[0][2] = 0.f;
+    if constexpr (K > 1) {
+        b[1] = -C1 * y;
+        b[2] = C1 * z;
+        b[3] = -C1 * x;
+        db[1][0] = 0.f; db[1][1] = -C1; db[1][2] = 0.f;
+        db[2][0] = 0.f; db[2][1] = 0.f; db[2][2] = C1;
+        db[3][0] = -C1; db[3][1] = 0.f; db[3][2] = 0.f;
+    }
+    if constexpr (K > 4) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        const float c20 = 1.0925484305920792f, c21 = -1.0925484305920792f, c22 = 0.31539156525252005f,
+                    c23 = -1.0925484305920792f, c24 = 0.5462742152960396f;
+        b[4] = c20 * x * y;
+        b[5] = c21 * y * z;
+        b[6] = c22 * (2.f * zz - xx - yy);
+        b[7] = c23 * x * z;
+        b[8] = c24 * (xx - yy);
+        db[4][0] = c20 * y; db[4][1] = c20 * x; db[4][2] = 0.f;
+        db[5][0] = 0.f; db[5][1] = c21 * z; db[5][2] = c21 * y;
+        db[6][0] = -2.f * c22 * x; db[6][1] = -2.f * c22 * y; db[6][2] = 4.f * c22 * z;
+        db[7][0] = c23 * z; db[7][1] = 0.f; db[7][2] = c23 * x;
+        db[8][0] = 2.f * c24 * x; db[8][1] = -2.f * c24 * y; db[8][2] = 0.f;
+        if constexpr (K > 9) {
+            const float c30 = -0.5900435899266435f, c31 = 2.890611442640554f, c32 = -0.4570457994644658f,
+                        c33 = 0.3731763325901154f, c34 = -0.4570457994644658f, c35 = 1.445305721320277f,
+                        c36 = -0.5900435899266435f;
+            b[9] = c30 * y * (3.f * xx - yy);
+            b[10] = c31 * x * y * z;
+            b[11] = c32 * y * (4.f * zz - xx - yy);
+            b[12] = c33 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            b[13] = c34 * x * (4.f * zz - xx - yy);
+            b[14] = c35 * z * (xx - yy);
+            b[15] = c36 * x * (xx - 3.f * yy);
+            db[9][0] = c30 * 6.f * x * y; db[9][1] = c30 * (3.f * xx - 3.f * yy); db[9][2] = 0.f;
+            db[10][0] = c31 * y * z; db[10][1] = c31 * x * z; db[10][2] = c31 * x * y;
+            db[11][0] = c32 * -2.f * x * y; db[11][1] = c32 * (4.f * zz - xx - 3.f * yy); db[11][2] = c32 * 8.f * y * z;
+            db[12][0] = c33 * -6.f * x * z; db[12][1] = c33 * -6.f * y * z; db[12][2] = c33 * (6.f * zz - 3.f * xx - 3.f * yy);
+            db[13][0] = c34 * (4.f * zz - 3.f * xx - yy); db[13][1] = c34 * -2.f * x * y; db[13][2] = c34 * 8.f * x * z;
+            db[14][0] = c35 * 2.f * x * z; db[14][1] = c35 * -2.f * y * z; db[14][2] = c35 * (xx - yy);
+            db[15][0] = c36 * (3.f * xx - 3.f * yy); db[15][1] = c36 * -6.f * x * y; db[15][2] = 0.f;
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a) {
+    const uint32_t V = a.f.ctr->visible;
+    const uint32_t c = blockIdx.x * BSR_BLOCK + threadIdx.x;
+    if (c >= V) return;
+    const float *acc = a.f.grad_acc + (int64_t)c * kGradStride;
+    const float4 g0 = *reinterpret_cast<const float4 *>(acc);
+    const float4 g1 = *reinterpret_cast<const float4 *>(acc + 4);
+    const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
+    const float dmx = g0.x, dmy = g0.y, dA = g0.z, dB = g0.w, dC = g1.x, d_o = g1.y, d_beta = g1.z;
+    const float dr = g1.w, dg = g2.x, dbl = g2.y, dz = g2.z;
+    const int64_t i = __float_as_int(a.f.rec[c].c.w);
+    const bsr_scene &sc = a.sc;
+    const KCam &cam = a.cam;
+
+    // ---- opacity / shape chains
+    const float oraw = sc.opacity_raw[i];
+    const float o = oraw >= 0.f ? 1.f / (1.f + expf(-oraw)) : expf(oraw) / (1.f + expf(oraw));
+    a.g.opacity_raw[i] += d_o * o * (1.f - o);
+    const float bsh = sc.shapes[i];
+    const float beta = 4.f * expf(fminf(fmaxf(bsh, -10.f), 10.f));
+    if (fabsf(bsh) <= 10.f) a.g.shapes[i] += d_beta * beta;
+
+    // ---- recompute projection (fp32)
+    const float px = sc.positions[3 * i], py = sc.positions[3 * i + 1], pz = sc.positions[3 * i + 2];
+    float R[9];
+    for (int k = 0; k < 9; ++k) R[k] = (float)cam.R[k];
+    const float tx = R[0] * px + R[1] * py + R[2] * pz + (float)cam.t[0];
+    const float ty = R[3] * px + R[4] * py + R[5] * pz + (float)cam.t[1];
+    const float tz = R[6] * px + R[7] * py + R[8] * pz + (float)cam.t[2];
+    const float fx = (float)cam.fx, fy = (float)cam.fy;
+    float qw = sc.rotations[4 * i], qx = sc.rotations[4 * i + 1], qy = sc.rotations[4 * i + 2],
+          qz = sc.rotations[4 * i + 3];
+    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= qn;
+    qx /= qn;
+    qy /= qn;
+    qz /= qn;
+    float Q[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                  2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                  2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+    float s2[3];
+    for (int k = 0; k < 3; ++k) {
+        const float s = expf(sc.log_scales[3 * i + k]);
+        s2[k] = s * s;
+    }
+    float Sig[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col)
+            Sig[3 * r + col] = Q[3 * r] * s2[0] * Q[3 * col] + Q[3 * r + 1] * s2[1] * Q[3 * col + 1] +
+                               Q[3 * r + 2] * s2[2] * Q[3 * col + 2];
+    const float itz = 1.f / tz, itz2 = itz * itz;
+    const float J00 = fx * itz, J02 = -fx * tx * itz2, J11 = fy * itz, J12 = -fy * ty * itz2;
+    float Am[6];
+    for (int j = 0; j < 3; ++j) {
+        Am[j] = J00 * R[j] + J02 * R[6 + j];
+        Am[3 + j] = J11 * R[3 + j] + J12 * R[6 + j];
+    }
+    float AS[6];
+    for (int r = 0; r < 2; ++r)
+        for (int j = 0; j < 3; ++j)
+            AS[3 * r + j] = Am[3 * r] * Sig[j] + Am[3 * r + 1] * Sig[3 + j] + Am[3 * r + 2] * Sig[6 + j];
+    const float c00 = AS[0] * Am[0] + AS[1] * Am[1] + AS[2] * Am[2] + 0.3f;
+    const float c01 = AS[0] * Am[3] + AS[1] * Am[4] + AS[2] * Am[5];
+    const float c11 = AS[3] * Am[3] + AS[4] * Am[4] + AS[5] * Am[5] + 0.3f;
+    const float idet = 1.f / (c00 * c11 - c01 * c01);
+    const float ia = c11 * idet, ib = -c01 * idet, ic = c00 * idet;
+    // d cov2d = -Inv G Inv, G = [[dA, dB/2], [dB/2, dC]]
+    const float Gb = 0.5f * dB;
+    const float m00 = dA * ia + Gb * ib, m01 = dA * ib + Gb * ic;  // G Inv
+    const float m10 = Gb * ia + dC * ib, m11 = Gb * ib + dC * ic;
+    const float gm00 = -(ia * m00 + ib * m10), gm01 = -(ia * m01 + ib * m11);
+    const float gm10 = -(ib * m00 + ic * m10), gm11 = -(ib * m01 + ic * m11);
+    // symmetrise (project_backward g_m = (d + d^T)/2)
+    const float gs01 = 0.5f * (gm01 + gm10);
+    const float Gm[4] = {gm00, gs01, gs01, gm11};
+    // g_sigma = A^T g_m A (3x3)
+    float gS[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col) {
+            float v = 0.f;
+            for (int u = 0; u < 2; ++u)
+                for (int w = 0; w < 2; ++w) v += Am[3 * u + r] * Gm[2 * u + w] * Am[3 * w + col];
+            gS[3 * r + col] = v;
+        }
+    // g_a = 2 g_m A Sigma (2x3); g_jac = g_a R^T
+    float gA[6];
+    for (int u = 0; u < 2; ++u)
+        for (int j = 0; j < 3; ++j) {
+            float v = 0.f;
+            for (int w = 0; w < 2; ++w)
+                for (int k = 0; k < 3; ++k) v += Gm[2 * u + w] * Am[3 * w + k] * Sig[3 * k + j];
+            gA[3 * u + j] = 2.f * v;
+        }
+    float gJ[6];
+    for (int u = 0; u < 2; ++u)
+        for (int j = 0; j < 3; ++j)
+            gJ[3 * u + j] = gA[3 * u] * R[3 * j] + gA[3 * u + 1] * R[3 * j + 1] + gA[3 * u + 2] * R[3 * j + 2];
+    // g_t = J^T d_mean + dJ/dt terms (primitive.py:328-337)
+    float gt0 = J00 * dmx, gt1 = J11 * dmy, gt2 = J02 * dmx + J12 * dmy;
+    gt0 += gJ[2] * (-fx * itz2);
+    gt1 += gJ[5] * (-fy * itz2);
+    gt2 += gJ[0] * (-fx * itz2) + gJ[2] * (2.f * fx * tx * itz2 * itz) + gJ[4] * (-fy * itz2) +
+           gJ[5] * (2.f * fy * ty * itz2 * itz);
+    gt2 += dz;  // depth extension: z = t_z
+    float dpx = gt0 * R[0] + gt1 * R[3] + gt2 * R[6];
+    float dpy = gt0 * R[1] + gt1 * R[4] + gt2 * R[7];
+    float dpz = gt0 * R[2] + gt1 * R[5] + gt2 * R[8];
+    // Sigma = Q diag(s^2) Q^T: g_rot = 2 gS Q diag(s^2); g_d_i = (Q^T gS Q)_ii
+    float gR[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col)
+            gR[3 * r + col] = 2.f * (gS[3 * r] * Q[col] + gS[3 * r + 1] * Q[3 + col] + gS[3 * r + 2] * Q[6 + col]) * s2[col];
+    for (int k = 0; k < 3; ++k) {
+        float v = 0.f;
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) v += Q[3 * j + k] * gS[3 * j + l] * Q[3 * l + k];
+        a.g.log_scales[3 * i + k] += v * 2.f * s2[k];
+    }
+    // _rotation_grad_to_quat (primitive.py:348-367)
+    {
+        const float w = qw, x = qx, y = qy, z = qz;
+        const float *g = gR;
+        const float gw = 2.f * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
+        const float gx = 2.f * (y * g[1] + z * g[2] + y * g[3] - 2.f * x * g[4] - w * g[5] + z * g[6] + w * g[7] - 2.f * x * g[8]);
+        const float gy = 2.f * (-2.f * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - 2.f * y * g[8]);
+        const float gz = 2.f * (-2.f * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2.f * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
+        const float dot = gw * w + gx * x + gy * y + gz * z;
+        a.g.rotations[4 * i] += (gw - dot * w) / qn;
+        a.g.rotations[4 * i + 1] += (gx - dot * x) / qn;
+        a.g.rotations[4 * i + 2] += (gy - dot * y) / qn;
+        a.g.rotations[4 * i + 3] += (gz - dot * z) / qn;
+    }
+    // ---- SH colour chain + view direction -> position
+    {
+        float vx = px - (float)cam.center[0], vy = py - (float)cam.center[1], vz = pz - (float)cam.center[2];
+        const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
+        const float ivn = 1.f / vn;
+        vx *= ivn;
+        vy *= ivn;
+        vz *= ivn;
+        float b[16], db[16][3];
+        sh_basis_and_grad<K>(vx, vy, vz, b, db);
+        float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+        const float *shp = sc.sh + i * 3 * K;
+        float *gsh = a.g.sh + i * 3 * K;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            gsh[3 * k] += b[k] * dr;
+            gsh[3 * k + 1] += b[k] * dg;
+            gsh[3 * k + 2] += b[k] * dbl;
+            const float dbk = shp[3 * k] * dr + shp[3 * k + 1] * dg + shp[3 * k + 2] * dbl;
+            ddx += db[k][0] * dbk;
+            ddy += db[k][1] * dbk;
+            ddz += db[k][2] * dbk;
+        }
+        const float dd = ddx * vx + ddy * vy + ddz * vz;
+        dpx += (ddx - dd * vx) * ivn;
+        dpy += (ddy - dd * vy) * ivn;
+        dpz += (ddz - dd * vz) * ivn;
+    }
+    a.g.positions[3 * i] += dpx;
+    a.g.positions[3 * i + 1] += dpy;
+    a.g.positions[3 * i + 2] += dpz;
+    if (a.screen_grad_norm) a.screen_grad_norm[i] = sqrtf(dmx * dmx + dmy * dmy);
+}
+
+int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView &f,
+                          const bsr_grads &g, float *screen_grad_norm, cudaStream_t st) {
+    if (f.n == 0) return BSR_OK;
+    PreBwdArgs a{sc, cam, f, g, screen_grad_norm};
+    const unsigned blocks = (unsigned)div_up(f.n, BSR_BLOCK);
+    switch (sc.sh_coeffs) {
+        case 1: preprocess_bwd_kernel<1><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
+        case 4: preprocess_bwd_kernel<4><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
+        case 9: preprocess_bwd_kernel<9><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
+        case 16: preprocess_bwd_kernel<16><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
+        default: return BSR_ERR_BAD_ARG;
+    }
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+}  // namespace bsr

@@ -1,0 +1,177 @@
+// fp64 projection + SH colour of one primitive.  Included ONLY by translation units
+// compiled with -fmad=false (preprocess.cu, replay.cu) so that every caller produces the
+// same bits, and so the operation order matches the reference's numpy/-ffp-contract=off
+// arithmetic as closely as a restatement can.
+#pragma once
+
+#include "common.cuh"
+
+namespace bsr {
+
+// primitive.py:28-35 (split-branch stable sigmoid)
+__device__ __forceinline__ double sigmoid64(double x) {
+    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+    double e = exp(x);
+    return e / (1.0 + e);
+}
+
+// kernel.py:42-44
+__device__ __forceinline__ double shape_to_exponent64(double b) {
+    return kBaseExponent * exp(fmin(fmax(b, -kShapeClamp), kShapeClamp));
+}
+
+// primitive.py:48-67 (normalised wxyz -> R)
+__device__ __forceinline__ bool quat_to_rot64(const float *q4, double R[9]) {
+    double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+    double nrm = sqrt(((w * w + x * x) + y * y) + z * z);
+    if (!(nrm >= 1e-12)) return false;
+    w /= nrm;
+    x /= nrm;
+    y /= nrm;
+    z /= nrm;
+    R[0] = 1 - 2 * (y * y + z * z);
+    R[1] = 2 * (x * y - w * z);
+    R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);
+    R[4] = 1 - 2 * (x * x + z * z);
+    R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);
+    R[7] = 2 * (y * z + w * x);
+    R[8] = 1 - 2 * (x * x + y * y);
+    return true;
+}
+
+// numpy's float64 -> int32 cast on x86 (cvttsd2si): out-of-range / NaN -> INT32_MIN,
+// followed by wrapping int32 arithmetic (primitive.py:254-261).
+__device__ __forceinline__ int np_i32(double v) {
+    return (v > -2147483649.0 && v < 2147483648.0) ? (int)v : (int)0x80000000;
+}
+__device__ __forceinline__ int np_i32_add(int a, int b) {
+    return (int)((unsigned)a + (unsigned)b);
+}
+
+// primitive.py:221-277 for one primitive.
+__device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat4,
+                                            const float *logs3, const KCam &cam) {
+    Proj64 p;
+    p.visible = false;
+    p.degenerate = false;
+    const double px = pos3[0], py = pos3[1], pz = pos3[2];
+    const double *R = cam.R;
+    // cam_pts = positions @ R^T + t
+    p.tx = ((px * R[0] + py * R[1]) + pz * R[2]) + cam.t[0];
+    p.ty = ((px * R[3] + py * R[4]) + pz * R[5]) + cam.t[1];
+    p.tz = ((px * R[6] + py * R[7]) + pz * R[8]) + cam.t[2];
+    if (!(p.tz > kNearPlane)) return p;
+    const double tx = p.tx, ty = p.ty, tz = p.tz;
+    p.mx = cam.fx * tx / tz + cam.cx;
+    p.my = cam.fy * ty / tz + cam.cy;
+    // Sigma = (R diag s)(R diag s)^T
+    double Q[9];
+    if (!quat_to_rot64(quat4, Q)) {
+        p.degenerate = true;
+        return p;
+    }
+    const double s0 = exp((double)logs3[0]), s1 = exp((double)logs3[1]), s2 = exp((double)logs3[2]);
+    double rs[9] = {Q[0] * s0, Q[1] * s1, Q[2] * s2, Q[3] * s0, Q[4] * s1,
+                    Q[5] * s2, Q[6] * s0, Q[7] * s1, Q[8] * s2};
+    double S[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            S[3 * i + j] = (rs[3 * i] * rs[3 * j] + rs[3 * i + 1] * rs[3 * j + 1]) +
+                           rs[3 * i + 2] * rs[3 * j + 2];
+    // J (2x3), a = J @ R_cam (2x3)
+    const double tz2 = tz * tz;
+    const double j00 = cam.fx / tz, j02 = -cam.fx * tx / tz2;
+    const double j11 = cam.fy / tz, j12 = -cam.fy * ty / tz2;
+    double A[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        A[j] = (j00 * R[j] + 0.0 * R[3 + j]) + j02 * R[6 + j];
+        A[3 + j] = (0.0 * R[j] + j11 * R[3 + j]) + j12 * R[6 + j];
+    }
+    // cov = (A @ S) @ A^T
+    double AS[6];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            AS[3 * i + j] = (A[3 * i] * S[j] + A[3 * i + 1] * S[3 + j]) + A[3 * i + 2] * S[6 + j];
+    double c00 = (AS[0] * A[0] + AS[1] * A[1]) + AS[2] * A[2];
+    double c01 = (AS[0] * A[3] + AS[1] * A[4]) + AS[2] * A[5];
+    double c11 = (AS[3] * A[3] + AS[4] * A[4]) + AS[5] * A[5];
+    c00 += kCovConditioning;
+    c11 += kCovConditioning;
+    p.c00 = c00;
+    p.c01 = c01;
+    p.c11 = c11;
+    const double det = c00 * c11 - c01 * c01;
+    p.ca = c11 / det;
+    p.cb = -c01 / det;
+    p.cc = c00 / det;
+    const double ex = sqrt(c00), ey = sqrt(c11);
+    p.x0 = max(np_i32_add(np_i32(floor(p.mx - ex)), -kBoundsGuard), 0);
+    p.x1 = min(np_i32_add(np_i32(ceil(p.mx + ex)), kBoundsGuard), cam.W - 1);
+    p.y0 = max(np_i32_add(np_i32(floor(p.my - ey)), -kBoundsGuard), 0);
+    p.y1 = min(np_i32_add(np_i32(ceil(p.my + ey)), kBoundsGuard), cam.H - 1);
+    p.visible = (p.x0 <= p.x1) && (p.y0 <= p.y1);
+    return p;
+}
+
+// appearance.py:192-261 real SH basis (degree <= 3), reference constants and signs.
+template <int K>
+__device__ __forceinline__ void sh_basis64(double x, double y, double z, double *b) {
+    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+    b[0] = C0;
+    if (K > 1) {
+        b[1] = -C1 * y;
+        b[2] = C1 * z;
+        b[3] = -C1 * x;
+    }
+    if (K > 4) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        b[4] = 1.0925484305920792 * x * y;
+        b[5] = -1.0925484305920792 * y * z;
+        b[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+        b[7] = -1.0925484305920792 * x * z;
+        b[8] = 0.5462742152960396 * (xx - yy);
+        if (K > 9) {
+            b[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+            b[10] = 2.890611442640554 * x * y * z;
+            b[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+            b[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            b[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+            b[14] = 1.445305721320277 * z * (xx - yy);
+            b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+// rasterizer.py:94-95 view direction + einsum(basis, sh) colour (SH adapter).
+template <int K>
+__device__ __forceinline__ void sh_color64(const float *sh, const float *pos3,
+                                           const KCam &cam, double rgb[3]) {
+    double dx = (double)pos3[0] - cam.center[0];
+    double dy = (double)pos3[1] - cam.center[1];
+    double dz = (double)pos3[2] - cam.center[2];
+    const double n = sqrt((dx * dx + dy * dy) + dz * dz);
+    dx /= n;
+    dy /= n;
+    dz /= n;
+    double b[16];
+    sh_basis64<K>(dx, dy, dz, b);
+    double r = 0.0, g = 0.0, bl = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        r += b[k] * (double)sh[3 * k + 0];
+        g += b[k] * (double)sh[3 * k + 1];
+        bl += b[k] * (double)sh[3 * k + 2];
+    }
+    rgb[0] = r;
+    rgb[1] = g;
+    rgb[2] = bl;
+}
+
+}  // namespace bsr

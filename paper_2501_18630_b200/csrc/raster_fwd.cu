@@ -1,0 +1,182 @@
+// K4 raster_fwd: per-16x16-tile front-to-back compositing (_raster.pyx:74-155).
+//
+// One CTA (256 threads) per tile, one pixel per thread; a warp owns an 8x4 pixel block so
+// compact footprints touch few warps.  Tile-list records (64 B) are gathered into shared
+// memory in batches of 256 with cp.async double buffering; every entry is first tested
+// against the warp's pixel rectangle (warp-uniform skip), then evaluated per pixel.
+// Termination: warp ballots count contributions, __syncthreads_count ends the tile once
+// every pixel has T < t_stop ("composite, then stop", _raster.pyx:116-123).
+//
+// Exactness: decisions alpha >= alpha_min and T < t_stop are taken in fp32
+// only when a rigorous error bound certifies them; otherwise the pixel is handed to the
+// fp64 replay (replay.cu) from that entry on.  Pixels with alpha > 0.999 (fp32 cannot
+// carry 1 - alpha) are handed over too.
+//
+// Roofline: FP32 + XU pipes, per evaluated pair ~27 FP32 FLOP + 2 XU.
+#include "raster.cuh"
+
+namespace bsr {
+
+struct RasterFwdArgs {
+    FrameView f;
+    bsr_outputs out;
+    float bg[3];
+    float alpha_min, t_stop;
+    // core seam: lists/ranges supplied externally instead of the frame's sorted buffers
+    const uint32_t *lists;   // entry -> record index
+    const uint2 *ranges;     // tile -> [start, end)
+    const Record *rec;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) {
+    __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
+    __shared__ int s_cnt[BSR_BLOCK];
+    const FrameView &f = a.f;
+    const int tile = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
+    const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const bool inside = px < f.W && py < f.H;
+    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const Record *rec = a.rec ? a.rec : f.rec;
+    const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
+    const int start = (int)range.x, end = (int)range.y;
+
+    float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
+    int cnt = 0, last = 0, flag_at = -1;
+    bool done = !inside;
+    s_cnt[t] = 0;
+
+    auto prefetch = [&](int b0, int buf) {
+        const int e = b0 + t;
+        if (e < end) {
+            const Record *src = rec + lists[e];
+            Record *dst = &s_rec[buf][t];
+            cp_async16(&dst->a, &src->a);
+            cp_async16(&dst->b, &src->b);
+            cp_async16(&dst->c, &src->c);
+            cp_async16(&dst->d, &src->d);
+        }
+        cp_async_commit();
+    };
+
+    if (start < end) prefetch(start, 0);
+    int buf = 0;
+    for (int b0 = start; b0 < end; b0 += BSR_BLOCK, buf ^= 1) {
+        const bool more = b0 + BSR_BLOCK < end;
+        if (more) prefetch(b0 + BSR_BLOCK, buf ^ 1);
+        if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+        if (__syncthreads_count(done) == BSR_BLOCK) break;
+        const int nb = min(BSR_BLOCK, end - b0);
+        for (int j = 0; j < nb; ++j) {
+            const int4 bd = s_rec[buf][j].d;
+            if (bd.y < wx0 || bd.x > wx0 + 7 || bd.w < wy0 || bd.z > wy0 + 3) continue;
+            bool took = false;
+            if (!done) {
+                const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b;
+                const Pair p = eval_pair(A, B, px - bd.x, py - bd.z);
+                bool ambiguous = false;
+                // rare path: alpha within 5% of the cutoff -> certify with the error bound
+                if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
+                    const float rel = alpha_rel_err(A, B, p);
+                    ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 1e-9f * a.alpha_min;
+                }
+                if (!ambiguous && p.alpha >= a.alpha_min) {
+                    const float Tn = __fmul_rn(T, __fsub_rn(1.0f, p.alpha));
+                    const float rel = alpha_rel_err(A, B, p);
+                    const float errTn = errT + 2.5f * 5.9604645e-08f + p.alpha * rel / fmaxf(1.0f - p.alpha, 1e-30f);
+                    if (p.alpha > 0.999f ||
+                        fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * 5.9604645e-08f * a.t_stop) {
+                        ambiguous = true;
+                    } else {
+                        const float4 C = s_rec[buf][j].c;
+                        const float w = __fmul_rn(p.alpha, T);
+                        c0 = __fmaf_rn(w, C.x, c0);
+                        c1 = __fmaf_rn(w, C.y, c1);
+                        c2 = __fmaf_rn(w, C.z, c2);
+                        dep = __fmaf_rn(w, B.w, dep);
+                        T = Tn;
+                        errT = errTn;
+                        ++cnt;
+                        last = b0 + j - start + 1;
+                        took = true;
+                        if (T < a.t_stop) done = true;
+                    }
+                }
+                if (ambiguous) {
+                    flag_at = b0 + j - start;
+                    done = true;
+                }
+            }
+            const unsigned ballot = __ballot_sync(0xffffffffu, took);
+            if (ballot && lane == 0) atomicAdd(&s_cnt[j], __popc(ballot));
+        }
+        __syncthreads();
+        if (t < nb && s_cnt[t]) {
+            if (a.out.contributions)
+                atomicAdd(a.out.contributions + __float_as_int(s_rec[buf][t].c.w), s_cnt[t]);
+            s_cnt[t] = 0;
+        }
+    }
+    cp_async_wait<0>();
+    if (!inside) return;
+    const int64_t pix = (int64_t)py * f.W + px;
+    if (flag_at >= 0) {
+        const uint32_t slot = atomicAdd(&f.ctr->flagged, 1u);
+        f.flags[slot] = make_uint2((uint32_t)pix, (uint32_t)flag_at);
+        f.last[pix] = 0;
+        return;  // every per-pixel output is written by the fp64 replay
+    }
+    const float r0 = __fmaf_rn(a.bg[0], T, c0), r1 = __fmaf_rn(a.bg[1], T, c1),
+                r2 = __fmaf_rn(a.bg[2], T, c2);
+    f.t_final[pix] = T;
+    // low 29 bits: local end index of the last contributor; bits 29..31: raw < 0 per
+    // channel (clamp chain of the backward, rasterizer.py:253)
+    f.last[pix] = (uint32_t)last | (!(r0 >= 0.f) ? 1u << 29 : 0u) | (!(r1 >= 0.f) ? 1u << 30 : 0u) |
+                  (!(r2 >= 0.f) ? 1u << 31 : 0u);
+    if (a.out.raw) {
+        a.out.raw[3 * pix] = r0;
+        a.out.raw[3 * pix + 1] = r1;
+        a.out.raw[3 * pix + 2] = r2;
+    }
+    if (a.out.color) {
+        a.out.color[3 * pix] = fmaxf(r0, 0.f);
+        a.out.color[3 * pix + 1] = fmaxf(r1, 0.f);
+        a.out.color[3 * pix + 2] = fmaxf(r2, 0.f);
+    }
+    if (a.out.alpha) a.out.alpha[pix] = 1.0f - T;
+    if (a.out.transmittance) a.out.transmittance[pix] = T;
+    if (a.out.depth) a.out.depth[pix] = dep;
+    if (a.out.pixel_count) a.out.pixel_count[pix] = cnt;
+}
+
+int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg[3], float alpha_min,
+                      float t_stop, const uint32_t *lists, const uint2 *ranges, const Record *rec,
+                      cudaStream_t st) {
+    if (f.n_tiles == 0) return BSR_OK;
+    RasterFwdArgs a;
+    a.f = f;
+    a.out = out;
+    a.bg[0] = bg[0];
+    a.bg[1] = bg[1];
+    a.bg[2] = bg[2];
+    a.alpha_min = alpha_min;
+    a.t_stop = t_stop;
+    a.lists = lists;
+    a.ranges = ranges;
+    a.rec = rec;
+    raster_fwd_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+}  // namespace bsr

@@ -1,0 +1,347 @@
+// fp64 replay of the pixels the fp32 raster could not certify.
+//
+// For each flagged pixel one warp re-walks the pixel's tile list with the reference's
+// fp64 arithmetic (_raster.pyx:101-127 forward, :191-241 backward; this file is compiled
+// with -fmad=false like pkg/setup.py's -ffp-contract=off).  Primitive values come from a
+// Provider: the full pipeline recomputes them with the same fp64 code as preprocess.cu
+// (project.cuh), the core seam reads the caller's fp64 arrays.  Lanes evaluate 32 list
+// entries in parallel; the compositing recurrence (order-dependent) runs redundantly in
+// every lane over the candidates, in list order.
+//
+// Forward writes every per-pixel output of the flagged pixel and counts contributions of
+// entries at or after the entry where fp32 stopped (entries before it were certified and
+// counted by the fp32 kernel).  Backward adds the pixel's gradients into grad_acc.
+#include "frame.cuh"
+#include "project.cuh"
+
+namespace bsr {
+
+struct Entry64 {
+    double mx, my, ca, cb, cc, o, beta, r, g, b, z;
+    int src;
+};
+
+// Full pipeline: recompute from the scene parameters (bit-identical to preprocess).
+template <int K>
+struct SceneProvider {
+    bsr_scene sc;
+    KCam cam;
+    const Record *rec;
+    __device__ __forceinline__ bool get(uint32_t c, int px, int py, Entry64 &e) const {
+        const int4 bd = rec[c].d;
+        if (px < bd.x || px > bd.y || py < bd.z || py > bd.w) return false;
+        const int64_t i = __float_as_int(rec[c].c.w);
+        const float pos[3] = {sc.positions[3 * i], sc.positions[3 * i + 1], sc.positions[3 * i + 2]};
+        const float q[4] = {sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2],
+                            sc.rotations[4 * i + 3]};
+        const float ls[3] = {sc.log_scales[3 * i], sc.log_scales[3 * i + 1], sc.log_scales[3 * i + 2]};
+        const Proj64 p = project64(pos, q, ls, cam);
+        float shv[3 * K];
+#pragma unroll
+        for (int j = 0; j < 3 * K; ++j) shv[j] = sc.sh[i * 3 * K + j];
+        double rgb[3];
+        sh_color64<K>(shv, pos, cam, rgb);
+        e.mx = p.mx;
+        e.my = p.my;
+        e.ca = p.ca;
+        e.cb = p.cb;
+        e.cc = p.cc;
+        e.o = sigmoid64((double)sc.opacity_raw[i]);
+        e.beta = shape_to_exponent64((double)sc.shapes[i]);
+        e.r = rgb[0];
+        e.g = rgb[1];
+        e.b = rgb[2];
+        e.z = p.tz;
+        e.src = (int)i;
+        return true;
+    }
+};
+
+// Core seam: the caller's depth-sorted fp64 arrays (_raster.pyx:130-134 inputs).
+struct ArrayProvider {
+    const double *means, *conics, *opac, *betas, *colors;
+    const int32_t *bounds;
+    __device__ __forceinline__ bool get(uint32_t c, int px, int py, Entry64 &e) const {
+        const int32_t *bd = bounds + 4 * (int64_t)c;
+        if (px < bd[0] || px > bd[1] || py < bd[2] || py > bd[3]) return false;
+        e.mx = means[2 * c];
+        e.my = means[2 * c + 1];
+        e.ca = conics[3 * c];
+        e.cb = conics[3 * c + 1];
+        e.cc = conics[3 * c + 2];
+        e.o = opac[c];
+        e.beta = betas[c];
+        e.r = colors[3 * c];
+        e.g = colors[3 * c + 1];
+        e.b = colors[3 * c + 2];
+        e.z = 0.0;
+        e.src = (int)c;
+        return true;
+    }
+};
+
+struct ReplayArgs {
+    FrameView f;
+    bsr_outputs out;
+    double bg[3];
+    double alpha_min, t_stop;
+    const uint32_t *lists;
+    const uint2 *ranges;
+    // backward only
+    const float *d_color, *d_depth;
+    bool mask_raw;  // apply d_raw = d_color * [raw >= 0] (full pipeline; core seam gets d_raw)
+};
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(0xffffffffu, v, src);
+}
+
+// Evaluate alpha exactly as _raster.pyx:107-113 (fp64, no contraction in this TU).
+__device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, double &dx, double &dy,
+                                          double &x, double &kernel) {
+    dx = px - e.mx;
+    dy = py - e.my;
+    const double r2 = e.ca * dx * dx + 2.0 * e.cb * dx * dy + e.cc * dy * dy;
+    x = fmin(fmax(r2, 0.0), 1.0);
+    kernel = pow(1.0 - x, e.beta);
+    return e.o * kernel;
+}
+
+template <typename P>
+__device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, int lane) {
+    const FrameView &f = a.f;
+    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
+    const uint2 fl = f.flags[slot];
+    const int64_t pix = fl.x;
+    const int px = (int)(pix % f.W), py = (int)(pix / f.W);
+    const int tile = (py / BSR_TILE) * f.tiles_x + px / BSR_TILE;
+    const int start = (int)ranges[tile].x, end = (int)ranges[tile].y;
+    const int flag_at = (int)fl.y;
+
+    double t = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dd = 0.0;
+    int count = 0, last = 0;
+    bool done = false;
+    for (int base = start; base < end && !done; base += 32) {
+        const int e = base + lane;
+        Entry64 en;
+        bool cand = false;
+        double alpha = 0.0;
+        if (e < end && prov.get(lists[e], px, py, en)) {
+            double dx, dy, x, k;
+            alpha = alpha64(en, px, py, dx, dy, x, k);
+            cand = !(alpha < a.alpha_min);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, cand);
+        bool mine = false;
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const double al = shfl_d(alpha, l);
+            const double weight = al * t;
+            c0 = c0 + weight * shfl_d(en.r, l);
+            c1 = c1 + weight * shfl_d(en.g, l);
+            c2 = c2 + weight * shfl_d(en.b, l);
+            dd = dd + weight * shfl_d(en.z, l);
+            t = t * (1.0 - al);
+            ++count;
+            last = base + l - start + 1;
+            if (l == lane) mine = true;
+            if (t < a.t_stop) {
+                done = true;
+                break;
+            }
+        }
+        if (mine && (e - start) >= flag_at && a.out.contributions)
+            atomicAdd(a.out.contributions + en.src, 1);
+    }
+    if (lane != 0) return;
+    const double r0 = c0 + a.bg[0] * t, r1 = c1 + a.bg[1] * t, r2 = c2 + a.bg[2] * t;
+    if (a.out.raw) {
+        a.out.raw[3 * pix] = (float)r0;
+        a.out.raw[3 * pix + 1] = (float)r1;
+        a.out.raw[3 * pix + 2] = (float)r2;
+    }
+    if (a.out.color) {
+        a.out.color[3 * pix] = (float)fmax(r0, 0.0);
+        a.out.color[3 * pix + 1] = (float)fmax(r1, 0.0);
+        a.out.color[3 * pix + 2] = (float)fmax(r2, 0.0);
+    }
+    if (a.out.alpha) a.out.alpha[pix] = (float)(1.0 - t);
+    if (a.out.transmittance) a.out.transmittance[pix] = (float)t;
+    if (a.out.depth) a.out.depth[pix] = (float)dd;
+    if (a.out.pixel_count) a.out.pixel_count[pix] = count;
+    f.t_final[pix] = (float)t;
+    double *st = f.replay_state + 6 * (int64_t)slot;
+    st[0] = r0;
+    st[1] = r1;
+    st[2] = r2;
+    st[3] = dd;
+    st[4] = t;
+    st[5] = (double)last;
+}
+
+template <typename P>
+__device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, int lane) {
+    const FrameView &f = a.f;
+    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
+    const uint2 fl = f.flags[slot];
+    const int64_t pix = fl.x;
+    const int px = (int)(pix % f.W), py = (int)(pix / f.W);
+    const int tile = (py / BSR_TILE) * f.tiles_x + px / BSR_TILE;
+    const int start = (int)ranges[tile].x;
+    const double *st = f.replay_state + 6 * (int64_t)slot;
+    const double raw0 = st[0], raw1 = st[1], raw2 = st[2], rawd = st[3];
+    const int end = start + (int)st[5];
+    // clamp chain d_raw = d_color * [raw >= 0] on the fp64 raw (rasterizer.py:253)
+    const double g0 = (!a.mask_raw || raw0 >= 0.0) ? (double)a.d_color[3 * pix] : 0.0;
+    const double g1 = (!a.mask_raw || raw1 >= 0.0) ? (double)a.d_color[3 * pix + 1] : 0.0;
+    const double g2 = (!a.mask_raw || raw2 >= 0.0) ? (double)a.d_color[3 * pix + 2] : 0.0;
+    const double gd = a.d_depth ? (double)a.d_depth[pix] : 0.0;
+
+    double t = 1.0, p0 = 0.0, p1 = 0.0, p2 = 0.0, pd = 0.0;
+    for (int base = start; base < end; base += 32) {
+        const int e = base + lane;
+        Entry64 en;
+        bool cand = false;
+        double alpha = 0.0, dx = 0, dy = 0, x = 1, kernel = 0;
+        uint32_t c = 0;
+        if (e < end) {
+            c = lists[e];
+            if (prov.get(c, px, py, en)) {
+                alpha = alpha64(en, px, py, dx, dy, x, kernel);
+                cand = !(alpha < a.alpha_min);
+            }
+        }
+        // sequential prefix: capture (t, prefix) before this lane's sample
+        double my_t = 0, my_p0 = 0, my_p1 = 0, my_p2 = 0, my_pd = 0;
+        unsigned m = __ballot_sync(0xffffffffu, cand);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            if (l == lane) {
+                my_t = t;
+                my_p0 = p0;
+                my_p1 = p1;
+                my_p2 = p2;
+                my_pd = pd;
+            }
+            const double al = shfl_d(alpha, l);
+            const double weight = al * t;
+            p0 = p0 + weight * shfl_d(en.r, l);
+            p1 = p1 + weight * shfl_d(en.g, l);
+            p2 = p2 + weight * shfl_d(en.b, l);
+            pd = pd + weight * shfl_d(en.z, l);
+            t = t * (1.0 - al);
+        }
+        if (!cand) continue;
+        // _raster.pyx:208-234 with the sample's own (t, prefix)
+        const double weight = alpha * my_t;
+        const double cr0 = weight * en.r, cr1 = weight * en.g, cr2 = weight * en.b, crd = weight * en.z;
+        const double behind0 = raw0 - my_p0 - cr0;
+        const double behind1 = raw1 - my_p1 - cr1;
+        const double behind2 = raw2 - my_p2 - cr2;
+        const double behindd = rawd - my_pd - crd;
+        const double g_dot_col = g0 * en.r + g1 * en.g + g2 * en.b;
+        const double g_dot_behind = g0 * behind0 + g1 * behind1 + g2 * behind2;
+        double d_alpha = g_dot_col * my_t - g_dot_behind / (1.0 - alpha);
+        d_alpha = d_alpha + (gd * en.z * my_t - gd * behindd / (1.0 - alpha));
+        float *acc = f.grad_acc + (int64_t)c * kGradStride;
+        atomicAdd(acc + 7, (float)(weight * g0));
+        atomicAdd(acc + 8, (float)(weight * g1));
+        atomicAdd(acc + 9, (float)(weight * g2));
+        atomicAdd(acc + 10, (float)(weight * gd));
+        atomicAdd(acc + 5, (float)(d_alpha * kernel));
+        const double d_kernel = d_alpha * en.o;
+        if (x < 1.0) {
+            atomicAdd(acc + 6, (float)(d_kernel * kernel * log(1.0 - x)));
+            double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
+            if (dkdx < -1e7) dkdx = -1e7;
+            const double d_x = d_kernel * dkdx;
+            atomicAdd(acc + 0, (float)(-d_x * 2.0 * (en.ca * dx + en.cb * dy)));
+            atomicAdd(acc + 1, (float)(-d_x * 2.0 * (en.cb * dx + en.cc * dy)));
+            atomicAdd(acc + 2, (float)(d_x * dx * dx));
+            atomicAdd(acc + 3, (float)(d_x * 2.0 * dx * dy));
+            atomicAdd(acc + 4, (float)(d_x * dy * dy));
+        }
+    }
+}
+
+template <typename P>
+__global__ void __launch_bounds__(BSR_BLOCK) replay_fwd_kernel(ReplayArgs a, P prov) {
+    const uint32_t nwarps = gridDim.x * (BSR_BLOCK / 32);
+    const uint32_t n = a.f.ctr->flagged;
+    for (uint32_t slot = (blockIdx.x * BSR_BLOCK + threadIdx.x) >> 5; slot < n; slot += nwarps)
+        replay_fwd_one(a, prov, slot, threadIdx.x & 31);
+}
+
+template <typename P>
+__global__ void __launch_bounds__(BSR_BLOCK) replay_bwd_kernel(ReplayArgs a, P prov) {
+    const uint32_t nwarps = gridDim.x * (BSR_BLOCK / 32);
+    const uint32_t n = a.f.ctr->flagged;
+    for (uint32_t slot = (blockIdx.x * BSR_BLOCK + threadIdx.x) >> 5; slot < n; slot += nwarps)
+        replay_bwd_one(a, prov, slot, threadIdx.x & 31);
+}
+
+static unsigned replay_blocks(const FrameView &f) {
+    // one warp per flagged pixel (grid-stride over the device-side count); the grid is
+    // capped and surplus warps exit immediately.
+    const int64_t warps = (int64_t)f.W * f.H;
+    return (unsigned)imax64(1, imin64(div_up(warps * 32, BSR_BLOCK), 148 * 64));
+}
+
+template <typename P>
+static int launch_replay(bool fwd, const ReplayArgs &a, const P &prov, cudaStream_t st) {
+    if (fwd)
+        replay_fwd_kernel<P><<<replay_blocks(a.f), BSR_BLOCK, 0, st>>>(a, prov);
+    else
+        replay_bwd_kernel<P><<<replay_blocks(a.f), BSR_BLOCK, 0, st>>>(a, prov);
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+int launch_replay_scene(bool fwd, const FrameView &f, const bsr_scene &sc, const KCam &cam,
+                        const bsr_outputs &out, const double bg[3], double alpha_min, double t_stop,
+                        const float *d_color, const float *d_depth, cudaStream_t st) {
+    ReplayArgs a;
+    a.f = f;
+    a.out = out;
+    for (int i = 0; i < 3; ++i) a.bg[i] = bg[i];
+    a.alpha_min = alpha_min;
+    a.t_stop = t_stop;
+    a.lists = nullptr;
+    a.ranges = nullptr;
+    a.d_color = d_color;
+    a.d_depth = d_depth;
+    a.mask_raw = true;
+    switch (sc.sh_coeffs) {
+        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec}, st);
+        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec}, st);
+        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec}, st);
+        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec}, st);
+        default: return BSR_ERR_BAD_ARG;
+    }
+}
+
+int launch_replay_arrays(bool fwd, const FrameView &f, const double *means, const double *conics,
+                         const double *opac, const double *betas, const double *colors,
+                         const int32_t *bounds, const uint32_t *lists, const uint2 *ranges,
+                         const bsr_outputs &out, const double bg[3], double alpha_min,
+                         double t_stop, const float *d_raw, cudaStream_t st) {
+    ReplayArgs a;
+    a.f = f;
+    a.out = out;
+    for (int i = 0; i < 3; ++i) a.bg[i] = bg[i];
+    a.alpha_min = alpha_min;
+    a.t_stop = t_stop;
+    a.lists = lists;
+    a.ranges = ranges;
+    a.d_color = d_raw;
+    a.d_depth = nullptr;
+    a.mask_raw = false;
+    ArrayProvider p{means, conics, opac, betas, colors, bounds};
+    return launch_replay(fwd, a, p, st);
+}
+
+}  // namespace bsr

@@ -1,0 +1,178 @@
+"""Training step on the device: loss, Adam, and the view-batch step (configs 1, 3, 4).
+
+``loss`` / ``adam_step`` mirror training.loss / training.adam_step
+(training.py:98-131, 258-273) through libbsr kernels (K7, K8).  ``TrainStep`` is the
+per-iteration hot path a user of the reference's ``train`` loop (training.py:357-366)
+switches to:
+
+    for each view of this rank:  render_tiled -> loss -> render_backward (accumulate)
+    [all-reduce of the flat gradient buffer over NCCL when world_size > 1]
+    fused Adam with per-group learning rates
+
+The sort is treated as locally constant and every kernel is stream ordered; no host
+synchronisation happens inside ``step(check=False)``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .camera import Camera
+from .primitive import GradientBuffer, PrimitiveSet
+from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, forward_raw, frame_status,
+                         grads_c, outputs_c)
+
+ADAM_BETA1 = 0.9  # training.py:31
+ADAM_BETA2 = 0.999  # training.py:32
+ADAM_EPS = 1e-15  # training.py:33
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class LossWorkspace:
+    def __init__(self, width, height, device="cuda"):
+        out = ctypes.c_uint64()
+        _lib.check(_lib.load().bsr_loss_scratch_bytes(width, height, ctypes.byref(out)), "loss")
+        self.nbytes = int(out.value)
+        self.scratch = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.values = torch.zeros(3, dtype=torch.float64, device=device)
+        self.width, self.height = width, height
+
+
+def loss_into(rendered, target, d_image, ws: LossWorkspace, lambda_ssim=0.2, raw=None):
+    """Device-side loss: writes d_image (optionally masked by raw >= 0) and ws.values =
+    [loss, l1, ssim] without a host sync."""
+    h, w = rendered.shape[:2]
+    rc = _lib.load().bsr_loss_l1_dssim(
+        rendered.data_ptr(), target.data_ptr(), _lib.ptr(raw), w, h, float(lambda_ssim),
+        ws.values.data_ptr(), d_image.data_ptr(), ws.scratch.data_ptr(), ws.nbytes, _stream())
+    _lib.check(rc, "loss")
+
+
+def loss(rendered, target, lambda_ssim=0.2):
+    """training.loss with lambda_opacity = lambda_scale = 0: returns (value, d_image)."""
+    _lib.require_cuda()
+    rendered = torch.as_tensor(rendered, dtype=torch.float32, device="cuda").contiguous()
+    target = torch.as_tensor(target, dtype=torch.float32, device="cuda").contiguous()
+    if rendered.shape != target.shape:
+        raise ValueError("rendered/target shapes differ")
+    if rendered.dim() != 3 or rendered.shape[2] != 3:
+        raise ValueError("images must be (H, W, 3)")
+    if rendered.shape[0] < 11 or rendered.shape[1] < 11:
+        raise ValueError("images must be at least 11x11")
+    ws = LossWorkspace(rendered.shape[1], rendered.shape[0])
+    d_image = torch.empty_like(rendered)
+    loss_into(rendered, target, d_image, ws, lambda_ssim)
+    vals = ws.values.cpu().numpy()
+    return float(vals[0]), d_image
+
+
+def ssim(a, b):
+    """Mean SSIM (training.py:51-83) via the loss kernel with lambda = 1."""
+    a = torch.as_tensor(a, dtype=torch.float32, device="cuda").contiguous()
+    b = torch.as_tensor(b, dtype=torch.float32, device="cuda").contiguous()
+    ws = LossWorkspace(a.shape[1], a.shape[0])
+    d = torch.empty_like(a)
+    loss_into(a, b, d, ws, 1.0)
+    return float(ws.values[2].item()), -d
+
+
+class AdamState:
+    """First/second moments as flat buffers aligned with the PrimitiveSet (training.py:230-255)."""
+
+    def __init__(self, prims: PrimitiveSet):
+        self.exp_avg = torch.zeros_like(prims.flat)
+        self.exp_avg_sq = torch.zeros_like(prims.flat)
+        self.step = 0
+
+
+def group_lrs(lr_means=1.6e-4, lr_other=5e-3):
+    """Config-3 learning rates (BASELINE.json configs[3]); per group in GROUPS order."""
+    return {"positions": lr_means, "rotations": lr_other, "log_scales": lr_other, "opacity_raw": lr_other,
+            "shapes": lr_other, "sh": lr_other}
+
+
+def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict):
+    """training.py:258-273 as one fused kernel over the flat buffers."""
+    state.step += 1
+    ends = (ctypes.c_int64 * 6)(*prims.group_ends())
+    lr = (ctypes.c_float * 6)(*[float(lrs[g]) for g in ("positions", "rotations", "log_scales",
+                                                          "opacity_raw", "shapes", "sh")])
+    rc = _lib.load().bsr_adam_step(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
+                                   state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr, state.step,
+                                   ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
+    _lib.check(rc, "adam")
+    return prims
+
+
+class TrainStep:
+    """One training iteration over this rank's views (fwd + L1/D-SSIM + bwd [+ all-reduce] + Adam)."""
+
+    def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
+                 lambda_ssim=0.2, process_group=None):
+        self.prims = prims
+        self.cameras = list(cameras)
+        self.targets = list(targets)
+        self.background = background
+        self.lrs = lrs or group_lrs()
+        self.lambda_ssim = lambda_ssim
+        self.pg = process_group
+        self.grads = GradientBuffer.zeros_for(prims)
+        self.adam = AdamState(prims)
+        self.scene = _prims_scene_c(prims)
+        self.gc = grads_c(self.grads)
+        dev = prims.flat.device
+        self.frames: dict = {}
+        self.bufs = {}
+        self.loss_ws = {}
+        for cam in self.cameras:
+            key = (cam.width, cam.height)
+            if key not in self.bufs:
+                h, w = cam.height, cam.width
+                self.bufs[key] = dict(color=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                      d_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev))
+                self.loss_ws[key] = LossWorkspace(w, h, dev)
+        self.loss_values = torch.zeros((len(self.cameras), 3), dtype=torch.float64, device=dev)
+        self.launches_per_step = None
+
+    def _frame(self, cam):
+        return self.frames.get((cam.width, cam.height))
+
+    def step(self, check=False):
+        self.grads.flat.zero_()
+        for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
+            key = (cam.width, cam.height)
+            b = self.bufs[key]
+            frame = forward_raw(self.scene, cam, self.background, outputs_c(color=b["color"]),
+                                frame=self._frame(cam), check=check)
+            self.frames[key] = frame
+            ws = self.loss_ws[key]
+            loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim)
+            self.loss_values[i].copy_(ws.values)
+            backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None)
+        if self.pg is not None:
+            torch.distributed.all_reduce(self.grads.flat, group=self.pg)
+        adam_step(self.prims, self.grads, self.adam, self.lrs)
+        return self.loss_values
+
+    def check_frames(self):
+        """Host-side check of every frame's device status (capacity / errors)."""
+        for f in self.frames.values():
+            frame_status(f)
+
+
+def render_targets(target_prims: PrimitiveSet, cameras, background):
+    """Per-view target images rendered once on the device (configs 1, 3)."""
+    from .rasterizer import render_tiled
+
+    return [render_tiled(target_prims, cam, background).color.contiguous() for cam in cameras]
+
+
+__all__ = ["loss", "ssim", "adam_step", "AdamState", "TrainStep", "render_targets", "group_lrs",
+           "LossWorkspace", "loss_into", "FrameState", "Camera", "np", "_bg_arr"]

@@ -1,0 +1,273 @@
+"""GPU parity: libbsr.so (through the C-ABI) against the oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): tile keys / sort order / binning / contributions /
+per-pixel counts BIT-EXACT; images within 1e-4 absolute (fp32); gradients within
+1e-3 relative / 1e-5 absolute (atol scaled by max|g| per group like the reference's FD
+test, tests/test_rasterizer.py:279-282).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_scene_camera, random_scene, toy_camera
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+
+
+def _gpu_prims(scene):
+    from paper_2501_18630_b200 import PrimitiveSet
+
+    return PrimitiveSet.from_scene(scene)
+
+
+def _oracle_fwd(scene, cam, bg):
+    from oracle import pipeline as orc
+
+    return orc.forward(scene, cam, bg, core="c")
+
+
+def _compare_forward(scene, cam, bg, cuda, check_bins=True):
+    from paper_2501_18630_b200 import render_tiled
+    from paper_2501_18630_b200.rasterizer import debug_export
+
+    ref = _oracle_fwd(scene, cam, bg)
+    out = render_tiled(_gpu_prims(scene), cam, bg)
+    np.testing.assert_array_equal(out.contributions.cpu().numpy(), ref["contributions"])
+    np.testing.assert_array_equal(out.pixel_count.cpu().numpy(), ref["pix_count"])
+    assert np.abs(out.raw_color.cpu().numpy() - ref["raw"]).max() <= IMG_TOL
+    assert np.abs(out.color.cpu().numpy() - ref["color"]).max() <= IMG_TOL
+    assert np.abs(out.transmittance.cpu().numpy() - ref["T"]).max() <= IMG_TOL
+    assert np.abs(out.alpha.cpu().numpy() - ref["alpha"]).max() <= IMG_TOL
+    zscale = max(1.0, float(np.abs(ref["depth"]).max()))
+    assert np.abs(out.depth.cpu().numpy() - ref["depth"]).max() <= IMG_TOL * zscale
+    if check_bins and ref["order"] is not None:
+        dbg = debug_export(out.frame)
+        assert dbg["visible"] == ref["V"] and dbg["entries"] == ref["E"]
+        np.testing.assert_array_equal(dbg["src"], ref["batch"]["indices"])
+        np.testing.assert_array_equal(dbg["order"], ref["order"])
+        np.testing.assert_array_equal(dbg["bounds"], ref["batch"]["bounds"])
+        np.testing.assert_array_equal(dbg["lists"], ref["order"][ref["lists"]])
+        off = ref["offsets"]
+        np.testing.assert_array_equal(dbg["ranges"][:, 1] - dbg["ranges"][:, 0], np.diff(off))
+        nz = np.diff(off) > 0
+        np.testing.assert_array_equal(dbg["ranges"][nz, 0], off[:-1][nz])
+    return out, ref
+
+
+@pytest.mark.parametrize("name", ["c0_forward.npz", "sh3_fwd_bwd.npz", "shapes_sh2.npz"])
+def test_forward_golden_scenes(cuda, name):
+    g = golden(name)
+    scene, cam = golden_scene_camera(g)
+    out, ref = _compare_forward(scene, cam, g["bg"], cuda)
+    # and against the reference's own golden vectors
+    np.testing.assert_array_equal(out.contributions.cpu().numpy(), g["contributions"])
+    assert np.abs(out.raw_color.cpu().numpy() - g["raw"]).max() <= IMG_TOL
+
+
+def test_forward_config1_full_size(cuda):
+    from paper_2501_18630_b200.scenes import make_workload
+
+    wl = make_workload("c1", seed=0)
+    _compare_forward(wl.scene, wl.cameras[0], wl.background, cuda)
+
+
+def test_forward_config2_reduced(cuda):
+    from paper_2501_18630_b200.scenes import make_workload
+
+    wl = make_workload("c2", seed=0, n=200_000, width=960, height=540)
+    _compare_forward(wl.scene, wl.cameras[0], wl.background, cuda)
+
+
+@pytest.mark.parametrize("seed,n,w,h", [(14, 1, 70, 50), (15, 7, 70, 50), (16, 60, 70, 50),
+                                        (17, 300, 70, 50), (18, 20, 16, 16), (19, 120, 96, 64)])
+def test_forward_random_scenes(cuda, seed, n, w, h):
+    """tests/test_rasterizer.py:150-166 analogues (non tile-multiple, single tile)."""
+    rng = np.random.default_rng(seed)
+    scene = random_scene(rng, n, degree=1 + seed % 3)
+    _compare_forward(scene, toy_camera(w, h), np.ones(3), cuda)
+
+
+def test_empty_and_culled_scenes(cuda):
+    from paper_2501_18630_b200 import render_tiled
+
+    cam = toy_camera()
+    rng = np.random.default_rng(3)
+    scene = random_scene(rng, 10)
+    scene.positions[:, 2] = -10.0  # everything behind the camera (eye at z=-4 looking +z)
+    out = render_tiled(_gpu_prims(scene), cam, np.ones(3))
+    np.testing.assert_array_equal(out.color.cpu().numpy(), np.ones((32, 32, 3), np.float32))
+    np.testing.assert_array_equal(out.alpha.cpu().numpy(), np.zeros((32, 32), np.float32))
+    assert int(out.contributions.sum()) == 0
+    empty = scene.take(np.zeros(0, dtype=np.int64))
+    out = render_tiled(_gpu_prims(empty), cam, np.ones(3))
+    np.testing.assert_array_equal(out.color.cpu().numpy(), np.ones((32, 32, 3), np.float32))
+
+
+def test_extinction_alpha_near_one(cuda):
+    """tests/test_rasterizer.py:68-90: opacity 1 - 1e-12 (fp64 replay path)."""
+    from paper_2501_18630_b200.scenes import SplatScene
+    from paper_2501_18630_b200 import render_tiled
+
+    cam = toy_camera(33, 33)
+
+    def mk(zs, cols, ops):
+        n = len(zs)
+        sh = np.asarray(cols, np.float64)[:, None, :] / 0.28209479177387814
+        op = np.asarray(ops, np.float64)
+        return SplatScene(positions=np.array([[0, 0, z] for z in zs], np.float32),
+                          rotations=np.tile(np.array([1, 0, 0, 0], np.float32), (n, 1)),
+                          log_scales=np.log(np.full((n, 3), 0.3)).astype(np.float32),
+                          opacity_raw=(np.log(op) - np.log1p(-op)).astype(np.float32),
+                          shapes=np.full(n, -2.0, np.float32), sh=sh.astype(np.float32))
+
+    front = mk([0.0], [[1, 0, 0]], [1 - 1e-12])
+    both = mk([0.0, 1.0], [[1, 0, 0], [1, 1, 1]], [1 - 1e-12, 0.9])
+    a = render_tiled(_gpu_prims(front), cam, np.zeros(3))
+    b = render_tiled(_gpu_prims(both), cam, np.zeros(3))
+    np.testing.assert_array_equal(a.color.cpu().numpy()[16, 16], b.color.cpu().numpy()[16, 16])
+    for s in (front, both):
+        _compare_forward(s, cam, np.zeros(3), cuda)
+
+
+def test_core_seam_forward_matches_reference_core(cuda):
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import backend
+
+    core = backend.get_core("cuda")
+    g = golden("sh3_fwd_bwd.npz")
+    scene, cam = golden_scene_camera(g)
+    _, order, shaded = orc.view_setup(scene, cam)
+    s = shaded["sorted"]
+    off, lists = orc.tile_bins(s["bounds"], cam.height, cam.width)
+    ref = orc.raster_forward(s, cam.height, cam.width, g["bg"], off, lists, core="c")
+    raw, alpha, trans, contrib, extra = core.forward_tiled(
+        s["means"], s["conics"], s["opac"], s["betas"], s["colors"], s["bounds"], cam.height, cam.width,
+        g["bg"], 16, off, lists, 8, orc.ALPHA_MIN, orc.T_STOP, return_extra=True)
+    np.testing.assert_array_equal(contrib, ref["contrib"])
+    np.testing.assert_array_equal(extra["pixel_count"], ref["pix_count"])
+    assert np.abs(raw - ref["raw"]).max() <= IMG_TOL
+    assert np.abs(trans - ref["T"]).max() <= IMG_TOL
+    naive = core.forward_naive(s["means"], s["conics"], s["opac"], s["betas"], s["colors"], s["bounds"],
+                               cam.height, cam.width, g["bg"], orc.ALPHA_MIN, orc.T_STOP)
+    np.testing.assert_array_equal(naive[3], ref["contrib"])
+
+
+def _grad_close(a, b, name):
+    scale = max(np.abs(b).max(), 1e-30)
+    np.testing.assert_allclose(a, b, rtol=1e-3, atol=1e-5 * scale, err_msg=name)
+
+
+def test_core_seam_backward_matches_reference_core(cuda):
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import backend
+
+    core = backend.get_core("cuda")
+    g = golden("shapes_sh2.npz")
+    scene, cam = golden_scene_camera(g)
+    _, order, shaded = orc.view_setup(scene, cam)
+    s = shaded["sorted"]
+    off, lists = orc.tile_bins(s["bounds"], cam.height, cam.width)
+    fwd = orc.raster_forward(s, cam.height, cam.width, g["bg"], off, lists, core="c")
+    d_raw = np.where(fwd["raw"] >= 0, g["upstream"], 0.0)
+    ref = orc.raster_backward(s, cam.height, cam.width, g["bg"], fwd["raw"], d_raw, off, lists, core="c")
+    got = core.backward(s["means"], s["conics"], s["opac"], s["betas"], s["colors"], s["bounds"],
+                        cam.height, cam.width, g["bg"], fwd["raw"], d_raw, 16, off, lists, 8,
+                        orc.ALPHA_MIN, orc.T_STOP)
+    for name, a, b in zip(("d_means", "d_conics", "d_opac", "d_betas", "d_colors"), got, ref[:5]):
+        _grad_close(a, b, name)
+
+
+@pytest.mark.parametrize("name", ["sh3_fwd_bwd.npz", "shapes_sh2.npz"])
+def test_backward_golden_scenes(cuda, name):
+    from paper_2501_18630_b200 import render_backward, render_tiled
+
+    g = golden(name)
+    scene, cam = golden_scene_camera(g)
+    prims = _gpu_prims(scene)
+    out = render_tiled(prims, cam, g["bg"])
+    grads = render_backward(prims, cam, g["bg"], g["upstream"].astype(np.float32), forward_out=out)
+    for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
+        _grad_close(getattr(grads, k).cpu().numpy(), g["g_" + k], k)
+
+
+def test_backward_with_depth_matches_oracle(cuda):
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import render_backward, render_tiled
+
+    rng = np.random.default_rng(31)
+    scene = random_scene(rng, 150, degree=3)
+    cam = toy_camera(64, 48)
+    bg = np.array([0.2, 0.5, 1.0])
+    up = rng.standard_normal((48, 64, 3))
+    upd = rng.standard_normal((48, 64))
+    fwd = orc.forward(scene, cam, bg, core="c")
+    ref = orc.backward(scene, cam, bg, up, fwd, core="c", d_depth=upd)
+    prims = _gpu_prims(scene)
+    out = render_tiled(prims, cam, bg)
+    grads = render_backward(prims, cam, bg, up.astype(np.float32), forward_out=out,
+                            d_depth=upd.astype(np.float32))
+    for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
+        _grad_close(getattr(grads, k).cpu().numpy(), ref[k], k)
+
+
+def test_zero_upstream_gives_zero_gradients(cuda):
+    """tests/test_rasterizer.py:221-227."""
+    from paper_2501_18630_b200 import render_backward
+
+    rng = np.random.default_rng(20)
+    prims = _gpu_prims(random_scene(rng, 8))
+    cam = toy_camera()
+    grads = render_backward(prims, cam, np.ones(3), np.zeros((32, 32, 3), np.float32))
+    assert float(grads.flat.abs().max()) == 0.0
+
+
+def test_occluded_primitive_gets_zero_opacity_gradient(cuda):
+    """tests/test_rasterizer.py:229-252."""
+    from paper_2501_18630_b200.scenes import SplatScene
+    from paper_2501_18630_b200 import render_backward
+
+    cam = toy_camera(17, 17)
+    op = np.array([1 - 1e-12, 0.5])
+    scene = SplatScene(positions=np.array([[0, 0, 0], [0, 0, 1.0]], np.float32),
+                       rotations=np.tile(np.array([1, 0, 0, 0], np.float32), (2, 1)),
+                       log_scales=np.log(np.array([[3.0] * 3, [0.05] * 3])).astype(np.float32),
+                       opacity_raw=(np.log(op) - np.log1p(-op)).astype(np.float32),
+                       shapes=np.full(2, -2.0, np.float32),
+                       sh=np.full((2, 1, 3), 0.5 / 0.28209479177387814, np.float32))
+    grads = render_backward(_gpu_prims(scene), cam, np.zeros(3), np.ones((17, 17, 3), np.float32))
+    assert float(grads.opacity_raw[1]) == 0.0
+
+
+def test_loss_matches_reference_golden(cuda):
+    from paper_2501_18630_b200 import training
+
+    g = golden("loss.npz")
+    value, d_image = training.loss(g["a"], g["b"])
+    assert value == pytest.approx(float(g["value"]), rel=1e-5)
+    d = d_image.cpu().numpy()
+    scale = np.abs(g["d_image"]).max()
+    np.testing.assert_allclose(d, g["d_image"], rtol=1e-3, atol=1e-4 * scale)
+
+
+def test_adam_matches_reference_golden(cuda):
+    import torch
+    from paper_2501_18630_b200 import training
+    from paper_2501_18630_b200.primitive import GradientBuffer, PrimitiveSet
+
+    g = golden("adam.npz")
+    n = g["p0_positions"].shape[0]
+    sh = np.zeros((n, 1, 3), np.float32)
+    prims = PrimitiveSet(g["p0_positions"], g["p0_rotations"], g["p0_log_scales"], g["p0_opacity_raw"],
+                         g["p0_shapes"], sh)
+    p64 = {k: g["p0_" + k].copy() for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes")}
+    state = training.AdamState(prims)
+    lrs = training.group_lrs()
+    for i in range(3):
+        gb = GradientBuffer.zeros_for(prims)
+        for k in p64:
+            getattr(gb, k).copy_(torch.from_numpy(g[f"g{i}_" + k].astype(np.float32)))
+        training.adam_step(prims, gb, state, lrs)
+    for k in p64:
+        np.testing.assert_allclose(getattr(prims, k).cpu().numpy(), g["p3_" + k], rtol=0, atol=2e-6, err_msg=k)
