@@ -1,0 +1,573 @@
+"""Benchmark of the hot path (BASELINE.json metric: render FPS / train it/s on B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4]
+    python bench.py --impl reference ...      (the reference's CPU implementation)
+
+Default workload (N=1): BASELINE config 1 -- one training step = forward render of
+N=100k SH-3 Gaussians at 800x800 + 0.8 L1 + 0.2 D-SSIM loss + backward + Adam, all on the
+device through libbsr.so.  With N>1 (torchrun, NCCL) every rank trains on its own view of
+the same scene (weak scaling: one 800x800 view per GPU per step) and the flat per-Gaussian
+gradient buffer is all-reduced before Adam.  --config c3 runs the 32-view batch of
+config 3 split across ranks (strong scaling), c2 the 1080p forward render, c4 the 4K
+stress forward + backward.
+
+Timing: W warm-up steps, then K steps each timed with CUDA events on the launching
+stream (L2 flushed with a 256 MiB write between steps, outside the events), bracketed by
+barrier + synchronize, max over ranks.  Stage times / pair counts for the roofline come
+from libbsr's caller-owned events and device counters recorded inside the same timed
+steps.  e2e repeats the step through the public API with the per-step inputs (target
+images) copied from pinned host memory and the loss read back, copies inside the timing.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FP32_FLOP_PER_PAIR_FWD = 27  # SURVEY 8(d), counted from _raster.pyx:107-123
+FP32_FLOP_PER_PAIR_BWD = 80  # SURVEY 8(d), counted from _raster.pyx:197-241
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return dict(hbm_gbs=float(p["hbm_gbs"]), sm_max_mhz=float(p.get("sm_max_mhz", 1965.0)),
+                    source="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback (B200_PROFILING.md)")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # median under load: drop idle samples below 50% of the max before the run ramps up
+        mx = max(smax)
+        loaded = [s for s in sm if s >= 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    import torch
+
+    if world == 1:
+        return float(x)
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    import torch
+
+    if world == 1:
+        return float(x)
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- workloads
+def rank_cameras(cfg, rank, world, views_per_gpu):
+    """Cameras of this rank.  c1: view r of a y-orbit at radius 4 (rank 0 == config-1
+    camera); c3: contiguous share of the 32 config-3 cameras."""
+    from paper_2501_18630_b200.camera import Camera
+    from paper_2501_18630_b200.scenes import make_workload
+
+    if cfg == "c1":
+        cams = []
+        for v in range(views_per_gpu):
+            k = rank * views_per_gpu + v
+            ang = 2 * np.pi * k / max(world * views_per_gpu, 1)
+            eye = (4 * np.sin(ang), 0.0, 4 * np.cos(ang))
+            cams.append(Camera.from_lookat(eye, (0, 0, 0), (0, 1, 0), np.deg2rad(60.0), 800, 800))
+        return cams
+    if cfg == "c3":
+        wl_cams = make_workload("c3", seed=0, n=16).cameras
+        per = len(wl_cams) // world
+        return wl_cams[rank * per:(rank + 1) * per]
+    return make_workload(cfg, seed=0, n=16).cameras
+
+
+def build_b200(cfg, rank, world, views_per_gpu):
+    import torch
+
+    from paper_2501_18630_b200 import PrimitiveSet
+    from paper_2501_18630_b200.scenes import make_workload, target_scene
+    from paper_2501_18630_b200.training import TrainStep, render_targets
+
+    n = {"c1": 100_000, "c2": 1_000_000, "c3": 3_000_000, "c4": 6_000_000}[cfg]
+    wl = make_workload(cfg, seed=0, n=n, views=1 if cfg != "c3" else 32)
+    prims = PrimitiveSet.from_scene(wl.scene)
+    cams = rank_cameras(cfg, rank, world, views_per_gpu)
+    bg = wl.background
+    if cfg == "c2":
+        return dict(kind="render", prims=prims, cams=cams, bg=bg, scene=wl.scene)
+    tgt = PrimitiveSet.from_scene(target_scene(cfg, 1, n))
+    targets = render_targets(tgt, cams, bg)
+    del tgt
+    torch.cuda.empty_cache()
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        pg = dist.group.WORLD
+    step = TrainStep(prims, cams, targets, bg, process_group=pg)
+    return dict(kind="train", prims=prims, cams=cams, bg=bg, step=step, targets=targets, scene=wl.scene,
+                adam=(cfg != "c4"))
+
+
+def run_step(w, prof=None):
+    """One hot-path step; returns the number of views processed."""
+    import torch
+
+    from paper_2501_18630_b200.rasterizer import _prims_scene_c, forward_raw, outputs_c
+
+    if w["kind"] == "render":
+        if "color" not in w:
+            c = w["cams"][0]
+            w["color"] = torch.empty((c.height, c.width, 3), dtype=torch.float32, device="cuda")
+            w["frame"] = None
+            w["sc"] = _prims_scene_c(w["prims"])
+        for cam in w["cams"]:
+            w["frame"] = forward_raw(w["sc"], cam, w["bg"], outputs_c(color=w["color"]), frame=w["frame"],
+                                     check=False, profile=None if prof is None else prof.fwd)
+        return len(w["cams"])
+    st = w["step"]
+    st.profile = prof
+    st.step(check=False, adam=w["adam"])
+    return len(w["cams"])
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def timed_loop(w, steps, world, prof=None, l2=None):
+    """K device-timed steps (CUDA events on the launching stream; L2 flush outside)."""
+    import torch
+
+    total_ms, views = 0.0, 0
+    barrier(world)
+    for _ in range(steps):
+        if l2 is not None:
+            flush_l2(l2)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        views += run_step(w, prof)
+        e.record()
+        e.synchronize()
+        total_ms += s.elapsed_time(e)
+        if prof is not None:
+            prof.collect_step(w)
+    barrier(world)
+    return total_ms, views
+
+
+def e2e_loop(w, steps, world):
+    """Same step through the public API with per-step host inputs (pinned) and the result
+    read back, copies inside the timing."""
+    import torch
+
+    bi = bo = 0
+    if w["kind"] == "train":
+        host = [t.cpu().pin_memory() for t in w["targets"]]
+        bi = sum(h.numel() * 4 for h in host)
+        bo = w["step"].loss_values.numel() * 8
+    else:
+        c = w["cams"][0]
+        host_img = torch.empty((c.height, c.width, 3), dtype=torch.float32).pin_memory()
+        bo = host_img.numel() * 4 * len(w["cams"])
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    views = 0
+    for _ in range(steps):
+        if w["kind"] == "train":
+            for dev_t, h in zip(w["targets"], host):
+                dev_t.copy_(h, non_blocking=True)
+            views += run_step(w)
+            loss = w["step"].loss_values.cpu()  # D2H + sync (the step's result)
+            del loss
+        else:
+            views += run_step(w)
+            host_img.copy_(w["color"], non_blocking=False)
+    e.record()
+    e.synchronize()
+    ms = s.elapsed_time(e)
+    barrier(world)
+    return ms, views, bi, bo
+
+
+class BenchProfiler:
+    """Per-step stage times + pair counts from libbsr's profiling hooks (bsr_profile)."""
+
+    def __init__(self):
+        from paper_2501_18630_b200.rasterizer import StageProfiler
+
+        self.sp = StageProfiler()
+
+    @property
+    def fwd(self):
+        return self.sp.fwd
+
+    @property
+    def bwd(self):
+        return self.sp.bwd
+
+    def collect_step(self, w):
+        # one view per step on the profiled path -> events hold this step's stages
+        self.sp.collect_forward()
+        if w["kind"] == "train":
+            self.sp.collect_backward()
+
+
+def kernel_launches_per_step(w):
+    from paper_2501_18630_b200.rasterizer import frame_status
+
+    cam = w["cams"][0]
+    tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    tile_passes = 1
+    while tile_passes < 4 and (tiles - 1) >= (1 << (8 * tile_passes)):
+        tile_passes += 1
+    fwd = 1 + (2 + 8) + 1 + (2 + tile_passes) + 1 + 1 + 1  # pre, depth sort, emit, tile sort, ranges, raster, replay
+    if w["kind"] == "render":
+        return fwd * len(w["cams"])
+    per_view = fwd + 3 + 4  # + loss (3) + backward (zero, raster, replay, chain)
+    return per_view * len(w["cams"]) + (1 if w["adam"] else 0)
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_reference_step_fn(cfg, threads):
+    """One step of the reference's CPU implementation: the reference's own compiled raster
+    core (oracle/_ref, built from /root/reference by oracle/Makefile) driven by the oracle's
+    numpy restatement of the per-frame glue (projection, SH adapter, sort, binning, chain),
+    L1 + D-SSIM and Adam.  Returns (step_fn, description)."""
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200.scenes import make_workload, target_scene
+
+    kind = "reference" if orc.have_ref_core() else "port"
+    core = "ref" if kind == "reference" else "c"
+    n = {"c1": 100_000, "c2": 1_000_000, "c3": 3_000_000, "c4": 6_000_000}[cfg]
+    wl = make_workload(cfg, seed=0, n=n, views=1 if cfg != "c3" else 32)
+    scene = wl.scene.astype(np.float64)
+    cam = rank_cameras(cfg, 0, 1, 1)[0] if cfg in ("c1",) else wl.cameras[0]
+    bg = wl.background
+    if cfg == "c2":
+        def step():
+            orc.forward(scene, cam, bg, core=core, threads=threads)
+        return step, kind, f"{cfg}: one forward render on {threads} host threads"
+    tgt = orc.forward(target_scene(cfg, 1, n).astype(np.float64), cam, bg, core=core, threads=threads)["color"]
+    params = {k: v.copy() for k, v in scene.arrays().items() if k != "shapes"}
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v2 = {k: np.zeros_like(v) for k, v in params.items()}
+    lrs = {k: (1.6e-4 if k == "positions" else 5e-3) for k in params}
+    state = {"t": 0}
+
+    def step():
+        fwd = orc.forward(scene, cam, bg, core=core, threads=threads)
+        _, d_img = orc.loss(fwd["color"], tgt)
+        g = orc.backward(scene, cam, bg, d_img, fwd, core=core, threads=threads)
+        if cfg != "c4":
+            state["t"] += 1
+            orc.adam_step(params, {k: g[k] for k in params}, m, v2, state["t"], lrs)
+    desc = (f"{cfg}: one training view (fwd + L1/D-SSIM + bwd" + (" + Adam" if cfg != "c4" else "") +
+            f") on {threads} host threads")
+    if cfg == "c3":
+        desc += "; 1 of the 32 views per step (multiply ms by 32 for one iteration)"
+    return step, kind, desc
+
+
+def cpu_baseline(cfg, budget_s=15.0):
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    step, kind, desc = cpu_reference_step_fn(cfg, threads)
+    step()  # warm-up (first-touch, BLAS init)
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        step()
+        k += 1
+        if time.perf_counter() - t0 >= budget_s or k >= 10:
+            break
+    dt = (time.perf_counter() - t0) / k
+    return dict(value=1.0 / dt, unit=unit_for(cfg), cores=threads, kind=kind,
+                sample=f"{desc}; {k} steps, {dt * 1e3:.0f} ms/step", ms_per_step=dt * 1e3)
+
+
+def unit_for(cfg):
+    return {"c1": "views/s", "c2": "frames/s", "c3": "views/s", "c4": "it/s"}[cfg]
+
+
+def metric_for(cfg):
+    return {
+        "c1": "train it/s (config 1: fwd + 0.8 L1 + 0.2 D-SSIM + bwd + Adam, N=100k SH-3, 800x800)",
+        "c2": "render FPS (config 2: forward, N=1M SH-3, 1920x1080)",
+        "c3": "train views/s (config 3: 32-view batch fwd + loss + bwd, all-reduce, Adam; N=3M SH-3, 1600x1067)",
+        "c4": "fwd+bwd it/s (config 4: N=6M SH-3, 3840x2160, L1 + D-SSIM upstream)",
+    }[cfg]
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    step, kind, desc = cpu_reference_step_fn(args.config, threads)
+    warm = min(args.warmup, 1)
+    steps = max(1, min(args.steps, 5 if args.config in ("c1", "c2") else 1))
+    for _ in range(warm):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    views = 1
+    val = views / dt
+    line = {
+        "impl": "reference", "metric": metric_for(args.config), "value": val, "unit": unit_for(args.config),
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config generators)",
+        "config": {"workload": args.config},
+        "cpu_baseline": {"value": val, "unit": unit_for(args.config), "cores": threads, "kind": kind,
+                         "sample": f"{desc}; steps capped at {steps} to bound the run"},
+        "e2e": {"value": val, "unit": unit_for(args.config), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--views-per-gpu", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    rank, world, local = dist_setup(args.gpus)
+    from paper_2501_18630_b200 import _lib
+
+    _lib.require_cuda()
+    W = max(args.warmup, 3)
+    K = max(args.steps, 1)
+    w = build_b200(args.config, rank, world, args.views_per_gpu)
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    # warm-up (also sizes the tile-entry capacity with a checked forward)
+    from paper_2501_18630_b200.rasterizer import frame_status
+
+    for _ in range(W):
+        run_step(w)
+    torch.cuda.synchronize()
+    frames = [w["frame"]] if w["kind"] == "render" else list(w["step"].frames.values())
+    for f in frames:
+        frame_status(f)
+
+    prof = BenchProfiler() if len(w["cams"]) == 1 else None
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, views = timed_loop(w, K, world, prof=prof, l2=l2)
+    clk = clocks.stop()
+    for f in frames:  # any device-side error or capacity overflow invalidates the run
+        frame_status(f)
+    ms_max = max_over_ranks(ms, world)
+    views_all = sum_over_ranks(views, world)
+    value = views_all / (ms_max / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        ke = max(min(K, 50), 5)
+        ems, eviews, bi, bo = e2e_loop(w, ke, world)
+        ems_max = max_over_ranks(ems, world)
+        e2e = {"value": sum_over_ranks(eviews, world) / (ems_max / 1e3), "unit": unit_for(args.config),
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo)}
+
+    pk = peaks()
+    roof, stages, extra = None, None, {}
+    if prof is not None:
+        stages = prof.sp.mean_ms()
+        st = prof.sp.stats.cpu().numpy().astype(np.float64) / K
+        pairs_f, contrib_f, pairs_b = st[0], st[1], st[2]
+        clk_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+        fp32_peak_max = SM_COUNT * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        fp32_peak_clk = SM_COUNT * FP32_LANES_PER_SM * 2 * clk_mhz * 1e6 / 1e12
+        rf = dict(raster_fwd=(pairs_f * FP32_FLOP_PER_PAIR_FWD, stages["raster_fwd"]))
+        if w["kind"] == "train":
+            rf["raster_bwd"] = (pairs_b * FP32_FLOP_PER_PAIR_BWD, stages["raster_bwd"])
+        dom = max(stages, key=lambda k: stages[k])
+        extra["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
+        extra["pairs_per_view"] = {"fwd": pairs_f, "bwd": pairs_b, "contributions": contrib_f}
+        extra["dominant_stage"] = dom
+        ach = {}
+        for k, (flop, t_ms) in rf.items():
+            a = flop / (t_ms * 1e-3) / 1e12
+            ach[k] = {"achieved_tflops": round(a, 3), "frac_of_fp32_peak_at_max_clock": round(a / fp32_peak_max, 4),
+                      "frac_of_fp32_peak_at_measured_clock": round(a / fp32_peak_clk, 4)}
+        extra["raster_roofline"] = ach
+        # HBM stages: algorithmic bytes / stage time
+        nscene = len(w["prims"])
+        k3 = w["prims"].sh_coeffs
+        info = frames[0].info
+        V, E = info["visible"], info["entries"]
+        hbm = {}
+        hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80) / (stages["preprocess"] * 1e-3) / 1e9
+        hbm["depth_sort"] = (V * 12 * 2 * 7) / (stages["depth_sort"] * 1e-3) / 1e9
+        hbm["tile_sort"] = (E * 8 * 2 * 2) / (stages["tile_sort"] * 1e-3) / 1e9
+        if w["kind"] == "train":
+            hbm["preprocess_bwd"] = V * (48 + 240 + 480) / (stages["preprocess_bwd"] * 1e-3) / 1e9
+        extra["hbm_stage_gbs"] = {k: round(v, 1) for k, v in hbm.items()}
+        extra["visible"], extra["entries"], extra["flagged_pixels"] = V, E, info["flagged_pixels"]
+        if dom in rf:
+            flop, t_ms = rf[dom]
+            a = flop / (t_ms * 1e-3) / 1e12
+            roof = {"bound": "fp32", "achieved": round(a, 3), "peak": round(fp32_peak_max, 2), "unit": "TFLOP/s",
+                    "frac": round(a / fp32_peak_max, 4), "traffic": None, "kernel": dom,
+                    "peak_source": "nominal FP32 FMA rate 148 SM x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json "
+                                   "has no FP32 figure; the raster is not a dense contraction, no tensor cores)",
+                    "algorithmic": f"{FP32_FLOP_PER_PAIR_FWD if dom == 'raster_fwd' else FP32_FLOP_PER_PAIR_BWD} "
+                                   f"FLOP per evaluated (pixel, entry) pair x pairs counted on device"}
+        else:
+            gbs = hbm.get(dom)
+            roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": None if gbs is None else gbs / pk["hbm_gbs"], "traffic": None, "kernel": dom}
+        ncu = os.path.join(REPO, "profiles", "ncu_traffic.json")
+        if os.path.exists(ncu) and roof is not None:
+            try:
+                tr = json.load(open(ncu)).get(args.config, {}).get(roof["kernel"])
+                if tr:
+                    roof["traffic"] = tr
+            except Exception:
+                pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config)
+        except Exception as e:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": unit_for(args.config), "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {e!r}"}
+
+    if rank == 0:
+        cam = w["cams"][0]
+        line = {
+            "metric": metric_for(args.config), "value": value, "unit": unit_for(args.config), "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "strong" if args.config == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE config generators, random-init Gaussians)",
+            "config": {"workload": args.config, "gaussians": len(w["prims"]), "sh_degree": 3,
+                       "width": cam.width, "height": cam.height, "views_per_gpu": len(w["cams"]),
+                       "parallelism": f"dp{world}" if world > 1 else "single", "l2": "flushed between steps"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": kernel_launches_per_step(w) * K, "clocks": clk, "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -77,6 +77,20 @@ typedef struct bsr_outputs {
     int32_t *contributions;/* (N,)    pixels each primitive contributed to, ADDED into       */
 } bsr_outputs;
 
+/* Optional profiling hooks (caller-owned; pass NULL to disable).
+ *   stats:  device uint64[4] the kernels ADD into: [0] forward evaluated (pixel, entry)
+ *           pairs (passing the bounds test, up to termination = the roofline's P_f),
+ *           [1] forward contributions, [2] backward evaluated pairs (P_b), [3] reserved.
+ *   events: caller-created cudaEvent_t handles (void*), recorded on the stream at stage
+ *           boundaries.  bsr_forward: [0] start, [1] preprocess, [2] depth sort,
+ *           [3] emit, [4] tile sort + ranges, [5] raster, [6] fp64 replay.
+ *           bsr_backward: [0] start, [1] raster backward, [2] fp64 replay,
+ *           [3] preprocess backward.  NULL entries are skipped. */
+typedef struct bsr_profile {
+    unsigned long long *stats;
+    void *events[8];
+} bsr_profile;
+
 typedef struct bsr_frame_info {
     int64_t visible;         /* V: primitives kept by projection                           */
     int64_t entries;         /* E: (tile, primitive) entries                               */
@@ -97,14 +111,14 @@ int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_cap,
 /* ---- full pipeline (render_tiled / render_backward) -------------------------------- */
 int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                 void *frame, uint64_t frame_bytes, int64_t entry_cap, const bsr_outputs *out,
-                void *stream);
+                const bsr_profile *profile, void *stream);
 /* Synchronises `stream`, then reports counters / device-side errors of the last forward. */
 int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream);
 /* d_color: (H,W,3) dL/d color (clamped image); d_depth: (H,W) or NULL. */
 int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                  void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
                  const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
-                 void *stream);
+                 const bsr_profile *profile, void *stream);
 
 /* ---- core seam (backend.get_core(): forward_tiled / backward on depth-sorted input) -- */
 /* Inputs are DEVICE fp64 arrays exactly as the reference core receives them

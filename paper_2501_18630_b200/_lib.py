@@ -57,6 +57,10 @@ class OutputsC(ctypes.Structure):
                 ("contributions", c_void_p)]
 
 
+class ProfileC(ctypes.Structure):
+    _fields_ = [("stats", c_void_p), ("events", c_void_p * 8)]
+
+
 class FrameInfoC(ctypes.Structure):
     _fields_ = [("visible", c_int64), ("entries", c_int64), ("entries_needed", c_int64),
                 ("flagged_pixels", c_int64), ("status", c_int32), ("reserved", c_int32)]
@@ -67,10 +71,10 @@ EXPORTS = {
     "bsr_status_string": (ctypes.c_char_p, [c_int32]),
     "bsr_frame_bytes": (c_int32, [c_int64, c_int32, c_int32, c_int64, c_void_p]),
     "bsr_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
-                              c_void_p]),
+                              c_void_p, c_void_p]),
     "bsr_frame_status": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "bsr_backward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
-                               c_void_p, c_void_p, c_void_p, c_void_p]),
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "bsr_core_scratch_bytes": (c_int32, [c_int64, c_int32, c_int32, c_int64, c_void_p]),
     "bsr_core_forward_tiled": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p,

@@ -13,9 +13,11 @@ int launch_emit(const FrameView &, cudaStream_t);
 int launch_tile_sort(const FrameView &, cudaStream_t);
 int launch_tile_ranges(const FrameView &, cudaStream_t);
 int launch_raster_fwd(const FrameView &, const bsr_outputs &, const float bg[3], float, float,
-                      const uint32_t *, const uint2 *, const Record *, cudaStream_t);
+                      const uint32_t *, const uint2 *, const Record *, unsigned long long *,
+                      cudaStream_t);
 int launch_raster_bwd(const FrameView &, const float *, bool, const float *, const float bg[3],
-                      float, const uint32_t *, const uint2 *, const Record *, cudaStream_t);
+                      float, const uint32_t *, const uint2 *, const Record *, unsigned long long *,
+                      cudaStream_t);
 int launch_replay_scene(bool, const FrameView &, const bsr_scene &, const KCam &, const bsr_outputs &,
                         const double bg[3], double, double, const float *, const float *,
                         cudaStream_t);
@@ -101,6 +103,11 @@ __global__ void core_unpack_kernel(int64_t v, const float *acc, float *d_means, 
 
 __global__ void set_visible_kernel(FrameView f, uint32_t v) { f.ctr->visible = v; }
 
+inline int mark(const bsr_profile *p, int i, cudaStream_t st) {
+    if (p && p->events[i]) BSR_CUDA_TRY(cudaEventRecord((cudaEvent_t)p->events[i], st));
+    return BSR_OK;
+}
+
 }  // namespace bsr
 
 using namespace bsr;
@@ -146,7 +153,7 @@ extern "C" int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t
 
 extern "C" int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                            void *frame, uint64_t frame_bytes, int64_t entry_cap,
-                           const bsr_outputs *out, void *stream) {
+                           const bsr_outputs *out, const bsr_profile *prof, void *stream) {
     if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !out ||
         entry_cap < 0 || entry_cap >= (1ll << 31))
         return BSR_ERR_BAD_ARG;
@@ -154,18 +161,27 @@ extern "C" int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, con
     const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
     if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
     const KCam cam = make_kcam(*camera);
-    BSR_CUDA_TRY(cudaMemsetAsync(frame, 0, f.zero_bytes, st));
     int rc;
+    unsigned long long *stats = prof ? prof->stats : nullptr;
+    if ((rc = mark(prof, 0, st))) return rc;
+    BSR_CUDA_TRY(cudaMemsetAsync(frame, 0, f.zero_bytes, st));
     if ((rc = launch_preprocess(*scene, cam, f, st))) return rc;
+    if ((rc = mark(prof, 1, st))) return rc;
     if ((rc = launch_depth_sort(f, st))) return rc;
+    if ((rc = mark(prof, 2, st))) return rc;
     if ((rc = launch_emit(f, st))) return rc;
+    if ((rc = mark(prof, 3, st))) return rc;
     if ((rc = launch_tile_sort(f, st))) return rc;
     if ((rc = launch_tile_ranges(f, st))) return rc;
+    if ((rc = mark(prof, 4, st))) return rc;
     if ((rc = launch_raster_fwd(f, *out, background, (float)kAlphaMin, (float)kTStop, nullptr, nullptr,
-                                nullptr, st)))
+                                nullptr, stats, st)))
         return rc;
+    if ((rc = mark(prof, 5, st))) return rc;
     const double bg64[3] = {background[0], background[1], background[2]};
-    return launch_replay_scene(true, f, *scene, cam, *out, bg64, kAlphaMin, kTStop, nullptr, nullptr, st);
+    if ((rc = launch_replay_scene(true, f, *scene, cam, *out, bg64, kAlphaMin, kTStop, nullptr, nullptr, st)))
+        return rc;
+    return mark(prof, 6, st);
 }
 
 extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream) {
@@ -186,7 +202,8 @@ extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *s
 extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
                             const float background[3], void *frame, uint64_t frame_bytes,
                             int64_t entry_cap, const float *d_color, const float *d_depth,
-                            const bsr_grads *grads, float *screen_grad_norm, void *stream) {
+                            const bsr_grads *grads, float *screen_grad_norm, const bsr_profile *prof,
+                            void *stream) {
     if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || !grads)
         return BSR_ERR_BAD_ARG;
     if (scene->n > 0 && (!grads->positions || !grads->rotations || !grads->log_scales ||
@@ -197,19 +214,23 @@ extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
     if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
     if (scene->n == 0) return BSR_OK;
     const KCam cam = make_kcam(*camera);
+    int rc;
+    if ((rc = mark(prof, 0, st))) return rc;
     zero_acc_kernel<<<(unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8), BSR_BLOCK,
                       0, st>>>(f);
     BSR_LAUNCH_CHECK();
-    int rc;
     if ((rc = launch_raster_bwd(f, d_color, true, d_depth, background, (float)kAlphaMin, nullptr, nullptr,
-                                nullptr, st)))
+                                nullptr, prof ? prof->stats : nullptr, st)))
         return rc;
+    if ((rc = mark(prof, 1, st))) return rc;
     bsr_outputs none;
     memset(&none, 0, sizeof(none));
     const double bg64[3] = {background[0], background[1], background[2]};
     if ((rc = launch_replay_scene(false, f, *scene, cam, none, bg64, kAlphaMin, kTStop, d_color, d_depth, st)))
         return rc;
-    return launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, st);
+    if ((rc = mark(prof, 2, st))) return rc;
+    if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, st))) return rc;
+    return mark(prof, 3, st);
 }
 
 // ---- core seam ---------------------------------------------------------------------
@@ -260,7 +281,7 @@ extern "C" int bsr_core_forward_tiled(int64_t v, const double *means, const doub
     out.contributions = contrib;
     out.pixel_count = pixel_count;
     const float bg[3] = {(float)background[0], (float)background[1], (float)background[2]};
-    if ((rc = launch_raster_fwd(c.f, out, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, st)))
+    if ((rc = launch_raster_fwd(c.f, out, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, nullptr, st)))
         return rc;
     if ((rc = launch_replay_arrays(true, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
                                    out, background, alpha_min, t_stop, nullptr, st)))
@@ -295,7 +316,8 @@ extern "C" int bsr_core_backward(int64_t v, const double *means, const double *c
     bsr_outputs none;
     memset(&none, 0, sizeof(none));
     const float bg[3] = {(float)background[0], (float)background[1], (float)background[2]};
-    if ((rc = launch_raster_fwd(c.f, none, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, st)))
+    if ((rc = launch_raster_fwd(c.f, none, bg, (float)alpha_min, (float)t_stop, c.lists, c.ranges, c.f.rec, nullptr,
+                                st)))
         return rc;
     if ((rc = launch_replay_arrays(true, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
                                    none, background, alpha_min, t_stop, nullptr, st)))
@@ -303,7 +325,7 @@ extern "C" int bsr_core_backward(int64_t v, const double *means, const double *c
     if (v > 0)
         BSR_CUDA_TRY(cudaMemsetAsync(c.f.grad_acc, 0, 4ull * kGradStride * v, st));
     if ((rc = launch_raster_bwd(c.f, d_raw, false, nullptr, bg, (float)alpha_min, c.lists, c.ranges, c.f.rec,
-                                st)))
+                                nullptr, st)))
         return rc;
     if ((rc = launch_replay_arrays(false, c.f, means, conics, opac, betas, colors, bounds, c.lists, c.ranges,
                                    none, background, alpha_min, t_stop, d_raw, st)))

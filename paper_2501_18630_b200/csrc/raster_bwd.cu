@@ -27,6 +27,7 @@ struct RasterBwdArgs {
     const uint32_t *lists;
     const uint2 *ranges;
     const Record *rec;
+    unsigned long long *stats;  // optional: [2] evaluated pairs
 };
 
 // Transpose-reduce 16 values across a warp: afterwards lane L holds the warp sum of value
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
     __syncthreads();
     const int maxlast = s_maxlast;
     float B0 = a.bg[0], B1 = a.bg[1], B2 = a.bg[2], BD = 0.f;
+    uint32_t pairs = 0;
 
     for (int hi = maxlast; hi > 0; hi -= BSR_BLOCK) {
         const int lo = max(0, hi - BSR_BLOCK);
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
             bool took = false;
             if (act) {
+                if (a.stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[j].a, Bq = s_rec[j].b;
                 const Pair p = eval_pair(A, Bq, px - bd.x, py - bd.z);
                 if (p.alpha >= a.alpha_min) {
@@ -155,12 +158,18 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
                 atomicAdd(f.grad_acc + (int64_t)s_cidx[j] * kGradStride + idx, sum);
         }
     }
+    if (a.stats) {
+        unsigned long long p2 = pairs;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+        if (lane == 0) atomicAdd(a.stats + 2, p2);
+    }
 }
 
 int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask,
                       const float *d_depth, const float bg[3], float alpha_min,
                       const uint32_t *lists, const uint2 *ranges, const Record *rec,
-                      cudaStream_t st) {
+                      unsigned long long *stats, cudaStream_t st) {
     if (f.n_tiles == 0) return BSR_OK;
     RasterBwdArgs a;
     a.f = f;
@@ -174,6 +183,7 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask,
     a.lists = lists;
     a.ranges = ranges;
     a.rec = rec;
+    a.stats = stats;
     raster_bwd_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     BSR_LAUNCH_CHECK();
     return BSR_OK;

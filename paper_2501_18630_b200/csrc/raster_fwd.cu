@@ -26,6 +26,7 @@ struct RasterFwdArgs {
     const uint32_t *lists;   // entry -> record index
     const uint2 *ranges;     // tile -> [start, end)
     const Record *rec;
+    unsigned long long *stats;  // optional: [0] evaluated pairs, [1] contributions
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
 
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
     int cnt = 0, last = 0, flag_at = -1;
+    uint32_t pairs = 0;
     bool done = !inside;
     s_cnt[t] = 0;
 
@@ -82,6 +84,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
             if (bd.y < wx0 || bd.x > wx0 + 7 || bd.w < wy0 || bd.z > wy0 + 3) continue;
             bool took = false;
             if (!done) {
+                if (a.stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b;
                 const Pair p = eval_pair(A, B, px - bd.x, py - bd.z);
                 bool ambiguous = false;
@@ -128,6 +131,18 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
         }
     }
     cp_async_wait<0>();
+    if (a.stats) {
+        unsigned long long p2 = pairs, c2s = (unsigned)cnt;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+            c2s += __shfl_xor_sync(0xffffffffu, c2s, o);
+        }
+        if (lane == 0) {
+            atomicAdd(a.stats, p2);
+            atomicAdd(a.stats + 1, c2s);
+        }
+    }
     if (!inside) return;
     const int64_t pix = (int64_t)py * f.W + px;
     if (flag_at >= 0) {
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
 
 int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg[3], float alpha_min,
                       float t_stop, const uint32_t *lists, const uint2 *ranges, const Record *rec,
-                      cudaStream_t st) {
+                      unsigned long long *stats, cudaStream_t st) {
     if (f.n_tiles == 0) return BSR_OK;
     RasterFwdArgs a;
     a.f = f;
@@ -174,6 +189,7 @@ int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg
     a.lists = lists;
     a.ranges = ranges;
     a.rec = rec;
+    a.stats = stats;
     raster_fwd_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     BSR_LAUNCH_CHECK();
     return BSR_OK;

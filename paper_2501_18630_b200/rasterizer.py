@@ -130,7 +130,7 @@ def initial_entry_cap(n, width, height) -> int:
 
 def forward_raw(scene: _lib.SceneC, camera: Camera, background, outputs: _lib.OutputsC,
                 frame: FrameState | None = None, check: bool = True,
-                contrib: torch.Tensor | None = None) -> FrameState:
+                contrib: torch.Tensor | None = None, profile: _lib.ProfileC | None = None) -> FrameState:
     """Run bsr_forward; on capacity overflow grow the entry capacity and retry.
 
     ``contrib`` is the tensor behind ``outputs.contributions`` (accumulated by the
@@ -145,8 +145,10 @@ def forward_raw(scene: _lib.SceneC, camera: Camera, background, outputs: _lib.Ou
     while True:
         if frame is None or frame.n != n or frame.width != w or frame.height != h:
             frame = new_frame(n, w, h, initial_entry_cap(n, w, h))
+            check = True  # a fresh capacity guess is always verified once
         rc = lib.bsr_forward(ctypes.byref(scene), ctypes.byref(cam), bg, ctypes.c_void_p(frame.ptr()),
-                             frame.nbytes, frame.entry_cap, ctypes.byref(outputs), _stream())
+                             frame.nbytes, frame.entry_cap, ctypes.byref(outputs),
+                             None if profile is None else ctypes.byref(profile), _stream())
         _lib.check(rc, "bsr_forward")
         if not check:
             return frame
@@ -172,7 +174,7 @@ def outputs_c(color=None, raw=None, alpha=None, trans=None, depth=None, pixel_co
 
 def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameState,
                  d_color: torch.Tensor, d_depth: torch.Tensor | None, grads: _lib.GradsC,
-                 screen_grad_norm: torch.Tensor | None = None):
+                 screen_grad_norm: torch.Tensor | None = None, profile: _lib.ProfileC | None = None):
     lib = _lib.load()
     cam = _lib.camera_c(camera)
     if d_color.dtype != torch.float32 or not d_color.is_contiguous() or not d_color.is_cuda:
@@ -183,7 +185,8 @@ def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameSta
                           ctypes.c_void_p(frame.ptr()), frame.nbytes, frame.entry_cap,
                           ctypes.c_void_p(d_color.data_ptr()),
                           None if d_depth is None else ctypes.c_void_p(d_depth.data_ptr()),
-                          ctypes.byref(grads), _lib.ptr(screen_grad_norm), _stream())
+                          ctypes.byref(grads), _lib.ptr(screen_grad_norm),
+                          None if profile is None else ctypes.byref(profile), _stream())
     _lib.check(rc, "bsr_backward")
 
 
@@ -303,3 +306,50 @@ def debug_export(frame: FrameState) -> dict:
     _lib.check(rc, "debug_export")
     return dict(order=order[:v].cpu().numpy(), src=src[:v].cpu().numpy(), bounds=bounds[:v].cpu().numpy(),
                 lists=lists[:e].cpu().numpy(), ranges=ranges.cpu().numpy(), **info)
+
+
+class StageProfiler:
+    """Caller-owned CUDA events + device pair counters for bsr_forward / bsr_backward
+    (bsr_profile in include/bsr.h): per-stage device times and the algorithmic pair
+    counts the raster rooflines are computed from."""
+
+    FWD = ("preprocess", "depth_sort", "emit", "tile_sort", "raster_fwd", "replay_fwd")
+    BWD = ("raster_bwd", "replay_bwd", "preprocess_bwd")
+
+    def __init__(self, device="cuda"):
+        self.stats = torch.zeros(4, dtype=torch.int64, device=device)
+        self.fwd_ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        self.bwd_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        for e in self.fwd_ev + self.bwd_ev:  # force creation so the raw handles exist
+            e.record()
+        torch.cuda.synchronize()
+        self.fwd = _lib.ProfileC()
+        self.fwd.stats = self.stats.data_ptr()
+        for i, e in enumerate(self.fwd_ev):
+            self.fwd.events[i] = e.cuda_event
+        self.bwd = _lib.ProfileC()
+        self.bwd.stats = self.stats.data_ptr()
+        for i, e in enumerate(self.bwd_ev):
+            self.bwd.events[i] = e.cuda_event
+        self.acc = {k: 0.0 for k in self.FWD + self.BWD}
+        self.calls_fwd = 0
+        self.calls_bwd = 0
+
+    def collect_forward(self):
+        """Accumulate stage times of the last forward (call after a synchronize)."""
+        for i, k in enumerate(self.FWD):
+            self.acc[k] += self.fwd_ev[i].elapsed_time(self.fwd_ev[i + 1])
+        self.calls_fwd += 1
+
+    def collect_backward(self):
+        for i, k in enumerate(self.BWD):
+            self.acc[k] += self.bwd_ev[i].elapsed_time(self.bwd_ev[i + 1])
+        self.calls_bwd += 1
+
+    def mean_ms(self):
+        out = {}
+        for k in self.FWD:
+            out[k] = self.acc[k] / max(self.calls_fwd, 1)
+        for k in self.BWD:
+            out[k] = self.acc[k] / max(self.calls_bwd, 1)
+        return out

@@ -139,26 +139,30 @@ class TrainStep:
                                       d_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev))
                 self.loss_ws[key] = LossWorkspace(w, h, dev)
         self.loss_values = torch.zeros((len(self.cameras), 3), dtype=torch.float64, device=dev)
-        self.launches_per_step = None
+        self.profile = None  # optional rasterizer.StageProfiler-like object with .fwd/.bwd
 
     def _frame(self, cam):
         return self.frames.get((cam.width, cam.height))
 
-    def step(self, check=False):
+    def step(self, check=False, adam=True):
+        prof_f = None if self.profile is None else self.profile.fwd
+        prof_b = None if self.profile is None else self.profile.bwd
         self.grads.flat.zero_()
         for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
             key = (cam.width, cam.height)
             b = self.bufs[key]
             frame = forward_raw(self.scene, cam, self.background, outputs_c(color=b["color"]),
-                                frame=self._frame(cam), check=check)
+                                frame=self._frame(cam), check=check, profile=prof_f)
             self.frames[key] = frame
             ws = self.loss_ws[key]
             loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim)
             self.loss_values[i].copy_(ws.values)
-            backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None)
+            backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
+                         profile=prof_b)
         if self.pg is not None:
             torch.distributed.all_reduce(self.grads.flat, group=self.pg)
-        adam_step(self.prims, self.grads, self.adam, self.lrs)
+        if adam:
+            adam_step(self.prims, self.grads, self.adam, self.lrs)
         return self.loss_values
 
     def check_frames(self):

@@ -54,7 +54,7 @@ def test_host_side_validation_without_gpu():
     bg = (ctypes.c_float * 3)(1, 1, 1)
     o = _lib.OutputsC()
     assert lib.bsr_forward(ctypes.byref(sc), ctypes.byref(cam), bg, ctypes.c_void_p(1), 1, 10,
-                           ctypes.byref(o), None) == _lib.BSR_ERR_BAD_ARG
+                           ctypes.byref(o), None, None) == _lib.BSR_ERR_BAD_ARG
 
 
 def test_frame_bytes_monotone_in_capacity():
