@@ -66,7 +66,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -465,6 +465,12 @@ def main():
         frame_status(f)
 
     prof = BenchProfiler() if len(w["cams"]) == 1 else None
+    if prof is not None:  # algorithmic pair counts (P_f, P_b) from one untimed step
+        prof.sp.count_pairs(True)
+        run_step(w, prof)
+        torch.cuda.synchronize()
+        pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64)
+        prof.sp.count_pairs(False)
     clocks = ClockSampler(local)
     clocks.start()
     ms, views = timed_loop(w, K, world, prof=prof, l2=l2)
@@ -487,8 +493,7 @@ def main():
     roof, stages, extra = None, None, {}
     if prof is not None:
         stages = prof.sp.mean_ms()
-        st = prof.sp.stats.cpu().numpy().astype(np.float64) / K
-        pairs_f, contrib_f, pairs_b = st[0], st[1], st[2]
+        pairs_f, contrib_f, pairs_b = pair_stats[0], pair_stats[1], pair_stats[2]
         clk_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
         fp32_peak_max = SM_COUNT * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
         fp32_peak_clk = SM_COUNT * FP32_LANES_PER_SM * 2 * clk_mhz * 1e6 / 1e12

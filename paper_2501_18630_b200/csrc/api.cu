@@ -63,7 +63,7 @@ inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
 
 __global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
                                  const double *opac, const double *betas, const double *colors,
-                                 const int32_t *bounds, Record *rec) {
+                                 const int32_t *bounds, Record *rec, uint32_t *src_of) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
@@ -71,10 +71,18 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     r.a = make_float4((float)(means[2 * k] - x0), (float)(means[2 * k + 1] - y0), (float)conics[3 * k],
                       (float)conics[3 * k + 1]);
     r.b = make_float4((float)conics[3 * k + 2], (float)opac[k], (float)betas[k], 0.f);
-    r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
-                      __int_as_float((int)k));
+    // r2 error coefficient as in preprocess.cu (extents from the conic's inverse)
+    const double ca = conics[3 * k], cb = conics[3 * k + 1], cc = conics[3 * k + 2];
+    const double det = ca * cc - cb * cb;
+    const double ex = det > 0 ? sqrt(fabs(cc / det)) : 1e30, ey = det > 0 ? sqrt(fabs(ca / det)) : 1e30;
+    const double a = fabs(ca), b = fabs(cb), c = fabs(cc);
+    const double S = a * ex * ex + 2.0 * b * ex * ey + c * ey * ey;
+    const double kr = 5.9604644775390625e-08 * (8.0 * S + 3.0 * ((a * ex + b * ey) * (2.0 * ex + 3.0) +
+                                                                (b * ex + c * ey) * (2.0 * ey + 3.0))) * 1.5;
+    r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2], (float)kr);
     r.d = make_int4(x0, x1, y0, y1);
     rec[k] = r;
+    src_of[k] = (uint32_t)k;
 }
 
 __global__ void core_lists_kernel(const int64_t *offsets, const int64_t *lists, int64_t e,
@@ -248,7 +256,7 @@ static int core_prepare(const CoreView &c, int64_t v, const double *means, const
     BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
     if (v > 0)
         core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
-                                                                               colors, bounds, c.f.rec);
+                                                                               colors, bounds, c.f.rec, c.f.src_of);
     const int64_t m = imax64(n_entries, c.f.n_tiles);
     core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
         offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);
@@ -345,7 +353,7 @@ __global__ void export_records_kernel(FrameView f, int32_t *src, int32_t *bounds
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= V) return;
     const Record r = f.rec[c];
-    if (src) src[c] = __float_as_int(r.c.w);
+    if (src) src[c] = (int32_t)f.src_of[c];
     if (bounds) {
         bounds[4 * c] = r.d.x;
         bounds[4 * c + 1] = r.d.y;

@@ -59,7 +59,8 @@ inline KCam make_kcam(const bsr_camera &c) {
 //   A: mean_x - x0, mean_y - y0, conic a, conic b      (mean stored relative to its
 //      bounds corner so dx = (px - x0) - rel loses no bits at large pixel coordinates)
 //   B: conic c, opacity, beta, depth z
-//   C: r, g, b, source index (bit-cast)
+//   C: r, g, b, kR = bound on |r2(fp32) - r2(exact)| over the footprint (error analysis,
+//      raster.cuh); the source index lives in FrameView::src_of
 //   D: x0, x1, y0, y1 (inclusive pixel bounds, primitive.py:252-262)
 struct __align__(16) Record {
     float4 a, b, c;

@@ -40,6 +40,7 @@ struct FrameView {
     uint2 *tile_ranges;      // [n_tiles] (start, end)
     // --- not zeroed ---
     Record *rec;             // [N] compact order
+    uint32_t *src_of;        // [N] compact -> source index (batch.indices)
     uint64_t *dkeys[2];      // [N] depth keys (ping-pong)
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched, compact order
@@ -97,6 +98,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     off = align_up(off, 256);
     f.zero_bytes = off;
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
+    f.src_of = (uint32_t *)take(4ull * n);
     f.dkeys[0] = (uint64_t *)take(8ull * n);
     f.dkeys[1] = (uint64_t *)take(8ull * n);
     f.dvals[0] = (uint32_t *)take(4ull * n);

@@ -18,6 +18,21 @@ struct PreArgs {
     FrameView f;
 };
 
+// Bound on |r2_fp32 - r2_exact| for any pixel of the footprint (r2 <= 1), accounting for
+// the fp32 rounding of the record (mean relative to the bounds corner, conic) and of the
+// r2 evaluation in eval_pair (raster.cuh):  eps * (8 S + 3 (GX + GY)) with
+//   S  = |a| ex^2 + 2|b| ex ey + |c| ey^2            (|terms| of the quadratic form)
+//   GX = (|a| ex + |b| ey)(2 ex + 3), GY = (|b| ex + |c| ey)(2 ey + 3)  (d r2 / d mean x
+//        the mean's representation error, |mean - corner| <= extent + 2)
+__device__ __forceinline__ double r2_error_bound(const Proj64 &p) {
+    const double ex = sqrt(p.c00), ey = sqrt(p.c11);
+    const double a = fabs(p.ca), b = fabs(p.cb), c = fabs(p.cc);
+    const double S = a * ex * ex + 2.0 * b * ex * ey + c * ey * ey;
+    const double GX = (a * ex + b * ey) * (2.0 * ex + 3.0);
+    const double GY = (b * ex + c * ey) * (2.0 * ey + 3.0);
+    return 5.9604644775390625e-08 * (8.0 * S + 3.0 * (GX + GY)) * 1.5;
+}
+
 template <int K>
 __device__ __forceinline__ void load_sh(const float *sh, int64_t i, float *dst) {
     const float *p = sh + i * (int64_t)K * 3;
@@ -71,7 +86,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
             const double beta = shape_to_exponent64((double)__ldg(args.sc.shapes + i));
             r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)p.ca, (float)p.cb);
             r.b = make_float4((float)p.cc, (float)o, (float)beta, (float)p.tz);
-            r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], __int_as_float((int)i));
+            r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)r2_error_bound(p));
             r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
             key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
             tcount = (uint32_t)((p.x1 / BSR_TILE - p.x0 / BSR_TILE + 1) *
@@ -114,6 +129,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     if (vis) {
         const uint32_t c = s_excl + s_warp[warp] + local;
         f.rec[c] = r;
+        f.src_of[c] = (uint32_t)i;
         f.dkeys[0][c] = key;
         f.dvals[0][c] = c;
         f.tile_count[c] = tcount;

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
     const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
     const float dmx = g0.x, dmy = g0.y, dA = g0.z, dB = g0.w, dC = g1.x, d_o = g1.y, d_beta = g1.z;
     const float dr = g1.w, dg = g2.x, dbl = g2.y, dz = g2.z;
-    const int64_t i = __float_as_int(a.f.rec[c].c.w);
+    const int64_t i = a.f.src_of[c];
     const bsr_scene &sc = a.sc;
     const KCam &cam = a.cam;
 

@@ -8,9 +8,21 @@
 
 namespace bsr {
 
+constexpr float kEps = 5.9604645e-08f;  // 2^-24
+
 struct Pair {
     float dx, dy, r2, x, om, k, alpha;
 };
+
+// (1-x)^beta: two squarings for the Gaussian-like beta == 4 (no XU op); otherwise
+// ex2(beta * lg2(1-x)) on the XU pipe.  Deterministic, shared by fwd/bwd.
+__device__ __forceinline__ float beta_pow(float om, float beta) {
+    if (beta == 4.0f) {
+        const float o2 = __fmul_rn(om, om);
+        return __fmul_rn(o2, o2);
+    }
+    return exp2f(__fmul_rn(beta, __log2f(om)));
+}
 
 // _raster.pyx:107-113:  r2 = a dx^2 + 2 b dx dy + c dy^2, x = clamp(r2, 0, 1),
 // kernel = (1 - x)^beta, alpha = o * kernel.  px_rel / py_rel are pixel coordinates
@@ -24,29 +36,63 @@ __device__ __forceinline__ Pair eval_pair(const float4 A, const float4 B, int px
     p.r2 = __fmaf_rn(__fmul_rn(A.z, p.dx), p.dx, t);
     p.x = fminf(fmaxf(p.r2, 0.0f), 1.0f);
     p.om = __fsub_rn(1.0f, p.x);
-    if (B.z == 4.0f) {
-        const float o2 = __fmul_rn(p.om, p.om);
-        p.k = __fmul_rn(o2, o2);
-    } else {
-        p.k = powf(p.om, B.z);
-    }
+    p.k = beta_pow(p.om, B.z);
     p.alpha = __fmul_rn(B.y, p.k);
     return p;
 }
 
-// Conservative bound on the relative error of the fp32 alpha versus the exact (fp64)
-// evaluation of the same primitive (record rounding, dx/dy rounding through the stored
-// mean, r2 evaluation, the (1-x)^beta evaluation).  Only evaluated on rare paths.
-__device__ __forceinline__ float alpha_rel_err(const float4 A, const float4 B, const Pair &p) {
-    const float eps = 5.9604645e-08f;  // 2^-24
-    const float s = fabsf(A.z * p.dx * p.dx) + fabsf(2.0f * A.w * p.dx * p.dy) +
-                    fabsf(B.x * p.dy * p.dy);
+// Relative error bound of the (1-x)^beta evaluation itself (inputs exact) + o * k rounding.
+__device__ __forceinline__ float pow_rel_err(float beta) {
+    // lg2.approx: <= 2^-22.6 abs on [0.5,2], 2 ulp of |lg2| <= 24 otherwise; ex2.approx 2 ulp;
+    // beta*lg2 rounding: ln2 * |beta lg2| * eps  ->  <= (4 beta + 2) 1e-6 overall
+    return beta == 4.0f ? 7.0f * kEps : (4.0f * fabsf(beta) + 2.0f) * 1.0e-6f + 3.0f * kEps;
+}
+
+// Rigorous relative error bound of the fp32 alpha versus the exact evaluation of the same
+// primitive: r2 error (<= kR, per primitive, preprocess.cu) propagated through
+// (1-x)^beta, plus the pow evaluation.  Used on the rare near-threshold paths.
+__device__ __forceinline__ float alpha_rel_err(const float4 B, const float4 C, const Pair &p) {
+    return B.z * C.w / fmaxf(p.om, 1e-30f) + pow_rel_err(B.z);
+}
+
+// Same bound with the r2 error evaluated at this pixel instead of the footprint maximum
+// (tighter; used on the rare alpha ~ alpha_min path):  |r2 error| <= eps (8 s + 3 (gx + gy)),
+// s = sum of |terms| of the quadratic form, g = |grad r2 / 2| x (|d| + |mean - corner| + 1).
+__device__ __forceinline__ float alpha_rel_err_pixel(const float4 A, const float4 B, const Pair &p) {
+    const float s = fabsf(A.z * p.dx * p.dx) + fabsf(2.0f * A.w * p.dx * p.dy) + fabsf(B.x * p.dy * p.dy);
     const float gx = fabsf(A.z * p.dx + A.w * p.dy) * (fabsf(p.dx) + fabsf(A.x) + 1.0f);
     const float gy = fabsf(A.w * p.dx + B.x * p.dy) * (fabsf(p.dy) + fabsf(A.y) + 1.0f);
-    const float dr2 = eps * (8.0f * s + 3.0f * (gx + gy));
-    const float beta = B.z;
-    const float pow_err = (beta == 4.0f) ? 4.0f * eps : 4.0f * eps * (1.0f + fabsf(beta * __logf(fmaxf(p.om, 1e-30f))));
-    return beta * dr2 / fmaxf(p.om, 1e-30f) + pow_err + 3.0f * eps;
+    const float dr2 = 1.5f * kEps * (8.0f * s + 3.0f * (gx + gy));
+    return B.z * dr2 / fmaxf(p.om, 1e-30f) + pow_rel_err(B.z);
+}
+
+// Does the ellipse r2 < 1 (+ fp32 slack) of a primitive touch the pixel-centre rectangle
+// [X0,X1] x [Y0,Y1]?  Exact minimum of the quadratic form over the rectangle (centre inside,
+// else the minimum over the four edges), conservative by the record's r2 error bound.
+__device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B, const float4 C,
+                                                  const int4 D, int X0, int X1, int Y0, int Y1) {
+    if (D.y < X0 || D.x > X1 || D.w < Y0 || D.z > Y1) return false;
+    const float mx = (float)D.x + A.x, my = (float)D.z + A.y;
+    if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
+    const float a = A.z, b = A.w, c = B.x;
+    const float ia = 1.0f / a, ic = 1.0f / c;
+    float q = 3.0e38f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        // vertical edges x = X0 / X1
+        const float dx = (float)(e ? X1 : X0) - mx;
+        const float dy = fminf(fmaxf(my - b * dx * ic, (float)Y0), (float)Y1) - my;
+        q = fminf(q, a * dx * dx + 2.0f * b * dx * dy + c * dy * dy);
+        // horizontal edges y = Y0 / Y1
+        const float ey = (float)(e ? Y1 : Y0) - my;
+        const float ex = fminf(fmaxf(mx - b * ey * ia, (float)X0), (float)X1) - mx;
+        q = fminf(q, a * ex * ex + 2.0f * b * ex * ey + c * ey * ey);
+    }
+    return q < 1.0f + 4.0f * C.w + 1e-4f;
+}
+
+__device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int Y0, int Y1) {
+    return !(D.y < X0 || D.x > X1 || D.w < Y0 || D.z > Y1);
 }
 
 }  // namespace bsr

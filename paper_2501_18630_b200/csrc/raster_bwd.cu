@@ -10,6 +10,8 @@
 // alpha >= alpha_min decisions are the forward's.  Pixels the forward handed to the fp64
 // replay have last == 0 here and are differentiated by replay.cu instead.
 //
+// Per batch each warp builds the compacted list of entries whose ellipse reaches its 8x4
+// block and that precede the warp's furthest last contributor, then walks it backwards.
 // Per pair the 11 partials (d mean2d x2, d conic x3, d opacity, d beta, d rgb x3, d z)
 // are reduced across the warp with a 16-shuffle transpose reduction and added with one
 // warp-wide RED instruction per (warp, entry) into grad_acc[compact][12].
@@ -49,6 +51,7 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) {
     __shared__ __align__(16) Record s_rec[BSR_BLOCK];
     __shared__ uint32_t s_cidx[BSR_BLOCK];
+    __shared__ uint8_t s_list[BSR_BLOCK / 32][BSR_BLOCK];
     __shared__ int s_maxlast;
     const FrameView &f = a.f;
     const int tile = blockIdx.x;
@@ -61,6 +64,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x;
+    const bool stats = a.stats != nullptr;
+    const uint32_t lt_mask = (1u << lane) - 1u;
 
     const int64_t pix = (int64_t)py * f.W + px;
     int last = 0;
@@ -82,8 +87,11 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
         }
     }
     if (t == 0) s_maxlast = 0;
+    int wlast = last;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
     __syncthreads();
-    if (last) atomicMax(&s_maxlast, last);
+    if (lane == 0 && wlast) atomicMax(&s_maxlast, wlast);
     __syncthreads();
     const int maxlast = s_maxlast;
     float B0 = a.bg[0], B1 = a.bg[1], B2 = a.bg[2], BD = 0.f;
@@ -99,18 +107,35 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
             s_rec[t] = rec[c];
         }
         __syncthreads();
-        for (int j = nb - 1; j >= 0; --j) {
+        // ---- per-warp list: entries before the warp's furthest last contributor that
+        //      reach its 8x4 block (ascending; walked backwards)
+        int nl = 0;
+        if (wlast > lo) {
+            for (int c0j = 0; c0j < nb; c0j += 32) {
+                const int j = c0j + lane;
+                bool hit = false;
+                if (j < nb && lo + j < wlast) {
+                    const Record &r = s_rec[j];
+                    hit = stats ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
+                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
+                nl += __popc(m);
+            }
+            __syncwarp();
+        }
+        for (int i = nl - 1; i >= 0; --i) {
+            const int j = s_list[warp][i];
             const int e = lo + j;  // local entry index
-            const int4 bd = s_rec[j].d;
-            if (bd.y < wx0 || bd.x > wx0 + 7 || bd.w < wy0 || bd.z > wy0 + 3) continue;
-            bool act = e < last;
-            if (!__any_sync(0xffffffffu, act)) continue;
+            const bool act = e < last;
             float v[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            for (int q = 0; q < 16; ++q) v[q] = 0.f;
             bool took = false;
             if (act) {
-                if (a.stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
+                const int4 bd = s_rec[j].d;
+                if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[j].a, Bq = s_rec[j].b;
                 const Pair p = eval_pair(A, Bq, px - bd.x, py - bd.z);
                 if (p.alpha >= a.alpha_min) {
@@ -133,12 +158,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
                     const float dk = dalpha * Bq.y;
                     if (p.x < 1.0f) {
                         const float beta = Bq.z;
-                        float pw;  // (1-x)^(beta-1)
-                        if (beta == 4.0f) {
-                            pw = p.om * p.om * p.om;
-                        } else {
-                            pw = powf(p.om, beta - 1.0f);
-                        }
+                        // (1-x)^(beta-1) = k / (1-x); ln(1-x) via the XU pipe
+                        const float pw = beta == 4.0f ? p.om * p.om * p.om : p.k / p.om;
                         v[6] = dk * p.k * __logf(p.om);
                         float dkdx = -beta * pw;
                         if (dkdx < -kEdgeGradClamp) dkdx = -kEdgeGradClamp;
@@ -158,7 +179,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
                 atomicAdd(f.grad_acc + (int64_t)s_cidx[j] * kGradStride + idx, sum);
         }
     }
-    if (a.stats) {
+    if (stats) {
         unsigned long long p2 = pairs;
 #pragma unroll
         for (int o = 16; o; o >>= 1) p2 += __shfl_xor_sync(0xffffffffu, p2, o);
@@ -166,10 +187,9 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
     }
 }
 
-int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask,
-                      const float *d_depth, const float bg[3], float alpha_min,
-                      const uint32_t *lists, const uint2 *ranges, const Record *rec,
-                      unsigned long long *stats, cudaStream_t st) {
+int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, const float *d_depth,
+                      const float bg[3], float alpha_min, const uint32_t *lists, const uint2 *ranges,
+                      const Record *rec, unsigned long long *stats, cudaStream_t st) {
     if (f.n_tiles == 0) return BSR_OK;
     RasterBwdArgs a;
     a.f = f;

@@ -1,13 +1,15 @@
 // K4 raster_fwd: per-16x16-tile front-to-back compositing (_raster.pyx:74-155).
 //
-// One CTA (256 threads) per tile, one pixel per thread; a warp owns an 8x4 pixel block so
-// compact footprints touch few warps.  Tile-list records (64 B) are gathered into shared
-// memory in batches of 256 with cp.async double buffering; every entry is first tested
-// against the warp's pixel rectangle (warp-uniform skip), then evaluated per pixel.
-// Termination: warp ballots count contributions, __syncthreads_count ends the tile once
-// every pixel has T < t_stop ("composite, then stop", _raster.pyx:116-123).
+// One CTA (256 threads) per tile, one pixel per thread; a warp owns an 8x4 pixel block.
+// Tile-list records (64 B) are gathered into shared memory in batches of 256 with
+// cp.async double buffering.  Per batch, every warp builds a compacted list of the entries
+// whose ellipse actually reaches its 8x4 block (exact minimum of the conic over the block,
+// one entry per lane, ballot-compacted), so the per-pixel loop only visits entries that
+// can contribute to that warp.  Termination: the warp leaves its list once all its pixels
+// reached T < t_stop, the CTA leaves the tile via __syncthreads_count ("composite, then
+// stop", _raster.pyx:116-123).
 //
-// Exactness: decisions alpha >= alpha_min and T < t_stop are taken in fp32
+// Exactness: the decisions alpha >= alpha_min and T < t_stop are taken in fp32
 // only when a rigorous error bound certifies them; otherwise the pixel is handed to the
 // fp64 replay (replay.cu) from that entry on.  Pixels with alpha > 0.999 (fp32 cannot
 // carry 1 - alpha) are handed over too.
@@ -39,6 +41,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) {
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
+    __shared__ uint32_t s_cidx[2][BSR_BLOCK];
+    __shared__ uint8_t s_list[BSR_BLOCK / 32][BSR_BLOCK];
     __shared__ int s_cnt[BSR_BLOCK];
     const FrameView &f = a.f;
     const int tile = blockIdx.x;
@@ -51,6 +55,9 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x, end = (int)range.y;
+    const bool want_contrib = a.out.contributions != nullptr;
+    const bool stats = a.stats != nullptr;
+    const uint32_t lt_mask = (1u << lane) - 1u;
 
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
     int cnt = 0, last = 0, flag_at = -1;
@@ -61,7 +68,9 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
     auto prefetch = [&](int b0, int buf) {
         const int e = b0 + t;
         if (e < end) {
-            const Record *src = rec + lists[e];
+            const uint32_t c = lists[e];
+            s_cidx[buf][t] = c;
+            const Record *src = rec + c;
             Record *dst = &s_rec[buf][t];
             cp_async16(&dst->a, &src->a);
             cp_async16(&dst->b, &src->b);
@@ -79,29 +88,49 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         if (__syncthreads_count(done) == BSR_BLOCK) break;
         const int nb = min(BSR_BLOCK, end - b0);
-        for (int j = 0; j < nb; ++j) {
-            const int4 bd = s_rec[buf][j].d;
-            if (bd.y < wx0 || bd.x > wx0 + 7 || bd.w < wy0 || bd.z > wy0 + 3) continue;
+        // ---- per-warp compacted list of entries reaching this warp's 8x4 block
+        int nl = 0;
+        if (!__all_sync(0xffffffffu, done)) {
+            for (int c0j = 0; c0j < nb; c0j += 32) {
+                const int j = c0j + lane;
+                bool hit = false;
+                if (j < nb) {
+                    const Record &r = s_rec[buf][j];
+                    hit = stats ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
+                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
+                nl += __popc(m);
+            }
+            __syncwarp();
+        }
+        for (int i = 0; i < nl; ++i) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const int j = s_list[warp][i];
             bool took = false;
             if (!done) {
-                if (a.stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
+                const int4 bd = s_rec[buf][j].d;
+                if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b;
                 const Pair p = eval_pair(A, B, px - bd.x, py - bd.z);
                 bool ambiguous = false;
                 // rare path: alpha within 5% of the cutoff -> certify with the error bound
                 if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
-                    const float rel = alpha_rel_err(A, B, p);
-                    ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 1e-9f * a.alpha_min;
+                    const float rel = alpha_rel_err_pixel(A, B, p);
+                    ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 4.0f * kEps * a.alpha_min;
                 }
                 if (!ambiguous && p.alpha >= a.alpha_min) {
-                    const float Tn = __fmul_rn(T, __fsub_rn(1.0f, p.alpha));
-                    const float rel = alpha_rel_err(A, B, p);
-                    const float errTn = errT + 2.5f * 5.9604645e-08f + p.alpha * rel / fmaxf(1.0f - p.alpha, 1e-30f);
-                    if (p.alpha > 0.999f ||
-                        fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * 5.9604645e-08f * a.t_stop) {
+                    const float4 C = s_rec[buf][j].c;
+                    const float one_m = __fsub_rn(1.0f, p.alpha);
+                    const float Tn = __fmul_rn(T, one_m);
+                    // relative error bound of T: sum over samples of
+                    //   alpha/(1-alpha) * rel_err(alpha) + rounding
+                    const float rel = B.z * C.w * __frcp_rn(fmaxf(p.om, 1e-30f)) + pow_rel_err(B.z);
+                    const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * __frcp_rn(fmaxf(one_m, 1e-30f));
+                    if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
                         ambiguous = true;
                     } else {
-                        const float4 C = s_rec[buf][j].c;
                         const float w = __fmul_rn(p.alpha, T);
                         c0 = __fmaf_rn(w, C.x, c0);
                         c1 = __fmaf_rn(w, C.y, c1);
@@ -120,18 +149,19 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
                     done = true;
                 }
             }
-            const unsigned ballot = __ballot_sync(0xffffffffu, took);
-            if (ballot && lane == 0) atomicAdd(&s_cnt[j], __popc(ballot));
+            if (want_contrib) {
+                const unsigned ballot = __ballot_sync(0xffffffffu, took);
+                if (ballot && lane == 0) atomicAdd(&s_cnt[j], __popc(ballot));
+            }
         }
         __syncthreads();
-        if (t < nb && s_cnt[t]) {
-            if (a.out.contributions)
-                atomicAdd(a.out.contributions + __float_as_int(s_rec[buf][t].c.w), s_cnt[t]);
+        if (want_contrib && t < nb && s_cnt[t]) {
+            atomicAdd(a.out.contributions + f.src_of[s_cidx[buf][t]], s_cnt[t]);
             s_cnt[t] = 0;
         }
     }
     cp_async_wait<0>();
-    if (a.stats) {
+    if (stats) {
         unsigned long long p2 = pairs, c2s = (unsigned)cnt;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {

@@ -27,20 +27,16 @@ struct SceneProvider {
     bsr_scene sc;
     KCam cam;
     const Record *rec;
+    const uint32_t *src_of;
     __device__ __forceinline__ bool get(uint32_t c, int px, int py, Entry64 &e) const {
         const int4 bd = rec[c].d;
         if (px < bd.x || px > bd.y || py < bd.z || py > bd.w) return false;
-        const int64_t i = __float_as_int(rec[c].c.w);
+        const int64_t i = src_of[c];
         const float pos[3] = {sc.positions[3 * i], sc.positions[3 * i + 1], sc.positions[3 * i + 2]};
         const float q[4] = {sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2],
                             sc.rotations[4 * i + 3]};
         const float ls[3] = {sc.log_scales[3 * i], sc.log_scales[3 * i + 1], sc.log_scales[3 * i + 2]};
         const Proj64 p = project64(pos, q, ls, cam);
-        float shv[3 * K];
-#pragma unroll
-        for (int j = 0; j < 3 * K; ++j) shv[j] = sc.sh[i * 3 * K + j];
-        double rgb[3];
-        sh_color64<K>(shv, pos, cam, rgb);
         e.mx = p.mx;
         e.my = p.my;
         e.ca = p.ca;
@@ -48,12 +44,22 @@ struct SceneProvider {
         e.cc = p.cc;
         e.o = sigmoid64((double)sc.opacity_raw[i]);
         e.beta = shape_to_exponent64((double)sc.shapes[i]);
-        e.r = rgb[0];
-        e.g = rgb[1];
-        e.b = rgb[2];
         e.z = p.tz;
         e.src = (int)i;
         return true;
+    }
+    // colour only for samples that pass the alpha cutoff
+    __device__ __forceinline__ void color(Entry64 &e) const {
+        const int64_t i = e.src;
+        const float pos[3] = {sc.positions[3 * i], sc.positions[3 * i + 1], sc.positions[3 * i + 2]};
+        float shv[3 * K];
+#pragma unroll
+        for (int j = 0; j < 3 * K; ++j) shv[j] = sc.sh[i * 3 * K + j];
+        double rgb[3];
+        sh_color64<K>(shv, pos, cam, rgb);
+        e.r = rgb[0];
+        e.g = rgb[1];
+        e.b = rgb[2];
     }
 };
 
@@ -71,12 +77,15 @@ struct ArrayProvider {
         e.cc = conics[3 * c + 2];
         e.o = opac[c];
         e.beta = betas[c];
-        e.r = colors[3 * c];
-        e.g = colors[3 * c + 1];
-        e.b = colors[3 * c + 2];
         e.z = 0.0;
         e.src = (int)c;
         return true;
+    }
+    __device__ __forceinline__ void color(Entry64 &e) const {
+        const int64_t c = e.src;
+        e.r = colors[3 * c];
+        e.g = colors[3 * c + 1];
+        e.b = colors[3 * c + 2];
     }
 };
 
@@ -107,9 +116,38 @@ __device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, doub
     return e.o * kernel;
 }
 
+// Candidates of one round (entries passing alpha >= alpha_min), compacted in list order.
+struct ReplaySmem {
+    double alpha[BSR_BLOCK], r[BSR_BLOCK], g[BSR_BLOCK], b[BSR_BLOCK], z[BSR_BLOCK];
+    double t_before[BSR_BLOCK], p0[BSR_BLOCK], p1[BSR_BLOCK], p2[BSR_BLOCK], pd[BSR_BLOCK];
+    int entry[BSR_BLOCK];
+    int warp_cnt[BSR_BLOCK / 32];
+    int n_cand, n_used;
+    bool done;
+};
+
+// Block-wide ordered compaction of `cand` into slots [0, n): returns this thread's slot.
+__device__ __forceinline__ int compact_slot(bool cand, ReplaySmem &sm) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) sm.warp_cnt[warp] = __popc(m);
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < BSR_BLOCK / 32; ++w) {
+        if (w < warp) base += sm.warp_cnt[w];
+        total += sm.warp_cnt[w];
+    }
+    if (t == 0) sm.n_cand = total;
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// One flagged pixel, one CTA: 256 list entries per round evaluated in parallel (fp64
+// projection on demand), the order-dependent recurrence runs on thread 0 over the
+// compacted candidates.  _raster.pyx:95-127.
 template <typename P>
-__device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, int lane) {
+__device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplaySmem &sm) {
     const FrameView &f = a.f;
+    const int t = threadIdx.x;
     const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
     const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
     const uint2 fl = f.flags[slot];
@@ -119,11 +157,13 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     const int start = (int)ranges[tile].x, end = (int)ranges[tile].y;
     const int flag_at = (int)fl.y;
 
-    double t = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dd = 0.0;
+    double t_acc = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dd = 0.0;  // thread 0's state
     int count = 0, last = 0;
-    bool done = false;
-    for (int base = start; base < end && !done; base += 32) {
-        const int e = base + lane;
+    if (t == 0) sm.done = false;
+    __syncthreads();
+    for (int base = start; base < end; base += BSR_BLOCK) {
+        if (sm.done) break;  // uniform (read after a barrier)
+        const int e = base + t;
         Entry64 en;
         bool cand = false;
         double alpha = 0.0;
@@ -131,32 +171,46 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
             double dx, dy, x, k;
             alpha = alpha64(en, px, py, dx, dy, x, k);
             cand = !(alpha < a.alpha_min);
+            if (cand) prov.color(en);
         }
-        unsigned m = __ballot_sync(0xffffffffu, cand);
-        bool mine = false;
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            const double al = shfl_d(alpha, l);
-            const double weight = al * t;
-            c0 = c0 + weight * shfl_d(en.r, l);
-            c1 = c1 + weight * shfl_d(en.g, l);
-            c2 = c2 + weight * shfl_d(en.b, l);
-            dd = dd + weight * shfl_d(en.z, l);
-            t = t * (1.0 - al);
-            ++count;
-            last = base + l - start + 1;
-            if (l == lane) mine = true;
-            if (t < a.t_stop) {
-                done = true;
-                break;
+        const int s = compact_slot(cand, sm);
+        if (cand) {
+            sm.alpha[s] = alpha;
+            sm.r[s] = en.r;
+            sm.g[s] = en.g;
+            sm.b[s] = en.b;
+            sm.z[s] = en.z;
+            sm.entry[s] = e - start;
+        }
+        __syncthreads();
+        if (t == 0) {
+            int used = sm.n_cand;
+            for (int q = 0; q < sm.n_cand; ++q) {
+                const double al = sm.alpha[q];
+                const double weight = al * t_acc;
+                c0 = c0 + weight * sm.r[q];
+                c1 = c1 + weight * sm.g[q];
+                c2 = c2 + weight * sm.b[q];
+                dd = dd + weight * sm.z[q];
+                t_acc = t_acc * (1.0 - al);
+                ++count;
+                last = sm.entry[q] + 1;
+                if (t_acc < a.t_stop) {
+                    used = q + 1;
+                    sm.done = true;
+                    break;
+                }
             }
+            sm.n_used = used;
         }
-        if (mine && (e - start) >= flag_at && a.out.contributions)
+        __syncthreads();
+        // contributions of entries at/after the fp32 flag point (earlier ones were counted)
+        if (cand && s < sm.n_used && sm.entry[s] >= flag_at && a.out.contributions)
             atomicAdd(a.out.contributions + en.src, 1);
+        __syncthreads();
     }
-    if (lane != 0) return;
-    const double r0 = c0 + a.bg[0] * t, r1 = c1 + a.bg[1] * t, r2 = c2 + a.bg[2] * t;
+    if (t != 0) return;
+    const double r0 = c0 + a.bg[0] * t_acc, r1 = c1 + a.bg[1] * t_acc, r2 = c2 + a.bg[2] * t_acc;
     if (a.out.raw) {
         a.out.raw[3 * pix] = (float)r0;
         a.out.raw[3 * pix + 1] = (float)r1;
@@ -167,23 +221,27 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
         a.out.color[3 * pix + 1] = (float)fmax(r1, 0.0);
         a.out.color[3 * pix + 2] = (float)fmax(r2, 0.0);
     }
-    if (a.out.alpha) a.out.alpha[pix] = (float)(1.0 - t);
-    if (a.out.transmittance) a.out.transmittance[pix] = (float)t;
+    if (a.out.alpha) a.out.alpha[pix] = (float)(1.0 - t_acc);
+    if (a.out.transmittance) a.out.transmittance[pix] = (float)t_acc;
     if (a.out.depth) a.out.depth[pix] = (float)dd;
     if (a.out.pixel_count) a.out.pixel_count[pix] = count;
-    f.t_final[pix] = (float)t;
+    f.t_final[pix] = (float)t_acc;
     double *st = f.replay_state + 6 * (int64_t)slot;
     st[0] = r0;
     st[1] = r1;
     st[2] = r2;
     st[3] = dd;
-    st[4] = t;
+    st[4] = t_acc;
     st[5] = (double)last;
 }
 
+// Backward of one flagged pixel (_raster.pyx:182-241 + depth), one CTA: parallel alpha,
+// thread 0 computes every candidate's (T, prefix) in order, then the per-candidate
+// gradients are evaluated in parallel and added into grad_acc.
 template <typename P>
-__device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, int lane) {
+__device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplaySmem &sm) {
     const FrameView &f = a.f;
+    const int t = threadIdx.x;
     const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
     const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
     const uint2 fl = f.flags[slot];
@@ -200,9 +258,9 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     const double g2 = (!a.mask_raw || raw2 >= 0.0) ? (double)a.d_color[3 * pix + 2] : 0.0;
     const double gd = a.d_depth ? (double)a.d_depth[pix] : 0.0;
 
-    double t = 1.0, p0 = 0.0, p1 = 0.0, p2 = 0.0, pd = 0.0;
-    for (int base = start; base < end; base += 32) {
-        const int e = base + lane;
+    double t_acc = 1.0, q0 = 0.0, q1 = 0.0, q2 = 0.0, qd = 0.0;  // thread 0's running state
+    for (int base = start; base < end; base += BSR_BLOCK) {
+        const int e = base + t;
         Entry64 en;
         bool cand = false;
         double alpha = 0.0, dx = 0, dy = 0, x = 1, kernel = 0;
@@ -212,83 +270,92 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
             if (prov.get(c, px, py, en)) {
                 alpha = alpha64(en, px, py, dx, dy, x, kernel);
                 cand = !(alpha < a.alpha_min);
+                if (cand) prov.color(en);
             }
         }
-        // sequential prefix: capture (t, prefix) before this lane's sample
-        double my_t = 0, my_p0 = 0, my_p1 = 0, my_p2 = 0, my_pd = 0;
-        unsigned m = __ballot_sync(0xffffffffu, cand);
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            if (l == lane) {
-                my_t = t;
-                my_p0 = p0;
-                my_p1 = p1;
-                my_p2 = p2;
-                my_pd = pd;
+        const int s = compact_slot(cand, sm);
+        if (cand) {
+            sm.alpha[s] = alpha;
+            sm.r[s] = en.r;
+            sm.g[s] = en.g;
+            sm.b[s] = en.b;
+            sm.z[s] = en.z;
+        }
+        __syncthreads();
+        if (t == 0) {
+            for (int q = 0; q < sm.n_cand; ++q) {
+                sm.t_before[q] = t_acc;
+                sm.p0[q] = q0;
+                sm.p1[q] = q1;
+                sm.p2[q] = q2;
+                sm.pd[q] = qd;
+                const double weight = sm.alpha[q] * t_acc;
+                q0 = q0 + weight * sm.r[q];
+                q1 = q1 + weight * sm.g[q];
+                q2 = q2 + weight * sm.b[q];
+                qd = qd + weight * sm.z[q];
+                t_acc = t_acc * (1.0 - sm.alpha[q]);
             }
-            const double al = shfl_d(alpha, l);
-            const double weight = al * t;
-            p0 = p0 + weight * shfl_d(en.r, l);
-            p1 = p1 + weight * shfl_d(en.g, l);
-            p2 = p2 + weight * shfl_d(en.b, l);
-            pd = pd + weight * shfl_d(en.z, l);
-            t = t * (1.0 - al);
         }
-        if (!cand) continue;
-        // _raster.pyx:208-234 with the sample's own (t, prefix)
-        const double weight = alpha * my_t;
-        const double cr0 = weight * en.r, cr1 = weight * en.g, cr2 = weight * en.b, crd = weight * en.z;
-        const double behind0 = raw0 - my_p0 - cr0;
-        const double behind1 = raw1 - my_p1 - cr1;
-        const double behind2 = raw2 - my_p2 - cr2;
-        const double behindd = rawd - my_pd - crd;
-        const double g_dot_col = g0 * en.r + g1 * en.g + g2 * en.b;
-        const double g_dot_behind = g0 * behind0 + g1 * behind1 + g2 * behind2;
-        double d_alpha = g_dot_col * my_t - g_dot_behind / (1.0 - alpha);
-        d_alpha = d_alpha + (gd * en.z * my_t - gd * behindd / (1.0 - alpha));
-        float *acc = f.grad_acc + (int64_t)c * kGradStride;
-        atomicAdd(acc + 7, (float)(weight * g0));
-        atomicAdd(acc + 8, (float)(weight * g1));
-        atomicAdd(acc + 9, (float)(weight * g2));
-        atomicAdd(acc + 10, (float)(weight * gd));
-        atomicAdd(acc + 5, (float)(d_alpha * kernel));
-        const double d_kernel = d_alpha * en.o;
-        if (x < 1.0) {
-            atomicAdd(acc + 6, (float)(d_kernel * kernel * log(1.0 - x)));
-            double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
-            if (dkdx < -1e7) dkdx = -1e7;
-            const double d_x = d_kernel * dkdx;
-            atomicAdd(acc + 0, (float)(-d_x * 2.0 * (en.ca * dx + en.cb * dy)));
-            atomicAdd(acc + 1, (float)(-d_x * 2.0 * (en.cb * dx + en.cc * dy)));
-            atomicAdd(acc + 2, (float)(d_x * dx * dx));
-            atomicAdd(acc + 3, (float)(d_x * 2.0 * dx * dy));
-            atomicAdd(acc + 4, (float)(d_x * dy * dy));
+        __syncthreads();
+        if (cand) {
+            const double my_t = sm.t_before[s];
+            const double weight = alpha * my_t;
+            const double cr0 = weight * en.r, cr1 = weight * en.g, cr2 = weight * en.b, crd = weight * en.z;
+            const double behind0 = raw0 - sm.p0[s] - cr0;
+            const double behind1 = raw1 - sm.p1[s] - cr1;
+            const double behind2 = raw2 - sm.p2[s] - cr2;
+            const double behindd = rawd - sm.pd[s] - crd;
+            const double g_dot_col = g0 * en.r + g1 * en.g + g2 * en.b;
+            const double g_dot_behind = g0 * behind0 + g1 * behind1 + g2 * behind2;
+            double d_alpha = g_dot_col * my_t - g_dot_behind / (1.0 - alpha);
+            d_alpha = d_alpha + (gd * en.z * my_t - gd * behindd / (1.0 - alpha));
+            float *acc = f.grad_acc + (int64_t)c * kGradStride;
+            atomicAdd(acc + 7, (float)(weight * g0));
+            atomicAdd(acc + 8, (float)(weight * g1));
+            atomicAdd(acc + 9, (float)(weight * g2));
+            atomicAdd(acc + 10, (float)(weight * gd));
+            atomicAdd(acc + 5, (float)(d_alpha * kernel));
+            const double d_kernel = d_alpha * en.o;
+            if (x < 1.0) {
+                atomicAdd(acc + 6, (float)(d_kernel * kernel * log(1.0 - x)));
+                double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
+                if (dkdx < -1e7) dkdx = -1e7;
+                const double d_x = d_kernel * dkdx;
+                atomicAdd(acc + 0, (float)(-d_x * 2.0 * (en.ca * dx + en.cb * dy)));
+                atomicAdd(acc + 1, (float)(-d_x * 2.0 * (en.cb * dx + en.cc * dy)));
+                atomicAdd(acc + 2, (float)(d_x * dx * dx));
+                atomicAdd(acc + 3, (float)(d_x * 2.0 * dx * dy));
+                atomicAdd(acc + 4, (float)(d_x * dy * dy));
+            }
         }
+        __syncthreads();
     }
 }
 
 template <typename P>
 __global__ void __launch_bounds__(BSR_BLOCK) replay_fwd_kernel(ReplayArgs a, P prov) {
-    const uint32_t nwarps = gridDim.x * (BSR_BLOCK / 32);
+    __shared__ ReplaySmem sm;
     const uint32_t n = a.f.ctr->flagged;
-    for (uint32_t slot = (blockIdx.x * BSR_BLOCK + threadIdx.x) >> 5; slot < n; slot += nwarps)
-        replay_fwd_one(a, prov, slot, threadIdx.x & 31);
+    for (uint32_t slot = blockIdx.x; slot < n; slot += gridDim.x) {
+        replay_fwd_one(a, prov, slot, sm);
+        __syncthreads();
+    }
 }
 
 template <typename P>
 __global__ void __launch_bounds__(BSR_BLOCK) replay_bwd_kernel(ReplayArgs a, P prov) {
-    const uint32_t nwarps = gridDim.x * (BSR_BLOCK / 32);
+    __shared__ ReplaySmem sm;
     const uint32_t n = a.f.ctr->flagged;
-    for (uint32_t slot = (blockIdx.x * BSR_BLOCK + threadIdx.x) >> 5; slot < n; slot += nwarps)
-        replay_bwd_one(a, prov, slot, threadIdx.x & 31);
+    for (uint32_t slot = blockIdx.x; slot < n; slot += gridDim.x) {
+        replay_bwd_one(a, prov, slot, sm);
+        __syncthreads();
+    }
 }
 
-static unsigned replay_blocks(const FrameView &f) {
-    // one warp per flagged pixel (grid-stride over the device-side count); the grid is
-    // capped and surplus warps exit immediately.
-    const int64_t warps = (int64_t)f.W * f.H;
-    return (unsigned)imax64(1, imin64(div_up(warps * 32, BSR_BLOCK), 148 * 64));
+static unsigned replay_blocks(const FrameView &) {
+    // one CTA per flagged pixel, grid-stride over the device-side count
+    return 148 * 2;
 }
 
 template <typename P>
@@ -316,10 +383,10 @@ int launch_replay_scene(bool fwd, const FrameView &f, const bsr_scene &sc, const
     a.d_depth = d_depth;
     a.mask_raw = true;
     switch (sc.sh_coeffs) {
-        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec}, st);
-        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec}, st);
-        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec}, st);
-        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec}, st);
+        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec, f.src_of}, st);
+        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec, f.src_of}, st);
+        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec, f.src_of}, st);
+        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec, f.src_of}, st);
         default: return BSR_ERR_BAD_ARG;
     }
 }

@@ -324,16 +324,23 @@ class StageProfiler:
             e.record()
         torch.cuda.synchronize()
         self.fwd = _lib.ProfileC()
-        self.fwd.stats = self.stats.data_ptr()
+        self.fwd.stats = None
         for i, e in enumerate(self.fwd_ev):
             self.fwd.events[i] = e.cuda_event
         self.bwd = _lib.ProfileC()
-        self.bwd.stats = self.stats.data_ptr()
+        self.bwd.stats = None
         for i, e in enumerate(self.bwd_ev):
             self.bwd.events[i] = e.cuda_event
         self.acc = {k: 0.0 for k in self.FWD + self.BWD}
         self.calls_fwd = 0
         self.calls_bwd = 0
+
+    def count_pairs(self, enable: bool):
+        """Pair counting switches the raster culling to the reference's bounds test (so the
+        count is the algorithmic P_f / P_b); use it on untimed steps only."""
+        p = self.stats.data_ptr() if enable else None
+        self.fwd.stats = p
+        self.bwd.stats = p
 
     def collect_forward(self):
         """Accumulate stage times of the last forward (call after a synchronize)."""

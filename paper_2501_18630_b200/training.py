@@ -92,10 +92,14 @@ class AdamState:
         self.step = 0
 
 
-def group_lrs(lr_means=1.6e-4, lr_other=5e-3):
-    """Config-3 learning rates (BASELINE.json configs[3]); per group in GROUPS order."""
+def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
+    """Config-3 learning rates (BASELINE.json configs[3]): 1.6e-4 for means, 5e-3 for the
+    other optimised attributes (quats, scales, opacities, SH).  The configs render the
+    Gaussian-like kernel (b = 0, beta = 4) and do not list the Beta shape among the
+    optimised attributes, so ``shapes`` is frozen by default (lr 0); pass lr_shapes to
+    train it like the reference's full DBS optimiser (training.py:217-227)."""
     return {"positions": lr_means, "rotations": lr_other, "log_scales": lr_other, "opacity_raw": lr_other,
-            "shapes": lr_other, "sh": lr_other}
+            "shapes": lr_shapes, "sh": lr_other}
 
 
 def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict):
