@@ -319,7 +319,8 @@ def kernel_launches_per_step(w):
     tile_passes = 1
     while tile_passes < 4 and (tiles - 1) >= (1 << (8 * tile_passes)):
         tile_passes += 1
-    fwd = 1 + (2 + 8) + 1 + (2 + tile_passes) + 1 + 1 + 1  # pre, depth sort, emit, tile sort, ranges, raster, replay
+    # pre, depth sort (hist, plan, 4 passes, fp64 tie fixup), emit, tile sort, ranges, raster, replay
+    fwd = 1 + (2 + 4 + 1) + 1 + (2 + tile_passes) + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
     per_view = fwd + 3 + 4  # + loss (3) + backward (zero, raster, replay, chain)

@@ -9,7 +9,7 @@ namespace bsr {
 
 constexpr int kSortItems = 16;                       // keys per thread in a sort pass
 constexpr int kSortTile = BSR_BLOCK * kSortItems;    // 4096 keys per partition
-constexpr int kDepthPasses = 8;                      // 64-bit depth keys
+constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
 
 struct Counters {
@@ -22,7 +22,8 @@ struct Counters {
     uint32_t emit_ticket;
     uint32_t depth_ticket[kDepthPasses];
     uint32_t tile_ticket[4];
-    unsigned long long depth_key_max_inv;  // max(~key) == ~min(key)
+    uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
+    uint32_t pad0;
     uint32_t depth_plan[kDepthPasses + 1];
     uint32_t tile_plan[4 + 1];
     uint32_t pad[6];
@@ -31,17 +32,18 @@ struct Counters {
 struct FrameView {
     // --- zeroed every forward (one memset) ---
     Counters *ctr;
-    uint32_t *depth_hist;    // [8][256]
+    uint32_t *depth_hist;    // [4][256]
     uint32_t *tile_hist;     // [4][256]
     uint32_t *pre_status;    // [ceil(N/256)]
-    uint32_t *depth_status;  // [8][ceil(N/4096)][256]
+    uint32_t *depth_status;  // [4][ceil(N/4096)][256]
     unsigned long long *emit_status;  // [ceil(N/4096)]
     uint32_t *tile_status;   // [tile_passes][ceil(Ecap/4096)][256]
     uint2 *tile_ranges;      // [n_tiles] (start, end)
     // --- not zeroed ---
     Record *rec;             // [N] compact order
     uint32_t *src_of;        // [N] compact -> source index (batch.indices)
-    uint64_t *dkeys[2];      // [N] depth keys (ping-pong)
+    uint32_t *dkeys[2];      // [N] fp32-depth keys (ping-pong)
+    uint64_t *dkey64;        // [N] fp64 depth bits, compact order (tie fixup)
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched, compact order
     uint32_t *tkeys[2];      // [Ecap] tile ids (ping-pong)
@@ -99,8 +101,9 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.zero_bytes = off;
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
     f.src_of = (uint32_t *)take(4ull * n);
-    f.dkeys[0] = (uint64_t *)take(8ull * n);
-    f.dkeys[1] = (uint64_t *)take(8ull * n);
+    f.dkeys[0] = (uint32_t *)take(4ull * n);
+    f.dkeys[1] = (uint32_t *)take(4ull * n);
+    f.dkey64 = (uint64_t *)take(8ull * n);
     f.dvals[0] = (uint32_t *)take(4ull * n);
     f.dvals[1] = (uint32_t *)take(4ull * n);
     f.tile_count = (uint32_t *)take(4ull * n);

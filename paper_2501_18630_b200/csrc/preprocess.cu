@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     bool vis = false;
     Record r;
     uint64_t key = 0;
+    uint32_t key32 = 0;
     uint32_t tcount = 0;
     if (i < n) {
         float pos[3] = {__ldg(args.sc.positions + 3 * i), __ldg(args.sc.positions + 3 * i + 1),
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
             r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)r2_error_bound(p));
             r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
             key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
+            key32 = (uint32_t)__float_as_int((float)p.tz);  // monotone rounding of tz
             tcount = (uint32_t)((p.x1 / BSR_TILE - p.x0 / BSR_TILE + 1) *
                                 (p.y1 / BSR_TILE - p.y0 / BSR_TILE + 1));
         }
@@ -98,12 +100,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     const uint32_t local = __popc(ballot & ((1u << lane) - 1));
     if (lane == 0) s_warp[warp] = __popc(ballot);
     // min depth key for the radix plan: max of the complement
-    unsigned long long inv = vis ? ~key : 0ull;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, inv, o);
-        inv = other > inv ? other : inv;
-    }
+    const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
     if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
     __syncthreads();
     if (tid == 0) {
@@ -130,7 +127,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
         const uint32_t c = s_excl + s_warp[warp] + local;
         f.rec[c] = r;
         f.src_of[c] = (uint32_t)i;
-        f.dkeys[0][c] = key;
+        f.dkeys[0][c] = key32;
+        f.dkey64[c] = key;
         f.dvals[0][c] = c;
         f.tile_count[c] = tcount;
     }

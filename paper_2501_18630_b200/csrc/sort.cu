@@ -25,7 +25,7 @@ struct SortArgs {
     K *keys[2];
     uint32_t *vals[2];
     const uint32_t *count;            // device element count
-    const unsigned long long *bias_inv;  // if non-null: bias = ~(*bias_inv) (min key)
+    const uint32_t *bias_inv;         // if non-null: bias = ~(*bias_inv) (min key)
     uint32_t *hist;                   // [passes][256], zeroed; becomes exclusive offsets
     uint32_t *plan;                   // [passes + 1]
     uint32_t *status;                 // [passes][max_parts][256], zeroed
@@ -243,8 +243,38 @@ int launch_sort(const SortArgs<K> &a, int64_t cap, cudaStream_t st) {
     return BSR_OK;
 }
 
+// After sorting the fp32-rounded depths, primitives whose fp32 keys tie are re-ordered by
+// their exact fp64 depth (then compact index): rounding is monotone, so this yields exactly
+// np.argsort(fp64 depths, kind="stable").  Runs of equal fp32 keys are short; the thread
+// at the start of each run insertion-sorts it.
+__global__ void depth_fixup_kernel(FrameView f) {
+    const uint32_t V = f.ctr->visible;
+    const uint32_t sel = f.ctr->depth_plan[kDepthPasses] & 1u;
+    const uint32_t *k = f.dkeys[sel];
+    uint32_t *v = f.dvals[sel];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < V; i += gridDim.x * blockDim.x) {
+        const uint32_t ki = k[i];
+        if (k[i + 1] != ki || (i > 0 && k[i - 1] == ki)) continue;  // not the start of a run
+        uint32_t j = i + 2;
+        while (j < V && k[j] == ki) ++j;
+        for (uint32_t a = i + 1; a < j; ++a) {
+            const uint32_t va = v[a];
+            const uint64_t da = f.dkey64[va];
+            uint32_t b = a;
+            while (b > i) {
+                const uint32_t vb = v[b - 1];
+                const uint64_t db = f.dkey64[vb];
+                if (db < da || (db == da && vb < va)) break;
+                v[b] = vb;
+                --b;
+            }
+            v[b] = va;
+        }
+    }
+}
+
 int launch_depth_sort(const FrameView &f, cudaStream_t st) {
-    SortArgs<uint64_t> a;
+    SortArgs<uint32_t> a;
     a.keys[0] = f.dkeys[0];
     a.keys[1] = f.dkeys[1];
     a.vals[0] = f.dvals[0];
@@ -257,7 +287,13 @@ int launch_depth_sort(const FrameView &f, cudaStream_t st) {
     a.tickets = f.ctr->depth_ticket;
     a.passes = kDepthPasses;
     a.max_parts = f.depth_parts;
-    return launch_sort(a, f.n, st);
+    int rc = launch_sort(a, f.n, st);
+    if (rc) return rc;
+    if (f.n > 1) {
+        depth_fixup_kernel<<<(unsigned)imin64(div_up(f.n, BSR_BLOCK), 148 * 8), BSR_BLOCK, 0, st>>>(f);
+        BSR_LAUNCH_CHECK();
+    }
+    return BSR_OK;
 }
 
 int launch_tile_sort(const FrameView &f, cudaStream_t st) {

@@ -89,6 +89,19 @@ def test_forward_random_scenes(cuda, seed, n, w, h):
     _compare_forward(scene, toy_camera(w, h), np.ones(3), cuda)
 
 
+def test_depth_ties_and_fp32_collisions(cuda):
+    """Exact and fp32-colliding depths: order must equal np.argsort(fp64 depth, stable)."""
+    rng = np.random.default_rng(41)
+    n = 400
+    scene = random_scene(rng, n, degree=0, spread=0.6)
+    # groups of identical depths (index tie-break) and depths 1e-8 apart (same fp32 key)
+    z = np.repeat(rng.uniform(-0.5, 0.5, n // 8), 8).astype(np.float32)
+    z[: n // 2] = (np.arange(n // 2) % 37 * 1e-8).astype(np.float32)
+    rng.shuffle(z)
+    scene.positions[:, 2] = z
+    _compare_forward(scene, toy_camera(64, 64), np.ones(3), cuda)
+
+
 def test_empty_and_culled_scenes(cuda):
     from paper_2501_18630_b200 import render_tiled
 
