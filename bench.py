@@ -218,9 +218,9 @@ def run_step(w, prof=None):
             w["color"] = torch.empty((c.height, c.width, 3), dtype=torch.float32, device="cuda")
             w["frame"] = None
             w["sc"] = _prims_scene_c(w["prims"])
-        for cam in w["cams"]:
+        for i, cam in enumerate(w["cams"]):
             w["frame"] = forward_raw(w["sc"], cam, w["bg"], outputs_c(color=w["color"]), frame=w["frame"],
-                                     check=False, profile=None if prof is None else prof.fwd)
+                                     check=False, profile=None if prof is None else prof.fwd(i))
         return len(w["cams"])
     st = w["step"]
     st.profile = prof
@@ -289,26 +289,21 @@ def e2e_loop(w, steps, world):
 
 
 class BenchProfiler:
-    """Per-step stage times + pair counts from libbsr's profiling hooks (bsr_profile)."""
+    """Per-view stage times + pair counts from libbsr's profiling hooks (bsr_profile)."""
 
-    def __init__(self):
+    def __init__(self, n_views):
         from paper_2501_18630_b200.rasterizer import StageProfiler
 
-        self.sp = StageProfiler()
+        self.sp = StageProfiler(n_views)
 
-    @property
-    def fwd(self):
-        return self.sp.fwd
+    def fwd(self, i):
+        return self.sp.fwd(i)
 
-    @property
-    def bwd(self):
-        return self.sp.bwd
+    def bwd(self, i):
+        return self.sp.bwd(i)
 
     def collect_step(self, w):
-        # one view per step on the profiled path -> events hold this step's stages
-        self.sp.collect_forward()
-        if w["kind"] == "train":
-            self.sp.collect_backward()
+        self.sp.collect_step()
 
 
 def kernel_launches_per_step(w):
@@ -320,7 +315,7 @@ def kernel_launches_per_step(w):
     while tile_passes < 4 and (tiles - 1) >= (1 << (8 * tile_passes)):
         tile_passes += 1
     # pre, depth sort (hist, plan, 4 passes, fp64 tie fixup), emit, tile sort, ranges, raster, replay
-    fwd = 1 + (2 + 4 + 1) + 1 + (2 + tile_passes) + 1 + 1 + 1
+    fwd = 1 + (2 + 4 + 1) + 2 + (2 + tile_passes) + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
     per_view = fwd + 3 + 4  # + loss (3) + backward (zero, raster, replay, chain)
@@ -465,13 +460,16 @@ def main():
     for f in frames:
         frame_status(f)
 
-    prof = BenchProfiler() if len(w["cams"]) == 1 else None
+    prof = BenchProfiler(len(w["cams"]))
     if prof is not None:  # algorithmic pair counts (P_f, P_b) from one untimed step
         prof.sp.count_pairs(True)
         run_step(w, prof)
         torch.cuda.synchronize()
-        pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64)
+        pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64) / len(w["cams"])
         prof.sp.count_pairs(False)
+        prof.sp.collect_step()
+        prof.sp.acc = {k: 0.0 for k in prof.sp.acc}
+        prof.sp.calls_fwd = prof.sp.calls_bwd = 0
     clocks = ClockSampler(local)
     clocks.start()
     ms, views = timed_loop(w, K, world, prof=prof, l2=l2)

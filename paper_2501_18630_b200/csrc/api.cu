@@ -63,7 +63,7 @@ inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
 
 __global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
                                  const double *opac, const double *betas, const double *colors,
-                                 const int32_t *bounds, Record *rec, uint32_t *src_of) {
+                                 const int32_t *bounds, Record *rec, uint32_t *src_of, double *rec64) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
@@ -79,7 +79,17 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     const double S = a * ex * ex + 2.0 * b * ex * ey + c * ey * ey;
     const double kr = 5.9604644775390625e-08 * (8.0 * S + 3.0 * ((a * ex + b * ey) * (2.0 * ex + 3.0) +
                                                                 (b * ex + c * ey) * (2.0 * ey + 3.0))) * 1.5;
-    r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2], (float)kr);
+    const bool unsafe = (float)kr > kUnsafeR2Err;
+    r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
+                      unsafe ? -(float)kr : (float)kr);
+    if (unsafe) {
+        double *d = rec64 + 6 * k;
+        d[0] = means[2 * k];
+        d[1] = means[2 * k + 1];
+        d[2] = ca;
+        d[3] = cb;
+        d[4] = cc;
+    }
     r.d = make_int4(x0, x1, y0, y1);
     rec[k] = r;
     src_of[k] = (uint32_t)k;
@@ -256,7 +266,8 @@ static int core_prepare(const CoreView &c, int64_t v, const double *means, const
     BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
     if (v > 0)
         core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
-                                                                               colors, bounds, c.f.rec, c.f.src_of);
+                                                                               colors, bounds, c.f.rec, c.f.src_of,
+                                                                               c.f.rec64);
     const int64_t m = imax64(n_entries, c.f.n_tiles);
     core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
         offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);

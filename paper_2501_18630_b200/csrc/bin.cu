@@ -13,6 +13,7 @@
 namespace bsr {
 
 constexpr int kEmitItems = 16;
+constexpr uint32_t kBigRect = 64;  // rectangles with more tiles are emitted by a whole CTA
 constexpr int kEmitTile = BSR_BLOCK * kEmitItems;
 constexpr unsigned long long kFlag64Agg = 1ull << 62;
 constexpr unsigned long long kFlag64Prefix = 2ull << 62;
@@ -98,6 +99,12 @@ __global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
     for (int i = 0; i < kEmitItems; ++i) {
         if (cnt[i] == 0) continue;
         if (off + cnt[i] > (unsigned long long)f.entry_cap) return;  // overflow: caller retries
+        if (cnt[i] > kBigRect) {  // load balance: near-plane primitives cover whole frames
+            const uint32_t slot = atomicAdd(&f.ctr->big_emit, 1u);
+            f.big[slot] = make_uint4(cidx[i], (uint32_t)off, (uint32_t)(off >> 32), cnt[i]);
+            off += cnt[i];
+            continue;
+        }
         const int4 bd = f.rec[cidx[i]].d;
         const int tx0 = bd.x / BSR_TILE, tx1 = bd.y / BSR_TILE;
         const int ty0 = bd.z / BSR_TILE, ty1 = bd.w / BSR_TILE;
@@ -110,6 +117,26 @@ __global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
                 vout[j] = cidx[i];
             }
         off += cnt[i];
+    }
+}
+
+// Cooperative emission of the big rectangles queued by emit_kernel: one CTA per rectangle,
+// consecutive threads write consecutive (row-major) entries.
+__global__ void __launch_bounds__(BSR_BLOCK) emit_big_kernel(FrameView f) {
+    const uint32_t nbig = f.ctr->big_emit;
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const uint4 it = f.big[b];
+        const int4 bd = f.rec[it.x].d;
+        const int tx0 = bd.x / BSR_TILE, ty0 = bd.z / BSR_TILE;
+        const uint32_t spanx = (uint32_t)(bd.y / BSR_TILE - tx0 + 1);
+        const unsigned long long off = (unsigned long long)it.y | ((unsigned long long)it.z << 32);
+        uint32_t *kout = f.tkeys[0] + off;
+        uint32_t *vout = f.tvals[0] + off;
+        for (uint32_t j = threadIdx.x; j < it.w; j += BSR_BLOCK) {
+            const uint32_t ty = ty0 + j / spanx, tx = tx0 + j % spanx;
+            kout[j] = ty * (uint32_t)f.tiles_x + tx;
+            vout[j] = it.x;
+        }
     }
 }
 
@@ -127,6 +154,7 @@ __global__ void tile_ranges_kernel(FrameView f) {
 int launch_emit(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
     emit_kernel<<<(unsigned)div_up(f.n, kEmitTile), BSR_BLOCK, 0, st>>>(f);
+    emit_big_kernel<<<148 * 4, BSR_BLOCK, 0, st>>>(f);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

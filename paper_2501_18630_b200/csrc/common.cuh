@@ -60,7 +60,9 @@ inline KCam make_kcam(const bsr_camera &c) {
 //      bounds corner so dx = (px - x0) - rel loses no bits at large pixel coordinates)
 //   B: conic c, opacity, beta, depth z
 //   C: r, g, b, kR = bound on |r2(fp32) - r2(exact)| over the footprint (error analysis,
-//      raster.cuh); the source index lives in FrameView::src_of
+//      raster.cuh); NEGATIVE kR marks an fp32-unsafe (ill-conditioned) primitive whose r2 /
+//      alpha the raster evaluates in fp64 from FrameView::rec64.  The source index lives
+//      in FrameView::src_of.
 //   D: x0, x1, y0, y1 (inclusive pixel bounds, primitive.py:252-262)
 struct __align__(16) Record {
     float4 a, b, c;

@@ -11,6 +11,8 @@ constexpr int kSortItems = 16;                       // keys per thread in a sor
 constexpr int kSortTile = BSR_BLOCK * kSortItems;    // 4096 keys per partition
 constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
+// primitives whose fp32 r2 error bound exceeds this are evaluated in fp64 by the raster
+constexpr float kUnsafeR2Err = 2.0e-5f;
 
 struct Counters {
     uint32_t visible;        // V
@@ -23,7 +25,7 @@ struct Counters {
     uint32_t depth_ticket[kDepthPasses];
     uint32_t tile_ticket[4];
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
-    uint32_t pad0;
+    uint32_t big_emit;           // primitives whose tile rectangle is emitted cooperatively
     uint32_t depth_plan[kDepthPasses + 1];
     uint32_t tile_plan[4 + 1];
     uint32_t pad[6];
@@ -42,10 +44,12 @@ struct FrameView {
     // --- not zeroed ---
     Record *rec;             // [N] compact order
     uint32_t *src_of;        // [N] compact -> source index (batch.indices)
+    double *rec64;           // [N][6] fp64 mean/conic of fp32-unsafe primitives (Record.c.w < 0)
     uint32_t *dkeys[2];      // [N] fp32-depth keys (ping-pong)
     uint64_t *dkey64;        // [N] fp64 depth bits, compact order (tie fixup)
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched, compact order
+    uint4 *big;              // [N] (compact index, entry offset lo, hi, count) of big rects
     uint32_t *tkeys[2];      // [Ecap] tile ids (ping-pong)
     uint32_t *tvals[2];      // [Ecap] compact index (ping-pong)
     float *t_final;          // [H*W]
@@ -101,12 +105,14 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.zero_bytes = off;
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
     f.src_of = (uint32_t *)take(4ull * n);
+    f.rec64 = (double *)take(48ull * n);
     f.dkeys[0] = (uint32_t *)take(4ull * n);
     f.dkeys[1] = (uint32_t *)take(4ull * n);
     f.dkey64 = (uint64_t *)take(8ull * n);
     f.dvals[0] = (uint32_t *)take(4ull * n);
     f.dvals[1] = (uint32_t *)take(4ull * n);
     f.tile_count = (uint32_t *)take(4ull * n);
+    f.big = (uint4 *)take(16ull * n);
     f.tkeys[0] = (uint32_t *)take(4ull * entry_cap);
     f.tkeys[1] = (uint32_t *)take(4ull * entry_cap);
     f.tvals[0] = (uint32_t *)take(4ull * entry_cap);

@@ -36,7 +36,7 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p) {
 template <int K>
 __device__ __forceinline__ void load_sh(const float *sh, int64_t i, float *dst) {
     const float *p = sh + i * (int64_t)K * 3;
-    if constexpr ((K * 3) % 4 == 0) {
+    if ((K * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(sh) & 15) == 0) {
         const float4 *p4 = reinterpret_cast<const float4 *>(p);
 #pragma unroll
         for (int j = 0; j < K * 3 / 4; ++j) {
@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     Record r;
     uint64_t key = 0;
     uint32_t key32 = 0;
+    bool unsafe = false;
+    double m64[5];
     uint32_t tcount = 0;
     if (i < n) {
         float pos[3] = {__ldg(args.sc.positions + 3 * i), __ldg(args.sc.positions + 3 * i + 1),
@@ -87,7 +89,14 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
             const double beta = shape_to_exponent64((double)__ldg(args.sc.shapes + i));
             r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)p.ca, (float)p.cb);
             r.b = make_float4((float)p.cc, (float)o, (float)beta, (float)p.tz);
-            r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)r2_error_bound(p));
+            const float kr = (float)r2_error_bound(p);
+            unsafe = kr > kUnsafeR2Err;
+            r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], unsafe ? -kr : kr);
+            m64[0] = p.mx;
+            m64[1] = p.my;
+            m64[2] = p.ca;
+            m64[3] = p.cb;
+            m64[4] = p.cc;
             r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
             key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
             key32 = (uint32_t)__float_as_int((float)p.tz);  // monotone rounding of tz
@@ -127,6 +136,10 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
         const uint32_t c = s_excl + s_warp[warp] + local;
         f.rec[c] = r;
         f.src_of[c] = (uint32_t)i;
+        if (unsafe) {
+            double *d = f.rec64 + 6 * (int64_t)c;
+            for (int q = 0; q < 5; ++q) d[q] = m64[q];
+        }
         f.dkeys[0][c] = key32;
         f.dkey64[c] = key;
         f.dvals[0][c] = c;

@@ -100,8 +100,14 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
     const float ty = R[3] * px + R[4] * py + R[5] * pz + (float)cam.t[1];
     const float tz = R[6] * px + R[7] * py + R[8] * pz + (float)cam.t[2];
     const float fx = (float)cam.fx, fy = (float)cam.fy;
-    float qw = sc.rotations[4 * i], qx = sc.rotations[4 * i + 1], qy = sc.rotations[4 * i + 2],
-          qz = sc.rotations[4 * i + 3];
+    const bool rot16 = ((reinterpret_cast<uintptr_t>(sc.rotations) | reinterpret_cast<uintptr_t>(a.g.rotations)) & 15) == 0;
+    float4 q4;
+    if (rot16) {
+        q4 = __ldg(reinterpret_cast<const float4 *>(sc.rotations) + i);
+    } else {
+        q4 = make_float4(sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2], sc.rotations[4 * i + 3]);
+    }
+    float qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
     const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
     qw /= qn;
     qx /= qn;
@@ -197,10 +203,21 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
         const float gy = 2.f * (-2.f * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - 2.f * y * g[8]);
         const float gz = 2.f * (-2.f * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2.f * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
         const float dot = gw * w + gx * x + gy * y + gz * z;
-        a.g.rotations[4 * i] += (gw - dot * w) / qn;
-        a.g.rotations[4 * i + 1] += (gx - dot * x) / qn;
-        a.g.rotations[4 * i + 2] += (gy - dot * y) / qn;
-        a.g.rotations[4 * i + 3] += (gz - dot * z) / qn;
+        const float iqn = 1.f / qn;
+        if (rot16) {
+            float4 *gr = reinterpret_cast<float4 *>(a.g.rotations) + i;
+            float4 gq = *gr;
+            gq.x += (gw - dot * w) * iqn;
+            gq.y += (gx - dot * x) * iqn;
+            gq.z += (gy - dot * y) * iqn;
+            gq.w += (gz - dot * z) * iqn;
+            *gr = gq;
+        } else {
+            a.g.rotations[4 * i] += (gw - dot * w) * iqn;
+            a.g.rotations[4 * i + 1] += (gx - dot * x) * iqn;
+            a.g.rotations[4 * i + 2] += (gy - dot * y) * iqn;
+            a.g.rotations[4 * i + 3] += (gz - dot * z) * iqn;
+        }
     }
     // ---- SH colour chain + view direction -> position
     {
@@ -213,17 +230,45 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
         float b[16], db[16][3];
         sh_basis_and_grad<K>(vx, vy, vz, b, db);
         float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+        // coefficients and their gradients move as float4 when a row of K*3 floats is
+        // 16-byte aligned (K = 4, 16); coalescing-friendly vs 3K scalar accesses
+        float shv[3 * K], gsv[3 * K];
         const float *shp = sc.sh + i * 3 * K;
         float *gsh = a.g.sh + i * 3 * K;
+        const bool sh16 = ((reinterpret_cast<uintptr_t>(sc.sh) | reinterpret_cast<uintptr_t>(a.g.sh)) & 15) == 0;
+        if ((3 * K) % 4 == 0 && sh16) {
+#pragma unroll
+            for (int q = 0; q < 3 * K / 4; ++q) {
+                const float4 x4 = __ldg(reinterpret_cast<const float4 *>(shp) + q);
+                const float4 g4 = reinterpret_cast<const float4 *>(gsh)[q];
+                shv[4 * q] = x4.x; shv[4 * q + 1] = x4.y; shv[4 * q + 2] = x4.z; shv[4 * q + 3] = x4.w;
+                gsv[4 * q] = g4.x; gsv[4 * q + 1] = g4.y; gsv[4 * q + 2] = g4.z; gsv[4 * q + 3] = g4.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3 * K; ++q) {
+                shv[q] = __ldg(shp + q);
+                gsv[q] = gsh[q];
+            }
+        }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            gsh[3 * k] += b[k] * dr;
-            gsh[3 * k + 1] += b[k] * dg;
-            gsh[3 * k + 2] += b[k] * dbl;
-            const float dbk = shp[3 * k] * dr + shp[3 * k + 1] * dg + shp[3 * k + 2] * dbl;
+            gsv[3 * k] += b[k] * dr;
+            gsv[3 * k + 1] += b[k] * dg;
+            gsv[3 * k + 2] += b[k] * dbl;
+            const float dbk = shv[3 * k] * dr + shv[3 * k + 1] * dg + shv[3 * k + 2] * dbl;
             ddx += db[k][0] * dbk;
             ddy += db[k][1] * dbk;
             ddz += db[k][2] * dbk;
+        }
+        if ((3 * K) % 4 == 0 && sh16) {
+#pragma unroll
+            for (int q = 0; q < 3 * K / 4; ++q)
+                reinterpret_cast<float4 *>(gsh)[q] =
+                    make_float4(gsv[4 * q], gsv[4 * q + 1], gsv[4 * q + 2], gsv[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3 * K; ++q) gsh[q] = gsv[q];
         }
         const float dd = ddx * vx + ddy * vy + ddz * vz;
         dpx += (ddx - dd * vx) * ivn;

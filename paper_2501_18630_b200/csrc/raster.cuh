@@ -41,6 +41,35 @@ __device__ __forceinline__ Pair eval_pair(const float4 A, const float4 B, int px
     return p;
 }
 
+// fp64 evaluation for fp32-unsafe primitives (record kR < 0): r2 from the fp64 mean/conic
+// side record (preprocess.cu), alpha in fp64, rounded once to fp32.  The fp32 conic form
+// cancels catastrophically for extremely ill-conditioned footprints (near-plane
+// primitives, condition numbers up to ~1e10); fp64 keeps their decisions certifiable.
+__device__ __forceinline__ Pair eval_pair64(const double *m, const float4 B, int px, int py) {
+    Pair p;
+    const double dx = (double)px - m[0], dy = (double)py - m[1];
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(m[2], dx), dx),
+                                          __dmul_rn(__dmul_rn(__dmul_rn(2.0, m[3]), dx), dy)),
+                                __dmul_rn(__dmul_rn(m[4], dy), dy));
+    const double x = fmin(fmax(r2, 0.0), 1.0);
+    const double om = __dadd_rn(1.0, -x);
+    double k;
+    if (B.z == 4.0f) {
+        const double o2 = __dmul_rn(om, om);
+        k = __dmul_rn(o2, o2);
+    } else {
+        k = pow(om, (double)B.z);
+    }
+    p.dx = (float)dx;
+    p.dy = (float)dy;
+    p.r2 = (float)r2;
+    p.x = (float)x;
+    p.om = (float)om;
+    p.k = (float)k;
+    p.alpha = (float)__dmul_rn((double)B.y, k);
+    return p;
+}
+
 // Relative error bound of the (1-x)^beta evaluation itself (inputs exact) + o * k rounding.
 __device__ __forceinline__ float pow_rel_err(float beta) {
     // lg2.approx: <= 2^-22.6 abs on [0.5,2], 2 ulp of |lg2| <= 24 otherwise; ex2.approx 2 ulp;
@@ -52,6 +81,7 @@ __device__ __forceinline__ float pow_rel_err(float beta) {
 // primitive: r2 error (<= kR, per primitive, preprocess.cu) propagated through
 // (1-x)^beta, plus the pow evaluation.  Used on the rare near-threshold paths.
 __device__ __forceinline__ float alpha_rel_err(const float4 B, const float4 C, const Pair &p) {
+    if (C.w < 0.f) return 8.0f * kEps;  // fp64-evaluated primitive
     return B.z * C.w / fmaxf(p.om, 1e-30f) + pow_rel_err(B.z);
 }
 
@@ -88,7 +118,7 @@ __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B
         const float ex = fminf(fmaxf(mx - b * ey * ia, (float)X0), (float)X1) - mx;
         q = fminf(q, a * ex * ex + 2.0f * b * ex * ey + c * ey * ey);
     }
-    return q < 1.0f + 4.0f * C.w + 1e-4f;
+    return q < 1.0f + 4.0f * fabsf(C.w) + 1e-4f;
 }
 
 __device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int Y0, int Y1) {

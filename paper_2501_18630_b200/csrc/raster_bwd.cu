@@ -136,11 +136,11 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
             if (act) {
                 const int4 bd = s_rec[j].d;
                 if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-                const float4 A = s_rec[j].a, Bq = s_rec[j].b;
-                const Pair p = eval_pair(A, Bq, px - bd.x, py - bd.z);
+                const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
+                const double *m64 = C.w < 0.f ? f.rec64 + 6 * (int64_t)s_cidx[j] : nullptr;
+                const Pair p = m64 ? eval_pair64(m64, Bq, px, py) : eval_pair(A, Bq, px - bd.x, py - bd.z);
                 if (p.alpha >= a.alpha_min) {
                     took = true;
-                    const float4 C = s_rec[j].c;
                     const float one_m = 1.0f - p.alpha;
                     T = T / one_m;  // T_k
                     const float w = p.alpha * T;
@@ -164,8 +164,17 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) 
                         float dkdx = -beta * pw;
                         if (dkdx < -kEdgeGradClamp) dkdx = -kEdgeGradClamp;
                         const float d_x = dk * dkdx;
-                        v[0] = -d_x * 2.0f * (A.z * p.dx + A.w * p.dy);
-                        v[1] = -d_x * 2.0f * (A.w * p.dx + Bq.x * p.dy);
+                        float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
+                        if (m64) {
+                            const double dx = (double)px - m64[0], dy = (double)py - m64[1];
+                            ga = (float)(m64[2] * dx + m64[3] * dy);
+                            gb = (float)(m64[3] * dx + m64[4] * dy);
+                        } else {
+                            ga = A.z * p.dx + A.w * p.dy;
+                            gb = A.w * p.dx + Bq.x * p.dy;
+                        }
+                        v[0] = -d_x * 2.0f * ga;
+                        v[1] = -d_x * 2.0f * gb;
                         v[2] = d_x * p.dx * p.dx;
                         v[3] = d_x * 2.0f * p.dx * p.dy;
                         v[4] = d_x * p.dy * p.dy;

@@ -112,21 +112,23 @@ __global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) 
             if (!done) {
                 const int4 bd = s_rec[buf][j].d;
                 if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-                const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b;
-                const Pair p = eval_pair(A, B, px - bd.x, py - bd.z);
+                const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
+                const bool unsafe = C.w < 0.f;
+                const Pair p = unsafe ? eval_pair64(f.rec64 + 6 * (int64_t)s_cidx[buf][j], B, px, py)
+                                      : eval_pair(A, B, px - bd.x, py - bd.z);
                 bool ambiguous = false;
                 // rare path: alpha within 5% of the cutoff -> certify with the error bound
                 if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
-                    const float rel = alpha_rel_err_pixel(A, B, p);
+                    const float rel = unsafe ? 8.0f * kEps : alpha_rel_err_pixel(A, B, p);
                     ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 4.0f * kEps * a.alpha_min;
                 }
                 if (!ambiguous && p.alpha >= a.alpha_min) {
-                    const float4 C = s_rec[buf][j].c;
                     const float one_m = __fsub_rn(1.0f, p.alpha);
                     const float Tn = __fmul_rn(T, one_m);
                     // relative error bound of T: sum over samples of
                     //   alpha/(1-alpha) * rel_err(alpha) + rounding
-                    const float rel = B.z * C.w * __frcp_rn(fmaxf(p.om, 1e-30f)) + pow_rel_err(B.z);
+                    const float rel = unsafe ? 8.0f * kEps
+                                             : B.z * C.w * __frcp_rn(fmaxf(p.om, 1e-30f)) + pow_rel_err(B.z);
                     const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * __frcp_rn(fmaxf(one_m, 1e-30f));
                     if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
                         ambiguous = true;

@@ -31,6 +31,7 @@ def group_layout(n: int, k: int):
     for g in GROUPS:
         out.append((g, off, off + widths[g] * n, shapes[g]))
         off += widths[g] * n
+        off = (off + 3) // 4 * 4  # every group starts 16-byte aligned (float4 access)
     return out, off
 
 
@@ -73,7 +74,7 @@ class PrimitiveSet(FlatGroups):
             if tuple(a.shape)[0] != n:
                 raise ValueError(f"{name} row count mismatch")
         _, total = group_layout(n, k)
-        flat = torch.empty(total, dtype=torch.float32, device=device)
+        flat = torch.zeros(total, dtype=torch.float32, device=device)
         super().__init__(n, k, flat)
         for name, a in arrs.items():
             t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))

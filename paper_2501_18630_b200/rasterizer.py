@@ -310,50 +310,71 @@ def debug_export(frame: FrameState) -> dict:
 
 class StageProfiler:
     """Caller-owned CUDA events + device pair counters for bsr_forward / bsr_backward
-    (bsr_profile in include/bsr.h): per-stage device times and the algorithmic pair
-    counts the raster rooflines are computed from."""
+    (bsr_profile in include/bsr.h): per-stage device times of every view of a step and
+    the algorithmic pair counts the raster rooflines are computed from.  Events are
+    per view, so a multi-view step needs no synchronisation until collect_step()."""
 
     FWD = ("preprocess", "depth_sort", "emit", "tile_sort", "raster_fwd", "replay_fwd")
     BWD = ("raster_bwd", "replay_bwd", "preprocess_bwd")
 
-    def __init__(self, device="cuda"):
+    def __init__(self, n_views=1, device="cuda"):
         self.stats = torch.zeros(4, dtype=torch.int64, device=device)
-        self.fwd_ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        self.bwd_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        for e in self.fwd_ev + self.bwd_ev:  # force creation so the raw handles exist
-            e.record()
+        self.n_views = n_views
+        self.fwd_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(n_views)]
+        self.bwd_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_views)]
+        for v in range(n_views):
+            for e in self.fwd_ev[v] + self.bwd_ev[v]:  # force creation so the raw handles exist
+                e.record()
         torch.cuda.synchronize()
-        self.fwd = _lib.ProfileC()
-        self.fwd.stats = None
-        for i, e in enumerate(self.fwd_ev):
-            self.fwd.events[i] = e.cuda_event
-        self.bwd = _lib.ProfileC()
-        self.bwd.stats = None
-        for i, e in enumerate(self.bwd_ev):
-            self.bwd.events[i] = e.cuda_event
+        self.fwd_p, self.bwd_p = [], []
+        for v in range(n_views):
+            pf, pb = _lib.ProfileC(), _lib.ProfileC()
+            for i, e in enumerate(self.fwd_ev[v]):
+                pf.events[i] = e.cuda_event
+            for i, e in enumerate(self.bwd_ev[v]):
+                pb.events[i] = e.cuda_event
+            self.fwd_p.append(pf)
+            self.bwd_p.append(pb)
         self.acc = {k: 0.0 for k in self.FWD + self.BWD}
         self.calls_fwd = 0
         self.calls_bwd = 0
+        self.used_fwd = set()
+        self.used_bwd = set()
+
+    def fwd(self, view=0):
+        self.used_fwd.add(view)
+        return self.fwd_p[view]
+
+    def bwd(self, view=0):
+        self.used_bwd.add(view)
+        return self.bwd_p[view]
 
     def count_pairs(self, enable: bool):
         """Pair counting switches the raster culling to the reference's bounds test (so the
         count is the algorithmic P_f / P_b); use it on untimed steps only."""
         p = self.stats.data_ptr() if enable else None
-        self.fwd.stats = p
-        self.bwd.stats = p
+        for pf, pb in zip(self.fwd_p, self.bwd_p):
+            pf.stats = p
+            pb.stats = p
 
-    def collect_forward(self):
-        """Accumulate stage times of the last forward (call after a synchronize)."""
-        for i, k in enumerate(self.FWD):
-            self.acc[k] += self.fwd_ev[i].elapsed_time(self.fwd_ev[i + 1])
-        self.calls_fwd += 1
-
-    def collect_backward(self):
-        for i, k in enumerate(self.BWD):
-            self.acc[k] += self.bwd_ev[i].elapsed_time(self.bwd_ev[i + 1])
-        self.calls_bwd += 1
+    def collect_step(self):
+        """Accumulate the stage times of every view recorded since the last call (call after
+        the step completed)."""
+        for v in sorted(self.used_fwd):
+            ev = self.fwd_ev[v]
+            for i, k in enumerate(self.FWD):
+                self.acc[k] += ev[i].elapsed_time(ev[i + 1])
+            self.calls_fwd += 1
+        for v in sorted(self.used_bwd):
+            ev = self.bwd_ev[v]
+            for i, k in enumerate(self.BWD):
+                self.acc[k] += ev[i].elapsed_time(ev[i + 1])
+            self.calls_bwd += 1
+        self.used_fwd.clear()
+        self.used_bwd.clear()
 
     def mean_ms(self):
+        """Mean per-view stage times (ms)."""
         out = {}
         for k in self.FWD:
             out[k] = self.acc[k] / max(self.calls_fwd, 1)

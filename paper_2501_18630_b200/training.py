@@ -149,20 +149,20 @@ class TrainStep:
         return self.frames.get((cam.width, cam.height))
 
     def step(self, check=False, adam=True):
-        prof_f = None if self.profile is None else self.profile.fwd
-        prof_b = None if self.profile is None else self.profile.bwd
+        prof = self.profile
         self.grads.flat.zero_()
         for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
             key = (cam.width, cam.height)
             b = self.bufs[key]
             frame = forward_raw(self.scene, cam, self.background, outputs_c(color=b["color"]),
-                                frame=self._frame(cam), check=check, profile=prof_f)
+                                frame=self._frame(cam), check=check,
+                                profile=None if prof is None else prof.fwd(i))
             self.frames[key] = frame
             ws = self.loss_ws[key]
             loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim)
             self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
-                         profile=prof_b)
+                         profile=None if prof is None else prof.bwd(i))
         if self.pg is not None:
             torch.distributed.all_reduce(self.grads.flat, group=self.pg)
         if adam:

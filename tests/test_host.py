@@ -101,12 +101,14 @@ def test_workloads_are_seeded_and_fp32():
 def test_flat_group_layout():
     from paper_2501_18630_b200.primitive import group_layout
 
-    layout, total = group_layout(10, 16)
-    assert total == 10 * (3 + 4 + 3 + 1 + 1 + 48)
-    names = [g for g, *_ in layout]
-    assert names == ["positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"]
-    sh_start = [a for g, a, *_ in layout if g == "sh"][0]
-    assert (sh_start * 4) % 16 == 0
+    for n in (10, 11, 100_001):
+        layout, total = group_layout(n, 16)
+        assert total >= n * (3 + 4 + 3 + 1 + 1 + 48)
+        names = [g for g, *_ in layout]
+        assert names == ["positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"]
+        for _, a, b, shape in layout:
+            assert (a * 4) % 16 == 0  # float4-aligned group starts
+            assert b - a == int(np.prod(shape))
 
 
 def test_backend_seam_errors():
