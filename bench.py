@@ -106,75 +106,44 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- distributed
 def dist_setup(n_gpus):
-    import torch
+    from paper_2501_18630_b200 import distributed as dd
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        if torch.cuda.is_available():
-            torch.cuda.set_device(0)
-    return rank, world, local
+    return dd.init("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
 
 
 def barrier(world):
     import torch
 
     if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
+        torch.distributed.barrier()
     torch.cuda.synchronize()
 
 
 def max_over_ranks(x, world):
-    import torch
+    from paper_2501_18630_b200 import distributed as dd
 
-    if world == 1:
-        return float(x)
-    import torch.distributed as dist
-
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return dd.max_over_ranks(x) if world > 1 else float(x)
 
 
 def sum_over_ranks(x, world):
-    import torch
+    from paper_2501_18630_b200 import distributed as dd
 
-    if world == 1:
-        return float(x)
-    import torch.distributed as dist
-
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t)
-    return float(t.item())
+    return dd.sum_over_ranks(x) if world > 1 else float(x)
 
 
 # ----------------------------------------------------------------------------- workloads
 def rank_cameras(cfg, rank, world, views_per_gpu):
     """Cameras of this rank.  c1: view r of a y-orbit at radius 4 (rank 0 == config-1
     camera); c3: contiguous share of the 32 config-3 cameras."""
-    from paper_2501_18630_b200.camera import Camera
+    from paper_2501_18630_b200.distributed import orbit_cameras, partition_views
     from paper_2501_18630_b200.scenes import make_workload
 
     if cfg == "c1":
-        cams = []
-        for v in range(views_per_gpu):
-            k = rank * views_per_gpu + v
-            ang = 2 * np.pi * k / max(world * views_per_gpu, 1)
-            eye = (4 * np.sin(ang), 0.0, 4 * np.cos(ang))
-            cams.append(Camera.from_lookat(eye, (0, 0, 0), (0, 1, 0), np.deg2rad(60.0), 800, 800))
-        return cams
+        cams = orbit_cameras(world * views_per_gpu)
+        return [cams[k] for k in partition_views(len(cams), world, rank)]
     if cfg == "c3":
         wl_cams = make_workload("c3", seed=0, n=16).cameras
-        per = len(wl_cams) // world
-        return wl_cams[rank * per:(rank + 1) * per]
+        return [wl_cams[k] for k in partition_views(len(wl_cams), world, rank)]
     return make_workload(cfg, seed=0, n=16).cameras
 
 

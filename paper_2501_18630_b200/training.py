@@ -22,6 +22,7 @@ import torch
 
 from . import _lib
 from .camera import Camera
+from .distributed import allreduce_grads
 from .primitive import GradientBuffer, PrimitiveSet
 from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, forward_raw, frame_status,
                          grads_c, outputs_c)
@@ -163,8 +164,8 @@ class TrainStep:
             self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
                          profile=None if prof is None else prof.bwd(i))
-        if self.pg is not None:
-            torch.distributed.all_reduce(self.grads.flat, group=self.pg)
+        if self.pg is not None:  # the one exchange step of view-batch DP (distributed.py)
+            allreduce_grads(self.grads.flat, group=self.pg)
         if adam:
             adam_step(self.prims, self.grads, self.adam, self.lrs)
         return self.loss_values
