@@ -33,35 +33,116 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p) {
     return 5.9604644775390625e-08 * (8.0 * S + 3.0 * (GX + GY)) * 1.5;
 }
 
+// appearance.py:235-261 in fp32 (the raster's colour is fp32 anyway; the fp64 replay
+// recomputes its own colours with sh_color64).
 template <int K>
-__device__ __forceinline__ void load_sh(const float *sh, int64_t i, float *dst) {
-    const float *p = sh + i * (int64_t)K * 3;
-    if ((K * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(sh) & 15) == 0) {
-        const float4 *p4 = reinterpret_cast<const float4 *>(p);
-#pragma unroll
-        for (int j = 0; j < K * 3 / 4; ++j) {
-            float4 v = __ldg(p4 + j);
-            dst[4 * j] = v.x;
-            dst[4 * j + 1] = v.y;
-            dst[4 * j + 2] = v.z;
-            dst[4 * j + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < K * 3; ++j) dst[j] = __ldg(p + j);
+__device__ __forceinline__ void sh_color32(const float *sh, const float *pos3, const KCam &cam, float rgb[3]) {
+    float x = pos3[0] - (float)cam.center[0], y = pos3[1] - (float)cam.center[1],
+          z = pos3[2] - (float)cam.center[2];
+    const float inv = rsqrtf(x * x + y * y + z * z);
+    x *= inv;
+    y *= inv;
+    z *= inv;
+    float b[16];
+    b[0] = 0.28209479177387814f;
+    if constexpr (K > 1) {
+        const float C1 = 0.4886025119029199f;
+        b[1] = -C1 * y;
+        b[2] = C1 * z;
+        b[3] = -C1 * x;
     }
+    if constexpr (K > 4) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        b[4] = 1.0925484305920792f * x * y;
+        b[5] = -1.0925484305920792f * y * z;
+        b[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+        b[7] = -1.0925484305920792f * x * z;
+        b[8] = 0.5462742152960396f * (xx - yy);
+        if constexpr (K > 9) {
+            b[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+            b[10] = 2.890611442640554f * x * y * z;
+            b[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            b[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+            b[14] = 1.445305721320277f * z * (xx - yy);
+            b[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+        }
+    }
+    float r = 0.f, g = 0.f, bl = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        r = __fmaf_rn(b[k], sh[3 * k], r);
+        g = __fmaf_rn(b[k], sh[3 * k + 1], g);
+        bl = __fmaf_rn(b[k], sh[3 * k + 2], bl);
+    }
+    rgb[0] = r;
+    rgb[1] = g;
+    rgb[2] = bl;
 }
 
+// Shared-memory staging of one CTA's 256 primitives: the parameter blocks are contiguous
+// per CTA, so one elected thread moves them with TMA bulk copies (cp.async.bulk +
+// mbarrier) while the other threads proceed; partial / misaligned blocks fall back to
+// cooperative loads.
 template <int K>
-__global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args) {
+struct PreSmem {
+    float pos[BSR_BLOCK * 3], rot[BSR_BLOCK * 4], ls[BSR_BLOCK * 3], op[BSR_BLOCK], shp[BSR_BLOCK];
+    float sh[BSR_BLOCK * 3 * K];
+};
+
+template <int K>
+__global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs args) {
     const FrameView &f = args.f;
+    extern __shared__ __align__(16) unsigned char pre_smem_raw[];
+    PreSmem<K> &sm = *reinterpret_cast<PreSmem<K> *>(pre_smem_raw);
     __shared__ uint32_t s_part, s_warp[BSR_BLOCK / 32], s_excl;
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ int s_bulk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_part = atomicAdd(&f.ctr->pre_ticket, 1u);
+    const int64_t n = args.sc.n;
+    const bsr_scene &sc = args.sc;
+    if (tid == 0) {
+        const uint32_t part = atomicAdd(&f.ctr->pre_ticket, 1u);
+        s_part = part;
+        const int64_t base = (int64_t)part * BSR_BLOCK;
+        const int64_t cnt = imin64(BSR_BLOCK, n - base);
+        const uintptr_t al = reinterpret_cast<uintptr_t>(sc.positions) | reinterpret_cast<uintptr_t>(sc.rotations) |
+                             reinterpret_cast<uintptr_t>(sc.log_scales) | reinterpret_cast<uintptr_t>(sc.opacity_raw) |
+                             reinterpret_cast<uintptr_t>(sc.shapes) | reinterpret_cast<uintptr_t>(sc.sh);
+        const bool bulk = cnt == BSR_BLOCK && (al & 15) == 0;
+        s_bulk = bulk;
+        if (bulk) {
+            mbar_init(&s_bar, 1);
+            const uint32_t b3 = BSR_BLOCK * 12, b4 = BSR_BLOCK * 16, b1 = BSR_BLOCK * 4, bsh = BSR_BLOCK * 12 * K;
+            mbar_expect_tx(&s_bar, 2 * b3 + b4 + 2 * b1 + bsh);
+            bulk_g2s(sm.pos, sc.positions + 3 * base, b3, &s_bar);
+            bulk_g2s(sm.rot, sc.rotations + 4 * base, b4, &s_bar);
+            bulk_g2s(sm.ls, sc.log_scales + 3 * base, b3, &s_bar);
+            bulk_g2s(sm.op, sc.opacity_raw + base, b1, &s_bar);
+            bulk_g2s(sm.shp, sc.shapes + base, b1, &s_bar);
+            bulk_g2s(sm.sh, sc.sh + 3 * K * base, bsh, &s_bar);
+        }
+    }
     __syncthreads();
     const int64_t part = s_part;
-    const int64_t i = part * BSR_BLOCK + tid;
-    const int64_t n = args.sc.n;
+    const int64_t base = part * BSR_BLOCK;
+    const int64_t i = base + tid;
+    if (s_bulk) {
+        mbar_wait(&s_bar, 0);
+    } else {
+        const int64_t cnt = imin64(BSR_BLOCK, n - base);
+        for (int q = tid; q < cnt * 3; q += BSR_BLOCK) {
+            sm.pos[q] = sc.positions[3 * base + q];
+            sm.ls[q] = sc.log_scales[3 * base + q];
+        }
+        for (int q = tid; q < cnt * 4; q += BSR_BLOCK) sm.rot[q] = sc.rotations[4 * base + q];
+        for (int q = tid; q < cnt; q += BSR_BLOCK) {
+            sm.op[q] = sc.opacity_raw[base + q];
+            sm.shp[q] = sc.shapes[base + q];
+        }
+        for (int q = tid; q < cnt * 3 * K; q += BSR_BLOCK) sm.sh[q] = sc.sh[3 * K * base + q];
+        __syncthreads();
+    }
 
     bool vis = false;
     Record r;
@@ -71,27 +152,20 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     double m64[5];
     uint32_t tcount = 0;
     if (i < n) {
-        float pos[3] = {__ldg(args.sc.positions + 3 * i), __ldg(args.sc.positions + 3 * i + 1),
-                        __ldg(args.sc.positions + 3 * i + 2)};
-        float q[4] = {__ldg(args.sc.rotations + 4 * i), __ldg(args.sc.rotations + 4 * i + 1),
-                      __ldg(args.sc.rotations + 4 * i + 2), __ldg(args.sc.rotations + 4 * i + 3)};
-        float ls[3] = {__ldg(args.sc.log_scales + 3 * i), __ldg(args.sc.log_scales + 3 * i + 1),
-                       __ldg(args.sc.log_scales + 3 * i + 2)};
-        Proj64 p = project64(pos, q, ls, args.cam);
+        const float *pos = sm.pos + 3 * tid;
+        Proj64 p = project64(pos, sm.rot + 4 * tid, sm.ls + 3 * tid, args.cam);
         if (p.degenerate) raise_status(&f.ctr->status, BSR_ERR_DEGENERATE_QUAT);
         if (p.visible) {
             vis = true;
-            float shv[3 * K];
-            load_sh<K>(args.sc.sh, i, shv);
-            double rgb[3];
-            sh_color64<K>(shv, pos, args.cam, rgb);
-            const double o = sigmoid64((double)__ldg(args.sc.opacity_raw + i));
-            const double beta = shape_to_exponent64((double)__ldg(args.sc.shapes + i));
+            float rgb[3];
+            sh_color32<K>(sm.sh + 3 * K * tid, pos, args.cam, rgb);
+            const double o = sigmoid64((double)sm.op[tid]);
+            const double beta = shape_to_exponent64((double)sm.shp[tid]);
             r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)p.ca, (float)p.cb);
             r.b = make_float4((float)p.cc, (float)o, (float)beta, (float)p.tz);
             const float kr = (float)r2_error_bound(p);
             unsafe = kr > kUnsafeR2Err;
-            r.c = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], unsafe ? -kr : kr);
+            r.c = make_float4(rgb[0], rgb[1], rgb[2], unsafe ? -kr : kr);
             m64[0] = p.mx;
             m64[1] = p.my;
             m64[2] = p.ca;
@@ -147,16 +221,32 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_fwd_kernel(PreArgs args)
     }
 }
 
+template <int K>
+static int launch_pre_k(const PreArgs &a, unsigned blocks, cudaStream_t st) {
+    const size_t smem = sizeof(PreSmem<K>);
+    static bool attr = false;
+    if (!attr) {
+        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr = true;
+    }
+    preprocess_fwd_kernel<K><<<blocks, BSR_BLOCK, smem, st>>>(a);
+    return BSR_OK;
+}
+
 int launch_preprocess(const bsr_scene &sc, const KCam &cam, const FrameView &f, cudaStream_t st) {
     if (sc.n == 0) return BSR_OK;
     PreArgs a{sc, cam, f};
+    int rc;
+    const unsigned blocks = (unsigned)f.pre_parts;
     switch (sc.sh_coeffs) {
-        case 1: preprocess_fwd_kernel<1><<<(unsigned)f.pre_parts, BSR_BLOCK, 0, st>>>(a); break;
-        case 4: preprocess_fwd_kernel<4><<<(unsigned)f.pre_parts, BSR_BLOCK, 0, st>>>(a); break;
-        case 9: preprocess_fwd_kernel<9><<<(unsigned)f.pre_parts, BSR_BLOCK, 0, st>>>(a); break;
-        case 16: preprocess_fwd_kernel<16><<<(unsigned)f.pre_parts, BSR_BLOCK, 0, st>>>(a); break;
+        case 1: rc = launch_pre_k<1>(a, blocks, st); break;
+        case 4: rc = launch_pre_k<4>(a, blocks, st); break;
+        case 9: rc = launch_pre_k<9>(a, blocks, st); break;
+        case 16: rc = launch_pre_k<16>(a, blocks, st); break;
         default: return BSR_ERR_BAD_ARG;
     }
+    if (rc) return rc;
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

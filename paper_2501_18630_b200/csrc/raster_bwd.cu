@@ -48,7 +48,7 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-__global__ void __launch_bounds__(BSR_BLOCK) raster_bwd_kernel(RasterBwdArgs a) {
+__global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
     __shared__ __align__(16) Record s_rec[BSR_BLOCK];
     __shared__ uint32_t s_cidx[BSR_BLOCK];
     __shared__ uint8_t s_list[BSR_BLOCK / 32][BSR_BLOCK];

@@ -39,7 +39,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__global__ void __launch_bounds__(BSR_BLOCK) raster_fwd_kernel(RasterFwdArgs a) {
+__global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
     __shared__ uint8_t s_list[BSR_BLOCK / 32][BSR_BLOCK];
