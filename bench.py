@@ -179,6 +179,10 @@ def run_step(w, prof=None):
     """One hot-path step; returns the number of views processed."""
     import torch
 
+    if "graph" in w:  # captured CUDA graph of the whole step (see make_graph)
+        w["graph"].replay()
+        return len(w["cams"])
+
     from paper_2501_18630_b200.rasterizer import _prims_scene_c, forward_raw, outputs_c
 
     if w["kind"] == "render":
@@ -195,6 +199,23 @@ def run_step(w, prof=None):
     st.profile = prof
     st.step(check=False, adam=w["adam"])
     return len(w["cams"])
+
+
+def make_graph(w, prof=None, warmup=2):
+    """Capture one whole step (all views, all kernels, all-reduce, Adam) in a CUDA graph."""
+    import torch
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(warmup):
+            run_step(w, prof)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run_step(w, prof)
+    torch.cuda.synchronize()
+    w["graph"] = g
 
 
 def flush_l2(buf):
@@ -404,6 +425,7 @@ def main():
     ap.add_argument("--views-per-gpu", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph capture of the step")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -439,9 +461,16 @@ def main():
         prof.sp.collect_step()
         prof.sp.acc = {k: 0.0 for k in prof.sp.acc}
         prof.sp.calls_fwd = prof.sp.calls_bwd = 0
+    timed_prof = prof
+    if not args.eager:
+        # per-stage kernel durations: eager steps with libbsr's stage events (kernel time is
+        # the same in and out of a graph; events cannot be timed inside a replayed graph)
+        timed_loop(w, min(K, 20), world, prof=prof, l2=l2)
+        make_graph(w, None)
+        timed_prof = None
     clocks = ClockSampler(local)
     clocks.start()
-    ms, views = timed_loop(w, K, world, prof=prof, l2=l2)
+    ms, views = timed_loop(w, K, world, prof=timed_prof, l2=l2)
     clk = clocks.stop()
     for f in frames:  # any device-side error or capacity overflow invalidates the run
         frame_status(f)
@@ -533,6 +562,7 @@ def main():
                        "parallelism": f"dp{world}" if world > 1 else "single", "l2": "flushed between steps"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernel_launches_per_step(w) * K, "clocks": clk, "extra": extra,
+            "cuda_graph": "graph" in w,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -157,6 +157,12 @@ int bsr_adam_step(float *params, const float *grads, float *exp_avg, float *exp_
                   int64_t count, int32_t n_groups, const int64_t *group_end /* host */,
                   const float *group_lr /* host */, int64_t step, double beta1, double beta2,
                   double eps, void *stream);
+/* Same update with the step count kept in device memory (int64, incremented by the call):
+ * no host value changes between steps, so a captured CUDA graph can replay it. */
+int bsr_adam_step_device(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
+                         int64_t count, int32_t n_groups, const int64_t *group_end /* host */,
+                         const float *group_lr /* host */, int64_t *step_counter, double beta1,
+                         double beta2, double eps, void *stream);
 
 /* ---- parity / debug: export the binning of the last forward (synchronises) ---------- */
 /* order (V): compact index per depth rank (== np.argsort(depths, kind="stable"),

@@ -92,6 +92,8 @@ EXPORTS = {
                                    c_void_p, c_void_p, c_void_p, c_void_p]),
     "bsr_adam_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
                                 c_void_p, c_int64, c_double, c_double, c_double, c_void_p]),
+    "bsr_adam_step_device": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
+                                       c_void_p, c_void_p, c_double, c_double, c_double, c_void_p]),
 }
 
 _LIB = None

@@ -18,6 +18,8 @@ struct AdamArgs {
     int64_t end[kMaxGroups];
     float lr[kMaxGroups];
     float b1, b2, omb1, omb2, inv_c1, inv_c2, eps;
+    const int64_t *step_dev;  // device step counter (graph-capturable variant) or nullptr
+    double beta1, beta2;
 };
 
 __device__ __forceinline__ float group_lr(const AdamArgs &a, int64_t i) {
@@ -35,6 +37,11 @@ __device__ __forceinline__ void adam1(const AdamArgs &a, float &p, float g, floa
 }
 
 __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
+    if (a.step_dev) {  // bias corrections from the device-side step (next value)
+        const double st = (double)(*a.step_dev + 1);
+        a.inv_c1 = (float)(1.0 / (1.0 - pow(a.beta1, st)));
+        a.inv_c2 = (float)(1.0 / (1.0 - pow(a.beta2, st)));
+    }
     const int64_t n4 = a.count / 4;
     const int64_t stride = (int64_t)gridDim.x * BSR_BLOCK;
     for (int64_t q = blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x; q < n4; q += stride) {
@@ -56,15 +63,17 @@ __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
         adam1(a, a.p[tail], a.g[tail], a.m[tail], a.v[tail], group_lr(a, tail));
 }
 
+__global__ void adam_bump_kernel(int64_t *step) { *step += 1; }
+
 }  // namespace bsr
 
 using namespace bsr;
 
-extern "C" int bsr_adam_step(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
-                             int64_t count, int32_t n_groups, const int64_t *group_end,
-                             const float *group_lr, int64_t step, double beta1, double beta2,
-                             double eps, void *stream) {
-    if (count < 0 || n_groups < 1 || n_groups > kMaxGroups || step < 1 || !group_end || !group_lr)
+static int adam_impl(float *params, const float *grads, float *exp_avg, float *exp_avg_sq, int64_t count,
+                     int32_t n_groups, const int64_t *group_end, const float *group_lr, int64_t step,
+                     int64_t *step_dev, double beta1, double beta2, double eps, void *stream) {
+    if (count < 0 || n_groups < 1 || n_groups > kMaxGroups || (!step_dev && step < 1) || !group_end ||
+        !group_lr)
         return BSR_ERR_BAD_ARG;
     if (count == 0) return BSR_OK;
     if (((uintptr_t)params | (uintptr_t)grads | (uintptr_t)exp_avg | (uintptr_t)exp_avg_sq) & 15)
@@ -84,12 +93,33 @@ extern "C" int bsr_adam_step(float *params, const float *grads, float *exp_avg, 
     a.b2 = (float)beta2;
     a.omb1 = (float)(1.0 - beta1);
     a.omb2 = (float)(1.0 - beta2);
-    a.inv_c1 = (float)(1.0 / (1.0 - pow(beta1, (double)step)));
-    a.inv_c2 = (float)(1.0 / (1.0 - pow(beta2, (double)step)));
+    a.inv_c1 = step_dev ? 1.f : (float)(1.0 / (1.0 - pow(beta1, (double)step)));
+    a.inv_c2 = step_dev ? 1.f : (float)(1.0 / (1.0 - pow(beta2, (double)step)));
     a.eps = (float)eps;
+    a.step_dev = step_dev;
+    a.beta1 = beta1;
+    a.beta2 = beta2;
     const int64_t n4 = count / 4;
     const unsigned blocks = (unsigned)imax64(1, imin64(div_up(imax64(n4, 1), BSR_BLOCK), 148 * 8));
     adam_kernel<<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
+    if (step_dev) adam_bump_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_dev);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
+}
+
+extern "C" int bsr_adam_step(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
+                             int64_t count, int32_t n_groups, const int64_t *group_end,
+                             const float *group_lr, int64_t step, double beta1, double beta2,
+                             double eps, void *stream) {
+    return adam_impl(params, grads, exp_avg, exp_avg_sq, count, n_groups, group_end, group_lr, step, nullptr,
+                     beta1, beta2, eps, stream);
+}
+
+extern "C" int bsr_adam_step_device(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
+                                    int64_t count, int32_t n_groups, const int64_t *group_end,
+                                    const float *group_lr, int64_t *step_counter, double beta1,
+                                    double beta2, double eps, void *stream) {
+    if (!step_counter) return BSR_ERR_BAD_ARG;
+    return adam_impl(params, grads, exp_avg, exp_avg_sq, count, n_groups, group_end, group_lr, 0, step_counter,
+                     beta1, beta2, eps, stream);
 }

@@ -82,14 +82,15 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     const bool unsafe = (float)kr > kUnsafeR2Err;
     r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
                       unsafe ? -(float)kr : (float)kr);
-    if (unsafe) {
-        double *d = rec64 + 6 * k;
-        d[0] = means[2 * k];
-        d[1] = means[2 * k + 1];
-        d[2] = ca;
-        d[3] = cb;
-        d[4] = cc;
-    }
+    double *d = rec64 + kRec64 * k;
+    d[0] = means[2 * k];
+    d[1] = means[2 * k + 1];
+    d[2] = ca;
+    d[3] = cb;
+    d[4] = cc;
+    d[5] = opac[k];
+    d[6] = betas[k];
+    d[7] = 0.0;
     r.d = make_int4(x0, x1, y0, y1);
     rec[k] = r;
     src_of[k] = (uint32_t)k;

@@ -10,6 +10,7 @@ namespace bsr {
 constexpr int kSortItems = 16;                       // keys per thread in a sort pass
 constexpr int kSortTile = BSR_BLOCK * kSortItems;    // 4096 keys per partition
 constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
+constexpr int kRec64 = 8;                            // doubles per fp64 side record
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
 // primitives whose fp32 r2 error bound exceeds this are evaluated in fp64 by the raster
 constexpr float kUnsafeR2Err = 2.0e-5f;
@@ -44,7 +45,9 @@ struct FrameView {
     // --- not zeroed ---
     Record *rec;             // [N] compact order
     uint32_t *src_of;        // [N] compact -> source index (batch.indices)
-    double *rec64;           // [N][6] fp64 mean/conic of fp32-unsafe primitives (Record.c.w < 0)
+    double *rec64;           // [N][8] fp64 {mean x, y, conic a, b, c, opacity, beta, depth}:
+                             // the fp64 replay's geometry and the raster's path for fp32-unsafe
+                             // primitives (Record.c.w < 0)
     uint32_t *dkeys[2];      // [N] fp32-depth keys (ping-pong)
     uint64_t *dkey64;        // [N] fp64 depth bits, compact order (tie fixup)
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
@@ -105,7 +108,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.zero_bytes = off;
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
     f.src_of = (uint32_t *)take(4ull * n);
-    f.rec64 = (double *)take(48ull * n);
+    f.rec64 = (double *)take(8ull * kRec64 * n);
     f.dkeys[0] = (uint32_t *)take(4ull * n);
     f.dkeys[1] = (uint32_t *)take(4ull * n);
     f.dkey64 = (uint64_t *)take(8ull * n);

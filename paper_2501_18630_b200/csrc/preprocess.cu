@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     uint64_t key = 0;
     uint32_t key32 = 0;
     bool unsafe = false;
-    double m64[5];
+    double m64[kRec64];
     uint32_t tcount = 0;
     if (i < n) {
         const float *pos = sm.pos + 3 * tid;
@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
             m64[2] = p.ca;
             m64[3] = p.cb;
             m64[4] = p.cc;
+            m64[5] = o;
+            m64[6] = beta;
+            m64[7] = p.tz;
             r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
             key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
             key32 = (uint32_t)__float_as_int((float)p.tz);  // monotone rounding of tz
@@ -210,10 +213,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         const uint32_t c = s_excl + s_warp[warp] + local;
         f.rec[c] = r;
         f.src_of[c] = (uint32_t)i;
-        if (unsafe) {
-            double *d = f.rec64 + 6 * (int64_t)c;
-            for (int q = 0; q < 5; ++q) d[q] = m64[q];
-        }
+        double4 *d = reinterpret_cast<double4 *>(f.rec64 + kRec64 * (int64_t)c);
+        d[0] = make_double4(m64[0], m64[1], m64[2], m64[3]);
+        d[1] = make_double4(m64[4], m64[5], m64[6], m64[7]);
         f.dkeys[0][c] = key32;
         f.dkey64[c] = key;
         f.dvals[0][c] = c;

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                 const int4 bd = s_rec[j].d;
                 if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
-                const double *m64 = C.w < 0.f ? f.rec64 + 6 * (int64_t)s_cidx[j] : nullptr;
+                const double *m64 = C.w < 0.f ? f.rec64 + kRec64 * (int64_t)s_cidx[j] : nullptr;
                 const Pair p = m64 ? eval_pair64(m64, Bq, px, py) : eval_pair(A, Bq, px - bd.x, py - bd.z);
                 if (p.alpha >= a.alpha_min) {
                     took = true;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
                 if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
                 const bool unsafe = C.w < 0.f;
-                const Pair p = unsafe ? eval_pair64(f.rec64 + 6 * (int64_t)s_cidx[buf][j], B, px, py)
+                const Pair p = unsafe ? eval_pair64(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py)
                                       : eval_pair(A, B, px - bd.x, py - bd.z);
                 bool ambiguous = false;
                 // rare path: alpha within 5% of the cutoff -> certify with the error bound

@@ -28,24 +28,23 @@ struct SceneProvider {
     KCam cam;
     const Record *rec;
     const uint32_t *src_of;
+    const double *rec64;
+    // fp64 geometry written by preprocess (project64, the same code and bits as the
+    // reference restatement); only the colour is recomputed, for candidates
     __device__ __forceinline__ bool get(uint32_t c, int px, int py, Entry64 &e) const {
         const int4 bd = rec[c].d;
         if (px < bd.x || px > bd.y || py < bd.z || py > bd.w) return false;
-        const int64_t i = src_of[c];
-        const float pos[3] = {sc.positions[3 * i], sc.positions[3 * i + 1], sc.positions[3 * i + 2]};
-        const float q[4] = {sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2],
-                            sc.rotations[4 * i + 3]};
-        const float ls[3] = {sc.log_scales[3 * i], sc.log_scales[3 * i + 1], sc.log_scales[3 * i + 2]};
-        const Proj64 p = project64(pos, q, ls, cam);
-        e.mx = p.mx;
-        e.my = p.my;
-        e.ca = p.ca;
-        e.cb = p.cb;
-        e.cc = p.cc;
-        e.o = sigmoid64((double)sc.opacity_raw[i]);
-        e.beta = shape_to_exponent64((double)sc.shapes[i]);
-        e.z = p.tz;
-        e.src = (int)i;
+        const double4 *d = reinterpret_cast<const double4 *>(rec64 + kRec64 * (int64_t)c);
+        const double4 d0 = d[0], d1 = d[1];
+        e.mx = d0.x;
+        e.my = d0.y;
+        e.ca = d0.z;
+        e.cb = d0.w;
+        e.cc = d1.x;
+        e.o = d1.y;
+        e.beta = d1.z;
+        e.z = d1.w;
+        e.src = (int)src_of[c];
         return true;
     }
     // colour only for samples that pass the alpha cutoff
@@ -383,10 +382,10 @@ int launch_replay_scene(bool fwd, const FrameView &f, const bsr_scene &sc, const
     a.d_depth = d_depth;
     a.mask_raw = true;
     switch (sc.sh_coeffs) {
-        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec, f.src_of}, st);
-        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec, f.src_of}, st);
-        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec, f.src_of}, st);
-        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec, f.src_of}, st);
+        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec, f.src_of, f.rec64}, st);
+        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec, f.src_of, f.rec64}, st);
+        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec, f.src_of, f.rec64}, st);
+        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec, f.src_of, f.rec64}, st);
         default: return BSR_ERR_BAD_ARG;
     }
 }

@@ -91,6 +91,8 @@ class AdamState:
         self.exp_avg = torch.zeros_like(prims.flat)
         self.exp_avg_sq = torch.zeros_like(prims.flat)
         self.step = 0
+        # device-side step counter for graph-captured steps (bsr_adam_step_device)
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=prims.flat.device)
 
 
 def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
@@ -103,15 +105,26 @@ def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
             "shapes": lr_shapes, "sh": lr_other}
 
 
-def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict):
-    """training.py:258-273 as one fused kernel over the flat buffers."""
-    state.step += 1
+def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict,
+              device_step: bool = False):
+    """training.py:258-273 as one fused kernel over the flat buffers.
+
+    ``device_step`` keeps the step count on the device (graph-capturable); the host-side
+    ``state.step`` then only counts calls made outside captured graphs."""
     ends = (ctypes.c_int64 * 6)(*prims.group_ends())
     lr = (ctypes.c_float * 6)(*[float(lrs[g]) for g in ("positions", "rotations", "log_scales",
                                                           "opacity_raw", "shapes", "sh")])
-    rc = _lib.load().bsr_adam_step(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
-                                   state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr, state.step,
-                                   ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
+    lib = _lib.load()
+    if device_step:
+        rc = lib.bsr_adam_step_device(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
+                                      state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr,
+                                      state.step_dev.data_ptr(), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
+    else:
+        state.step += 1
+        state.step_dev.fill_(state.step)
+        rc = lib.bsr_adam_step(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
+                               state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr, state.step,
+                               ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
     _lib.check(rc, "adam")
     return prims
 
@@ -167,7 +180,26 @@ class TrainStep:
         if self.pg is not None:  # the one exchange step of view-batch DP (distributed.py)
             allreduce_grads(self.grads.flat, group=self.pg)
         if adam:
-            adam_step(self.prims, self.grads, self.adam, self.lrs)
+            adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True)
+        return self.loss_values
+
+    def capture(self, adam=True, warmup=2):
+        """Capture one whole step (every view's fwd + loss + bwd [+ all-reduce] + Adam) in a
+        CUDA graph: ~30 kernel launches become one graph launch.  Frames must already be
+        sized (run step(check=True) once first); capacity is re-checked by check_frames()."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.step(check=False, adam=adam)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.step(check=False, adam=adam)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
         return self.loss_values
 
     def check_frames(self):
