@@ -231,6 +231,10 @@ def timed_loop(w, steps, world, prof=None, l2=None):
     for _ in range(steps):
         if l2 is not None:
             flush_l2(l2)
+        if prof is not None and "graph" not in w:
+            # profiled eager steps: a ~10 ms spin kernel lets the host enqueue the whole step
+            # before the GPU reaches it, so stage events measure device time, not launch gaps
+            torch.cuda._sleep(20_000_000)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         views += run_step(w, prof)
@@ -285,6 +289,12 @@ class BenchProfiler:
         from paper_2501_18630_b200.rasterizer import StageProfiler
 
         self.sp = StageProfiler(n_views)
+
+    def mark_loss(self, i, end=False):
+        self.sp.mark_loss(i, end)
+
+    def mark_adam(self, end=False):
+        self.sp.mark_adam(end)
 
     def fwd(self, i):
         return self.sp.fwd(i)
@@ -459,8 +469,7 @@ def main():
         pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64) / len(w["cams"])
         prof.sp.count_pairs(False)
         prof.sp.collect_step()
-        prof.sp.acc = {k: 0.0 for k in prof.sp.acc}
-        prof.sp.calls_fwd = prof.sp.calls_bwd = 0
+        prof.sp.reset()
     timed_prof = prof
     if not args.eager:
         # per-stage kernel durations: eager steps with libbsr's stage events (kernel time is
@@ -518,6 +527,11 @@ def main():
         hbm["tile_sort"] = (E * 8 * 2 * 2) / (stages["tile_sort"] * 1e-3) / 1e9
         if w["kind"] == "train":
             hbm["preprocess_bwd"] = V * (48 + 240 + 480) / (stages["preprocess_bwd"] * 1e-3) / 1e9
+            cam0 = w["cams"][0]
+            if stages.get("loss", 0) > 0:
+                hbm["loss"] = 12 * 3 * cam0.width * cam0.height * 4 / (stages["loss"] * 1e-3) / 1e9
+            if stages.get("adam", 0) > 0:
+                hbm["adam"] = 28 * w["prims"].flat.numel() / (stages["adam"] * 1e-3) / 1e9
         extra["hbm_stage_gbs"] = {k: round(v, 1) for k, v in hbm.items()}
         extra["visible"], extra["entries"], extra["flagged_pixels"] = V, E, info["flagged_pixels"]
         if dom in rf:

@@ -21,14 +21,15 @@ struct LossArgs {
     const float *a, *b, *raw;
     float *dmu, *dqa, *dqab;  // scratch maps (H,W,3)
     float *d_image;
-    double *sums;             // [2]: sum of ssim map, sum |a-b|
+    double *sums;             // [2][nblocks]: per-block sums of the ssim map and |a - b|
+    int nblocks;
     double *loss_out;         // [3]
     int W, H;
     float w[11];
     double lambda;
 };
 
-__global__ void __launch_bounds__(256) ssim_maps_kernel(LossArgs p) {
+__global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     __shared__ float sa[kLI][kLI], sb[kLI][kLI];
     __shared__ float h[5][kLI][kLT];
     __shared__ double red[2][8];
@@ -105,18 +106,19 @@ __global__ void __launch_bounds__(256) ssim_maps_kernel(LossArgs p) {
         red[1][t >> 5] = l1_sum;
     }
     __syncthreads();
-    if (t == 0) {
+    if (t == 0) {  // per-block partials (no same-address atomics across 1e3+ blocks)
         double s = 0, l = 0;
         for (int i = 0; i < 8; ++i) {
             s += red[0][i];
             l += red[1][i];
         }
-        atomicAdd(p.sums, s);
-        atomicAdd(p.sums + 1, l);
+        const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+        p.sums[blk] = s;
+        p.sums[p.nblocks + blk] = l;
     }
 }
 
-__global__ void __launch_bounds__(256) ssim_grad_kernel(LossArgs p) {
+__global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
     __shared__ float s[3][kLI][kLI];
     __shared__ float h[3][kLI][kLT];
     const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
@@ -173,12 +175,35 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(LossArgs p) {
     }
 }
 
-__global__ void loss_finish_kernel(LossArgs p) {
-    const double n = 3.0 * p.W * p.H;
-    const double ssim = p.sums[0] / n, l1 = p.sums[1] / n;
-    p.loss_out[0] = (1.0 - p.lambda) * l1 + p.lambda * (1.0 - ssim);
-    p.loss_out[1] = l1;
-    p.loss_out[2] = ssim;
+__global__ void __launch_bounds__(256) loss_finish_kernel(LossArgs p) {
+    __shared__ double red[2][8];
+    double sv = 0, l = 0;
+    for (int i = threadIdx.x; i < p.nblocks; i += 256) {
+        sv += p.sums[i];
+        l += p.sums[p.nblocks + i];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sv;
+        red[1][threadIdx.x >> 5] = l;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sv = l = 0;
+        for (int i = 0; i < 8; ++i) {
+            sv += red[0][i];
+            l += red[1][i];
+        }
+        const double n = 3.0 * p.W * p.H;
+        const double ssim = sv / n, l1 = l / n;
+        p.loss_out[0] = (1.0 - p.lambda) * l1 + p.lambda * (1.0 - ssim);
+        p.loss_out[1] = l1;
+        p.loss_out[2] = ssim;
+    }
 }
 
 }  // namespace bsr
@@ -187,7 +212,8 @@ using namespace bsr;
 
 extern "C" int bsr_loss_scratch_bytes(int32_t width, int32_t height, uint64_t *bytes) {
     if (!bytes || width < 11 || height < 11) return BSR_ERR_BAD_ARG;
-    *bytes = align_up(3ull * 4 * 3 * (uint64_t)width * height, 256) + 256;
+    const uint64_t nb = (uint64_t)div_up(width, kLT) * div_up(height, kLT);
+    *bytes = align_up(3ull * 4 * 3 * (uint64_t)width * height, 256) + align_up(16ull * nb, 256);
     return BSR_OK;
 }
 
@@ -202,8 +228,9 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     LossArgs p;
     const uint64_t plane = 3ull * width * height;
     char *base = (char *)scratch;
+    p.nblocks = (int)(div_up(width, kLT) * div_up(height, kLT));
     p.sums = (double *)base;
-    p.dmu = (float *)(base + 256);
+    p.dmu = (float *)(base + align_up(16ull * p.nblocks, 256));
     p.dqa = p.dmu + plane;
     p.dqab = p.dqa + plane;
     p.a = rendered;
@@ -221,11 +248,10 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
         sum += w[i];
     }
     for (int i = 0; i < 11; ++i) p.w[i] = (float)(w[i] / sum);
-    BSR_CUDA_TRY(cudaMemsetAsync(p.sums, 0, 2 * sizeof(double), st));
     dim3 grid((unsigned)div_up(width, kLT), (unsigned)div_up(height, kLT));
     ssim_maps_kernel<<<grid, 256, 0, st>>>(p);
     ssim_grad_kernel<<<grid, 256, 0, st>>>(p);
-    loss_finish_kernel<<<1, 1, 0, st>>>(p);
+    loss_finish_kernel<<<1, 256, 0, st>>>(p);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -316,6 +316,7 @@ class StageProfiler:
 
     FWD = ("preprocess", "depth_sort", "emit", "tile_sort", "raster_fwd", "replay_fwd")
     BWD = ("raster_bwd", "replay_bwd", "preprocess_bwd")
+    EXTRA = ("loss", "adam")
 
     def __init__(self, n_views=1, device="cuda"):
         self.stats = torch.zeros(4, dtype=torch.int64, device=device)
@@ -335,11 +336,28 @@ class StageProfiler:
                 pb.events[i] = e.cuda_event
             self.fwd_p.append(pf)
             self.bwd_p.append(pb)
-        self.acc = {k: 0.0 for k in self.FWD + self.BWD}
+        # torch-side events around the loss (per view) and the optimizer step
+        self.loss_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                        for _ in range(n_views)]
+        self.adam_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.acc = {k: 0.0 for k in self.FWD + self.BWD + self.EXTRA}
+        self.calls = {k: 0 for k in self.EXTRA}
         self.calls_fwd = 0
         self.calls_bwd = 0
         self.used_fwd = set()
         self.used_bwd = set()
+        self.used_loss = set()
+        self.used_adam = False
+
+    def mark_loss(self, view, end=False):
+        self.loss_ev[view][1 if end else 0].record()
+        if end:
+            self.used_loss.add(view)
+
+    def mark_adam(self, end=False):
+        self.adam_ev[1 if end else 0].record()
+        if end:
+            self.used_adam = True
 
     def fwd(self, view=0):
         self.used_fwd.add(view)
@@ -370,8 +388,16 @@ class StageProfiler:
             for i, k in enumerate(self.BWD):
                 self.acc[k] += ev[i].elapsed_time(ev[i + 1])
             self.calls_bwd += 1
+        for v in sorted(self.used_loss):
+            self.acc["loss"] += self.loss_ev[v][0].elapsed_time(self.loss_ev[v][1])
+            self.calls["loss"] += 1
+        if self.used_adam:
+            self.acc["adam"] += self.adam_ev[0].elapsed_time(self.adam_ev[1])
+            self.calls["adam"] += 1
         self.used_fwd.clear()
         self.used_bwd.clear()
+        self.used_loss.clear()
+        self.used_adam = False
 
     def mean_ms(self):
         """Mean per-view stage times (ms)."""
@@ -380,4 +406,11 @@ class StageProfiler:
             out[k] = self.acc[k] / max(self.calls_fwd, 1)
         for k in self.BWD:
             out[k] = self.acc[k] / max(self.calls_bwd, 1)
+        for k in self.EXTRA:
+            out[k] = self.acc[k] / max(self.calls[k], 1)
         return out
+
+    def reset(self):
+        self.acc = {k: 0.0 for k in self.acc}
+        self.calls = {k: 0 for k in self.EXTRA}
+        self.calls_fwd = self.calls_bwd = 0

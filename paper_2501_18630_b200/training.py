@@ -173,14 +173,22 @@ class TrainStep:
                                 profile=None if prof is None else prof.fwd(i))
             self.frames[key] = frame
             ws = self.loss_ws[key]
+            if prof is not None:
+                prof.mark_loss(i)
             loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim)
+            if prof is not None:
+                prof.mark_loss(i, end=True)
             self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
                          profile=None if prof is None else prof.bwd(i))
         if self.pg is not None:  # the one exchange step of view-batch DP (distributed.py)
             allreduce_grads(self.grads.flat, group=self.pg)
         if adam:
+            if prof is not None:
+                prof.mark_adam()
             adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True)
+            if prof is not None:
+                prof.mark_adam(end=True)
         return self.loss_values
 
     def capture(self, adam=True, warmup=2):
