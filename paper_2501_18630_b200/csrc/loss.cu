@@ -30,7 +30,7 @@ struct LossArgs {
 };
 
 __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
-    __shared__ float sa[kLI][kLI], sb[kLI][kLI];
+    __shared__ float sa[3][kLI][kLI], sb[3][kLI][kLI];
     __shared__ float h[5][kLI][kLT];
     __shared__ double red[2][8];
     const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
@@ -38,15 +38,16 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     const int x = tx0 + lx, y = ty0 + ly;
     const bool in = x < p.W && y < p.H;
     double s_sum = 0.0, l1_sum = 0.0;
+    // all three channels of the halo tile at once: one global-latency exposure per block
+    for (int i = t; i < kLI * kLI * 3; i += 256) {
+        const int px = i / 3, c = i - px * 3;
+        const int yy = ty0 - kHalo + px / kLI, xx = tx0 - kHalo + px % kLI;
+        const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
+        const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
+        sa[c][px / kLI][px % kLI] = ok ? p.a[o] : 0.f;
+        sb[c][px / kLI][px % kLI] = ok ? p.b[o] : 0.f;
+    }
     for (int c = 0; c < 3; ++c) {
-        __syncthreads();
-        for (int i = t; i < kLI * kLI; i += 256) {
-            const int yy = ty0 - kHalo + i / kLI, xx = tx0 - kHalo + i % kLI;
-            const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
-            const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
-            sa[i / kLI][i % kLI] = ok ? p.a[o] : 0.f;
-            sb[i / kLI][i % kLI] = ok ? p.b[o] : 0.f;
-        }
         __syncthreads();
         // horizontal pass over all kLI rows, kLT output columns
         for (int i = t; i < kLI * kLT; i += 256) {
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
             float m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
 #pragma unroll
             for (int k = 0; k < 11; ++k) {
-                const float av = sa[r][col + k], bv = sb[r][col + k], wk = p.w[k];
+                const float av = sa[c][r][col + k], bv = sb[c][r][col + k], wk = p.w[k];
                 m0 += wk * av;
                 m1 += wk * bv;
                 m2 += wk * av * av;
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
             p.dqa[o] = -s / b2;
             p.dqab[o] = 2.f * a1 * ib;
             s_sum += s;
-            l1_sum += fabsf(sa[ly + kHalo][lx + kHalo] - sb[ly + kHalo][lx + kHalo]);
+            l1_sum += fabsf(sa[c][ly + kHalo][lx + kHalo] - sb[c][ly + kHalo][lx + kHalo]);
         }
     }
     // block reduction of the two sums
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
 }
 
 __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
-    __shared__ float s[3][kLI][kLI];
+    __shared__ float s[3][3][kLI][kLI];
     __shared__ float h[3][kLI][kLT];
     const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
     const int t = threadIdx.x, lx = t % kLT, ly = t / kLT;
@@ -128,16 +129,16 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
     const double n = 3.0 * p.W * p.H;
     const float inv_n = (float)(1.0 / n);
     const float l1w = (float)((1.0 - p.lambda) / n), sw = (float)p.lambda;
+    for (int i = t; i < kLI * kLI * 3; i += 256) {
+        const int px = i / 3, c = i - px * 3;
+        const int yy = ty0 - kHalo + px / kLI, xx = tx0 - kHalo + px % kLI;
+        const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
+        const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
+        s[c][0][px / kLI][px % kLI] = ok ? p.dmu[o] : 0.f;
+        s[c][1][px / kLI][px % kLI] = ok ? p.dqa[o] : 0.f;
+        s[c][2][px / kLI][px % kLI] = ok ? p.dqab[o] : 0.f;
+    }
     for (int c = 0; c < 3; ++c) {
-        __syncthreads();
-        for (int i = t; i < kLI * kLI; i += 256) {
-            const int yy = ty0 - kHalo + i / kLI, xx = tx0 - kHalo + i % kLI;
-            const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
-            const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
-            s[0][i / kLI][i % kLI] = ok ? p.dmu[o] : 0.f;
-            s[1][i / kLI][i % kLI] = ok ? p.dqa[o] : 0.f;
-            s[2][i / kLI][i % kLI] = ok ? p.dqab[o] : 0.f;
-        }
         __syncthreads();
         for (int i = t; i < kLI * kLT; i += 256) {
             const int r = i / kLT, col = i % kLT;
@@ -145,9 +146,9 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
 #pragma unroll
             for (int k = 0; k < 11; ++k) {
                 const float wk = p.w[k];
-                m0 += wk * s[0][r][col + k];
-                m1 += wk * s[1][r][col + k];
-                m2 += wk * s[2][r][col + k];
+                m0 += wk * s[c][0][r][col + k];
+                m1 += wk * s[c][1][r][col + k];
+                m2 += wk * s[c][2][r][col + k];
             }
             h[0][r][col] = m0;
             h[1][r][col] = m1;
