@@ -100,7 +100,8 @@ __device__ __forceinline__ float alpha_rel_err_pixel(const float4 A, const float
 // [X0,X1] x [Y0,Y1]?  Exact minimum of the quadratic form over the rectangle (centre inside,
 // else the minimum over the four edges), conservative by the record's r2 error bound.
 __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B, const float4 C,
-                                                  const int4 D, int X0, int X1, int Y0, int Y1) {
+                                                  const int4 D, int X0, int X1, int Y0, int Y1,
+                                                  float alpha_min) {
     if (D.y < X0 || D.x > X1 || D.w < Y0 || D.z > Y1) return false;
     const float mx = (float)D.x + A.x, my = (float)D.z + A.y;
     if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
@@ -118,7 +119,11 @@ __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B
         const float ex = fminf(fmaxf(mx - b * ey * ia, (float)X0), (float)X1) - mx;
         q = fminf(q, a * ex * ex + 2.0f * b * ex * ey + c * ey * ey);
     }
-    return q < 1.0f + 4.0f * fabsf(C.w) + 1e-4f;
+    // a sample can only pass alpha >= alpha_min where r2 < x_max = 1 - (alpha_min / o)^(1/beta)
+    // (o, beta as stored); relative slack 1e-4 covers the approximate lg2/ex2 and rounding
+    if (B.y < alpha_min) return false;
+    const float xmax = 1.0f - exp2f(__log2f(alpha_min / B.y) / B.z);
+    return q < fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.0f * fabsf(C.w) + 1e-4f;
 }
 
 __device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int Y0, int Y1) {

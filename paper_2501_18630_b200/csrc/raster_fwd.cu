@@ -39,6 +39,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// fp64 evaluation of an fp32-unsafe primitive, out of line so the common fp32 path is not
+// if-converted into predicated fp64 code
+__device__ __noinline__ Pair unsafe_pair_fwd(const double *m64, float4 B, int px, int py) {
+    return eval_pair64(m64, B, px, py);
+}
+
 __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
                 if (j < nb) {
                     const Record &r = s_rec[buf][j];
                     hit = stats ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
-                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3);
+                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3, a.alpha_min);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
                 if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
@@ -114,8 +120,11 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
                 if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
                 const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
                 const bool unsafe = C.w < 0.f;
-                const Pair p = unsafe ? eval_pair64(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py)
-                                      : eval_pair(A, B, px - bd.x, py - bd.z);
+                Pair p;
+                if (unsafe)  // uniform per entry
+                    p = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
+                else
+                    p = eval_pair(A, B, px - bd.x, py - bd.z);
                 bool ambiguous = false;
                 // rare path: alpha within 5% of the cutoff -> certify with the error bound
                 if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
