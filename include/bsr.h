@@ -54,16 +54,29 @@ typedef struct bsr_camera {
     int32_t width, height;
 } bsr_camera;
 
-/* Primitive parameters, device fp32 SoA (PrimitiveSet layout + SH). */
+/* Colour models (appearance.py). */
+enum bsr_color_model {
+    BSR_COLOR_SH = 0, /* real SH, sh (N,K,3), K = (degree+1)^2 <= 16 (SH adapter) */
+    BSR_COLOR_SB = 1, /* Spherical Beta (the reference's default): base_colors (N,3),
+                         lobe_axes (N,M,3), lobe_colors (N,M,3), M <= 4 (appearance.py:82-163) */
+};
+
+/* Primitive parameters, device fp32 SoA (PrimitiveSet layout, primitive.py:387-426). */
 typedef struct bsr_scene {
     const float *positions, *rotations, *log_scales, *opacity_raw, *shapes, *sh;
     int64_t n;
-    int32_t sh_coeffs; /* K = (degree+1)^2, degree <= 3 */
+    int32_t sh_coeffs;   /* SH: K = (degree+1)^2, degree <= 3 */
+    int32_t color_model; /* bsr_color_model */
+    const float *base_colors, *lobe_axes, *lobe_colors; /* SB arrays */
+    int32_t lobes;       /* SB: M */
+    int32_t reserved;
 } bsr_scene;
 
-/* Per-parameter gradient buffers (device fp32, same shapes); bsr_backward ADDS into them. */
+/* Per-parameter gradient buffers (device fp32, same shapes); bsr_backward ADDS into them.
+ * Only the pointers of the scene's colour model are used. */
 typedef struct bsr_grads {
     float *positions, *rotations, *log_scales, *opacity_raw, *shapes, *sh;
+    float *base_colors, *lobe_axes, *lobe_colors;
 } bsr_grads;
 
 /* Forward outputs (device; any pointer may be NULL to skip that output). */

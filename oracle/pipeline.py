@@ -235,6 +235,52 @@ def sh_basis_grad(degree, dirs):
     return np.stack(out, axis=-2)
 
 
+AXIS_EPS = 1e-8  # appearance.py:24
+
+
+def _effective_axes(axes):
+    norms = np.linalg.norm(axes, axis=-1, keepdims=True)
+    return np.where(norms < AXIS_EPS, np.array([0.0, 0.0, 1.0]), axes)
+
+
+def sb_eval_many(base, axes, cols, dirs):
+    """appearance.py:108-124: Spherical-Beta colour and lobe responses."""
+    ax = _effective_axes(axes)
+    norms = np.linalg.norm(ax, axis=-1)
+    units = ax / norms[..., None]
+    w = np.clip(np.einsum("nmk,nk->nm", units, dirs), 0.0, 1.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        resp = np.where(w > 0.0, w ** (BASE_EXPONENT * norms), 0.0)
+    return base + np.einsum("nm,nmk->nk", resp, cols), resp
+
+
+def sb_grad_many(base, axes, cols, dirs, up):
+    """appearance.py:127-163: gradients (d base, d axes, d colours, d view)."""
+    ax = _effective_axes(axes)
+    norms = np.linalg.norm(ax, axis=-1)
+    units = ax / norms[..., None]
+    w = np.clip(np.einsum("nmk,nk->nm", units, dirs), 0.0, 1.0)
+    expo = BASE_EXPONENT * norms
+    act = w > 1e-12
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        resp = np.where(act, w**expo, 0.0)
+        resp_dw = np.where(act, expo * w ** (expo - 1.0), 0.0)
+        log_w = np.where(act, np.log(np.maximum(w, 1e-300)), 0.0)
+    d_resp = np.einsum("nk,nmk->nm", up, cols)
+    d_cols = resp[..., None] * up[:, None, :]
+    d_w = d_resp * resp_dw
+    d_norm = d_resp * resp * log_w * BASE_EXPONENT
+    d_units = d_w[..., None] * dirs[:, None, :]
+    d_axes = (d_units - np.einsum("nmk,nmk->nm", d_units, units)[..., None] * units) / norms[..., None]
+    d_axes += d_norm[..., None] * units
+    d_axes = np.where(act[..., None], d_axes, 0.0)
+    return up.copy(), d_axes, d_cols, np.einsum("nm,nmk->nk", d_w, units)
+
+
+def is_sb(scene):
+    return getattr(scene, "sh", None) is None
+
+
 def shape_to_exponent(b):
     return BASE_EXPONENT * np.exp(np.clip(b, -SHAPE_CLAMP, SHAPE_CLAMP))
 
@@ -280,10 +326,16 @@ def view_setup(scene, cam):
     order = depth_order(batch["depths"])
     dirs = pos[idx] - cam.center
     dirs = dirs / np.linalg.norm(dirs, axis=-1, keepdims=True)
-    sh = np.asarray(scene.sh, np.float64)
-    deg = int(round(np.sqrt(sh.shape[1]))) - 1
-    basis = sh_basis(deg, dirs)
-    colors = np.einsum("vk,vkc->vc", basis, sh[idx])
+    if is_sb(scene):
+        colors, _ = sb_eval_many(np.asarray(scene.base_colors, np.float64)[idx],
+                                 np.asarray(scene.lobe_axes, np.float64)[idx],
+                                 np.asarray(scene.lobe_colors, np.float64)[idx], dirs)
+        basis, deg = None, None
+    else:
+        sh = np.asarray(scene.sh, np.float64)
+        deg = int(round(np.sqrt(sh.shape[1]))) - 1
+        basis = sh_basis(deg, dirs)
+        colors = np.einsum("vk,vkc->vc", basis, sh[idx])
     betas = shape_to_exponent(np.asarray(scene.shapes, np.float64)[idx])
     opac = sigmoid(np.asarray(scene.opacity_raw, np.float64))[idx]
     s = dict(
@@ -431,10 +483,13 @@ def backward(scene, cam, bg, d_color, fwd, core="c", threads=None, d_depth=None)
     """
     n = len(scene.positions)
     pos = np.asarray(scene.positions, np.float64)
-    k = scene.sh.shape[1]
     grads = dict(positions=np.zeros((n, 3)), rotations=np.zeros((n, 4)), log_scales=np.zeros((n, 3)),
-                 opacity_raw=np.zeros(n), shapes=np.zeros(n), sh=np.zeros((n, k, 3)),
-                 screen_grad_norm=np.zeros(n))
+                 opacity_raw=np.zeros(n), shapes=np.zeros(n), screen_grad_norm=np.zeros(n))
+    if is_sb(scene):
+        m = scene.lobe_axes.shape[1]
+        grads.update(base_colors=np.zeros((n, 3)), lobe_axes=np.zeros((n, m, 3)), lobe_colors=np.zeros((n, m, 3)))
+    else:
+        grads["sh"] = np.zeros((n, scene.sh.shape[1], 3))
     order = fwd["order"]
     if order is None:
         return grads
@@ -451,12 +506,20 @@ def backward(scene, cam, bg, d_color, fwd, core="c", threads=None, d_depth=None)
         dm_s[inv], dc_s[inv], do_s[inv], db_s[inv], dcol_s[inv], dz_s[inv])
     idx = batch["indices"]
     grads["screen_grad_norm"][idx] = np.linalg.norm(d_means2d, axis=-1)
-    # SH chain: d_sh = basis (x) d_rgb ; d_dir = dbasis^T (sh . d_rgb)   (appearance.py:310-318)
     dirs = shaded["dirs"]
-    grads["sh"][idx] = shaded["basis"][:, :, None] * d_colors[:, None, :]
-    sh = np.asarray(scene.sh, np.float64)[idx]
-    d_basis = np.einsum("vkc,vc->vk", sh, d_colors)
-    d_view = np.einsum("vkj,vk->vj", sh_basis_grad(shaded["degree"], dirs), d_basis)
+    if is_sb(scene):  # rasterizer.py:275-284
+        d_base, d_axes, d_cols, d_view = sb_grad_many(
+            np.asarray(scene.base_colors, np.float64)[idx], np.asarray(scene.lobe_axes, np.float64)[idx],
+            np.asarray(scene.lobe_colors, np.float64)[idx], dirs, d_colors)
+        grads["base_colors"][idx] = d_base
+        grads["lobe_axes"][idx] = d_axes
+        grads["lobe_colors"][idx] = d_cols
+    else:
+        # SH chain: d_sh = basis (x) d_rgb ; d_dir = dbasis^T (sh . d_rgb)   (appearance.py:310-318)
+        grads["sh"][idx] = shaded["basis"][:, :, None] * d_colors[:, None, :]
+        sh = np.asarray(scene.sh, np.float64)[idx]
+        d_basis = np.einsum("vkc,vc->vk", sh, d_colors)
+        d_view = np.einsum("vkj,vk->vj", sh_basis_grad(shaded["degree"], dirs), d_basis)
     delta = pos[idx] - cam.center
     nrm = np.linalg.norm(delta, axis=-1, keepdims=True)
     d_pos_view = (d_view - np.einsum("vk,vk->v", d_view, dirs)[:, None] * dirs) / nrm

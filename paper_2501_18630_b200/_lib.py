@@ -40,15 +40,22 @@ class CameraC(ctypes.Structure):
                 ("cx", c_double), ("cy", c_double), ("width", c_int32), ("height", c_int32)]
 
 
+BSR_COLOR_SH = 0
+BSR_COLOR_SB = 1
+
+
 class SceneC(ctypes.Structure):
     _fields_ = [("positions", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p),
                 ("opacity_raw", c_void_p), ("shapes", c_void_p), ("sh", c_void_p), ("n", c_int64),
-                ("sh_coeffs", c_int32)]
+                ("sh_coeffs", c_int32), ("color_model", c_int32), ("base_colors", c_void_p),
+                ("lobe_axes", c_void_p), ("lobe_colors", c_void_p), ("lobes", c_int32),
+                ("reserved", c_int32)]
 
 
 class GradsC(ctypes.Structure):
     _fields_ = [("positions", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p),
-                ("opacity_raw", c_void_p), ("shapes", c_void_p), ("sh", c_void_p)]
+                ("opacity_raw", c_void_p), ("shapes", c_void_p), ("sh", c_void_p),
+                ("base_colors", c_void_p), ("lobe_axes", c_void_p), ("lobe_colors", c_void_p)]
 
 
 class OutputsC(ctypes.Structure):

@@ -137,11 +137,25 @@ static bool bad_camera(const bsr_camera *c) {
 
 static bool bad_scene(const bsr_scene *s) {
     if (!s || s->n < 0 || s->n >= (1ll << 31)) return true;
-    if (!(s->sh_coeffs == 1 || s->sh_coeffs == 4 || s->sh_coeffs == 9 || s->sh_coeffs == 16)) return true;
-    if (s->n > 0 && (!s->positions || !s->rotations || !s->log_scales || !s->opacity_raw || !s->shapes ||
-                     !s->sh))
+    if (s->n > 0 && (!s->positions || !s->rotations || !s->log_scales || !s->opacity_raw || !s->shapes))
         return true;
-    return false;
+    if (s->color_model == BSR_COLOR_SB) {
+        if (s->lobes < 0 || s->lobes > BSR_MAX_LOBES) return true;
+        if (s->n > 0 && (!s->base_colors || (s->lobes > 0 && (!s->lobe_axes || !s->lobe_colors)))) return true;
+        return false;
+    }
+    if (s->color_model != BSR_COLOR_SH) return true;
+    if (!(s->sh_coeffs == 1 || s->sh_coeffs == 4 || s->sh_coeffs == 9 || s->sh_coeffs == 16)) return true;
+    return s->n > 0 && !s->sh;
+}
+
+static bool bad_grads(const bsr_scene *s, const bsr_grads *g) {
+    if (!g) return true;
+    if (s->n == 0) return false;
+    if (!g->positions || !g->rotations || !g->log_scales || !g->opacity_raw || !g->shapes) return true;
+    if (s->color_model == BSR_COLOR_SB)
+        return !g->base_colors || (s->lobes > 0 && (!g->lobe_axes || !g->lobe_colors));
+    return !g->sh;
 }
 
 extern "C" int bsr_version(int32_t *major, int32_t *minor) {
@@ -223,10 +237,7 @@ extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
                             int64_t entry_cap, const float *d_color, const float *d_depth,
                             const bsr_grads *grads, float *screen_grad_norm, const bsr_profile *prof,
                             void *stream) {
-    if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || !grads)
-        return BSR_ERR_BAD_ARG;
-    if (scene->n > 0 && (!grads->positions || !grads->rotations || !grads->log_scales ||
-                         !grads->opacity_raw || !grads->shapes || !grads->sh))
+    if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || bad_grads(scene, grads))
         return BSR_ERR_BAD_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);

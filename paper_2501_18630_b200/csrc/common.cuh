@@ -7,6 +7,7 @@
 #include "bsr.h"
 
 #define BSR_TILE 16
+#define BSR_MAX_LOBES 4
 #define BSR_BLOCK 256
 
 namespace bsr {
@@ -134,6 +135,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+
+// Dispatch a templated launcher on the colour model: CM = K (SH coefficients) or -M (SB).
+#define BSR_DISPATCH_CM(sc, LAUNCH)                                         \
+    do {                                                                   \
+        if ((sc).color_model == BSR_COLOR_SB) {                            \
+            switch ((sc).lobes) {                                          \
+                case 0: LAUNCH(0); break;                                  \
+                case 1: LAUNCH(-1); break;                                 \
+                case 2: LAUNCH(-2); break;                                 \
+                case 3: LAUNCH(-3); break;                                 \
+                case 4: LAUNCH(-4); break;                                 \
+                default: return BSR_ERR_BAD_ARG;                           \
+            }                                                              \
+        } else {                                                           \
+            switch ((sc).sh_coeffs) {                                      \
+                case 1: LAUNCH(1); break;                                  \
+                case 4: LAUNCH(4); break;                                  \
+                case 9: LAUNCH(9); break;                                  \
+                case 16: LAUNCH(16); break;                                \
+                default: return BSR_ERR_BAD_ARG;                           \
+            }                                                              \
+        }                                                                  \
+    } while (0)
 
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }

@@ -8,6 +8,7 @@
 //
 // HBM roofline: N*(48 + 12K) B read, V*(64 + 8 + 4 + 4) B written.
 #include "frame.cuh"
+#include "appearance.cuh"
 #include "project.cuh"
 
 namespace bsr {
@@ -33,68 +34,26 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p) {
     return 5.9604644775390625e-08 * (8.0 * S + 3.0 * (GX + GY)) * 1.5;
 }
 
-// appearance.py:235-261 in fp32 (the raster's colour is fp32 anyway; the fp64 replay
-// recomputes its own colours with sh_color64).
-template <int K>
-__device__ __forceinline__ void sh_color32(const float *sh, const float *pos3, const KCam &cam, float rgb[3]) {
-    float x = pos3[0] - (float)cam.center[0], y = pos3[1] - (float)cam.center[1],
-          z = pos3[2] - (float)cam.center[2];
-    const float inv = rsqrtf(x * x + y * y + z * z);
-    x *= inv;
-    y *= inv;
-    z *= inv;
-    float b[16];
-    b[0] = 0.28209479177387814f;
-    if constexpr (K > 1) {
-        const float C1 = 0.4886025119029199f;
-        b[1] = -C1 * y;
-        b[2] = C1 * z;
-        b[3] = -C1 * x;
-    }
-    if constexpr (K > 4) {
-        const float xx = x * x, yy = y * y, zz = z * z;
-        b[4] = 1.0925484305920792f * x * y;
-        b[5] = -1.0925484305920792f * y * z;
-        b[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
-        b[7] = -1.0925484305920792f * x * z;
-        b[8] = 0.5462742152960396f * (xx - yy);
-        if constexpr (K > 9) {
-            b[9] = -0.5900435899266435f * y * (3.f * xx - yy);
-            b[10] = 2.890611442640554f * x * y * z;
-            b[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
-            b[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
-            b[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
-            b[14] = 1.445305721320277f * z * (xx - yy);
-            b[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
-        }
-    }
-    float r = 0.f, g = 0.f, bl = 0.f;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        r = __fmaf_rn(b[k], sh[3 * k], r);
-        g = __fmaf_rn(b[k], sh[3 * k + 1], g);
-        bl = __fmaf_rn(b[k], sh[3 * k + 2], bl);
-    }
-    rgb[0] = r;
-    rgb[1] = g;
-    rgb[2] = bl;
-}
-
 // Shared-memory staging of one CTA's 256 primitives: the parameter blocks are contiguous
 // per CTA, so one elected thread moves them with TMA bulk copies (cp.async.bulk +
 // mbarrier) while the other threads proceed; partial / misaligned blocks fall back to
 // cooperative loads.
-template <int K>
+// Appearance payload: SH -> sh[256][3K];  SB -> base[256][3] | axes[256][3M] | cols[256][3M]
+template <int CM>
 struct PreSmem {
     float pos[BSR_BLOCK * 3], rot[BSR_BLOCK * 4], ls[BSR_BLOCK * 3], op[BSR_BLOCK], shp[BSR_BLOCK];
-    float sh[BSR_BLOCK * 3 * K];
+    float app[BSR_BLOCK * AppTraits<CM>::floats];
 };
 
-template <int K>
+template <int CM>
 __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs args) {
+    using Tr = AppTraits<CM>;
     const FrameView &f = args.f;
     extern __shared__ __align__(16) unsigned char pre_smem_raw[];
-    PreSmem<K> &sm = *reinterpret_cast<PreSmem<K> *>(pre_smem_raw);
+    PreSmem<CM> &sm = *reinterpret_cast<PreSmem<CM> *>(pre_smem_raw);
+    float *app_a = sm.app;                                  // SH coeffs / SB base colours
+    float *app_b = sm.app + BSR_BLOCK * (Tr::sh ? 0 : 3);   // SB lobe axes
+    float *app_c = app_b + BSR_BLOCK * 3 * Tr::M;           // SB lobe colours
     __shared__ uint32_t s_part, s_warp[BSR_BLOCK / 32], s_excl;
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ int s_bulk;
@@ -106,21 +65,35 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         s_part = part;
         const int64_t base = (int64_t)part * BSR_BLOCK;
         const int64_t cnt = imin64(BSR_BLOCK, n - base);
-        const uintptr_t al = reinterpret_cast<uintptr_t>(sc.positions) | reinterpret_cast<uintptr_t>(sc.rotations) |
-                             reinterpret_cast<uintptr_t>(sc.log_scales) | reinterpret_cast<uintptr_t>(sc.opacity_raw) |
-                             reinterpret_cast<uintptr_t>(sc.shapes) | reinterpret_cast<uintptr_t>(sc.sh);
+        uintptr_t al = reinterpret_cast<uintptr_t>(sc.positions) | reinterpret_cast<uintptr_t>(sc.rotations) |
+                       reinterpret_cast<uintptr_t>(sc.log_scales) | reinterpret_cast<uintptr_t>(sc.opacity_raw) |
+                       reinterpret_cast<uintptr_t>(sc.shapes);
+        if constexpr (Tr::sh)
+            al |= reinterpret_cast<uintptr_t>(sc.sh);
+        else
+            al |= reinterpret_cast<uintptr_t>(sc.base_colors) | reinterpret_cast<uintptr_t>(sc.lobe_axes) |
+                  reinterpret_cast<uintptr_t>(sc.lobe_colors);
         const bool bulk = cnt == BSR_BLOCK && (al & 15) == 0;
         s_bulk = bulk;
         if (bulk) {
             mbar_init(&s_bar, 1);
-            const uint32_t b3 = BSR_BLOCK * 12, b4 = BSR_BLOCK * 16, b1 = BSR_BLOCK * 4, bsh = BSR_BLOCK * 12 * K;
-            mbar_expect_tx(&s_bar, 2 * b3 + b4 + 2 * b1 + bsh);
+            const uint32_t b3 = BSR_BLOCK * 12, b4 = BSR_BLOCK * 16, b1 = BSR_BLOCK * 4;
+            const uint32_t bapp = BSR_BLOCK * 4 * Tr::floats;
+            mbar_expect_tx(&s_bar, 2 * b3 + b4 + 2 * b1 + bapp);
             bulk_g2s(sm.pos, sc.positions + 3 * base, b3, &s_bar);
             bulk_g2s(sm.rot, sc.rotations + 4 * base, b4, &s_bar);
             bulk_g2s(sm.ls, sc.log_scales + 3 * base, b3, &s_bar);
             bulk_g2s(sm.op, sc.opacity_raw + base, b1, &s_bar);
             bulk_g2s(sm.shp, sc.shapes + base, b1, &s_bar);
-            bulk_g2s(sm.sh, sc.sh + 3 * K * base, bsh, &s_bar);
+            if constexpr (Tr::sh) {
+                bulk_g2s(app_a, sc.sh + 3 * Tr::K * base, bapp, &s_bar);
+            } else {
+                bulk_g2s(app_a, sc.base_colors + 3 * base, b3, &s_bar);
+                if constexpr (Tr::M > 0) {
+                    bulk_g2s(app_b, sc.lobe_axes + 3 * Tr::M * base, b3 * Tr::M, &s_bar);
+                    bulk_g2s(app_c, sc.lobe_colors + 3 * Tr::M * base, b3 * Tr::M, &s_bar);
+                }
+            }
         }
     }
     __syncthreads();
@@ -140,7 +113,15 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
             sm.op[q] = sc.opacity_raw[base + q];
             sm.shp[q] = sc.shapes[base + q];
         }
-        for (int q = tid; q < cnt * 3 * K; q += BSR_BLOCK) sm.sh[q] = sc.sh[3 * K * base + q];
+        if constexpr (Tr::sh) {
+            for (int q = tid; q < cnt * 3 * Tr::K; q += BSR_BLOCK) app_a[q] = sc.sh[3 * Tr::K * base + q];
+        } else {
+            for (int q = tid; q < cnt * 3; q += BSR_BLOCK) app_a[q] = sc.base_colors[3 * base + q];
+            for (int q = tid; q < cnt * 3 * Tr::M; q += BSR_BLOCK) {
+                app_b[q] = sc.lobe_axes[3 * Tr::M * base + q];
+                app_c[q] = sc.lobe_colors[3 * Tr::M * base + q];
+            }
+        }
         __syncthreads();
     }
 
@@ -158,7 +139,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         if (p.visible) {
             vis = true;
             float rgb[3];
-            sh_color32<K>(sm.sh + 3 * K * tid, pos, args.cam, rgb);
+            float vx = pos[0] - (float)args.cam.center[0], vy = pos[1] - (float)args.cam.center[1],
+                  vz = pos[2] - (float)args.cam.center[2];
+            const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+            if constexpr (Tr::sh)
+                app_color32<CM>(app_a + 3 * Tr::K * tid, nullptr, nullptr, vx * inv, vy * inv, vz * inv, rgb);
+            else
+                app_color32<CM>(app_a + 3 * tid, app_b + 3 * Tr::M * tid, app_c + 3 * Tr::M * tid, vx * inv,
+                                vy * inv, vz * inv, rgb);
             const double o = sigmoid64((double)sm.op[tid]);
             const double beta = shape_to_exponent64((double)sm.shp[tid]);
             r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)p.ca, (float)p.cb);
@@ -223,31 +211,27 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     }
 }
 
-template <int K>
+template <int CM>
 static int launch_pre_k(const PreArgs &a, unsigned blocks, cudaStream_t st) {
-    const size_t smem = sizeof(PreSmem<K>);
+    const size_t smem = sizeof(PreSmem<CM>);
     static bool attr = false;
     if (!attr) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr = true;
     }
-    preprocess_fwd_kernel<K><<<blocks, BSR_BLOCK, smem, st>>>(a);
+    preprocess_fwd_kernel<CM><<<blocks, BSR_BLOCK, smem, st>>>(a);
     return BSR_OK;
 }
 
 int launch_preprocess(const bsr_scene &sc, const KCam &cam, const FrameView &f, cudaStream_t st) {
     if (sc.n == 0) return BSR_OK;
     PreArgs a{sc, cam, f};
-    int rc;
+    int rc = BSR_OK;
     const unsigned blocks = (unsigned)f.pre_parts;
-    switch (sc.sh_coeffs) {
-        case 1: rc = launch_pre_k<1>(a, blocks, st); break;
-        case 4: rc = launch_pre_k<4>(a, blocks, st); break;
-        case 9: rc = launch_pre_k<9>(a, blocks, st); break;
-        case 16: rc = launch_pre_k<16>(a, blocks, st); break;
-        default: return BSR_ERR_BAD_ARG;
-    }
+#define BSR_PRE_LAUNCH(CM) rc = launch_pre_k<CM>(a, blocks, st)
+    BSR_DISPATCH_CM(sc, BSR_PRE_LAUNCH);
+#undef BSR_PRE_LAUNCH
     if (rc) return rc;
     BSR_LAUNCH_CHECK();
     return BSR_OK;

@@ -8,6 +8,7 @@
 //   plus the depth extension  z = R[2].p + t[2].
 // Gradients are ADDED into the caller's per-parameter buffers (multi-view accumulation).
 // HBM roofline: V * (48 B grad_acc + 240 B params read + 240 B grads RMW) at SH-3.
+#include "appearance.cuh"
 #include "frame.cuh"
 
 namespace bsr {
@@ -65,6 +66,102 @@ __device__ __forceinline__ void sh_basis_and_grad(float x, float y, float z, flo
             db[13][0] = c34 * (4.f * zz - 3.f * xx - yy); db[13][1] = c34 * -2.f * x * y; db[13][2] = c34 * 8.f * x * z;
             db[14][0] = c35 * 2.f * x * z; db[14][1] = c35 * -2.f * y * z; db[14][2] = c35 * (xx - yy);
             db[15][0] = c36 * (3.f * xx - 3.f * yy); db[15][1] = c36 * -6.f * x * y; db[15][2] = 0.f;
+        }
+    }
+}
+
+// Colour-model backward: accumulates the parameter gradients of primitive i and returns
+// d rgb / d view-direction (added into ddx/ddy/ddz).
+//   SH: d_sh[k,c] = basis_k d_rgb[c];  d_dir = dbasis^T (sh . d_rgb)     (appearance.py:264-318)
+//   SB: sb_grad_many (appearance.py:127-163)
+template <int CM>
+__device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grads &g, int64_t i, float vx,
+                                             float vy, float vz, float dr, float dg, float dbl, float &ddx,
+                                             float &ddy, float &ddz) {
+    using Tr = AppTraits<CM>;
+    if constexpr (Tr::sh) {
+        constexpr int K = Tr::K;
+        float b[16], db[16][3];
+        sh_basis_and_grad<K>(vx, vy, vz, b, db);
+        // coefficients and their gradients move as float4 when a row of K*3 floats is
+        // 16-byte aligned (K = 4, 16); coalescing-friendly vs 3K scalar accesses
+        float shv[3 * K], gsv[3 * K];
+        const float *shp = sc.sh + i * 3 * K;
+        float *gsh = g.sh + i * 3 * K;
+        const bool sh16 = ((reinterpret_cast<uintptr_t>(sc.sh) | reinterpret_cast<uintptr_t>(g.sh)) & 15) == 0;
+        if ((3 * K) % 4 == 0 && sh16) {
+#pragma unroll
+            for (int q = 0; q < 3 * K / 4; ++q) {
+                const float4 x4 = __ldg(reinterpret_cast<const float4 *>(shp) + q);
+                const float4 g4 = reinterpret_cast<const float4 *>(gsh)[q];
+                shv[4 * q] = x4.x; shv[4 * q + 1] = x4.y; shv[4 * q + 2] = x4.z; shv[4 * q + 3] = x4.w;
+                gsv[4 * q] = g4.x; gsv[4 * q + 1] = g4.y; gsv[4 * q + 2] = g4.z; gsv[4 * q + 3] = g4.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3 * K; ++q) {
+                shv[q] = __ldg(shp + q);
+                gsv[q] = gsh[q];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            gsv[3 * k] += b[k] * dr;
+            gsv[3 * k + 1] += b[k] * dg;
+            gsv[3 * k + 2] += b[k] * dbl;
+            const float dbk = shv[3 * k] * dr + shv[3 * k + 1] * dg + shv[3 * k + 2] * dbl;
+            ddx += db[k][0] * dbk;
+            ddy += db[k][1] * dbk;
+            ddz += db[k][2] * dbk;
+        }
+        if ((3 * K) % 4 == 0 && sh16) {
+#pragma unroll
+            for (int q = 0; q < 3 * K / 4; ++q)
+                reinterpret_cast<float4 *>(gsh)[q] =
+                    make_float4(gsv[4 * q], gsv[4 * q + 1], gsv[4 * q + 2], gsv[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3 * K; ++q) gsh[q] = gsv[q];
+        }
+    } else {
+        constexpr int M = Tr::M;
+        g.base_colors[3 * i] += dr;  // d base = upstream
+        g.base_colors[3 * i + 1] += dg;
+        g.base_colors[3 * i + 2] += dbl;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const int64_t o = (i * M + m) * 3;
+            float ax = sc.lobe_axes[o], ay = sc.lobe_axes[o + 1], az = sc.lobe_axes[o + 2];
+            float nrm = sqrtf(ax * ax + ay * ay + az * az);
+            if (nrm < (float)kAxisEps) {  // effective axis +z (appearance.py:76-78)
+                ax = 0.f;
+                ay = 0.f;
+                az = 1.f;
+                nrm = 1.f;
+            }
+            const float inrm = 1.f / nrm;
+            const float ux = ax * inrm, uy = ay * inrm, uz = az * inrm;
+            const float w = fminf(fmaxf(ux * vx + uy * vy + uz * vz, 0.f), 1.f);
+            const float expo = 4.0f * nrm;
+            const float cr = sc.lobe_colors[o], cg = sc.lobe_colors[o + 1], cb = sc.lobe_colors[o + 2];
+            if (!(w > 1e-12f)) continue;  // outside the lobe's support: exactly zero gradients
+            const float lw = __logf(w);
+            const float resp = __expf(expo * lw);
+            const float resp_dw = expo * __expf((expo - 1.0f) * lw);
+            g.lobe_colors[o] += resp * dr;
+            g.lobe_colors[o + 1] += resp * dg;
+            g.lobe_colors[o + 2] += resp * dbl;
+            const float d_resp = dr * cr + dg * cg + dbl * cb;
+            const float d_w = d_resp * resp_dw;
+            const float d_norm = d_resp * resp * lw * 4.0f;
+            const float dux = d_w * vx, duy = d_w * vy, duz = d_w * vz;
+            const float dot = dux * ux + duy * uy + duz * uz;
+            g.lobe_axes[o] += (dux - dot * ux) * inrm + d_norm * ux;
+            g.lobe_axes[o + 1] += (duy - dot * uy) * inrm + d_norm * uy;
+            g.lobe_axes[o + 2] += (duz - dot * uz) * inrm + d_norm * uz;
+            ddx += d_w * ux;
+            ddy += d_w * uy;
+            ddz += d_w * uz;
         }
     }
 }
@@ -219,7 +316,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
             a.g.rotations[4 * i + 3] += (gz - dot * z) * iqn;
         }
     }
-    // ---- SH colour chain + view direction -> position
+    // ---- colour chain (SH or Spherical Beta) + view direction -> position
     {
         float vx = px - (float)cam.center[0], vy = py - (float)cam.center[1], vz = pz - (float)cam.center[2];
         const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
@@ -227,49 +324,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
         vx *= ivn;
         vy *= ivn;
         vz *= ivn;
-        float b[16], db[16][3];
-        sh_basis_and_grad<K>(vx, vy, vz, b, db);
         float ddx = 0.f, ddy = 0.f, ddz = 0.f;
-        // coefficients and their gradients move as float4 when a row of K*3 floats is
-        // 16-byte aligned (K = 4, 16); coalescing-friendly vs 3K scalar accesses
-        float shv[3 * K], gsv[3 * K];
-        const float *shp = sc.sh + i * 3 * K;
-        float *gsh = a.g.sh + i * 3 * K;
-        const bool sh16 = ((reinterpret_cast<uintptr_t>(sc.sh) | reinterpret_cast<uintptr_t>(a.g.sh)) & 15) == 0;
-        if ((3 * K) % 4 == 0 && sh16) {
-#pragma unroll
-            for (int q = 0; q < 3 * K / 4; ++q) {
-                const float4 x4 = __ldg(reinterpret_cast<const float4 *>(shp) + q);
-                const float4 g4 = reinterpret_cast<const float4 *>(gsh)[q];
-                shv[4 * q] = x4.x; shv[4 * q + 1] = x4.y; shv[4 * q + 2] = x4.z; shv[4 * q + 3] = x4.w;
-                gsv[4 * q] = g4.x; gsv[4 * q + 1] = g4.y; gsv[4 * q + 2] = g4.z; gsv[4 * q + 3] = g4.w;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 3 * K; ++q) {
-                shv[q] = __ldg(shp + q);
-                gsv[q] = gsh[q];
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            gsv[3 * k] += b[k] * dr;
-            gsv[3 * k + 1] += b[k] * dg;
-            gsv[3 * k + 2] += b[k] * dbl;
-            const float dbk = shv[3 * k] * dr + shv[3 * k + 1] * dg + shv[3 * k + 2] * dbl;
-            ddx += db[k][0] * dbk;
-            ddy += db[k][1] * dbk;
-            ddz += db[k][2] * dbk;
-        }
-        if ((3 * K) % 4 == 0 && sh16) {
-#pragma unroll
-            for (int q = 0; q < 3 * K / 4; ++q)
-                reinterpret_cast<float4 *>(gsh)[q] =
-                    make_float4(gsv[4 * q], gsv[4 * q + 1], gsv[4 * q + 2], gsv[4 * q + 3]);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 3 * K; ++q) gsh[q] = gsv[q];
-        }
+        app_backward<K>(sc, a.g, i, vx, vy, vz, dr, dg, dbl, ddx, ddy, ddz);
         const float dd = ddx * vx + ddy * vy + ddz * vz;
         dpx += (ddx - dd * vx) * ivn;
         dpy += (ddy - dd * vy) * ivn;
@@ -286,13 +342,9 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
     if (f.n == 0) return BSR_OK;
     PreBwdArgs a{sc, cam, f, g, screen_grad_norm};
     const unsigned blocks = (unsigned)div_up(f.n, BSR_BLOCK);
-    switch (sc.sh_coeffs) {
-        case 1: preprocess_bwd_kernel<1><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
-        case 4: preprocess_bwd_kernel<4><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
-        case 9: preprocess_bwd_kernel<9><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
-        case 16: preprocess_bwd_kernel<16><<<blocks, BSR_BLOCK, 0, st>>>(a); break;
-        default: return BSR_ERR_BAD_ARG;
-    }
+#define BSR_PREBWD_LAUNCH(CM) preprocess_bwd_kernel<CM><<<blocks, BSR_BLOCK, 0, st>>>(a)
+    BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
+#undef BSR_PREBWD_LAUNCH
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -120,58 +120,4 @@ __device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat
     return p;
 }
 
-// appearance.py:192-261 real SH basis (degree <= 3), reference constants and signs.
-template <int K>
-__device__ __forceinline__ void sh_basis64(double x, double y, double z, double *b) {
-    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
-    b[0] = C0;
-    if (K > 1) {
-        b[1] = -C1 * y;
-        b[2] = C1 * z;
-        b[3] = -C1 * x;
-    }
-    if (K > 4) {
-        const double xx = x * x, yy = y * y, zz = z * z;
-        b[4] = 1.0925484305920792 * x * y;
-        b[5] = -1.0925484305920792 * y * z;
-        b[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
-        b[7] = -1.0925484305920792 * x * z;
-        b[8] = 0.5462742152960396 * (xx - yy);
-        if (K > 9) {
-            b[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
-            b[10] = 2.890611442640554 * x * y * z;
-            b[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
-            b[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-            b[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
-            b[14] = 1.445305721320277 * z * (xx - yy);
-            b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
-        }
-    }
-}
-
-// rasterizer.py:94-95 view direction + einsum(basis, sh) colour (SH adapter).
-template <int K>
-__device__ __forceinline__ void sh_color64(const float *sh, const float *pos3,
-                                           const KCam &cam, double rgb[3]) {
-    double dx = (double)pos3[0] - cam.center[0];
-    double dy = (double)pos3[1] - cam.center[1];
-    double dz = (double)pos3[2] - cam.center[2];
-    const double n = sqrt((dx * dx + dy * dy) + dz * dz);
-    dx /= n;
-    dy /= n;
-    dz /= n;
-    double b[16];
-    sh_basis64<K>(dx, dy, dz, b);
-    double r = 0.0, g = 0.0, bl = 0.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        r += b[k] * (double)sh[3 * k + 0];
-        g += b[k] * (double)sh[3 * k + 1];
-        bl += b[k] * (double)sh[3 * k + 2];
-    }
-    rgb[0] = r;
-    rgb[1] = g;
-    rgb[2] = bl;
-}
-
 }  // namespace bsr

@@ -12,6 +12,7 @@
 // entries at or after the entry where fp32 stopped (entries before it were certified and
 // counted by the fp32 kernel).  Backward adds the pixel's gradients into grad_acc.
 #include "frame.cuh"
+#include "appearance.cuh"
 #include "project.cuh"
 
 namespace bsr {
@@ -47,15 +48,15 @@ struct SceneProvider {
         e.src = (int)src_of[c];
         return true;
     }
-    // colour only for samples that pass the alpha cutoff
+    // colour only for samples that pass the alpha cutoff (view dir as rasterizer.py:94-95)
     __device__ __forceinline__ void color(Entry64 &e) const {
         const int64_t i = e.src;
-        const float pos[3] = {sc.positions[3 * i], sc.positions[3 * i + 1], sc.positions[3 * i + 2]};
-        float shv[3 * K];
-#pragma unroll
-        for (int j = 0; j < 3 * K; ++j) shv[j] = sc.sh[i * 3 * K + j];
+        double dx = (double)sc.positions[3 * i] - cam.center[0];
+        double dy = (double)sc.positions[3 * i + 1] - cam.center[1];
+        double dz = (double)sc.positions[3 * i + 2] - cam.center[2];
+        const double n = sqrt((dx * dx + dy * dy) + dz * dz);
         double rgb[3];
-        sh_color64<K>(shv, pos, cam, rgb);
+        app_color64<K>(sc, i, dx / n, dy / n, dz / n, rgb);
         e.r = rgb[0];
         e.g = rgb[1];
         e.b = rgb[2];
@@ -381,13 +382,11 @@ int launch_replay_scene(bool fwd, const FrameView &f, const bsr_scene &sc, const
     a.d_color = d_color;
     a.d_depth = d_depth;
     a.mask_raw = true;
-    switch (sc.sh_coeffs) {
-        case 1: return launch_replay(fwd, a, SceneProvider<1>{sc, cam, f.rec, f.src_of, f.rec64}, st);
-        case 4: return launch_replay(fwd, a, SceneProvider<4>{sc, cam, f.rec, f.src_of, f.rec64}, st);
-        case 9: return launch_replay(fwd, a, SceneProvider<9>{sc, cam, f.rec, f.src_of, f.rec64}, st);
-        case 16: return launch_replay(fwd, a, SceneProvider<16>{sc, cam, f.rec, f.src_of, f.rec64}, st);
-        default: return BSR_ERR_BAD_ARG;
-    }
+    int rc = BSR_OK;
+#define BSR_REPLAY_LAUNCH(CM) rc = launch_replay(fwd, a, SceneProvider<CM>{sc, cam, f.rec, f.src_of, f.rec64}, st)
+    BSR_DISPATCH_CM(sc, BSR_REPLAY_LAUNCH);
+#undef BSR_REPLAY_LAUNCH
+    return rc;
 }
 
 int launch_replay_arrays(bool fwd, const FrameView &f, const double *means, const double *conics,

@@ -75,26 +75,48 @@ def _bg_arr(background):
     return (ctypes.c_float * 3)(*bg.tolist())
 
 
-def scene_c(positions, rotations, log_scales, opacity_raw, shapes, sh) -> _lib.SceneC:
+def _check_t(name, t, n):
+    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    if t.shape[0] != n:
+        raise ValueError(f"{name} row count mismatch")
+
+
+def scene_c(positions, rotations, log_scales, opacity_raw, shapes, sh=None, base_colors=None,
+            lobe_axes=None, lobe_colors=None) -> _lib.SceneC:
+    """bsr_scene for the SH model (``sh``) or the Spherical-Beta model (``base_colors``...)."""
     n = int(positions.shape[0])
     for name, t in (("positions", positions), ("rotations", rotations), ("log_scales", log_scales),
-                    ("opacity_raw", opacity_raw), ("shapes", shapes), ("sh", sh)):
-        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
-        if t.shape[0] != n:
-            raise ValueError(f"{name} row count mismatch")
-    if sh.dim() != 3 or sh.shape[2] != 3:
-        raise ValueError("sh must be (N, K, 3)")
+                    ("opacity_raw", opacity_raw), ("shapes", shapes)):
+        _check_t(name, t, n)
     s = _lib.SceneC()
     s.positions, s.rotations, s.log_scales = positions.data_ptr(), rotations.data_ptr(), log_scales.data_ptr()
-    s.opacity_raw, s.shapes, s.sh = opacity_raw.data_ptr(), shapes.data_ptr(), sh.data_ptr()
-    s.n, s.sh_coeffs = n, int(sh.shape[1])
+    s.opacity_raw, s.shapes = opacity_raw.data_ptr(), shapes.data_ptr()
+    s.n = n
+    if sh is not None:
+        _check_t("sh", sh, n)
+        if sh.dim() != 3 or sh.shape[2] != 3:
+            raise ValueError("sh must be (N, K, 3)")
+        s.sh, s.sh_coeffs, s.color_model = sh.data_ptr(), int(sh.shape[1]), _lib.BSR_COLOR_SH
+    else:
+        if base_colors is None:
+            raise ValueError("need sh or base_colors")
+        _check_t("base_colors", base_colors, n)
+        s.color_model, s.base_colors = _lib.BSR_COLOR_SB, base_colors.data_ptr()
+        s.lobes = 0 if lobe_axes is None else int(lobe_axes.shape[1])
+        if s.lobes:
+            _check_t("lobe_axes", lobe_axes, n)
+            _check_t("lobe_colors", lobe_colors, n)
+            s.lobe_axes, s.lobe_colors = lobe_axes.data_ptr(), lobe_colors.data_ptr()
     return s
 
 
 def _prims_scene_c(prims: PrimitiveSet) -> _lib.SceneC:
+    if prims.color_model == "sh":
+        return scene_c(prims.positions, prims.rotations, prims.log_scales, prims.opacity_raw, prims.shapes,
+                       sh=prims.sh)
     return scene_c(prims.positions, prims.rotations, prims.log_scales, prims.opacity_raw, prims.shapes,
-                   prims.sh)
+                   base_colors=prims.base_colors, lobe_axes=prims.lobe_axes, lobe_colors=prims.lobe_colors)
 
 
 def frame_bytes(n, width, height, entry_cap) -> int:
@@ -193,7 +215,13 @@ def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameSta
 def grads_c(g: GradientBuffer) -> _lib.GradsC:
     c = _lib.GradsC()
     c.positions, c.rotations, c.log_scales = g.positions.data_ptr(), g.rotations.data_ptr(), g.log_scales.data_ptr()
-    c.opacity_raw, c.shapes, c.sh = g.opacity_raw.data_ptr(), g.shapes.data_ptr(), g.sh.data_ptr()
+    c.opacity_raw, c.shapes = g.opacity_raw.data_ptr(), g.shapes.data_ptr()
+    if g.color_model == "sh":
+        c.sh = g.sh.data_ptr()
+    else:
+        c.base_colors = g.base_colors.data_ptr()
+        if g.lobes:
+            c.lobe_axes, c.lobe_colors = g.lobe_axes.data_ptr(), g.lobe_colors.data_ptr()
     return c
 
 

@@ -53,6 +53,64 @@ class SplatScene:
 
 
 @dataclass
+class SbSplatScene:
+    """SoA parameters with the reference's Spherical-Beta colour (primitive.py:387-426)."""
+
+    positions: np.ndarray  # (N, 3)
+    rotations: np.ndarray  # (N, 4)
+    log_scales: np.ndarray  # (N, 3)
+    opacity_raw: np.ndarray  # (N,)
+    shapes: np.ndarray  # (N,)
+    base_colors: np.ndarray  # (N, 3)
+    lobe_axes: np.ndarray  # (N, M, 3)
+    lobe_colors: np.ndarray  # (N, M, 3)
+
+    def __len__(self):
+        return int(self.positions.shape[0])
+
+    def arrays(self) -> dict:
+        return {k: getattr(self, k) for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes",
+                                             "base_colors", "lobe_axes", "lobe_colors")}
+
+    def astype(self, dtype) -> "SbSplatScene":
+        return SbSplatScene(**{k: np.ascontiguousarray(v, dtype=dtype) for k, v in self.arrays().items()})
+
+    def take(self, idx) -> "SbSplatScene":
+        return SbSplatScene(**{k: v[idx].copy() for k, v in self.arrays().items()})
+
+
+def fibonacci_directions(m):
+    """appearance.py:29-37: m quasi-uniform unit directions."""
+    if m == 0:
+        return np.zeros((0, 3))
+    i = np.arange(m) + 0.5
+    phi = np.pi * (3.0 - np.sqrt(5.0)) * i
+    z = 1.0 - 2.0 * i / m
+    rho = np.sqrt(np.maximum(1.0 - z * z, 0.0))
+    return np.stack([rho * np.cos(phi), rho * np.sin(phi), z], axis=-1)
+
+
+def sb_random_scene(rng, n, lobes=2, spread=0.8, scale_range=(0.05, 0.35), opacity_range=(0.2, 0.8),
+                    lobe_color_scale=0.3) -> SbSplatScene:
+    """The reference tests' random scene generator (tests/conftest.py:15-31), fp32-rounded."""
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    axes = fibonacci_directions(lobes)[None] * np.exp(rng.uniform(-0.3, 0.8, (n, lobes, 1)))
+    op = rng.uniform(*opacity_range, n)
+    f = np.float32
+    return SbSplatScene(
+        positions=rng.uniform(-spread, spread, (n, 3)).astype(f),
+        opacity_raw=(np.log(op) - np.log1p(-op)).astype(f),
+        rotations=q.astype(f),
+        log_scales=np.log(rng.uniform(*scale_range, (n, 3))).astype(f),
+        shapes=rng.uniform(-1.5, 1.5, n).astype(f),
+        base_colors=rng.uniform(0.0, 1.0, (n, 3)).astype(f),
+        lobe_axes=axes.astype(f),
+        lobe_colors=(rng.uniform(-0.2, 1.0, (n, lobes, 3)) * lobe_color_scale).astype(f),
+    )
+
+
+@dataclass
 class Workload:
     name: str
     scene: SplatScene

@@ -95,6 +95,13 @@ class AdamState:
         self.step_dev = torch.zeros(1, dtype=torch.int64, device=prims.flat.device)
 
 
+def sb_group_lrs(lr_means=1.6e-4):
+    """The reference's default per-group learning rates (TrainConfig.group_lrs,
+    training.py:217-227) for a Spherical-Beta set."""
+    return {"positions": lr_means, "opacity_raw": 5e-2, "rotations": 1e-3, "log_scales": 5e-3,
+            "shapes": 1e-3, "base_colors": 2.5e-3, "lobe_axes": 2.5e-3, "lobe_colors": 2.5e-3}
+
+
 def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
     """Config-3 learning rates (BASELINE.json configs[3]): 1.6e-4 for means, 5e-3 for the
     other optimised attributes (quats, scales, opacities, SH).  The configs render the
@@ -111,19 +118,19 @@ def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs:
 
     ``device_step`` keeps the step count on the device (graph-capturable); the host-side
     ``state.step`` then only counts calls made outside captured graphs."""
-    ends = (ctypes.c_int64 * 6)(*prims.group_ends())
-    lr = (ctypes.c_float * 6)(*[float(lrs[g]) for g in ("positions", "rotations", "log_scales",
-                                                          "opacity_raw", "shapes", "sh")])
+    groups = prims.groups
+    ends = (ctypes.c_int64 * len(groups))(*prims.group_ends())
+    lr = (ctypes.c_float * len(groups))(*[float(lrs[g]) for g in groups])
     lib = _lib.load()
     if device_step:
         rc = lib.bsr_adam_step_device(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
-                                      state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr,
+                                      state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
                                       state.step_dev.data_ptr(), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
     else:
         state.step += 1
         state.step_dev.fill_(state.step)
         rc = lib.bsr_adam_step(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
-                               state.exp_avg_sq.data_ptr(), prims.flat.numel(), 6, ends, lr, state.step,
+                               state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr, state.step,
                                ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
     _lib.check(rc, "adam")
     return prims
@@ -138,7 +145,7 @@ class TrainStep:
         self.cameras = list(cameras)
         self.targets = list(targets)
         self.background = background
-        self.lrs = lrs or group_lrs()
+        self.lrs = lrs or (group_lrs() if prims.color_model == "sh" else sb_group_lrs())
         self.lambda_ssim = lambda_ssim
         self.pg = process_group
         self.grads = GradientBuffer.zeros_for(prims)

@@ -26,10 +26,15 @@ def golden(name):
 
 def golden_scene_camera(g):
     from paper_2501_18630_b200.camera import Camera
-    from paper_2501_18630_b200.scenes import SplatScene
+    from paper_2501_18630_b200.scenes import SbSplatScene, SplatScene
 
-    scene = SplatScene(positions=g["positions"], rotations=g["rotations"], log_scales=g["log_scales"],
-                       opacity_raw=g["opacity_raw"], shapes=g["shapes"], sh=g["sh"])
+    if "sh" in g:
+        scene = SplatScene(positions=g["positions"], rotations=g["rotations"], log_scales=g["log_scales"],
+                           opacity_raw=g["opacity_raw"], shapes=g["shapes"], sh=g["sh"])
+    else:
+        scene = SbSplatScene(positions=g["positions"], rotations=g["rotations"], log_scales=g["log_scales"],
+                             opacity_raw=g["opacity_raw"], shapes=g["shapes"], base_colors=g["base_colors"],
+                             lobe_axes=g["lobe_axes"], lobe_colors=g["lobe_colors"])
     fx, fy, cx, cy = g["intr"]
     w, h = (int(v) for v in g["size"])
     return scene, Camera(g["w2c"], fx, fy, cx, cy, w, h)

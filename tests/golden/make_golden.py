@@ -266,6 +266,29 @@ def main():
         for i, g in enumerate(gs):
             save[f"g{i}_" + k] = g[k]
     np.savez_compressed(os.path.join(OUT, "adam.npz"), **save)
+    # ---- G6: the reference's DEFAULT path (Spherical-Beta colour), unmodified render_tiled /
+    #      render_backward, on its own random-scene distribution (tests/conftest.py:15-31)
+    from betasplat import rasterizer as rz
+    from betasplat.primitive import PrimitiveSet as RefPS
+    from paper_2501_18630_b200.scenes import sb_random_scene
+
+    for name, seed, n, (w, h), lobes in (("sb_small.npz", 21, 60, (48, 40), 2),
+                                         ("sb_medium.npz", 22, 1500, (96, 72), 3)):
+        rng = np.random.default_rng(seed)
+        sc = sb_random_scene(rng, n, lobes=lobes)
+        ref = RefPS(**{k: v.astype(np.float64) for k, v in sc.arrays().items()})
+        from paper_2501_18630_b200.camera import Camera
+
+        cam = Camera.from_lookat((0.2, -0.3, -4.0), (0, 0, 0), (0, 1, 0), 0.9, w, h)
+        up = rng.standard_normal((h, w, 3))
+        out = rz.render_tiled(ref, ref_camera(cam), white)
+        gr = rz.render_backward(ref, ref_camera(cam), white, up, forward_out=out)
+        np.savez_compressed(
+            os.path.join(OUT, name), **sc.arrays(), w2c=cam.world_to_camera,
+            intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy]), size=np.array([cam.width, cam.height]),
+            bg=white, upstream=up, color=out.color, raw=out.raw_color, T=out.transmittance,
+            contributions=out.contributions, **{"g_" + k: v for k, v in gr.parameters().items()},
+            g_screen_grad_norm=gr.screen_grad_norm)
     print("golden vectors written to", OUT)
 
 

@@ -136,3 +136,19 @@ def test_bounds_worked_example():
     y0 = max(int(np.floor(mean[1] - ey)) - orc.BOUNDS_GUARD, 0)
     y1 = min(int(np.ceil(mean[1] + ey)) + orc.BOUNDS_GUARD, h - 1)
     assert (x0, x1, y0, y1) == (7, 13, 6, 14)
+
+
+@pytest.mark.parametrize("name", ["sb_small.npz", "sb_medium.npz"])
+def test_spherical_beta_matches_unmodified_reference(name):
+    """The oracle's Spherical-Beta path == the reference's own render_tiled / render_backward."""
+    g = golden(name)
+    scene, cam = golden_scene_camera(g)
+    out = orc.forward(scene, cam, g["bg"], core="c", threads=3)
+    np.testing.assert_array_equal(out["contributions"], g["contributions"])
+    np.testing.assert_array_equal(out["raw"], g["raw"])
+    grads = orc.backward(scene, cam, g["bg"], g["upstream"], out, core="c", threads=3)
+    for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "base_colors", "lobe_axes",
+              "lobe_colors"):
+        ref = g["g_" + k]
+        scale = max(np.abs(ref).max(), 1e-30)
+        np.testing.assert_allclose(grads[k], ref, rtol=1e-10, atol=1e-12 * scale, err_msg=k)
