@@ -55,40 +55,45 @@ __global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
     }
     if (lane == 31) s_warp[warp] = x;
     __syncthreads();
-    if (t == 0) {
-        unsigned long long run = 0;
-        for (int w = 0; w < BSR_BLOCK / 32; ++w) {
-            const unsigned long long c = s_warp[w];
-            s_warp[w] = run;
-            run += c;
+    if (warp == 0) {  // block total -> aggregate, warp-parallel look-back -> prefix
+        const unsigned long long mine = lane < BSR_BLOCK / 32 ? s_warp[lane] : 0ull;
+        unsigned long long incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
+        const unsigned long long run = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane < BSR_BLOCK / 32) s_warp[lane] = incl - mine;
         unsigned long long excl = 0;
         volatile unsigned long long *st = f.emit_status;
         if (part == 0) {
-            __threadfence();
-            st[0] = kFlag64Prefix | run;
-        } else {
-            __threadfence();
-            st[part] = kFlag64Agg | run;
-            for (int64_t j = part - 1; j >= 0;) {
-                const unsigned long long s = st[j];
-                if ((s & ~kValue64Mask) == 0) continue;
-                excl += s & kValue64Mask;
-                if (s & kFlag64Prefix) break;
-                --j;
+            if (lane == 0) {
+                __threadfence();
+                st[0] = kFlag64Prefix | run;
             }
-            __threadfence();
-            st[part] = kFlag64Prefix | (excl + run);
+        } else {
+            if (lane == 0) {
+                __threadfence();
+                st[part] = kFlag64Agg | run;
+            }
+            excl = warp_lookback<unsigned long long>(f.emit_status, part, 1, kFlag64Prefix, kValue64Mask);
+            if (lane == 0) {
+                __threadfence();
+                st[part] = kFlag64Prefix | (excl + run);
+            }
         }
-        s_excl = excl;
-        if (part == nparts - 1) {
-            const unsigned long long total = excl + run;
-            f.ctr->entries_needed = total;
-            if (total > (unsigned long long)f.entry_cap) {
-                f.ctr->entries = 0;
-                raise_status(&f.ctr->status, BSR_ERR_CAPACITY);
-            } else {
-                f.ctr->entries = (uint32_t)total;
+        if (lane == 0) {
+            s_excl = excl;
+            if (part == nparts - 1) {
+                const unsigned long long total = excl + run;
+                f.ctr->entries_needed = total;
+                if (total > (unsigned long long)f.entry_cap) {
+                    f.ctr->entries = 0;
+                    raise_status(&f.ctr->status, BSR_ERR_CAPACITY);
+                } else {
+                    f.ctr->entries = (uint32_t)total;
+                }
             }
         }
     }

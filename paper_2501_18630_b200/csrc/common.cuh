@@ -159,6 +159,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         }                                                                  \
     } while (0)
 
+// Warp-parallel decoupled look-back (called by ALL 32 lanes of one warp): lane l reads the
+// status of predecessor part-1-l, 32 predecessors per L2 round trip instead of one; the
+// nearest inclusive prefix ends the walk.  `stride` separates consecutive partitions.
+template <typename W>
+__device__ __forceinline__ W warp_lookback(const W *status, int64_t part, int64_t stride, W flag_prefix,
+                                           W value_mask) {
+    const int lane = threadIdx.x & 31;
+    W excl = 0;
+    int64_t hi = part - 1;
+    while (true) {
+        const int64_t j = hi - lane;
+        W s;
+        if (j >= 0) {
+            do {
+                s = *reinterpret_cast<const volatile W *>(status + j * stride);
+            } while ((s & ~value_mask) == 0);
+        } else {
+            s = flag_prefix;  // virtual inclusive prefix 0 before partition 0
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, (s & flag_prefix) != 0);
+        const int first = pm ? __ffs(pm) - 1 : 32;
+        W v = lane <= first ? (s & value_mask) : (W)0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pm) return excl;
+        hi -= 32;
+    }
+}
+
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __host__ __device__ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }

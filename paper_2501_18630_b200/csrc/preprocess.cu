@@ -177,24 +177,28 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
     if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
     __syncthreads();
-    if (tid == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < BSR_BLOCK / 32; ++w) {
-            uint32_t c = s_warp[w];
-            s_warp[w] = run;
-            run += c;
+    if (warp == 0) {  // block total -> aggregate, warp-parallel look-back -> prefix
+        const uint32_t mine = lane < BSR_BLOCK / 32 ? s_warp[lane] : 0u;
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        const uint32_t total = run;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane < BSR_BLOCK / 32) s_warp[lane] = incl - mine;
+        uint32_t excl = 0;
         if (part == 0) {
-            st_release(f.pre_status, kFlagPrefix | total);
-            s_excl = 0;
+            if (lane == 0) st_release(f.pre_status, kFlagPrefix | total);
         } else {
-            st_release(f.pre_status + part, kFlagAgg | total);
-            const uint32_t excl = lookback_exclusive(f.pre_status, (int)part);
-            st_release(f.pre_status + part, kFlagPrefix | (excl + total));
-            s_excl = excl;
+            if (lane == 0) st_release(f.pre_status + part, kFlagAgg | total);
+            excl = warp_lookback<uint32_t>(f.pre_status, part, 1, kFlagPrefix, kValueMask);
+            if (lane == 0) st_release(f.pre_status + part, kFlagPrefix | (excl + total));
         }
-        if (part == f.pre_parts - 1) f.ctr->visible = s_excl + total;
+        if (lane == 0) {
+            s_excl = excl;
+            if (part == f.pre_parts - 1) f.ctr->visible = excl + total;
+        }
     }
     __syncthreads();
     if (vis) {

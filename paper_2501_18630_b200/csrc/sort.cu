@@ -164,12 +164,22 @@ __global__ void __launch_bounds__(BSR_BLOCK) sort_pass_kernel(SortArgs<K> a, int
             st_release(st, kFlagPrefix | run);
         } else {
             st_release(st + part * 256, kFlagAgg | run);
-            for (int64_t j = part - 1; j >= 0;) {
-                const uint32_t s = ld_volatile(st + j * 256);
-                if ((s & ~kValueMask) == 0) continue;
-                excl += s & kValueMask;
-                if (s & kFlagPrefix) break;
-                --j;
+            // look back 8 predecessors per round trip (independent loads in flight)
+            for (int64_t hi = part - 1; hi >= 0; hi -= 8) {
+                uint32_t s[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s[q] = hi - q >= 0 ? ld_volatile(st + (hi - q) * 256) : kFlagPrefix;
+                bool done = false;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    while ((s[q] & ~kValueMask) == 0) s[q] = ld_volatile(st + (hi - q) * 256);
+                    excl += s[q] & kValueMask;
+                    if (s[q] & kFlagPrefix) {
+                        done = true;
+                        break;
+                    }
+                }
+                if (done) break;
             }
             st_release(st + part * 256, kFlagPrefix | (excl + run));
         }
