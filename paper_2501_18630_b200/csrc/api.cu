@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include "frame.cuh"
+#include "raster.cuh"
 
 namespace bsr {
 // kernel launchers (one per translation unit)
@@ -81,7 +82,7 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
                                                                 (b * ex + c * ey) * (2.0 * ey + 3.0))) * 1.5;
     const bool unsafe = (float)kr > kUnsafeR2Err;
     r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
-                      unsafe ? -(float)kr : (float)kr);
+                      record_err_word(kr, (double)r.b.z, unsafe));
     double *d = rec64 + kRec64 * k;
     d[0] = means[2 * k];
     d[1] = means[2 * k + 1];

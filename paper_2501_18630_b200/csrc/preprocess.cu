@@ -10,6 +10,7 @@
 #include "frame.cuh"
 #include "appearance.cuh"
 #include "project.cuh"
+#include "raster.cuh"
 
 namespace bsr {
 
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
             r.b = make_float4((float)p.cc, (float)o, (float)beta, (float)p.tz);
             const float kr = (float)r2_error_bound(p);
             unsafe = kr > kUnsafeR2Err;
-            r.c = make_float4(rgb[0], rgb[1], rgb[2], unsafe ? -kr : kr);
+            r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
             m64[0] = p.mx;
             m64[1] = p.my;
             m64[2] = p.ca;

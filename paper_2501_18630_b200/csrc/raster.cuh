@@ -77,12 +77,24 @@ __device__ __forceinline__ float pow_rel_err(float beta) {
     return beta == 4.0f ? 7.0f * kEps : (4.0f * fabsf(beta) + 2.0f) * 1.0e-6f + 3.0f * kEps;
 }
 
-// Rigorous relative error bound of the fp32 alpha versus the exact evaluation of the same
-// primitive: r2 error (<= kR, per primitive, preprocess.cu) propagated through
-// (1-x)^beta, plus the pow evaluation.  Used on the rare near-threshold paths.
-__device__ __forceinline__ float alpha_rel_err(const float4 B, const float4 C, const Pair &p) {
-    if (C.w < 0.f) return 8.0f * kEps;  // fp64-evaluated primitive
-    return B.z * C.w / fmaxf(p.om, 1e-30f) + pow_rel_err(B.z);
+// rcp.approx (relative error < 2^-22): only used inside error BOUNDS that carry a >= 1%
+// safety factor, never in a value that is composited
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Record error word (Record.c.w, written by preprocess / the core seam):
+//   Q = beta * kR + pow_rel_err(beta), rounded up, negative for fp32-unsafe primitives.
+// The fp32 alpha of a sample with 1 - x = om then has relative error
+//   <= beta kR / om + pow_rel_err(beta) <= Q / om        (om <= 1)
+// (kR = r2 error bound of the primitive, propagated through (1-x)^beta).
+__host__ __device__ inline float record_err_word(double kr, double beta, bool unsafe) {
+    const double pe = beta == 4.0 ? 7.0 * 5.9604644775390625e-08
+                                  : (4.0 * fabs(beta) + 2.0) * 1.0e-6 + 3.0 * 5.9604644775390625e-08;
+    const float q = (float)((beta * kr + pe) * (1.0 + 1e-6));
+    return unsafe ? -q : q;
 }
 
 // Same bound with the r2 error evaluated at this pixel instead of the footprint maximum
@@ -123,7 +135,8 @@ __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B
     // (o, beta as stored); relative slack 1e-4 covers the approximate lg2/ex2 and rounding
     if (B.y < alpha_min) return false;
     const float xmax = 1.0f - exp2f(__log2f(alpha_min / B.y) / B.z);
-    return q < fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.0f * fabsf(C.w) + 1e-4f;
+    // r2 slack 4 kR with kR <= |Q| / beta (record_err_word)
+    return q < fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.04f * fabsf(C.w) * rcp_approx(B.z) + 1e-4f;
 }
 
 __device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int Y0, int Y1) {

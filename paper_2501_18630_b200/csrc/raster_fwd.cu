@@ -41,10 +41,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // fp64 evaluation of an fp32-unsafe primitive, out of line so the common fp32 path is not
 // if-converted into predicated fp64 code
-__device__ __noinline__ Pair unsafe_pair_fwd(const double *m64, float4 B, int px, int py) {
-    return eval_pair64(m64, B, px, py);
+// (only alpha and 1 - x leave the call: the fp32 error bounds are not used for it)
+__device__ __noinline__ float2 unsafe_pair_fwd(const double *m64, float4 B, int px, int py) {
+    const Pair p = eval_pair64(m64, B, px, py);
+    return make_float2(p.alpha, p.om);
 }
 
+template <bool STATS, bool CONTRIB>
 __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
@@ -61,8 +64,8 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x, end = (int)range.y;
-    const bool want_contrib = a.out.contributions != nullptr;
-    const bool stats = a.stats != nullptr;
+    constexpr bool want_contrib = CONTRIB;
+    constexpr bool stats = STATS;
     const uint32_t lt_mask = (1u << lane) - 1u;
 
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
@@ -121,10 +124,13 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
                 const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
                 const bool unsafe = C.w < 0.f;
                 Pair p;
-                if (unsafe)  // uniform per entry
-                    p = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
-                else
+                if (unsafe) {  // uniform per entry
+                    const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
+                    p.alpha = u.x;
+                    p.om = u.y;
+                } else {
                     p = eval_pair(A, B, px - bd.x, py - bd.z);
+                }
                 bool ambiguous = false;
                 // rare path: alpha within 5% of the cutoff -> certify with the error bound
                 if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
@@ -136,9 +142,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
                     const float Tn = __fmul_rn(T, one_m);
                     // relative error bound of T: sum over samples of
                     //   alpha/(1-alpha) * rel_err(alpha) + rounding
-                    const float rel = unsafe ? 8.0f * kEps
-                                             : B.z * C.w * __frcp_rn(fmaxf(p.om, 1e-30f)) + pow_rel_err(B.z);
-                    const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * __frcp_rn(fmaxf(one_m, 1e-30f));
+                    // (record_err_word: rel(alpha) <= Q / om)
+                    const float rel = unsafe ? 8.0f * kEps : C.w * rcp_approx(fmaxf(p.om, 1e-30f));
+                    const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * rcp_approx(fmaxf(one_m, 1e-30f));
                     if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
                         ambiguous = true;
                     } else {
@@ -231,7 +237,14 @@ int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg
     a.ranges = ranges;
     a.rec = rec;
     a.stats = stats;
-    raster_fwd_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    if (stats && out.contributions)
+        raster_fwd_kernel<true, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    else if (stats)
+        raster_fwd_kernel<true, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    else if (out.contributions)
+        raster_fwd_kernel<false, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    else
+        raster_fwd_kernel<false, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
