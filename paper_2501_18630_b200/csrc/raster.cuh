@@ -10,6 +10,15 @@ namespace bsr {
 
 constexpr float kEps = 5.9604645e-08f;  // 2^-24
 
+// 16-byte global -> shared copies (record gathers, double-buffered)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 struct Pair {
     float dx, dy, r2, x, om, k, alpha;
 };

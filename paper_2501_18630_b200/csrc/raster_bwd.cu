@@ -62,11 +62,11 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
 // PIX pixels per thread (stacked vertically 4 rows apart): a warp owns an 8 x 4*PIX block,
 // so the per-(warp, entry) costs -- record loads, list walk, the reduction, the atomics --
 // are shared by 32*PIX pixels.
-template <int PIX, int MINB>
+template <int PIX, int MINB, bool STATS>
 __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(RasterBwdArgs a) {
     constexpr int NT = BSR_BLOCK / PIX, NW = NT / 32, WH = 4 * PIX;
-    __shared__ __align__(16) Record s_rec[BSR_BLOCK];
-    __shared__ uint32_t s_cidx[BSR_BLOCK];
+    __shared__ __align__(16) Record s_recb[2][BSR_BLOCK];
+    __shared__ uint32_t s_cidxb[2][BSR_BLOCK];
     __shared__ uint8_t s_list[NW][BSR_BLOCK];
     __shared__ int s_maxlast;
     const FrameView &f = a.f;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x;
-    const bool stats = a.stats != nullptr;
+    constexpr bool stats = STATS;
     const uint32_t lt_mask = (1u << lane) - 1u;
 
     int py[PIX], last[PIX];
@@ -123,16 +123,34 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
     const int maxlast = s_maxlast;
     uint32_t pairs = 0;
 
-    for (int hi = maxlast; hi > 0; hi -= BSR_BLOCK) {
+    // batches [lo, hi) walked from the back; the next (earlier) batch is gathered with
+    // cp.async while this one is processed
+    auto prefetch = [&](int hi, int buf) {
+        const int lo = max(0, hi - BSR_BLOCK);
+        for (int q = t; q < hi - lo; q += NT) {
+            const uint32_t c = lists[start + lo + q];
+            s_cidxb[buf][q] = c;
+            const Record *src = rec + c;
+            Record *dst = &s_recb[buf][q];
+            cp_async16(&dst->a, &src->a);
+            cp_async16(&dst->b, &src->b);
+            cp_async16(&dst->c, &src->c);
+            cp_async16(&dst->d, &src->d);
+        }
+        cp_async_commit();
+    };
+    if (maxlast > 0) prefetch(maxlast, 0);
+    int buf = 0;
+    for (int hi = maxlast; hi > 0; hi -= BSR_BLOCK, buf ^= 1) {
         const int lo = max(0, hi - BSR_BLOCK);
         const int nb = hi - lo;
+        const bool more = lo > 0;
+        __syncthreads();  // the buffer about to be refilled is no longer read
+        if (more) prefetch(lo, buf ^ 1);
+        if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncthreads();
-        for (int q = t; q < nb; q += NT) {
-            const uint32_t c = lists[start + lo + q];
-            s_cidx[q] = c;
-            s_rec[q] = rec[c];
-        }
-        __syncthreads();
+        const Record *s_rec = s_recb[buf];
+        const uint32_t *s_cidx = s_cidxb[buf];
         // ---- per-warp list: entries before the warp's furthest last contributor that
         //      reach its block (ascending; walked backwards)
         int nl = 0;
@@ -252,12 +270,14 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, c
         const char *e = getenv("BSR_BWD_VARIANT");
         return e ? atoi(e) : 0;
     }();
-    if (variant == 1)
-        raster_bwd_kernel<1, 4><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    if (stats)
+        raster_bwd_kernel<1, 3, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    else if (variant == 1)
+        raster_bwd_kernel<1, 4, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     else if (variant == 2)
-        raster_bwd_kernel<2, 5><<<f.n_tiles, BSR_BLOCK / 2, 0, st>>>(a);
+        raster_bwd_kernel<2, 5, false><<<f.n_tiles, BSR_BLOCK / 2, 0, st>>>(a);
     else
-        raster_bwd_kernel<1, 3><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+        raster_bwd_kernel<1, 3, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

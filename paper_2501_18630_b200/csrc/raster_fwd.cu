@@ -31,14 +31,6 @@ struct RasterFwdArgs {
     unsigned long long *stats;  // optional: [0] evaluated pairs, [1] contributions
 };
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 // fp64 evaluation of an fp32-unsafe primitive, out of line so the common fp32 path is not
 // if-converted into predicated fp64 code
 // (only alpha and 1 - x leave the call: the fp32 error bounds are not used for it)
