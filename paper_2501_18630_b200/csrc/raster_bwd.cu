@@ -32,6 +32,7 @@ struct RasterBwdArgs {
     const uint2 *ranges;
     const Record *rec;
     unsigned long long *stats;  // optional: [2] evaluated pairs
+    int direct_max;
 };
 
 // fp64 pair evaluation + the two conic-gradient terms for fp32-unsafe primitives; kept
@@ -59,12 +60,19 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// PIX pixels per thread (stacked vertically 4 rows apart): a warp owns an 8 x 4*PIX block,
-// so the per-(warp, entry) costs -- record loads, list walk, the reduction, the atomics --
-// are shared by 32*PIX pixels.
-template <int PIX, int MINB, bool STATS>
-__global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(RasterBwdArgs a) {
-    constexpr int NT = BSR_BLOCK / PIX, NW = NT / 32, WH = 4 * PIX;
+__device__ __forceinline__ float lg2_approx(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// One pixel per thread; a warp owns an 8x4 block.  The per-pair body is branch-free: a
+// lane that does not take the pair (outside its last contributor, alpha < alpha_min) runs
+// it with alpha = 0 and dL/dalpha = 0, which leaves its state (T, behind colour) exactly
+// unchanged and all 11 partials exactly 0.
+template <bool STATS>
+__global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
+    constexpr int NW = BSR_BLOCK / 32;
     __shared__ __align__(16) Record s_recb[2][BSR_BLOCK];
     __shared__ uint32_t s_cidxb[2][BSR_BLOCK];
     __shared__ uint8_t s_list[NW][BSR_BLOCK];
@@ -73,47 +81,35 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
     const int tile = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
-    const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * WH;
-    const int px = wx0 + (lane & 7);
+    const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
     const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x;
-    constexpr bool stats = STATS;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const int direct_max = a.direct_max;
 
-    int py[PIX], last[PIX];
-    float T[PIX], g0[PIX], g1[PIX], g2[PIX], gd[PIX], B0[PIX], B1[PIX], B2[PIX], BD[PIX];
-    int wlast = 0;
-#pragma unroll
-    for (int q = 0; q < PIX; ++q) {
-        py[q] = wy0 + (lane >> 3) + 4 * q;
-        last[q] = 0;
-        T[q] = 1.f;
-        g0[q] = g1[q] = g2[q] = gd[q] = 0.f;
-        B0[q] = a.bg[0];
-        B1[q] = a.bg[1];
-        B2[q] = a.bg[2];
-        BD[q] = 0.f;
-        if (px < f.W && py[q] < f.H) {
-            const int64_t pix = (int64_t)py[q] * f.W + px;
-            const uint32_t packed = f.last[pix];
-            last[q] = (int)(packed & 0x1FFFFFFFu);
-            if (last[q] > 0) {
-                T[q] = f.t_final[pix];
-                g0[q] = a.d_color[3 * pix];
-                g1[q] = a.d_color[3 * pix + 1];
-                g2[q] = a.d_color[3 * pix + 2];
-                if (a.use_mask) {
-                    if (packed & (1u << 29)) g0[q] = 0.f;
-                    if (packed & (1u << 30)) g1[q] = 0.f;
-                    if (packed & (1u << 31)) g2[q] = 0.f;
-                }
-                if (a.d_depth) gd[q] = a.d_depth[pix];
+    int last = 0;
+    float T = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, gd = 0.f, B0 = a.bg[0], B1 = a.bg[1], B2 = a.bg[2], BD = 0.f;
+    if (px < f.W && py < f.H) {
+        const int64_t pix = (int64_t)py * f.W + px;
+        const uint32_t packed = f.last[pix];
+        last = (int)(packed & 0x1FFFFFFFu);
+        if (last > 0) {
+            T = f.t_final[pix];
+            g0 = a.d_color[3 * pix];
+            g1 = a.d_color[3 * pix + 1];
+            g2 = a.d_color[3 * pix + 2];
+            if (a.use_mask) {
+                if (packed & (1u << 29)) g0 = 0.f;
+                if (packed & (1u << 30)) g1 = 0.f;
+                if (packed & (1u << 31)) g2 = 0.f;
             }
+            if (a.d_depth) gd = a.d_depth[pix];
         }
-        wlast = max(wlast, last[q]);
     }
+    int wlast = last;
     if (t == 0) s_maxlast = 0;
 #pragma unroll
     for (int o = 16; o; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
@@ -127,7 +123,7 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
     // cp.async while this one is processed
     auto prefetch = [&](int hi, int buf) {
         const int lo = max(0, hi - BSR_BLOCK);
-        for (int q = t; q < hi - lo; q += NT) {
+        for (int q = t; q < hi - lo; q += BSR_BLOCK) {
             const uint32_t c = lists[start + lo + q];
             s_cidxb[buf][q] = c;
             const Record *src = rec + c;
@@ -160,8 +156,8 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
                 bool hit = false;
                 if (j < nb && lo + j < wlast) {
                     const Record &r = s_rec[j];
-                    hit = stats ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + WH - 1)
-                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + WH - 1, a.alpha_min);
+                    hit = STATS ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
+                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3, a.alpha_min);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
                 if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
@@ -174,60 +170,49 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
             const int e = lo + j;  // local entry index
             const int4 bd = s_rec[j].d;
             const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
-            const bool unsafe = C.w < 0.f;  // uniform per entry
-            float v[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = 0.f;
-            bool took = false;
-#pragma unroll
-            for (int q = 0; q < PIX; ++q) {
-                if (e >= last[q]) continue;
-                if (stats) pairs += (px >= bd.x && px <= bd.y && py[q] >= bd.z && py[q] <= bd.w);
-                float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
-                Pair p;
-                if (unsafe) {
-                    p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py[q], &ga, &gb);
-                } else {
-                    p = eval_pair(A, Bq, px - bd.x, py[q] - bd.z);
-                    ga = A.z * p.dx + A.w * p.dy;
-                    gb = A.w * p.dx + Bq.x * p.dy;
-                }
-                if (!(p.alpha >= a.alpha_min)) continue;
-                took = true;
-                const float one_m = 1.0f - p.alpha;
-                T[q] = __fdividef(T[q], one_m);  // T_k
-                const float w = p.alpha * T[q];
-                const float dalpha = T[q] * (g0[q] * (C.x - B0[q]) + g1[q] * (C.y - B1[q]) +
-                                             g2[q] * (C.z - B2[q]) + gd[q] * (Bq.w - BD[q]));
-                B0[q] = p.alpha * C.x + one_m * B0[q];
-                B1[q] = p.alpha * C.y + one_m * B1[q];
-                B2[q] = p.alpha * C.z + one_m * B2[q];
-                BD[q] = p.alpha * Bq.w + one_m * BD[q];
-                v[7] += w * g0[q];
-                v[8] += w * g1[q];
-                v[9] += w * g2[q];
-                v[10] += w * gd[q];
-                v[5] += dalpha * p.k;
-                const float dk = dalpha * Bq.y;
-                if (p.x < 1.0f) {
-                    const float beta = Bq.z;
-                    // (1-x)^(beta-1) = k / (1-x); ln(1-x) via the XU pipe
-                    const float pw = beta == 4.0f ? p.om * p.om * p.om : p.k / p.om;
-                    v[6] += dk * p.k * __logf(p.om);
-                    float dkdx = -beta * pw;
-                    if (dkdx < -kEdgeGradClamp) dkdx = -kEdgeGradClamp;
-                    const float d_x = dk * dkdx;
-                    v[0] += -d_x * 2.0f * ga;
-                    v[1] += -d_x * 2.0f * gb;
-                    v[2] += d_x * p.dx * p.dx;
-                    v[3] += d_x * 2.0f * p.dx * p.dy;
-                    v[4] += d_x * p.dy * p.dy;
-                }
+            if (STATS) pairs += (e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
+            float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
+            Pair p;
+            if (C.w < 0.f) {  // fp32-unsafe primitive, uniform per entry
+                p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py, &ga, &gb);
+            } else {
+                p = eval_pair(A, Bq, px - bd.x, py - bd.z);
+                ga = A.z * p.dx + A.w * p.dy;
+                gb = A.w * p.dx + Bq.x * p.dy;
             }
+            const bool took = e < last && p.alpha >= a.alpha_min;
             const unsigned tm = __ballot_sync(0xffffffffu, took);
             if (!tm) continue;
+            const float alpha = took ? p.alpha : 0.f;
+            const float one_m = 1.0f - alpha;     // alpha <= 0.999 (forward flags larger)
+            T = took ? T * rcp_approx(one_m) : T;  // T_k
+            const float w = alpha * T;
+            float dalpha = T * (g0 * (C.x - B0) + g1 * (C.y - B1) + g2 * (C.z - B2) + gd * (Bq.w - BD));
+            dalpha = took ? dalpha : 0.f;
+            B0 = alpha * C.x + one_m * B0;
+            B1 = alpha * C.y + one_m * B1;
+            B2 = alpha * C.z + one_m * B2;
+            BD = alpha * Bq.w + one_m * BD;
+            // kernel derivative; a taken sample has alpha > 0, hence 1 - x > 0
+            const float beta = Bq.z;
+            const float om = fmaxf(p.om, 1e-30f);
+            const float pw = beta == 4.0f ? om * om * om : p.k * rcp_approx(om);  // (1-x)^(beta-1)
+            const float dk = dalpha * Bq.y;
+            const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
+            float v[16];
+            v[0] = -2.0f * d_x * ga;
+            v[1] = -2.0f * d_x * gb;
+            v[2] = d_x * p.dx * p.dx;
+            v[3] = 2.0f * d_x * p.dx * p.dy;
+            v[4] = d_x * p.dy * p.dy;
+            v[5] = dalpha * p.k;
+            v[6] = dk * p.k * (0.69314718f * lg2_approx(om));
+            v[7] = w * g0;
+            v[8] = w * g1;
+            v[9] = w * g2;
+            v[10] = w * gd;
             float *dst = f.grad_acc + (int64_t)s_cidx[j] * kGradStride;
-            if (__popc(tm) <= 2) {  // few contributors: direct atomics beat a 62-op reduction
+            if (__popc(tm) <= direct_max) {  // few contributors: direct atomics beat the reduction
                 if (took) {
 #pragma unroll
                     for (int q = 0; q < 11; ++q)
@@ -235,12 +220,14 @@ __global__ void __launch_bounds__(BSR_BLOCK / PIX, MINB) raster_bwd_kernel(Raste
                 }
                 continue;
             }
+#pragma unroll
+            for (int q = 11; q < 16; ++q) v[q] = 0.f;
             const float sum = warp_reduce16(v, lane);
             const int idx = (lane >> 1) & 15;
             if (!(lane & 1) && idx < 11 && sum != 0.0f) atomicAdd(dst + idx, sum);
         }
     }
-    if (stats) {
+    if (STATS) {
         unsigned long long p2 = pairs;
 #pragma unroll
         for (int o = 16; o; o >>= 1) p2 += __shfl_xor_sync(0xffffffffu, p2, o);
@@ -265,19 +252,17 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, c
     a.ranges = ranges;
     a.rec = rec;
     a.stats = stats;
-    // variant selection for A/B measurements (default: one pixel per thread, 3 CTAs/SM)
-    static const int variant = [] {
-        const char *e = getenv("BSR_BWD_VARIANT");
-        return e ? atoi(e) : 0;
+    // warps with at most this many contributing lanes add their partials with direct
+    // atomics instead of the 16-shuffle reduction (BSR_BWD_DIRECT overrides, for A/B)
+    static const int direct_max = [] {
+        const char *e = getenv("BSR_BWD_DIRECT");
+        return e ? atoi(e) : 2;
     }();
+    a.direct_max = direct_max;
     if (stats)
-        raster_bwd_kernel<1, 3, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else if (variant == 1)
-        raster_bwd_kernel<1, 4, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else if (variant == 2)
-        raster_bwd_kernel<2, 5, false><<<f.n_tiles, BSR_BLOCK / 2, 0, st>>>(a);
+        raster_bwd_kernel<true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     else
-        raster_bwd_kernel<1, 3, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+        raster_bwd_kernel<false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
