@@ -13,13 +13,17 @@
 
 namespace bsr {
 
-constexpr int kLT = 16;           // output tile edge
-constexpr int kHalo = 5;
-constexpr int kLI = kLT + 2 * kHalo;  // 26
+// Tiles of 32 x 16 outputs with a 5-pixel halo.  The Gaussian blur runs on packed FP32
+// pairs (FFMA2, sm_100): the maps kernel blurs (a, b) and (a^2, b^2) as pairs and a*b as a
+// scalar; the gradient kernel blurs (d_mu, d_qa) as a pair and d_qab as a scalar.  Each
+// thread produces two adjacent outputs per pass so the loaded taps are reused.
+constexpr int kTW = 32, kTH = 16, kHalo = 5;
+constexpr int kIW = kTW + 2 * kHalo, kIH = kTH + 2 * kHalo;  // 42 x 26
 
 struct LossArgs {
     const float *a, *b, *raw;
-    float *dmu, *dqa, *dqab;  // scratch maps (H,W,3)
+    float2 *pq;               // scratch planes [3][H][W]: (d_mu, d_qa)
+    float *px;                // scratch planes [3][H][W]: d_qab
     float *d_image;
     double *sums;             // [2][nblocks]: per-block sums of the ssim map and |a - b|
     int nblocks;
@@ -29,57 +33,99 @@ struct LossArgs {
     double lambda;
 };
 
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+
+// horizontal pass of one row item: 12 consecutive input pairs -> 2 outputs
+struct HPair {
+    float2 p0, p1, q0, q1;
+    float x0, x1;
+};
+
 __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
-    __shared__ float sa[3][kLI][kLI], sb[3][kLI][kLI];
-    __shared__ float h[5][kLI][kLT];
+    __shared__ float2 s_in[3][kIH][kIW];  // (a, b) per channel, zero outside the image
+    __shared__ float2 s_hp[kIH][kTW], s_hq[kIH][kTW];
+    __shared__ __align__(16) float s_hx[kIH][kTW];
     __shared__ double red[2][8];
-    const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
-    const int t = threadIdx.x, lx = t % kLT, ly = t / kLT;
-    const int x = tx0 + lx, y = ty0 + ly;
-    const bool in = x < p.W && y < p.H;
-    double s_sum = 0.0, l1_sum = 0.0;
-    // all three channels of the halo tile at once: one global-latency exposure per block
-    for (int i = t; i < kLI * kLI * 3; i += 256) {
-        const int px = i / 3, c = i - px * 3;
-        const int yy = ty0 - kHalo + px / kLI, xx = tx0 - kHalo + px % kLI;
-        const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
-        const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
-        sa[c][px / kLI][px % kLI] = ok ? p.a[o] : 0.f;
-        sb[c][px / kLI][px % kLI] = ok ? p.b[o] : 0.f;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
+    // rows of kIW pixels x 3 channels = 126 contiguous floats: two rows per pass
+    if (t < 2 * 3 * kIW) {
+        const int half = t / (3 * kIW), q = t - half * 3 * kIW;
+        const int c = q % 3, xx = q / 3, gx = x0 - kHalo + xx;
+        const bool okx = gx >= 0 && gx < p.W;
+        for (int r = half; r < kIH; r += 2) {
+            const int gy = y0 - kHalo + r;
+            float va = 0.f, vb = 0.f;
+            if (okx && gy >= 0 && gy < p.H) {
+                const int64_t o = ((int64_t)gy * p.W + gx) * 3 + c;
+                va = p.a[o];
+                vb = p.b[o];
+            }
+            s_in[c][r][xx] = make_float2(va, vb);
+        }
     }
+    float w[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) w[k] = p.w[k];
+    const int tx = t & 31, r0 = 2 * (t >> 5);
+    double s_sum = 0.0, l1_sum = 0.0;
     for (int c = 0; c < 3; ++c) {
         __syncthreads();
-        // horizontal pass over all kLI rows, kLT output columns
-        for (int i = t; i < kLI * kLT; i += 256) {
-            const int r = i / kLT, col = i % kLT;
-            float m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+        for (int it = t; it < kIH * (kTW / 2); it += 256) {
+            const int r = it >> 4, cp = it & 15;
+            float2 v[12], sq[12];
+            float xp[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) {
+                v[k] = s_in[c][r][2 * cp + k];
+                sq[k] = __fmul2_rn(v[k], v[k]);
+                xp[k] = v[k].x * v[k].y;
+            }
+            float2 p0 = f2(0.f), p1 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f);
+            float xa = 0.f, xb = 0.f;
 #pragma unroll
             for (int k = 0; k < 11; ++k) {
-                const float av = sa[c][r][col + k], bv = sb[c][r][col + k], wk = p.w[k];
-                m0 += wk * av;
-                m1 += wk * bv;
-                m2 += wk * av * av;
-                m3 += wk * bv * bv;
-                m4 += wk * av * bv;
+                const float2 wk = f2(w[k]);
+                p0 = __ffma2_rn(wk, v[k], p0);
+                p1 = __ffma2_rn(wk, v[k + 1], p1);
+                q0 = __ffma2_rn(wk, sq[k], q0);
+                q1 = __ffma2_rn(wk, sq[k + 1], q1);
+                xa = fmaf(w[k], xp[k], xa);
+                xb = fmaf(w[k], xp[k + 1], xb);
             }
-            h[0][r][col] = m0;
-            h[1][r][col] = m1;
-            h[2][r][col] = m2;
-            h[3][r][col] = m3;
-            h[4][r][col] = m4;
+            s_hp[r][2 * cp] = p0;
+            s_hp[r][2 * cp + 1] = p1;
+            s_hq[r][2 * cp] = q0;
+            s_hq[r][2 * cp + 1] = q1;
+            reinterpret_cast<float2 *>(&s_hx[r][0])[cp] = make_float2(xa, xb);
         }
         __syncthreads();
-        float mu_a = 0, mu_b = 0, qa = 0, qb = 0, qab = 0;
+        // vertical pass: column tx, output rows r0 and r0 + 1
+        float2 P0 = f2(0.f), P1 = f2(0.f), Q0 = f2(0.f), Q1 = f2(0.f);
+        float X0 = 0.f, X1 = 0.f;
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float wk = p.w[k];
-            mu_a += wk * h[0][ly + k][lx];
-            mu_b += wk * h[1][ly + k][lx];
-            qa += wk * h[2][ly + k][lx];
-            qb += wk * h[3][ly + k][lx];
-            qab += wk * h[4][ly + k][lx];
+        for (int k = 0; k < 12; ++k) {
+            const float2 hp = s_hp[r0 + k][tx], hq = s_hq[r0 + k][tx];
+            const float hx = s_hx[r0 + k][tx];
+            if (k < 11) {
+                const float2 wk = f2(w[k]);
+                P0 = __ffma2_rn(wk, hp, P0);
+                Q0 = __ffma2_rn(wk, hq, Q0);
+                X0 = fmaf(w[k], hx, X0);
+            }
+            if (k > 0) {
+                const float2 wk = f2(w[k - 1]);
+                P1 = __ffma2_rn(wk, hp, P1);
+                Q1 = __ffma2_rn(wk, hq, Q1);
+                X1 = fmaf(w[k - 1], hx, X1);
+            }
         }
-        if (in) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int x = x0 + tx, y = y0 + r0 + u;
+            if (x >= p.W || y >= p.H) continue;
+            const float2 P = u ? P1 : P0, Q = u ? Q1 : Q0;
+            const float qab = u ? X1 : X0;
+            const float mu_a = P.x, mu_b = P.y, qa = Q.x, qb = Q.y;
             const float C1 = 1e-4f, C2 = 9e-4f;
             const float var_b = qb - mu_b * mu_b;
             const float a1 = 2.f * mu_a * mu_b + C1;
@@ -87,13 +133,13 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
             const float b1 = mu_a * mu_a + mu_b * mu_b + C1;
             const float b2 = (qa - mu_a * mu_a) + var_b + C2;
             const float ib = 1.f / (b1 * b2);
-            const float s = a1 * a2 * ib;
-            const int64_t o = ((int64_t)y * p.W + x) * 3 + c;
-            p.dmu[o] = 2.f * mu_b * (a2 - a1) * ib - s * (2.f * mu_a / b1 - 2.f * mu_a / b2);
-            p.dqa[o] = -s / b2;
-            p.dqab[o] = 2.f * a1 * ib;
-            s_sum += s;
-            l1_sum += fabsf(sa[c][ly + kHalo][lx + kHalo] - sb[c][ly + kHalo][lx + kHalo]);
+            const float sv = a1 * a2 * ib;
+            const int64_t o = (int64_t)c * p.H * p.W + (int64_t)y * p.W + x;
+            p.pq[o] = make_float2(2.f * mu_b * (a2 - a1) * ib - sv * (2.f * mu_a / b1 - 2.f * mu_a / b2), -sv / b2);
+            p.px[o] = 2.f * a1 * ib;
+            s_sum += sv;
+            const float2 ctr = s_in[c][kHalo + r0 + u][kHalo + tx];
+            l1_sum += fabsf(ctr.x - ctr.y);
         }
     }
     // block reduction of the two sums
@@ -108,65 +154,99 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     }
     __syncthreads();
     if (t == 0) {  // per-block partials (no same-address atomics across 1e3+ blocks)
-        double s = 0, l = 0;
+        double sv = 0, l = 0;
         for (int i = 0; i < 8; ++i) {
-            s += red[0][i];
+            sv += red[0][i];
             l += red[1][i];
         }
         const int blk = blockIdx.y * gridDim.x + blockIdx.x;
-        p.sums[blk] = s;
+        p.sums[blk] = sv;
         p.sums[p.nblocks + blk] = l;
     }
 }
 
 __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
-    __shared__ float s[3][3][kLI][kLI];
-    __shared__ float h[3][kLI][kLT];
-    const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
-    const int t = threadIdx.x, lx = t % kLT, ly = t / kLT;
-    const int x = tx0 + lx, y = ty0 + ly;
-    const bool in = x < p.W && y < p.H;
+    __shared__ float2 s_p[kIH][kIW];  // (d_mu, d_qa) of the current channel
+    __shared__ float s_x[kIH][kIW];   // d_qab
+    __shared__ float2 s_hp[kIH][kTW];
+    __shared__ __align__(16) float s_hx[kIH][kTW];
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
     const double n = 3.0 * p.W * p.H;
     const float inv_n = (float)(1.0 / n);
     const float l1w = (float)((1.0 - p.lambda) / n), sw = (float)p.lambda;
-    for (int i = t; i < kLI * kLI * 3; i += 256) {
-        const int px = i / 3, c = i - px * 3;
-        const int yy = ty0 - kHalo + px / kLI, xx = tx0 - kHalo + px % kLI;
-        const bool ok = xx >= 0 && yy >= 0 && xx < p.W && yy < p.H;
-        const int64_t o = ((int64_t)yy * p.W + xx) * 3 + c;
-        s[c][0][px / kLI][px % kLI] = ok ? p.dmu[o] : 0.f;
-        s[c][1][px / kLI][px % kLI] = ok ? p.dqa[o] : 0.f;
-        s[c][2][px / kLI][px % kLI] = ok ? p.dqab[o] : 0.f;
-    }
+    float w[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) w[k] = p.w[k];
+    const int tx = t & 31, r0 = 2 * (t >> 5);
+    const int lrow = t / kIW, lcol = t - lrow * kIW;  // load mapping: 6 rows of 42 per pass
+    const int64_t plane = (int64_t)p.H * p.W;
     for (int c = 0; c < 3; ++c) {
         __syncthreads();
-        for (int i = t; i < kLI * kLT; i += 256) {
-            const int r = i / kLT, col = i % kLT;
-            float m0 = 0, m1 = 0, m2 = 0;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                const float wk = p.w[k];
-                m0 += wk * s[c][0][r][col + k];
-                m1 += wk * s[c][1][r][col + k];
-                m2 += wk * s[c][2][r][col + k];
+        if (t < 6 * kIW) {
+            const int gx = x0 - kHalo + lcol;
+            const bool okx = gx >= 0 && gx < p.W;
+            for (int r = lrow; r < kIH; r += 6) {
+                const int gy = y0 - kHalo + r;
+                float2 vp = f2(0.f);
+                float vx = 0.f;
+                if (okx && gy >= 0 && gy < p.H) {
+                    const int64_t o = c * plane + (int64_t)gy * p.W + gx;
+                    vp = p.pq[o];
+                    vx = p.px[o];
+                }
+                s_p[r][lcol] = vp;
+                s_x[r][lcol] = vx;
             }
-            h[0][r][col] = m0;
-            h[1][r][col] = m1;
-            h[2][r][col] = m2;
         }
         __syncthreads();
-        float b0 = 0, b1 = 0, b2 = 0;
+        for (int it = t; it < kIH * (kTW / 2); it += 256) {
+            const int r = it >> 4, cp = it & 15;
+            float2 v[12];
+            float u[12];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float wk = p.w[k];
-            b0 += wk * h[0][ly + k][lx];
-            b1 += wk * h[1][ly + k][lx];
-            b2 += wk * h[2][ly + k][lx];
+            for (int k = 0; k < 12; ++k) {
+                v[k] = s_p[r][2 * cp + k];
+                u[k] = s_x[r][2 * cp + k];
+            }
+            float2 p0 = f2(0.f), p1 = f2(0.f);
+            float xa = 0.f, xb = 0.f;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                const float2 wk = f2(w[k]);
+                p0 = __ffma2_rn(wk, v[k], p0);
+                p1 = __ffma2_rn(wk, v[k + 1], p1);
+                xa = fmaf(w[k], u[k], xa);
+                xb = fmaf(w[k], u[k + 1], xb);
+            }
+            s_hp[r][2 * cp] = p0;
+            s_hp[r][2 * cp + 1] = p1;
+            reinterpret_cast<float2 *>(&s_hx[r][0])[cp] = make_float2(xa, xb);
         }
-        if (in) {
+        __syncthreads();
+        float2 P0 = f2(0.f), P1 = f2(0.f);
+        float X0 = 0.f, X1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            const float2 hp = s_hp[r0 + k][tx];
+            const float hx = s_hx[r0 + k][tx];
+            if (k < 11) {
+                P0 = __ffma2_rn(f2(w[k]), hp, P0);
+                X0 = fmaf(w[k], hx, X0);
+            }
+            if (k > 0) {
+                P1 = __ffma2_rn(f2(w[k - 1]), hp, P1);
+                X1 = fmaf(w[k - 1], hx, X1);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int x = x0 + tx, y = y0 + r0 + q;
+            if (x >= p.W || y >= p.H) continue;
+            const float2 P = q ? P1 : P0;
+            const float b2 = q ? X1 : X0;
             const int64_t o = ((int64_t)y * p.W + x) * 3 + c;
             const float av = p.a[o], bv = p.b[o];
-            const float grad = (b0 + 2.f * av * b1 + bv * b2) * inv_n;
+            const float grad = (P.x + 2.f * av * P.y + bv * b2) * inv_n;
             const float diff = av - bv;
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
             float d = l1w * sgn - sw * grad;
@@ -213,8 +293,9 @@ using namespace bsr;
 
 extern "C" int bsr_loss_scratch_bytes(int32_t width, int32_t height, uint64_t *bytes) {
     if (!bytes || width < 11 || height < 11) return BSR_ERR_BAD_ARG;
-    const uint64_t nb = (uint64_t)div_up(width, kLT) * div_up(height, kLT);
-    *bytes = align_up(3ull * 4 * 3 * (uint64_t)width * height, 256) + align_up(16ull * nb, 256);
+    const uint64_t nb = (uint64_t)div_up(width, kTW) * div_up(height, kTH);
+    const uint64_t plane = 3ull * width * height;
+    *bytes = align_up(16ull * nb, 256) + align_up(8ull * plane, 256) + align_up(4ull * plane, 256);
     return BSR_OK;
 }
 
@@ -229,11 +310,10 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     LossArgs p;
     const uint64_t plane = 3ull * width * height;
     char *base = (char *)scratch;
-    p.nblocks = (int)(div_up(width, kLT) * div_up(height, kLT));
+    p.nblocks = (int)(div_up(width, kTW) * div_up(height, kTH));
     p.sums = (double *)base;
-    p.dmu = (float *)(base + align_up(16ull * p.nblocks, 256));
-    p.dqa = p.dmu + plane;
-    p.dqab = p.dqa + plane;
+    p.pq = (float2 *)(base + align_up(16ull * p.nblocks, 256));
+    p.px = (float *)((char *)p.pq + align_up(8ull * plane, 256));
     p.a = rendered;
     p.b = target;
     p.raw = raw;
@@ -249,7 +329,7 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
         sum += w[i];
     }
     for (int i = 0; i < 11; ++i) p.w[i] = (float)(w[i] / sum);
-    dim3 grid((unsigned)div_up(width, kLT), (unsigned)div_up(height, kLT));
+    dim3 grid((unsigned)div_up(width, kTW), (unsigned)div_up(height, kTH));
     ssim_maps_kernel<<<grid, 256, 0, st>>>(p);
     ssim_grad_kernel<<<grid, 256, 0, st>>>(p);
     loss_finish_kernel<<<1, 256, 0, st>>>(p);
