@@ -320,7 +320,7 @@ def kernel_launches_per_step(w):
     fwd = 1 + (2 + 4 + 1) + 2 + (2 + tile_passes) + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
-    per_view = fwd + 3 + 4  # + loss (maps, grad, finish) + backward (zero, raster, replay, chain)
+    per_view = fwd + 2 + 4  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain)
     return per_view * len(w["cams"]) + (1 if w["adam"] else 0)
 
 

@@ -35,6 +35,17 @@ struct LossArgs {
 
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
+// 4 / 8-byte cp.async with zero fill (src_bytes = 0 -> the destination is zeroed)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void *smem, const void *gmem, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES),
+                 "r"(ok ? BYTES : 0));
+}
+__device__ __forceinline__ void cp_async_commit_l() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_l() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // horizontal pass of one row item: 12 consecutive input pairs -> 2 outputs
 struct HPair {
     float2 p0, p1, q0, q1;
@@ -48,21 +59,22 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     __shared__ double red[2][8];
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
     // rows of kIW pixels x 3 channels = 126 contiguous floats: two rows per pass
+    // (asynchronous copies: all 26 rows in flight at once, zero fill outside the image)
     if (t < 2 * 3 * kIW) {
         const int half = t / (3 * kIW), q = t - half * 3 * kIW;
         const int c = q % 3, xx = q / 3, gx = x0 - kHalo + xx;
         const bool okx = gx >= 0 && gx < p.W;
+#pragma unroll
         for (int r = half; r < kIH; r += 2) {
             const int gy = y0 - kHalo + r;
-            float va = 0.f, vb = 0.f;
-            if (okx && gy >= 0 && gy < p.H) {
-                const int64_t o = ((int64_t)gy * p.W + gx) * 3 + c;
-                va = p.a[o];
-                vb = p.b[o];
-            }
-            s_in[c][r][xx] = make_float2(va, vb);
+            const bool ok = okx && gy >= 0 && gy < p.H;
+            const int64_t o = ok ? ((int64_t)gy * p.W + gx) * 3 + c : 0;
+            cp_async_zfill<4>(&s_in[c][r][xx].x, p.a + o, ok);
+            cp_async_zfill<4>(&s_in[c][r][xx].y, p.b + o, ok);
         }
     }
+    cp_async_commit_l();
+    cp_async_wait_l<0>();
     float w[11];
 #pragma unroll
     for (int k = 0; k < 11; ++k) w[k] = p.w[k];
@@ -165,12 +177,46 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     }
 }
 
+// loss = (1 - lambda) L1 + lambda (1 - SSIM) from the maps kernel's per-block partials
+// (run by block (0, 0) of the gradient kernel, which is stream-ordered after all of them)
+__device__ __forceinline__ void loss_finish(const LossArgs &p) {
+    __shared__ double red[2][8];
+    double sv = 0, l = 0;
+    for (int i = threadIdx.x; i < p.nblocks; i += 256) {
+        sv += p.sums[i];
+        l += p.sums[p.nblocks + i];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sv;
+        red[1][threadIdx.x >> 5] = l;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sv = l = 0;
+        for (int i = 0; i < 8; ++i) {
+            sv += red[0][i];
+            l += red[1][i];
+        }
+        const double n = 3.0 * p.W * p.H;
+        const double ssim = sv / n, l1 = l / n;
+        p.loss_out[0] = (1.0 - p.lambda) * l1 + p.lambda * (1.0 - ssim);
+        p.loss_out[1] = l1;
+        p.loss_out[2] = ssim;
+    }
+}
+
 __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
-    __shared__ float2 s_p[kIH][kIW];  // (d_mu, d_qa) of the current channel
-    __shared__ float s_x[kIH][kIW];   // d_qab
+    __shared__ float2 s_p[2][kIH][kIW];  // (d_mu, d_qa), double-buffered over channels
+    __shared__ float s_x[2][kIH][kIW];   // d_qab
     __shared__ float2 s_hp[kIH][kTW];
     __shared__ __align__(16) float s_hx[kIH][kTW];
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
+    if (blockIdx.x == 0 && blockIdx.y == 0) loss_finish(p);
     const double n = 3.0 * p.W * p.H;
     const float inv_n = (float)(1.0 / n);
     const float l1w = (float)((1.0 - p.lambda) / n), sw = (float)p.lambda;
@@ -180,23 +226,44 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
     const int tx = t & 31, r0 = 2 * (t >> 5);
     const int lrow = t / kIW, lcol = t - lrow * kIW;  // load mapping: 6 rows of 42 per pass
     const int64_t plane = (int64_t)p.H * p.W;
-    for (int c = 0; c < 3; ++c) {
-        __syncthreads();
+    auto load_plane = [&](int c, int buf) {
         if (t < 6 * kIW) {
             const int gx = x0 - kHalo + lcol;
             const bool okx = gx >= 0 && gx < p.W;
+#pragma unroll
             for (int r = lrow; r < kIH; r += 6) {
                 const int gy = y0 - kHalo + r;
-                float2 vp = f2(0.f);
-                float vx = 0.f;
-                if (okx && gy >= 0 && gy < p.H) {
-                    const int64_t o = c * plane + (int64_t)gy * p.W + gx;
-                    vp = p.pq[o];
-                    vx = p.px[o];
-                }
-                s_p[r][lcol] = vp;
-                s_x[r][lcol] = vx;
+                const bool ok = okx && gy >= 0 && gy < p.H;
+                const int64_t o = ok ? c * plane + (int64_t)gy * p.W + gx : 0;
+                cp_async_zfill<8>(&s_p[buf][r][lcol], p.pq + o, ok);
+                cp_async_zfill<4>(&s_x[buf][r][lcol], p.px + o, ok);
             }
+        }
+        cp_async_commit_l();
+    };
+    load_plane(0, 0);
+    for (int c = 0; c < 3; ++c) {
+        const int buf = c & 1;
+        // centre values for the epilogue, in flight during the blur
+        float av[2], bv[2], rv[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int x = x0 + tx, y = y0 + r0 + q;
+            av[q] = bv[q] = 0.f;
+            rv[q] = 1.f;
+            if (x < p.W && y < p.H) {
+                const int64_t o = ((int64_t)y * p.W + x) * 3 + c;
+                av[q] = p.a[o];
+                bv[q] = p.b[o];
+                if (p.raw) rv[q] = p.raw[o];
+            }
+        }
+        __syncthreads();  // buffer buf ^ 1 and s_hp / s_hx are free
+        if (c < 2) {
+            load_plane(c + 1, buf ^ 1);
+            cp_async_wait_l<1>();
+        } else {
+            cp_async_wait_l<0>();
         }
         __syncthreads();
         for (int it = t; it < kIH * (kTW / 2); it += 256) {
@@ -205,8 +272,8 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
             float u[12];
 #pragma unroll
             for (int k = 0; k < 12; ++k) {
-                v[k] = s_p[r][2 * cp + k];
-                u[k] = s_x[r][2 * cp + k];
+                v[k] = s_p[buf][r][2 * cp + k];
+                u[k] = s_x[buf][r][2 * cp + k];
             }
             float2 p0 = f2(0.f), p1 = f2(0.f);
             float xa = 0.f, xb = 0.f;
@@ -244,46 +311,13 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
             if (x >= p.W || y >= p.H) continue;
             const float2 P = q ? P1 : P0;
             const float b2 = q ? X1 : X0;
-            const int64_t o = ((int64_t)y * p.W + x) * 3 + c;
-            const float av = p.a[o], bv = p.b[o];
-            const float grad = (P.x + 2.f * av * P.y + bv * b2) * inv_n;
-            const float diff = av - bv;
+            const float grad = (P.x + 2.f * av[q] * P.y + bv[q] * b2) * inv_n;
+            const float diff = av[q] - bv[q];
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
             float d = l1w * sgn - sw * grad;
-            if (p.raw && !(p.raw[o] >= 0.f)) d = 0.f;
-            p.d_image[o] = d;
+            if (!(rv[q] >= 0.f)) d = 0.f;
+            p.d_image[((int64_t)y * p.W + x) * 3 + c] = d;
         }
-    }
-}
-
-__global__ void __launch_bounds__(256) loss_finish_kernel(LossArgs p) {
-    __shared__ double red[2][8];
-    double sv = 0, l = 0;
-    for (int i = threadIdx.x; i < p.nblocks; i += 256) {
-        sv += p.sums[i];
-        l += p.sums[p.nblocks + i];
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        sv += __shfl_xor_sync(0xffffffffu, sv, o);
-        l += __shfl_xor_sync(0xffffffffu, l, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = sv;
-        red[1][threadIdx.x >> 5] = l;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        sv = l = 0;
-        for (int i = 0; i < 8; ++i) {
-            sv += red[0][i];
-            l += red[1][i];
-        }
-        const double n = 3.0 * p.W * p.H;
-        const double ssim = sv / n, l1 = l / n;
-        p.loss_out[0] = (1.0 - p.lambda) * l1 + p.lambda * (1.0 - ssim);
-        p.loss_out[1] = l1;
-        p.loss_out[2] = ssim;
     }
 }
 
@@ -332,7 +366,6 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     dim3 grid((unsigned)div_up(width, kTW), (unsigned)div_up(height, kTH));
     ssim_maps_kernel<<<grid, 256, 0, st>>>(p);
     ssim_grad_kernel<<<grid, 256, 0, st>>>(p);
-    loss_finish_kernel<<<1, 256, 0, st>>>(p);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -127,7 +127,8 @@ __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B
     const float mx = (float)D.x + A.x, my = (float)D.z + A.y;
     if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
     const float a = A.z, b = A.w, c = B.x;
-    const float ia = 1.0f / a, ic = 1.0f / c;
+    // approximate reciprocals only perturb the edge minimiser (second-order in q)
+    const float ia = rcp_approx(a), ic = rcp_approx(c);
     float q = 3.0e38f;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -143,7 +144,7 @@ __device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B
     // a sample can only pass alpha >= alpha_min where r2 < x_max = 1 - (alpha_min / o)^(1/beta)
     // (o, beta as stored); relative slack 1e-4 covers the approximate lg2/ex2 and rounding
     if (B.y < alpha_min) return false;
-    const float xmax = 1.0f - exp2f(__log2f(alpha_min / B.y) / B.z);
+    const float xmax = 1.0f - exp2f(__log2f(__fdividef(alpha_min, B.y)) * rcp_approx(B.z));
     // r2 slack 4 kR with kR <= |Q| / beta (record_err_word)
     return q < fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.04f * fabsf(C.w) * rcp_approx(B.z) + 1e-4f;
 }
