@@ -30,37 +30,61 @@ __device__ __forceinline__ float group_lr(const AdamArgs &a, int64_t i) {
 }
 
 __device__ __forceinline__ void adam1(const AdamArgs &a, float &p, float g, float &m, float &v,
-                                      float lr) {
+                                      float lr, float inv_c1, float inv_c2) {
     m = a.b1 * m + a.omb1 * g;
     v = a.b2 * v + a.omb2 * g * g;
-    p -= lr * (m * a.inv_c1) / (sqrtf(v * a.inv_c2) + a.eps);
+    p -= lr * __fdividef(m * inv_c1, sqrtf(v * inv_c2) + a.eps);
 }
 
+// Two float4 per thread, all loads issued before any arithmetic (bytes in flight);
+// ALIGNED4: every group boundary is a multiple of 4 (the flat 16-byte group layout of
+// primitive.py), so one learning rate serves a whole float4.
+template <bool ALIGNED4>
 __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
-    if (a.step_dev) {  // bias corrections from the device-side step (next value)
-        const double st = (double)(*a.step_dev + 1);
-        a.inv_c1 = (float)(1.0 / (1.0 - pow(a.beta1, st)));
-        a.inv_c2 = (float)(1.0 / (1.0 - pow(a.beta2, st)));
+    __shared__ float s_c[2];
+    if (threadIdx.x == 0) {
+        float c1 = a.inv_c1, c2 = a.inv_c2;
+        if (a.step_dev) {  // bias corrections from the device-side step (next value)
+            const double st = (double)(*a.step_dev + 1);
+            c1 = (float)(1.0 / (1.0 - pow(a.beta1, st)));
+            c2 = (float)(1.0 / (1.0 - pow(a.beta2, st)));
+        }
+        s_c[0] = c1;
+        s_c[1] = c2;
     }
+    __syncthreads();
+    const float inv_c1 = s_c[0], inv_c2 = s_c[1];
     const int64_t n4 = a.count / 4;
-    const int64_t stride = (int64_t)gridDim.x * BSR_BLOCK;
-    for (int64_t q = blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x; q < n4; q += stride) {
-        float4 p = reinterpret_cast<float4 *>(a.p)[q];
-        const float4 g = reinterpret_cast<const float4 *>(a.g)[q];
-        float4 m = reinterpret_cast<float4 *>(a.m)[q];
-        float4 v = reinterpret_cast<float4 *>(a.v)[q];
-        const int64_t i = 4 * q;
-        adam1(a, p.x, g.x, m.x, v.x, group_lr(a, i));
-        adam1(a, p.y, g.y, m.y, v.y, group_lr(a, i + 1));
-        adam1(a, p.z, g.z, m.z, v.z, group_lr(a, i + 2));
-        adam1(a, p.w, g.w, m.w, v.w, group_lr(a, i + 3));
-        reinterpret_cast<float4 *>(a.p)[q] = p;
-        reinterpret_cast<float4 *>(a.m)[q] = m;
-        reinterpret_cast<float4 *>(a.v)[q] = v;
+    const int64_t q0 = blockIdx.x * (int64_t)(2 * BSR_BLOCK) + threadIdx.x;
+    float4 p[2], g[2], m[2], v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + u * BSR_BLOCK;
+        if (q < n4) {
+            p[u] = reinterpret_cast<const float4 *>(a.p)[q];
+            g[u] = reinterpret_cast<const float4 *>(a.g)[q];
+            m[u] = reinterpret_cast<const float4 *>(a.m)[q];
+            v[u] = reinterpret_cast<const float4 *>(a.v)[q];
+        }
     }
-    const int64_t tail = 4 * n4 + blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x;
-    if (tail < a.count && tail < 4 * n4 + 4)
-        adam1(a, a.p[tail], a.g[tail], a.m[tail], a.v[tail], group_lr(a, tail));
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + u * BSR_BLOCK;
+        if (q >= n4) continue;
+        const int64_t i = 4 * q;
+        const float l0 = group_lr(a, i);
+        adam1(a, p[u].x, g[u].x, m[u].x, v[u].x, l0, inv_c1, inv_c2);
+        adam1(a, p[u].y, g[u].y, m[u].y, v[u].y, ALIGNED4 ? l0 : group_lr(a, i + 1), inv_c1, inv_c2);
+        adam1(a, p[u].z, g[u].z, m[u].z, v[u].z, ALIGNED4 ? l0 : group_lr(a, i + 2), inv_c1, inv_c2);
+        adam1(a, p[u].w, g[u].w, m[u].w, v[u].w, ALIGNED4 ? l0 : group_lr(a, i + 3), inv_c1, inv_c2);
+        reinterpret_cast<float4 *>(a.p)[q] = p[u];
+        reinterpret_cast<float4 *>(a.m)[q] = m[u];
+        reinterpret_cast<float4 *>(a.v)[q] = v[u];
+    }
+    if (blockIdx.x == 0 && threadIdx.x < a.count - 4 * n4) {  // tail (< 4 elements)
+        const int64_t i = 4 * n4 + threadIdx.x;
+        adam1(a, a.p[i], a.g[i], a.m[i], a.v[i], group_lr(a, i), inv_c1, inv_c2);
+    }
 }
 
 __global__ void adam_bump_kernel(int64_t *step) { *step += 1; }
@@ -100,8 +124,13 @@ static int adam_impl(float *params, const float *grads, float *exp_avg, float *e
     a.beta1 = beta1;
     a.beta2 = beta2;
     const int64_t n4 = count / 4;
-    const unsigned blocks = (unsigned)imax64(1, imin64(div_up(imax64(n4, 1), BSR_BLOCK), 148 * 8));
-    adam_kernel<<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
+    const unsigned blocks = (unsigned)imax64(1, div_up(imax64(n4, 1), 2 * BSR_BLOCK));
+    bool aligned4 = true;
+    for (int k = 0; k < n_groups - 1; ++k) aligned4 = aligned4 && (group_end[k] % 4 == 0);
+    if (aligned4)
+        adam_kernel<true><<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
+    else
+        adam_kernel<false><<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
     if (step_dev) adam_bump_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_dev);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
