@@ -12,14 +12,14 @@
 
 namespace bsr {
 
-constexpr int kEmitItems = 16;
 constexpr uint32_t kBigRect = 64;  // rectangles with more tiles are emitted by a whole CTA
-constexpr int kEmitTile = BSR_BLOCK * kEmitItems;
 constexpr unsigned long long kFlag64Agg = 1ull << 62;
 constexpr unsigned long long kFlag64Prefix = 2ull << 62;
 constexpr unsigned long long kValue64Mask = (1ull << 62) - 1;
 
+template <int kEmitItems>
 __global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
+    constexpr int kEmitTile = BSR_BLOCK * kEmitItems;
     __shared__ uint32_t s_part;
     __shared__ unsigned long long s_warp[BSR_BLOCK / 32], s_excl;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
     if (base >= (int64_t)V) return;
     const int64_t nparts = div_up(V, kEmitTile);
     const uint32_t *perm = f.dvals[f.ctr->depth_plan[kDepthPasses] & 1u];
-    // blocked arrangement: thread t owns ranks base + t*16 .. +16
+    // blocked arrangement: thread t owns ranks base + t*ITEMS .. +ITEMS
     uint32_t cidx[kEmitItems], cnt[kEmitItems];
     unsigned long long tsum = 0;
 #pragma unroll
@@ -158,7 +158,10 @@ __global__ void tile_ranges_kernel(FrameView f) {
 
 int launch_emit(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    emit_kernel<<<(unsigned)div_up(f.n, kEmitTile), BSR_BLOCK, 0, st>>>(f);
+    if (f.depth_items == 4)
+        emit_kernel<4><<<(unsigned)div_up(f.n, BSR_BLOCK * 4), BSR_BLOCK, 0, st>>>(f);
+    else
+        emit_kernel<16><<<(unsigned)div_up(f.n, BSR_BLOCK * 16), BSR_BLOCK, 0, st>>>(f);
     emit_big_kernel<<<148 * 4, BSR_BLOCK, 0, st>>>(f);
     BSR_LAUNCH_CHECK();
     return BSR_OK;

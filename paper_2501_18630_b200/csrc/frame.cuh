@@ -7,8 +7,10 @@
 
 namespace bsr {
 
-constexpr int kSortItems = 16;                       // keys per thread in a sort pass
-constexpr int kSortTile = BSR_BLOCK * kSortItems;    // 4096 keys per partition
+// Keys per thread in a sort / emit partition: 16 (4096 per CTA) for large inputs, 4 (1024
+// per CTA) while the input would give fewer than ~2 CTAs per SM at 16.
+constexpr int64_t kSmallSortCap = 148 * 2 * 4096;
+inline int sort_items(int64_t cap) { return cap <= kSmallSortCap ? 4 : 16; }
 constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
 constexpr int kRec64 = 8;                            // doubles per fp64 side record
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
@@ -64,6 +66,7 @@ struct FrameView {
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles, tile_passes;
     int64_t pre_parts, depth_parts, tile_parts;
+    int depth_items, tile_items;  // sort_items() of the depth sort / emission and the tile sort
     uint64_t zero_bytes, total_bytes;
 };
 
@@ -85,8 +88,10 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.n_tiles = f.tiles_x * f.tiles_y;
     f.tile_passes = tile_key_passes(f.n_tiles);
     f.pre_parts = div_up(n > 0 ? n : 1, BSR_BLOCK);
-    f.depth_parts = div_up(n > 0 ? n : 1, kSortTile);
-    f.tile_parts = div_up(entry_cap > 0 ? entry_cap : 1, kSortTile);
+    f.depth_items = sort_items(n);
+    f.tile_items = sort_items(entry_cap);
+    f.depth_parts = div_up(n > 0 ? n : 1, (int64_t)BSR_BLOCK * f.depth_items);
+    f.tile_parts = div_up(entry_cap > 0 ? entry_cap : 1, (int64_t)BSR_BLOCK * f.tile_items);
     const int64_t npx = (int64_t)W * H;
     uint64_t off = 0;
     char *b = static_cast<char *>(base);

@@ -31,6 +31,7 @@ struct SortArgs {
     uint32_t *status;                 // [passes][max_parts][256], zeroed
     uint32_t *tickets;                // [passes], zeroed
     int passes;
+    int items;                        // keys per thread (4 or 16), see sort_items()
     int64_t max_parts;
 };
 
@@ -96,8 +97,9 @@ __global__ void __launch_bounds__(BSR_BLOCK) sort_plan_kernel(SortArgs<K> a) {
     if (t == 0) a.plan[a.passes] = cur;
 }
 
-template <typename K>
+template <typename K, int kSortItems>
 __global__ void __launch_bounds__(BSR_BLOCK) sort_pass_kernel(SortArgs<K> a, int pass) {
+    constexpr int kSortTile = BSR_BLOCK * kSortItems;
     const uint32_t plan = a.plan[pass];
     if (!(plan & 0x100u)) return;
     const uint32_t src = plan & 1u;
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) sort_pass_kernel(SortArgs<K> a, int
     uint32_t *vals_out = a.vals[src ^ 1u];
 #pragma unroll 4
     for (int i = 0; i < kSortItems; ++i) {
-        const int pos = i * BSR_BLOCK + t;
+        const int pos = i * BSR_BLOCK + t;  // (coalesced within each digit run)
         if (pos < cnt) {
             const K key = s_keys[pos];
             const uint32_t dg = digit_of(key, bias, pass);
@@ -229,26 +231,33 @@ __global__ void __launch_bounds__(BSR_BLOCK) sort_pass_kernel(SortArgs<K> a, int
     }
 }
 
-template <typename K>
+template <typename K, int ITEMS>
 size_t sort_smem_bytes() {
-    return (size_t)kSortTile * (sizeof(K) + 4) + 4 * (8 * 256 + 256 + 256);
+    return (size_t)BSR_BLOCK * ITEMS * (sizeof(K) + 4) + 4 * (8 * 256 + 256 + 256);
+}
+
+template <typename K, int ITEMS>
+static int launch_passes(const SortArgs<K> &a, int64_t cap, cudaStream_t st) {
+    static bool attr_set = false;  // idempotent attribute, safe to race
+    const size_t smem = sort_smem_bytes<K, ITEMS>();
+    if (!attr_set) {
+        BSR_CUDA_TRY(cudaFuncSetAttribute(sort_pass_kernel<K, ITEMS>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    const unsigned parts = (unsigned)div_up(cap, BSR_BLOCK * ITEMS);
+    for (int p = 0; p < a.passes; ++p) sort_pass_kernel<K, ITEMS><<<parts, BSR_BLOCK, smem, st>>>(a, p);
+    return BSR_OK;
 }
 
 template <typename K>
 int launch_sort(const SortArgs<K> &a, int64_t cap, cudaStream_t st) {
-    static bool attr_set = false;  // idempotent attribute, safe to race
-    const size_t smem = sort_smem_bytes<K>();
-    if (!attr_set) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(sort_pass_kernel<K>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
     if (cap <= 0) return BSR_OK;
-    const unsigned hist_blocks = (unsigned)imin64(div_up(cap, kSortTile), 148 * 4);
+    const unsigned hist_blocks = (unsigned)imin64(div_up(cap, 4096), 148 * 4);
     sort_hist_kernel<K><<<hist_blocks, BSR_BLOCK, 0, st>>>(a);
     sort_plan_kernel<K><<<1, BSR_BLOCK, 0, st>>>(a);
-    const unsigned parts = (unsigned)div_up(cap, kSortTile);
-    for (int p = 0; p < a.passes; ++p) sort_pass_kernel<K><<<parts, BSR_BLOCK, smem, st>>>(a, p);
+    const int rc = a.items == 4 ? launch_passes<K, 4>(a, cap, st) : launch_passes<K, 16>(a, cap, st);
+    if (rc) return rc;
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -296,6 +305,7 @@ int launch_depth_sort(const FrameView &f, cudaStream_t st) {
     a.status = f.depth_status;
     a.tickets = f.ctr->depth_ticket;
     a.passes = kDepthPasses;
+    a.items = f.depth_items;
     a.max_parts = f.depth_parts;
     int rc = launch_sort(a, f.n, st);
     if (rc) return rc;
@@ -319,6 +329,7 @@ int launch_tile_sort(const FrameView &f, cudaStream_t st) {
     a.status = f.tile_status;
     a.tickets = f.ctr->tile_ticket;
     a.passes = f.tile_passes;
+    a.items = f.tile_items;
     a.max_parts = f.tile_parts;
     return launch_sort(a, f.entry_cap, st);
 }
