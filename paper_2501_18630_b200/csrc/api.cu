@@ -123,6 +123,34 @@ __global__ void core_unpack_kernel(int64_t v, const float *acc, float *d_means, 
 
 __global__ void set_visible_kernel(FrameView f, uint32_t v) { f.ctr->visible = v; }
 
+// Per host thread and device: a side stream plus fork/join events, used to run the fp64
+// replay of the flagged pixels concurrently with the fp32 raster backward (both only add
+// into grad_acc; the pixels are disjoint).  Works eagerly and under stream capture (the
+// fork/join become graph edges).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+inline int side_stream(SideStream **out) {
+    static thread_local SideStream per_dev[64];
+    int dev = 0;
+    BSR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return BSR_ERR_CUDA;
+    SideStream &ss = per_dev[dev];
+    if (!ss.s) {
+        // highest priority: the latency-bound replay CTAs are dispatched as soon as raster
+        // CTAs retire instead of queueing behind the whole raster grid
+        int lo = 0, hi = 0;
+        BSR_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        BSR_CUDA_TRY(cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi));
+        BSR_CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+        BSR_CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    }
+    *out = &ss;
+    return BSR_OK;
+}
+
 inline int mark(const bsr_profile *p, int i, cudaStream_t st) {
     if (p && p->events[i]) BSR_CUDA_TRY(cudaEventRecord((cudaEvent_t)p->events[i], st));
     return BSR_OK;
@@ -250,15 +278,23 @@ extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
     zero_acc_kernel<<<(unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8), BSR_BLOCK,
                       0, st>>>(f);
     BSR_LAUNCH_CHECK();
+    // fork: the fp64 replay of the flagged pixels runs beside the fp32 raster backward
+    SideStream *ss = nullptr;
+    if ((rc = side_stream(&ss))) return rc;
+    BSR_CUDA_TRY(cudaEventRecord(ss->fork, st));
+    BSR_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    bsr_outputs none;
+    memset(&none, 0, sizeof(none));
+    const double bg64[3] = {background[0], background[1], background[2]};
+    if ((rc = launch_replay_scene(false, f, *scene, cam, none, bg64, kAlphaMin, kTStop, d_color, d_depth,
+                                  ss->s)))
+        return rc;
+    BSR_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
     if ((rc = launch_raster_bwd(f, d_color, true, d_depth, background, (float)kAlphaMin, nullptr, nullptr,
                                 nullptr, prof ? prof->stats : nullptr, st)))
         return rc;
     if ((rc = mark(prof, 1, st))) return rc;
-    bsr_outputs none;
-    memset(&none, 0, sizeof(none));
-    const double bg64[3] = {background[0], background[1], background[2]};
-    if ((rc = launch_replay_scene(false, f, *scene, cam, none, bg64, kAlphaMin, kTStop, d_color, d_depth, st)))
-        return rc;
+    BSR_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));  // join
     if ((rc = mark(prof, 2, st))) return rc;
     if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, st))) return rc;
     return mark(prof, 3, st);
