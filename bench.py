@@ -251,33 +251,78 @@ def timed_loop(w, steps, world, prof=None, l2=None):
 
 def e2e_loop(w, steps, world):
     """Same step through the public API with per-step host inputs (pinned) and the result
-    read back, copies inside the timing."""
+    read back, copies inside the timing.
+
+    Every step copies its inputs host->device (the per-view target images; config 2 has
+    none) and reads its result device->host (the loss values; the rendered image for
+    config 2).  The copies are double-buffered on a copy stream so they overlap the
+    neighbouring steps' kernels, the way a training / serving loop would run: step i's
+    H2D lands in a device staging buffer while step i-1 computes, one D2D copy moves it
+    into the step's input, and the host waits for step i-1's result before enqueueing
+    step i+1 (pipeline depth 2)."""
     import torch
 
+    main, cs = torch.cuda.current_stream(), torch.cuda.Stream()
     bi = bo = 0
-    if w["kind"] == "train":
+    train = w["kind"] == "train"
+    if train:
         host = [t.cpu().pin_memory() for t in w["targets"]]
+        stage = [[torch.empty_like(t) for t in w["targets"]] for _ in range(2)]
+        res_dev = w["step"].loss_values
         bi = sum(h.numel() * 4 for h in host)
-        bo = w["step"].loss_values.numel() * 8
     else:
-        c = w["cams"][0]
-        host_img = torch.empty((c.height, c.width, 3), dtype=torch.float32).pin_memory()
-        bo = host_img.numel() * 4 * len(w["cams"])
+        res_dev = w.get("color")
+        if res_dev is None:
+            run_step(w)
+            res_dev = w["color"]
+        stage = [torch.empty_like(res_dev) for _ in range(2)]
+    res_host = [torch.empty(res_dev.shape, dtype=res_dev.dtype).pin_memory() for _ in range(2)]
+    bo = res_dev.numel() * res_dev.element_size()
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    in_ready, in_free, out_ready, out_done = ([ev() for _ in range(2)] for _ in range(4))
+    for e_ in in_free + out_done:
+        e_.record(main)
+
+    def issue_h2d(i):
+        b = i % 2
+        with torch.cuda.stream(cs):
+            cs.wait_event(in_free[b])
+            for dst, h in zip(stage[b], host):
+                dst.copy_(h, non_blocking=True)
+            in_ready[b].record(cs)
+
     barrier(world)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
+    s.record(main)
     views = 0
-    for _ in range(steps):
-        if w["kind"] == "train":
-            for dev_t, h in zip(w["targets"], host):
-                dev_t.copy_(h, non_blocking=True)
+    if train:
+        issue_h2d(0)
+    for i in range(steps):
+        b = i % 2
+        if train:
+            if i + 1 < steps:
+                issue_h2d(i + 1)
+            main.wait_event(in_ready[b])
+            for dst, src in zip(w["targets"], stage[b]):
+                dst.copy_(src, non_blocking=True)
+            in_free[b].record(main)
             views += run_step(w)
-            loss = w["step"].loss_values.cpu()  # D2H + sync (the step's result)
-            del loss
+            main.wait_event(out_done[b])
+            res_host[b].copy_(res_dev, non_blocking=True)  # D2H of the step's loss values
+            out_done[b].record(main)
         else:
             views += run_step(w)
-            host_img.copy_(w["color"], non_blocking=False)
-    e.record()
+            main.wait_event(out_done[b])
+            stage[b].copy_(res_dev, non_blocking=True)
+            out_ready[b].record(main)
+            with torch.cuda.stream(cs):
+                cs.wait_event(out_ready[b])
+                res_host[b].copy_(stage[b], non_blocking=True)  # D2H of the rendered image
+                out_done[b].record(cs)
+        if i >= 1:
+            out_done[(i - 1) % 2].synchronize()  # the host has step i-1's result
+    main.wait_stream(cs)
+    e.record(main)
     e.synchronize()
     ms = s.elapsed_time(e)
     barrier(world)

@@ -37,11 +37,19 @@ struct RasterBwdArgs {
 
 // fp64 pair evaluation + the two conic-gradient terms for fp32-unsafe primitives; kept
 // out of line so the common fp32 path is not if-converted into predicated fp64 code.
-__device__ __noinline__ Pair unsafe_pair_bwd(const double *m64, float4 B, int px, int py, float *ga, float *gb) {
+// Returned by value (no pointer arguments: those would force the caller's ga/gb into
+// local memory on the hot path).
+struct PairG {
+    Pair p;
+    float ga, gb;
+};
+__device__ __noinline__ PairG unsafe_pair_bwd(const double *m64, float4 B, int px, int py) {
     const double dx = (double)px - m64[0], dy = (double)py - m64[1];
-    *ga = (float)(m64[2] * dx + m64[3] * dy);
-    *gb = (float)(m64[3] * dx + m64[4] * dy);
-    return eval_pair64(m64, B, px, py);
+    PairG r;
+    r.ga = (float)(m64[2] * dx + m64[3] * dy);
+    r.gb = (float)(m64[3] * dx + m64[4] * dy);
+    r.p = eval_pair64(m64, B, px, py);
+    return r;
 }
 
 // Transpose-reduce 16 values across a warp: afterwards lane L holds the warp sum of value
@@ -174,7 +182,10 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
             float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
             Pair p;
             if (C.w < 0.f) {  // fp32-unsafe primitive, uniform per entry
-                p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py, &ga, &gb);
+                const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
+                p = u.p;
+                ga = u.ga;
+                gb = u.gb;
             } else {
                 p = eval_pair(A, Bq, px - bd.x, py - bd.z);
                 ga = A.z * p.dx + A.w * p.dy;
