@@ -14,6 +14,13 @@
  *   core.backward                  _raster.pyx:244-287     bsr_core_backward
  *   training.loss / ssim           training.py:51-131      bsr_loss_l1_dssim
  *   training.adam_step             training.py:258-273     bsr_adam_step
+ *   training.loss direct terms     training.py:112-124     bsr_regularizers
+ *   training.inject_noise          training.py:276-292     bsr_inject_noise
+ *   training.exponential_lr        training.py:134-145     bsr_lr_schedule (device-side)
+ *   mcmc.find_dead                 mcmc.py:32-36           bsr_find_dead
+ *   mcmc.plan_relocation           mcmc.py:49-70           bsr_sample_live
+ *   mcmc.apply_relocation          mcmc.py:86-106          bsr_apply_relocation
+ *   mcmc.grow                      mcmc.py:108-146         bsr_sample_live + bsr_grow
  *
  * Conventions
  *   - Every pointer is DEVICE memory owned by the caller unless stated; the library
@@ -176,6 +183,85 @@ int bsr_adam_step_device(float *params, const float *grads, float *exp_avg, floa
                          int64_t count, int32_t n_groups, const int64_t *group_end /* host */,
                          const float *group_lr /* host */, int64_t *step_counter, double beta1,
                          double beta2, double eps, void *stream);
+
+/* ---- training-loop neighbours ---------------------------------- */
+/* Group table of a flat, group-major parameter buffer (primitive.group_layout): group g
+ * occupies elements [start[g], start[g] + width[g] * n) with width[g] floats per primitive.
+ * The four named groups must have widths 3 / 4 / 3 / 1. */
+#define BSR_MAX_GROUPS 16
+typedef struct bsr_layout {
+    int64_t n;
+    int32_t n_groups;
+    int32_t width[BSR_MAX_GROUPS];
+    int64_t start[BSR_MAX_GROUPS];
+    int32_t g_positions, g_rotations, g_log_scales, g_opacity; /* group indices */
+} bsr_layout;
+
+/* training.exponential_lr x scene scale (training.py:134-145, TrainConfig.position_lr
+ * :206-215) evaluated on the device from a step counter, so a captured CUDA graph of the
+ * training step follows the schedule. */
+typedef struct bsr_lr_schedule {
+    double lr_init, lr_final;
+    int64_t max_steps, delay_steps;
+    double delay_mult, scale;
+} bsr_lr_schedule;
+double bsr_scheduled_lr(const bsr_lr_schedule *sched, int64_t step); /* host helper */
+
+/* Device-step Adam whose group `sched_group` (the positions) takes its learning rate from
+ * `sched` at the step being taken (TrainConfig.group_lrs, training.py:217-227). */
+int bsr_adam_step_scheduled(float *params, const float *grads, float *exp_avg, float *exp_avg_sq,
+                            int64_t count, int32_t n_groups, const int64_t *group_end /* host */,
+                            const float *group_lr /* host */, int64_t *step_counter,
+                            const bsr_lr_schedule *sched, int32_t sched_group, double beta1,
+                            double beta2, double eps, void *stream);
+
+
+/* training.loss direct terms (training.py:112-124): grads[opacity_raw] += lo * o (1 - o),
+ * grads[log_scales] += ls * exp(log_scales); loss[0] += lo * sum(o) + ls * sum(s) (device
+ * double, may be NULL). */
+int bsr_regularizers(const float *params, const bsr_layout *layout, double lambda_opacity,
+                     double lambda_scale, float *grads, double *loss, void *stream);
+
+/* training.inject_noise (training.py:276-292): positions += noise_lr * position_lr *
+ * (1 - o)^100 * Sigma * eta.  eta: device (N,3) fp32 normals, or NULL for on-device
+ * Philox4x32-10 + Box-Muller keyed by (seed, offset + *step_counter, index).  sched != NULL
+ * replaces position_lr by the schedule at *step_counter (device int64).  status (device
+ * int32, may be NULL) receives BSR_ERR_DEGENERATE_QUAT. */
+int bsr_inject_noise(float *params, const bsr_layout *layout, double noise_lr, double position_lr,
+                     const bsr_lr_schedule *sched, const int64_t *step_counter, const float *eta,
+                     uint64_t seed, uint64_t offset, int32_t *status, void *stream);
+
+/* MCMC densification (mcmc.py).  scratch: bsr_mcmc_scratch_bytes(n) device bytes. */
+int bsr_mcmc_scratch_bytes(int64_t n, uint64_t *bytes);
+/* mcmc.find_dead (mcmc.py:32-36): dead[0..*count) = ascending indices with
+ * sigmoid(opacity_raw) < threshold.  dead: device int64 capacity n; count: device int64. */
+int bsr_find_dead(const float *opacity_raw, int64_t n, double threshold, int64_t *dead,
+                  int64_t *count, void *scratch, uint64_t scratch_bytes, void *stream);
+/* The multinomial draw of mcmc.plan_relocation / mcmc.grow (mcmc.py:49-70, 108-128):
+ * live = {o >= threshold} minus exclude[0..*exclude_count); out[k] = live index drawn
+ * with odds o / sum(o), k < min(*n_draw_dev, n_draw) (n_draw_dev may be NULL), exactly
+ * numpy Generator.choice(live, p=...) when `uniforms` holds numpy's rng.random(draws)
+ * (else Philox uniforms from (seed, offset)).  counts (device int32, n) = draws per index
+ * (zeroed by the call); live_count (device int64) = |live| (0: nothing drawn, the
+ * caller raises AllDeadError). */
+int bsr_sample_live(const float *opacity_raw, int64_t n, double threshold, const int64_t *exclude,
+                    const int64_t *exclude_count, int64_t exclude_cap, const int64_t *n_draw_dev,
+                    int64_t n_draw, const double *uniforms, uint64_t seed, uint64_t offset,
+                    int64_t *out, int32_t *counts, int64_t *live_count, void *scratch,
+                    uint64_t scratch_bytes, void *stream);
+/* mcmc.apply_relocation (mcmc.py:86-106): every dead row takes its target's parameters,
+ * dead and target rows the opacity logit(max(1 - (1 - o)^(1/(counts[t]+1)), floor)) and
+ * zeroed moments (exp_avg / exp_avg_sq may be NULL). */
+int bsr_apply_relocation(float *params, const bsr_layout *layout, float *exp_avg, float *exp_avg_sq,
+                         const int64_t *dead, const int64_t *targets, const int64_t *dead_count,
+                         int64_t dead_cap, const int32_t *counts, double floor_, void *stream);
+/* mcmc.grow after the draw (mcmc.py:128-146): dst (layout for n + n_add) = src rows, then
+ * n_add copies of sources[] with the adjusted opacity (also written to the sources);
+ * moments copied, zeroed for the sources and the new rows. */
+int bsr_grow(const float *src_params, const bsr_layout *src_layout, const float *src_exp_avg,
+             const float *src_exp_avg_sq, float *dst_params, const bsr_layout *dst_layout,
+             float *dst_exp_avg, float *dst_exp_avg_sq, const int64_t *sources, int64_t n_add,
+             const int32_t *counts, double floor_, void *stream);
 
 /* ---- parity / debug: export the binning of the last forward (synchronises) ---------- */
 /* order (V): compact index per depth rank (== np.argsort(depths, kind="stable"),

@@ -64,6 +64,20 @@ class OutputsC(ctypes.Structure):
                 ("contributions", c_void_p)]
 
 
+BSR_MAX_GROUPS = 16
+
+
+class LayoutC(ctypes.Structure):
+    _fields_ = [("n", c_int64), ("n_groups", c_int32), ("width", c_int32 * BSR_MAX_GROUPS),
+                ("start", c_int64 * BSR_MAX_GROUPS), ("g_positions", c_int32), ("g_rotations", c_int32),
+                ("g_log_scales", c_int32), ("g_opacity", c_int32)]
+
+
+class LrScheduleC(ctypes.Structure):
+    _fields_ = [("lr_init", c_double), ("lr_final", c_double), ("max_steps", c_int64),
+                ("delay_steps", c_int64), ("delay_mult", c_double), ("scale", c_double)]
+
+
 class ProfileC(ctypes.Structure):
     _fields_ = [("stats", c_void_p), ("events", c_void_p * 8)]
 
@@ -101,6 +115,23 @@ EXPORTS = {
                                 c_void_p, c_int64, c_double, c_double, c_double, c_void_p]),
     "bsr_adam_step_device": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
                                        c_void_p, c_void_p, c_double, c_double, c_double, c_void_p]),
+    "bsr_adam_step_scheduled": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_double,
+                                          c_double, c_double, c_void_p]),
+    "bsr_scheduled_lr": (c_double, [c_void_p, c_int64]),
+    "bsr_regularizers": (c_int32, [c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p]),
+    "bsr_inject_noise": (c_int32, [c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p,
+                                   c_uint64, c_uint64, c_void_p, c_void_p]),
+    "bsr_mcmc_scratch_bytes": (c_int32, [c_int64, c_void_p]),
+    "bsr_find_dead": (c_int32, [c_void_p, c_int64, c_double, c_void_p, c_void_p, c_void_p, c_uint64,
+                                c_void_p]),
+    "bsr_sample_live": (c_int32, [c_void_p, c_int64, c_double, c_void_p, c_void_p, c_int64, c_void_p,
+                                  c_int64, c_void_p, c_uint64, c_uint64, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_uint64, c_void_p]),
+    "bsr_apply_relocation": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_int64, c_void_p, c_double, c_void_p]),
+    "bsr_grow": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                           c_void_p, c_int64, c_void_p, c_double, c_void_p]),
 }
 
 _LIB = None

@@ -27,6 +27,16 @@ SB_PARAM_NAMES = ("positions", "opacity_raw", "rotations", "log_scales", "shapes
 MAX_LOBES = 4  # BSR_MAX_LOBES (include/bsr.h)
 
 
+def group_widths(k: int | None = None, lobes: int | None = None) -> dict:
+    """Floats per primitive of every group."""
+    w = {"positions": 3, "rotations": 4, "log_scales": 3, "opacity_raw": 1, "shapes": 1}
+    if lobes is None:
+        w["sh"] = 3 * k
+    else:
+        w.update(base_colors=3, lobe_axes=3 * lobes, lobe_colors=3 * lobes)
+    return w
+
+
 def group_layout(n: int, k: int | None = None, lobes: int | None = None):
     """[(name, start, stop, shape)] of the flat buffer for the SH (k) or SB (lobes) model."""
     widths = {"positions": 3, "rotations": 4, "log_scales": 3, "opacity_raw": 1, "shapes": 1}
@@ -83,6 +93,22 @@ class FlatGroups:
 
     def group_ends(self):
         return [b for _, _, b, _ in self.layout]
+
+    def layout_c(self):
+        """The group table as the C-ABI's bsr_layout (include/bsr.h)."""
+        from . import _lib
+
+        lc = _lib.LayoutC()
+        lc.n = self.n
+        lc.n_groups = len(self.layout)
+        widths = group_widths(self.k, self.lobes)
+        for g, (name, a, _, _) in enumerate(self.layout):
+            lc.width[g] = widths[name]
+            lc.start[g] = a
+        names = self.groups
+        lc.g_positions, lc.g_rotations = names.index("positions"), names.index("rotations")
+        lc.g_log_scales, lc.g_opacity = names.index("log_scales"), names.index("opacity_raw")
+        return lc
 
 
 class PrimitiveSet(FlatGroups):

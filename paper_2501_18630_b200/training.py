@@ -16,6 +16,7 @@ synchronisation happens inside ``step(check=False)``.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass, field, fields
 
 import numpy as np
 import torch
@@ -56,17 +57,59 @@ def loss_into(rendered, target, d_image, ws: LossWorkspace, lambda_ssim=0.2, raw
     _lib.check(rc, "loss")
 
 
-def loss(rendered, target, lambda_ssim=0.2):
-    """training.loss with lambda_opacity = lambda_scale = 0: returns (value, d_image)."""
+def regularizers_into(prims: PrimitiveSet, grads: GradientBuffer, lambda_opacity: float, lambda_scale: float,
+                      loss_out=None):
+    """training.loss direct terms (training.py:112-124) on the device: grads.opacity_raw +=
+    lo * o (1 - o), grads.log_scales += ls * s; loss_out[0] += lo * sum(o) + ls * sum(s)."""
+    lc = prims.layout_c()
+    rc = _lib.load().bsr_regularizers(prims.flat.data_ptr(), ctypes.byref(lc), float(lambda_opacity),
+                                      float(lambda_scale), grads.flat.data_ptr(), _lib.ptr(loss_out), _stream())
+    _lib.check(rc, "regularizers")
+
+
+def loss(rendered, target, prims=None, cfg=None, return_parts=False, lambda_ssim=None):
+    """training.loss (training.py:98-131).
+
+    ``loss(rendered, target)`` -> (value, d_image) with lambda_ssim = 0.2 and no
+    regularisers (the BASELINE configs).  With ``prims`` (and optionally a TrainConfig
+    ``cfg``) it returns the reference's ``(value, d_image, direct[, parts])``: ``direct``
+    holds the opacity / log-scale regulariser gradients as device tensors."""
+    lam = (cfg.lambda_ssim if cfg is not None else 0.2) if lambda_ssim is None else lambda_ssim
+    if prims is None:
+        return _image_loss(rendered, target, lam)
     _lib.require_cuda()
+    lo = cfg.lambda_opacity if cfg is not None else TrainConfig.lambda_opacity
+    ls = cfg.lambda_scale if cfg is not None else TrainConfig.lambda_scale
     rendered = torch.as_tensor(rendered, dtype=torch.float32, device="cuda").contiguous()
     target = torch.as_tensor(target, dtype=torch.float32, device="cuda").contiguous()
+    _check_images(rendered, target)
+    ws = LossWorkspace(rendered.shape[1], rendered.shape[0])
+    d_image = torch.empty_like(rendered)
+    loss_into(rendered, target, d_image, ws, lam)
+    g = GradientBuffer.zeros_for(prims)
+    regularizers_into(prims, g, lo, ls, ws.values)
+    vals = ws.values.cpu().numpy()
+    direct = {"opacity_raw": g.opacity_raw, "log_scales": g.log_scales}
+    if return_parts:
+        return float(vals[0]), d_image, direct, {"l1": float(vals[1]), "ssim_term": 1.0 - float(vals[2])}
+    return float(vals[0]), d_image, direct
+
+
+def _check_images(rendered, target):
     if rendered.shape != target.shape:
         raise ValueError("rendered/target shapes differ")
     if rendered.dim() != 3 or rendered.shape[2] != 3:
         raise ValueError("images must be (H, W, 3)")
     if rendered.shape[0] < 11 or rendered.shape[1] < 11:
         raise ValueError("images must be at least 11x11")
+
+
+def _image_loss(rendered, target, lambda_ssim=0.2):
+    """training.loss with lambda_opacity = lambda_scale = 0: returns (value, d_image)."""
+    _lib.require_cuda()
+    rendered = torch.as_tensor(rendered, dtype=torch.float32, device="cuda").contiguous()
+    target = torch.as_tensor(target, dtype=torch.float32, device="cuda").contiguous()
+    _check_images(rendered, target)
     ws = LossWorkspace(rendered.shape[1], rendered.shape[0])
     d_image = torch.empty_like(rendered)
     loss_into(rendered, target, d_image, ws, lambda_ssim)
@@ -93,6 +136,20 @@ class AdamState:
         self.step = 0
         # device-side step counter for graph-captured steps (bsr_adam_step_device)
         self.step_dev = torch.zeros(1, dtype=torch.int64, device=prims.flat.device)
+        self._prims = prims
+
+    @classmethod
+    def zeros_for(cls, prims: PrimitiveSet) -> "AdamState":
+        return cls(prims)
+
+    def zero_rows(self, indices):
+        """Zero both moments of the given primitives in every group (training.py:243-246)."""
+        idx = torch.as_tensor(indices, dtype=torch.long, device=self.exp_avg.device)
+        p = self._prims
+        for buf in (self.exp_avg, self.exp_avg_sq):
+            view = PrimitiveSet.from_flat(p.n, p.k, buf, p.lobes)
+            for g in view.groups:
+                getattr(view, g)[idx] = 0.0
 
 
 def sb_group_lrs(lr_means=1.6e-4):
@@ -113,7 +170,7 @@ def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
 
 
 def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict,
-              device_step: bool = False):
+              device_step: bool = False, schedule=None):
     """training.py:258-273 as one fused kernel over the flat buffers.
 
     ``device_step`` keeps the step count on the device (graph-capturable); the host-side
@@ -122,7 +179,12 @@ def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs:
     ends = (ctypes.c_int64 * len(groups))(*prims.group_ends())
     lr = (ctypes.c_float * len(groups))(*[float(lrs[g]) for g in groups])
     lib = _lib.load()
-    if device_step:
+    if schedule is not None:  # positions follow the lr schedule at the device step
+        rc = lib.bsr_adam_step_scheduled(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
+                                         state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
+                                         state.step_dev.data_ptr(), ctypes.byref(schedule),
+                                         groups.index("positions"), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
+    elif device_step:
         rc = lib.bsr_adam_step_device(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
                                       state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
                                       state.step_dev.data_ptr(), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
@@ -136,12 +198,150 @@ def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs:
     return prims
 
 
+# ----------------------------------------------------------------------------- schedules
+def _sched_c(lr_init, lr_final, max_steps, delay_steps=0, delay_mult=0.01, scale=1.0):
+    c = _lib.LrScheduleC()
+    c.lr_init, c.lr_final, c.max_steps = float(lr_init), float(lr_final), int(max_steps)
+    c.delay_steps, c.delay_mult, c.scale = int(delay_steps), float(delay_mult), float(scale)
+    return c
+
+
+def exponential_lr(step, lr_init, lr_final, max_steps, delay_steps=0, delay_mult=0.01):
+    """Log-linear interpolation from init to final over ``max_steps`` (training.py:134-145),
+    evaluated by the same code the device uses inside Adam / inject_noise."""
+    c = _sched_c(lr_init, lr_final, max_steps, delay_steps, delay_mult)
+    return float(_lib.load().bsr_scheduled_lr(ctypes.byref(c), int(step)))
+
+
+@dataclass
+class TrainConfig:
+    """Hyperparameters of the reference's optimiser (training.py:148-204); field names
+    double as config-file keys.  Only the fields the device training step uses are
+    consumed here; the rest are carried for drop-in compatibility."""
+
+    lambda_ssim: float = 0.2
+    lambda_opacity: float = 0.01
+    lambda_scale: float = 0.01
+    noise_lr: float = 5e4
+    lr_position_init: float = 1.6e-4
+    lr_position_final: float = 1.6e-6
+    lr_position_delay_steps: int = 0
+    lr_position_delay_mult: float = 0.01
+    lr_position_max_steps: int = 30_000
+    lr_base_color: float = 2.5e-3
+    lr_lobes: float = 2.5e-3
+    lr_opacity: float = 5e-2
+    lr_shape: float = 1e-3
+    lr_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_sh: float = 2.5e-3
+    densify_interval: int = 100
+    densify_start: int = 500
+    densify_end: int = 25_000
+    dead_threshold: float = 0.005
+    growth_rate: float = 0.05
+    max_primitives: int = 1_000_000
+    total_steps: int = 30_000
+    patience: int = 10_000
+    mode: str = "30k"
+    sb_lobes: int = 2
+    init_opacity: float = 0.1
+    init_count: int = 2000
+    init_mode: str = "auto"
+    scene_scale: float = 0.0
+    background: str = "white"
+    holdout: int = 8
+    eval_interval: int = 250
+    max_steps_cap: int = 300_000
+
+    def __post_init__(self):
+        for f in fields(self):
+            if f.name.startswith("lr_") and f.name not in ("lr_position_delay_steps", "lr_position_delay_mult",
+                                                            "lr_position_max_steps"):
+                if getattr(self, f.name) <= 0:
+                    raise ValueError(f"{f.name} must be positive")
+        if self.densify_start >= self.densify_end:
+            raise ValueError("densify_start must be below densify_end")
+        if self.mode not in ("30k", "full"):
+            raise ValueError("mode must be '30k' or 'full'")
+
+    def background_rgb(self):
+        if self.background == "white":
+            return np.ones(3)
+        if self.background == "black":
+            return np.zeros(3)
+        return np.array([float(v) for v in self.background.split(",")], dtype=np.float64)
+
+    def position_schedule(self, scene_scale=1.0):
+        return _sched_c(self.lr_position_init, self.lr_position_final, self.lr_position_max_steps,
+                        self.lr_position_delay_steps, self.lr_position_delay_mult, scene_scale)
+
+    def position_lr(self, step, scene_scale=1.0):
+        return scene_scale * exponential_lr(step, self.lr_position_init, self.lr_position_final,
+                                            self.lr_position_max_steps, self.lr_position_delay_steps,
+                                            self.lr_position_delay_mult)
+
+    def group_lrs(self, step, scene_scale=1.0):
+        return {"positions": self.position_lr(step, scene_scale), "opacity_raw": self.lr_opacity,
+                "rotations": self.lr_rotation, "log_scales": self.lr_scale, "shapes": self.lr_shape,
+                "base_colors": self.lr_base_color, "lobe_axes": self.lr_lobes, "lobe_colors": self.lr_lobes,
+                "sh": self.lr_sh}
+
+
+def inject_noise(prims: PrimitiveSet, cfg: TrainConfig, position_lr, rng, step_counter=None, schedule=None):
+    """Covariance-shaped, opacity-gated position noise (training.py:276-292), in place.
+
+    ``rng``: a numpy Generator (eta = rng.standard_normal((n, 3)), the reference's draw) or
+    an ``mcmc.DeviceRNG`` (Philox on the device, keyed by the device step counter when one
+    is given, so a captured graph draws fresh noise every replay)."""
+    from .mcmc import DeviceRNG
+
+    n = len(prims)
+    if n == 0:
+        return prims.positions
+    lc = prims.layout_c()
+    eta = None
+    seed = offset = 0
+    if isinstance(rng, DeviceRNG):
+        seed, offset = rng.seed, rng.advance(1 << 32) if step_counter is None else 0
+    else:
+        eta = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((n, 3)), dtype=np.float32)).to(
+            prims.flat.device)
+    status = torch.zeros(1, dtype=torch.int32, device=prims.flat.device)
+    rc = _lib.load().bsr_inject_noise(prims.flat.data_ptr(), ctypes.byref(lc), float(cfg.noise_lr),
+                                      float(position_lr if position_lr is not None else 0.0),
+                                      None if schedule is None else ctypes.byref(schedule),
+                                      _lib.ptr(step_counter), _lib.ptr(eta), seed, offset, status.data_ptr(),
+                                      _stream())
+    _lib.check(rc, "inject_noise")
+    if step_counter is None and int(status.item()) != 0:
+        _lib.check(int(status.item()), "inject_noise")
+    return prims.positions
+
+
 class TrainStep:
     """One training iteration over this rank's views (fwd + L1/D-SSIM + bwd [+ all-reduce] + Adam)."""
 
     def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
-                 lambda_ssim=0.2, process_group=None):
+                 lambda_ssim=0.2, process_group=None, cfg: TrainConfig | None = None, scene_scale=1.0,
+                 noise_rng=None):
+        """``cfg`` switches on the reference's full optimiser step (training.py:357-366):
+        opacity / scale regularisers, the exponential position-lr schedule and the
+        covariance-shaped position noise, all evaluated on the device from the device step
+        counter (graph-capturable).  Without it the step is the BASELINE configs' (L1 +
+        D-SSIM, constant group learning rates, no noise)."""
         self.prims = prims
+        self.cfg = cfg
+        self.scene_scale = float(scene_scale)
+        if cfg is not None:
+            from .mcmc import DeviceRNG
+
+            lambda_ssim = cfg.lambda_ssim
+            lrs = lrs or cfg.group_lrs(0, scene_scale)
+            self.noise_rng = noise_rng or DeviceRNG(0)
+            self.noise_offset = self.noise_rng.advance(1 << 40)
+            self.schedule = cfg.position_schedule(scene_scale)
+            self.rank0 = process_group is None or torch.distributed.get_rank(process_group) == 0
         self.cameras = list(cameras)
         self.targets = list(targets)
         self.background = background
@@ -188,12 +388,24 @@ class TrainStep:
             self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
                          profile=None if prof is None else prof.bwd(i))
+        cfg = self.cfg
+        if cfg is not None and self.rank0:  # direct regulariser terms, once per iteration
+            regularizers_into(self.prims, self.grads, cfg.lambda_opacity, cfg.lambda_scale, self.loss_values[0])
         if self.pg is not None:  # the one exchange step of view-batch DP (distributed.py)
             allreduce_grads(self.grads.flat, group=self.pg)
         if adam:
             if prof is not None:
                 prof.mark_adam()
-            adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True)
+            if cfg is None:
+                adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True)
+            else:
+                adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True, schedule=self.schedule)
+                # position noise at this step's scheduled lr (Adam bumped the device step)
+                lc = self.prims.layout_c()
+                rc = _lib.load().bsr_inject_noise(self.prims.flat.data_ptr(), ctypes.byref(lc), float(cfg.noise_lr),
+                                                  0.0, ctypes.byref(self.schedule), self.adam.step_dev.data_ptr(),
+                                                  None, self.noise_rng.seed, self.noise_offset, None, _stream())
+                _lib.check(rc, "inject_noise")
             if prof is not None:
                 prof.mark_adam(end=True)
         return self.loss_values
@@ -230,5 +442,171 @@ def render_targets(target_prims: PrimitiveSet, cameras, background):
     return [render_tiled(target_prims, cam, background).color.contiguous() for cam in cameras]
 
 
+# ----------------------------------------------------------------------------- train loop
+@dataclass
+class TrainResult:
+    primitives: object
+    metrics: list = field(default_factory=list)
+    best_psnr: float = -np.inf
+    best_step: int = 0
+    steps_run: int = 0
+    diverged: bool = False
+    abort_reason: str = ""
+
+
+def scene_scale_from_cameras(cameras):
+    """training.py:307-311."""
+    centers = np.stack([c.center for c in cameras])
+    return max(float(np.max(np.linalg.norm(centers - centers.mean(axis=0), axis=1))), 1e-6)
+
+
+def psnr(a, b):
+    """``10 log10(1 / MSE)`` (training.py:86-95), reduced on the device."""
+    a = torch.as_tensor(a, device="cuda", dtype=torch.float32)
+    b = torch.as_tensor(b, device="cuda", dtype=torch.float32)
+    if a.shape != b.shape:
+        raise ValueError(f"image shapes differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    mse = float(torch.mean((a.double() - b.double()) ** 2))
+    return np.inf if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
+
+
+def evaluate_psnr(prims, dataset, view_ids, background):
+    from .rasterizer import render_tiled
+
+    vals = [psnr(render_tiled(prims, dataset.cameras[v], background).color, _device_image(dataset.images[v]))
+            for v in view_ids]
+    return float(np.mean(vals)) if vals else float("nan")
+
+
+def _device_image(img):
+    return torch.as_tensor(np.asarray(img) if not isinstance(img, torch.Tensor) else img, dtype=torch.float32,
+                           device="cuda").contiguous()
+
+
+class _Trainer:
+    """Device buffers of one primitive count (rebuilt after mcmc.grow)."""
+
+    def __init__(self, prims, cfg, scale, background):
+        self.prims, self.cfg, self.background = prims, cfg, background
+        self.grads = GradientBuffer.zeros_for(prims)
+        self.scene = _prims_scene_c(prims)
+        self.gc = grads_c(self.grads)
+        self.frames, self.bufs = {}, {}
+        self.schedule = cfg.position_schedule(scale)
+        self.values = torch.zeros(3, dtype=torch.float64, device=prims.flat.device)
+
+    def step(self, cam, target, adam: AdamState, lrs, noise):
+        key = (cam.width, cam.height)
+        if key not in self.bufs:
+            h, w = cam.height, cam.width
+            dev = self.prims.flat.device
+            self.bufs[key] = (torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                              torch.empty((h, w, 3), dtype=torch.float32, device=dev), LossWorkspace(w, h, dev))
+        color, d_img, ws = self.bufs[key]
+        self.frames[key] = frame = forward_raw(self.scene, cam, self.background, outputs_c(color=color),
+                                               frame=self.frames.get(key), check=True)
+        loss_into(color, target, d_img, ws, self.cfg.lambda_ssim)
+        self.grads.flat.zero_()
+        regularizers_into(self.prims, self.grads, self.cfg.lambda_opacity, self.cfg.lambda_scale, ws.values)
+        backward_raw(self.scene, cam, self.background, frame, d_img, None, self.gc, None)
+        adam_step(self.prims, self.grads, adam, lrs, device_step=True, schedule=self.schedule)
+        adam.step += 1
+        noise(self)
+        return ws.values
+
+
+def _densify(prims, state, cfg, rng):
+    """training.py:420-428 on the device."""
+    from . import mcmc
+
+    dead = mcmc.find_dead(prims, cfg.dead_threshold)
+    if dead.numel():
+        plan = mcmc.plan_relocation(prims, dead, rng, threshold=cfg.dead_threshold)
+        mcmc.apply_relocation(prims, plan, state, floor=cfg.dead_threshold)
+    return mcmc.grow(prims, cfg.max_primitives, rng, state, rate=cfg.growth_rate,
+                     dead_threshold=cfg.dead_threshold)
+
+
+def train(dataset, cfg: TrainConfig, rng, initial=None, progress=None, on_eval=None, device_rng=None):
+    """The reference's training loop (training.py:314-406) with every per-step kernel on the
+    device: render -> loss (+ regularisers) -> backward -> Adam (scheduled position lr)
+    -> position noise, MCMC densification every ``densify_interval`` steps.
+
+    ``dataset`` provides ``cameras``, ``images`` and ``train_indices()`` (sceneio.Dataset);
+    ``initial`` is the starting PrimitiveSet (scene initialisation from SfM points is host
+    I/O, outside the hot path).  ``rng`` (numpy Generator) drives the view order; the noise
+    and MCMC draws use ``device_rng`` (mcmc.DeviceRNG) when given, else ``rng`` itself,
+    draw for draw like the reference."""
+    from . import mcmc
+
+    if len(dataset.cameras) < 2:
+        raise ValueError("training needs at least 2 views")
+    train_ids = list(dataset.train_indices())
+    if not train_ids:
+        raise ValueError("dataset has no training views")
+    if initial is None:
+        raise ValueError("train() needs initial primitives (scene initialisation is host I/O)")
+    _lib.require_cuda()
+    val_ids = train_ids
+    prims = initial.copy()
+    scale = cfg.scene_scale or scene_scale_from_cameras(dataset.cameras)
+    background = cfg.background_rgb()
+    state = AdamState(prims)
+    result = TrainResult(primitives=prims)
+    targets = {v: _device_image(dataset.images[v]) for v in train_ids}
+    drng = device_rng if device_rng is not None else rng
+    tr = _Trainer(prims, cfg, scale, background)
+
+    def noise(t):
+        if isinstance(drng, mcmc.DeviceRNG):
+            inject_noise(t.prims, cfg, None, drng, step_counter=state.step_dev, schedule=t.schedule)
+        else:
+            inject_noise(t.prims, cfg, cfg.position_lr(state.step, scale), drng)
+
+    order, step = [], 0
+    while True:
+        if cfg.mode == "30k":
+            if step >= cfg.total_steps:
+                break
+        else:
+            plateaued = step - result.best_step >= cfg.patience
+            if (step >= cfg.total_steps and plateaued) or step >= cfg.max_steps_cap:
+                break
+        step += 1
+        if not order:
+            order = [int(i) for i in rng.permutation(train_ids)]
+        view = order.pop()
+        vals = tr.step(dataset.cameras[view], targets[view], state, cfg.group_lrs(step, scale), noise)
+        if cfg.densify_start <= step <= cfg.densify_end and step % cfg.densify_interval == 0:
+            try:
+                grown = _densify(prims, state, cfg, drng)
+            except mcmc.AllDeadError as exc:
+                result.diverged, result.abort_reason = True, str(exc)
+                break
+            if grown is not prims:
+                prims = grown
+                state._prims = prims
+                tr = _Trainer(prims, cfg, scale, background)
+            result.primitives = prims
+        v = vals.cpu().numpy()
+        row = {"step": step, "loss": float(v[0]), "l1": float(v[1]), "ssim_term": 1.0 - float(v[2]),
+               "mean_opacity": float(prims.opacities.mean()), "count": len(prims), "psnr": ""}
+        if step % cfg.eval_interval == 0 or step == 1:
+            val_psnr = evaluate_psnr(prims, dataset, val_ids, background)
+            row["psnr"] = val_psnr
+            if val_psnr > result.best_psnr:
+                result.best_psnr, result.best_step = val_psnr, step
+            if on_eval is not None:
+                on_eval(step, prims)
+        result.metrics.append(row)
+        if progress is not None:
+            progress(row)
+    result.steps_run = step
+    result.primitives = prims
+    return result
+
+
 __all__ = ["loss", "ssim", "adam_step", "AdamState", "TrainStep", "render_targets", "group_lrs",
-           "LossWorkspace", "loss_into", "FrameState", "Camera", "np", "_bg_arr"]
+           "LossWorkspace", "loss_into", "FrameState", "Camera", "np", "_bg_arr", "TrainConfig", "TrainResult",
+           "exponential_lr", "inject_noise", "regularizers_into", "train", "evaluate_psnr", "psnr",
+           "scene_scale_from_cameras"]
