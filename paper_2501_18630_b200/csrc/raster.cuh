@@ -153,4 +153,109 @@ __device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int
     return !(D.y < X0 || D.x > X1 || D.w < Y0 || D.z > Y1);
 }
 
+// ---- sub-warp pixel groups -----------------------------------------------------------
+// A warp owns an 8x4 pixel block.  With G groups the block splits into G sub-blocks
+// (G = 1: 8x4, G = 2: two 4x4, G = 4: four 4x2) of 32/G lanes each; every group walks its
+// own compacted entry list, so a warp-iteration evaluates G different entries and a pixel
+// only visits entries whose support reaches its sub-block (tiny footprints: the 8x4 list
+// is mostly entries that touch a few of its pixels).
+template <int G>
+struct SubBlock {
+    static constexpr int lanes = 32 / G;
+    static constexpr int w = G == 1 ? 8 : 4;
+    static constexpr int h = G == 4 ? 2 : 4;
+    __device__ static int group(int lane) { return lane / lanes; }
+    __device__ static int ox(int q) { return G == 1 ? 0 : 4 * (q & 1); }
+    __device__ static int oy(int q) { return G == 4 ? 2 * (q >> 1) : 0; }
+    __device__ static int px(int lane) { return ox(group(lane)) + (lane % lanes) % w; }
+    __device__ static int py(int lane) { return oy(group(lane)) + (lane % lanes) / w; }
+    __device__ static unsigned mask(int q) { return G == 1 ? 0xffffffffu : (((1u << lanes) - 1u) << (q * lanes)); }
+};
+
+// Sub-block occupancy mask of one entry over a whole 16x16 tile (computed once per entry
+// and batch by one thread, then read by every warp to build its groups' lists).  The tile
+// is a grid of (16 / w) x (16 / h) sub-blocks, bit = row * (16 / w) + col; warp v's
+// group q sits at col 2 (v & 1) + (q & 1) [G = 4] / 2 (v & 1) + q [G = 2] / v & 1 [G = 1],
+// row 2 (v >> 1) + (q >> 1) [G = 4] / v >> 1.
+//
+// The test is exact per pixel row: for every pixel row y the ellipse {r2 <= xlim} (xlim =
+// the alpha cutoff plus the record's r2 error slack, as in ellipse_hits_rect) spans
+// dx in [(-b dy - sqrt(D)) / a, (-b dy + sqrt(D)) / a], D = a xlim - det dy^2; the span is
+// padded for fp32 rounding (the D cancellation costs at most ~3e-4 of the half width) and
+// clipped to the record bounds.  det = ac - b^2 of the record's fp32 conic is evaluated
+// with Kahan's FMA scheme (accurate to ~1.5 ulp of det even for needle-like footprints,
+// where the plain product difference cancels); fp32-unsafe records use the same spans
+// with their larger r2 slack.  Non-positive-definite fp32 conics and the pair-counting
+// variant (BBOX) use the bounds box.
+template <int G>
+struct TileGrid {
+    static constexpr int w = SubBlock<G>::w, h = SubBlock<G>::h;
+    static constexpr int cols = BSR_TILE / w, rows = BSR_TILE / h;
+    __device__ static int bit(int warp, int q) {
+        const int col = G == 4 ? 2 * (warp & 1) + (q & 1) : (G == 2 ? 2 * (warp & 1) + q : (warp & 1));
+        const int row = G == 4 ? 2 * (warp >> 1) + (q >> 1) : (warp >> 1);
+        return row * cols + col;
+    }
+};
+
+// 32 x 32 bit transpose across a warp: lane r holds row r on entry; on exit lane c holds
+// column c (bit r = bit c of row r).  Five butterfly stages of block swaps.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t m0 = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                          : s == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+        x = (lane & s) ? ((x & ~m0) | ((y & ~m0) >> s)) : ((x & m0) | ((y & m0) << s));
+    }
+    return x;
+}
+
+template <int G>
+__device__ __forceinline__ uint32_t row_bits(int cx0, int cx1) {  // pixel columns (tile-relative)
+    constexpr int w = TileGrid<G>::w;
+    return ((2u << (cx1 / w)) - 1u) & ~((1u << (cx0 / w)) - 1u);
+}
+
+template <int G, bool BBOX>
+__device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4 B, const float4 C, const int4 D,
+                                                    int X0, int Y0, float alpha_min) {
+    using TG = TileGrid<G>;
+    // bounds box clipped to the tile (tile-relative pixel coordinates)
+    const int bx0 = max(D.x - X0, 0), bx1 = min(D.y - X0, BSR_TILE - 1);
+    const int by0 = max(D.z - Y0, 0), by1 = min(D.w - Y0, BSR_TILE - 1);
+    if (bx0 > bx1 || by0 > by1) return 0u;
+    if (!BBOX && B.y < alpha_min) return 0u;
+    const float a = A.z, b = A.w, c = B.x;
+    const float bb = __fmul_rn(b, b);
+    const float det = __fadd_rn(__fmaf_rn(a, c, -bb), __fmaf_rn(-b, b, bb));  // Kahan 2x2
+    if (BBOX || !(det > 0.f && a > 0.f)) {
+        const uint32_t rb = row_bits<G>(bx0, bx1);
+        uint32_t m = 0;
+        for (int r = by0 / TG::h; r <= by1 / TG::h; ++r) m |= rb << (r * TG::cols);
+        return m;
+    }
+    const float xmax = 1.0f - exp2f(__log2f(__fdividef(alpha_min, B.y)) * rcp_approx(B.z));
+    const float xl = fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.04f * fabsf(C.w) * rcp_approx(B.z) + 1e-4f;
+    const float ia = rcp_approx(a), id = rcp_approx(det);
+    const float hy = sqrtf(xl * a * id) * 1.01f + 1e-3f;
+    // fp32 error of a row span: sqrt of the D cancellation (<= 3.5e-4 sqrt(xl / a), the span
+    // at dy = 0) plus a few ulp of the centre offset b dy / a
+    const float pad0 = 1e-3f * sqrtf(xl * ia) + 2e-3f;
+    // mean relative to the tile origin (exact: small integers plus the record's offset)
+    const float mx = (float)(D.x - X0) + A.x, my = (float)(D.z - Y0) + A.y;
+    const int y0 = max(by0, (int)ceilf(my - hy)), y1 = min(by1, (int)floorf(my + hy));
+    uint32_t m = 0;
+    for (int y = y0; y <= y1; ++y) {
+        const float dy = (float)y - my;
+        const float disc = fmaxf(a * xl - det * dy * dy, 0.f);
+        const float off = b * dy * ia;
+        const float half = sqrtf(disc) * ia * 1.001f + pad0 + 4e-7f * fabsf(off);
+        const float cx = mx - off;
+        const int x0 = max(bx0, (int)ceilf(cx - half)), x1 = min(bx1, (int)floorf(cx + half));
+        if (x0 <= x1) m |= row_bits<G>(x0, x1) << ((y / TG::h) * TG::cols);
+    }
+    return m;
+}
+
 }  // namespace bsr

@@ -17,6 +17,8 @@
 // warp-wide RED instruction per (warp, entry) into grad_acc[compact][12].
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "raster.cuh"
 
 namespace bsr {
@@ -52,11 +54,15 @@ __device__ __noinline__ PairG unsafe_pair_bwd(const double *m64, float4 B, int p
     return r;
 }
 
-// Transpose-reduce 16 values across a warp: afterwards lane L holds the warp sum of value
-// index  ((L >> 1) & 15)  (lanes 2i and 2i+1 hold the same value).
-__device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
+// Transpose-reduce 16 values across the L lanes of a group (L = 32 / G): afterwards each
+// lane holds group sums of NV = max(1, 32 / L / 2)... concretely
+//   L = 32: lane k holds value (k >> 1)            (lanes 2i, 2i+1 equal), returned in r0
+//   L = 16: lane k holds value k                    in r0
+//   L =  8: lane k holds values 2k, 2k + 1          in r0, r1
+template <int L>
+__device__ __forceinline__ void group_reduce16(float (&v)[16], int lane, float &r0, float &r1) {
 #pragma unroll
-    for (int half = 8, bit = 16; half >= 1; half >>= 1, bit >>= 1) {
+    for (int half = 8, bit = L / 2; half >= 1 && bit >= 1; half >>= 1, bit >>= 1) {
         const bool upper = lane & bit;
 #pragma unroll
         for (int i = 0; i < half; ++i) {
@@ -65,7 +71,17 @@ __device__ __forceinline__ float warp_reduce16(float (&v)[16], int lane) {
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
         }
     }
-    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+    if (L == 32) {
+        r0 = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+        r1 = 0.f;
+    } else {
+        r0 = v[0];
+        r1 = v[1];
+    }
+}
+template <int L>
+__device__ __forceinline__ int reduce_index(int k) {
+    return L == 32 ? (k >> 1) : (L == 16 ? k : 2 * k);
 }
 
 __device__ __forceinline__ float lg2_approx(float x) {
@@ -74,29 +90,33 @@ __device__ __forceinline__ float lg2_approx(float x) {
     return r;
 }
 
-// One pixel per thread; a warp owns an 8x4 block.  The per-pair body is branch-free: a
-// lane that does not take the pair (outside its last contributor, alpha < alpha_min) runs
-// it with alpha = 0 and dL/dalpha = 0, which leaves its state (T, behind colour) exactly
-// unchanged and all 11 partials exactly 0.
-template <bool STATS>
+// One pixel per thread; a warp owns an 8x4 block split into G sub-blocks whose lane groups
+// walk their own entry lists (raster.cuh SubBlock).  The per-pair body is branch-free: a
+// lane that does not take the pair (outside its last contributor, alpha < alpha_min, or
+// its group's list exhausted) runs it with alpha = 0 and dL/dalpha = 0, which leaves its
+// state (T, behind colour) exactly unchanged and all 11 partials exactly 0.
+template <bool STATS, int G>
 __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
-    constexpr int NW = BSR_BLOCK / 32;
+    using SB = SubBlock<G>;
+    using TG = TileGrid<G>;
+    constexpr int L = SB::lanes;
     __shared__ __align__(16) Record s_recb[2][BSR_BLOCK];
     __shared__ uint32_t s_cidxb[2][BSR_BLOCK];
-    __shared__ uint8_t s_list[NW][BSR_BLOCK];
+    __shared__ uint32_t s_col[BSR_BLOCK / 32][32];  // [chunk of 32 entries][tile sub-block]
     __shared__ int s_maxlast;
     const FrameView &f = a.f;
     const int tile = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
-    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const int q = SB::group(lane), k = lane % L;
+    const int px = wx0 + SB::px(lane), py = wy0 + SB::py(lane);
     const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     const int direct_max = a.direct_max;
+    const int my_bit = TG::bit(warp, q);
 
     int last = 0;
     float T = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, gd = 0.f, B0 = a.bg[0], B1 = a.bg[1], B2 = a.bg[2], BD = 0.f;
@@ -117,10 +137,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
             if (a.d_depth) gd = a.d_depth[pix];
         }
     }
-    int wlast = last;
-    if (t == 0) s_maxlast = 0;
+    // furthest last contributor of the group / warp / CTA
+    int glast = last;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    for (int o = L / 2; o; o >>= 1) glast = max(glast, __shfl_xor_sync(0xffffffffu, glast, o));
+    int wlast = glast;
+#pragma unroll
+    for (int o = 16; o >= L; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (t == 0) s_maxlast = 0;
     __syncthreads();
     if (lane == 0 && wlast) atomicMax(&s_maxlast, wlast);
     __syncthreads();
@@ -131,11 +155,11 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     // cp.async while this one is processed
     auto prefetch = [&](int hi, int buf) {
         const int lo = max(0, hi - BSR_BLOCK);
-        for (int q = t; q < hi - lo; q += BSR_BLOCK) {
-            const uint32_t c = lists[start + lo + q];
-            s_cidxb[buf][q] = c;
+        for (int qq = t; qq < hi - lo; qq += BSR_BLOCK) {
+            const uint32_t c = lists[start + lo + qq];
+            s_cidxb[buf][qq] = c;
             const Record *src = rec + c;
-            Record *dst = &s_recb[buf][q];
+            Record *dst = &s_recb[buf][qq];
             cp_async16(&dst->a, &src->a);
             cp_async16(&dst->b, &src->b);
             cp_async16(&dst->c, &src->c);
@@ -143,6 +167,88 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         }
         cp_async_commit();
     };
+
+    // one (pixel, entry) pair of the back-to-front replay (_raster.pyx:197-241) plus the
+    // accumulation of its 11 partials; GL = lanes reduced together (32: the whole warp
+    // walks one entry, L: every group its own)
+    auto pair = [&](const Record *s_rec, const uint32_t *s_cidx, int lo, int j, bool act, auto gl_tag) {
+        constexpr int GL = decltype(gl_tag)::value;
+        const int e = lo + j;  // local entry index
+        const int4 bd = s_rec[j].d;
+        const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
+        if (STATS) pairs += (act && e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
+        float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
+        Pair p;
+        if (C.w < 0.f) {  // fp32-unsafe primitive
+            const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
+            p = u.p;
+            ga = u.ga;
+            gb = u.gb;
+        } else {
+            p = eval_pair(A, Bq, px - bd.x, py - bd.z);
+            ga = A.z * p.dx + A.w * p.dy;
+            gb = A.w * p.dx + Bq.x * p.dy;
+        }
+        const bool took = act && e < last && p.alpha >= a.alpha_min;
+        const unsigned tm = __ballot_sync(0xffffffffu, took);
+        if (!tm) return;
+        const float alpha = took ? p.alpha : 0.f;
+        const float one_m = 1.0f - alpha;     // alpha <= 0.999 (forward flags larger)
+        T = took ? T * rcp_approx(one_m) : T;  // T_k
+        const float w = alpha * T;
+        float dalpha = T * (g0 * (C.x - B0) + g1 * (C.y - B1) + g2 * (C.z - B2) + gd * (Bq.w - BD));
+        dalpha = took ? dalpha : 0.f;
+        B0 = alpha * C.x + one_m * B0;
+        B1 = alpha * C.y + one_m * B1;
+        B2 = alpha * C.z + one_m * B2;
+        BD = alpha * Bq.w + one_m * BD;
+        // kernel derivative; a taken sample has alpha > 0, hence 1 - x > 0
+        const float beta = Bq.z;
+        const float om = fmaxf(p.om, 1e-30f);
+        const float pw = beta == 4.0f ? om * om * om : p.k * rcp_approx(om);  // (1-x)^(beta-1)
+        const float dk = dalpha * Bq.y;
+        const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
+        float v[16];
+        v[0] = -2.0f * d_x * ga;
+        v[1] = -2.0f * d_x * gb;
+        v[2] = d_x * p.dx * p.dx;
+        v[3] = 2.0f * d_x * p.dx * p.dy;
+        v[4] = d_x * p.dy * p.dy;
+        v[5] = dalpha * p.k;
+        v[6] = dk * p.k * (0.69314718f * lg2_approx(om));
+        v[7] = w * g0;
+        v[8] = w * g1;
+        v[9] = w * g2;
+        v[10] = w * gd;
+        float *dst = f.grad_acc + (int64_t)s_cidx[j] * kGradStride;
+        // few contributors: direct atomics beat the reduction
+        int most = __popc(tm);
+        if (GL < 32) {
+            most = 0;
+#pragma unroll
+            for (int g = 0; g < 32 / GL; ++g) most = max(most, __popc(tm & (((1u << GL) - 1u) << (g * GL))));
+        }
+        if (most <= direct_max) {
+            if (took) {
+#pragma unroll
+                for (int qq = 0; qq < 11; ++qq)
+                    if (v[qq] != 0.0f) atomicAdd(dst + qq, v[qq]);
+            }
+            return;
+        }
+#pragma unroll
+        for (int qq = 11; qq < 16; ++qq) v[qq] = 0.f;
+        float r0, r1;
+        group_reduce16<GL>(v, lane, r0, r1);
+        const int idx = reduce_index<GL>(lane % GL);
+        if (GL == 32) {
+            if (!(lane & 1) && idx < 11 && r0 != 0.0f) atomicAdd(dst + idx, r0);
+        } else {
+            if (idx < 11 && r0 != 0.0f) atomicAdd(dst + idx, r0);
+            if (GL == 8 && idx + 1 < 11 && r1 != 0.0f) atomicAdd(dst + idx + 1, r1);
+        }
+    };
+
     if (maxlast > 0) prefetch(maxlast, 0);
     int buf = 0;
     for (int hi = maxlast; hi > 0; hi -= BSR_BLOCK, buf ^= 1) {
@@ -155,87 +261,71 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         __syncthreads();
         const Record *s_rec = s_recb[buf];
         const uint32_t *s_cidx = s_cidxb[buf];
-        // ---- per-warp list: entries before the warp's furthest last contributor that
-        //      reach its block (ascending; walked backwards)
-        int nl = 0;
-        if (wlast > lo) {
-            for (int c0j = 0; c0j < nb; c0j += 32) {
-                const int j = c0j + lane;
-                bool hit = false;
-                if (j < nb && lo + j < wlast) {
-                    const Record &r = s_rec[j];
-                    hit = STATS ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
-                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3, a.alpha_min);
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
-                nl += __popc(m);
+        // ---- one thread per entry: which sub-blocks of the tile can it reach (bit columns
+        //      per chunk of 32 entries, see raster_fwd.cu)
+        {
+            uint32_t m = 0;
+            if (t < nb) {
+                const Record &r = s_rec[t];
+                m = entry_tile_mask<G, STATS>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
             }
-            __syncwarp();
+            s_col[warp][lane] = warp_transpose32(m, lane);
         }
-        for (int i = nl - 1; i >= 0; --i) {
-            const int j = s_list[warp][i];
-            const int e = lo + j;  // local entry index
-            const int4 bd = s_rec[j].d;
-            const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
-            if (STATS) pairs += (e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-            float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
-            Pair p;
-            if (C.w < 0.f) {  // fp32-unsafe primitive, uniform per entry
-                const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
-                p = u.p;
-                ga = u.ga;
-                gb = u.gb;
-            } else {
-                p = eval_pair(A, Bq, px - bd.x, py - bd.z);
-                ga = A.z * p.dx + A.w * p.dy;
-                gb = A.w * p.dx + Bq.x * p.dy;
-            }
-            const bool took = e < last && p.alpha >= a.alpha_min;
-            const unsigned tm = __ballot_sync(0xffffffffu, took);
-            if (!tm) continue;
-            const float alpha = took ? p.alpha : 0.f;
-            const float one_m = 1.0f - alpha;     // alpha <= 0.999 (forward flags larger)
-            T = took ? T * rcp_approx(one_m) : T;  // T_k
-            const float w = alpha * T;
-            float dalpha = T * (g0 * (C.x - B0) + g1 * (C.y - B1) + g2 * (C.z - B2) + gd * (Bq.w - BD));
-            dalpha = took ? dalpha : 0.f;
-            B0 = alpha * C.x + one_m * B0;
-            B1 = alpha * C.y + one_m * B1;
-            B2 = alpha * C.z + one_m * B2;
-            BD = alpha * Bq.w + one_m * BD;
-            // kernel derivative; a taken sample has alpha > 0, hence 1 - x > 0
-            const float beta = Bq.z;
-            const float om = fmaxf(p.om, 1e-30f);
-            const float pw = beta == 4.0f ? om * om * om : p.k * rcp_approx(om);  // (1-x)^(beta-1)
-            const float dk = dalpha * Bq.y;
-            const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
-            float v[16];
-            v[0] = -2.0f * d_x * ga;
-            v[1] = -2.0f * d_x * gb;
-            v[2] = d_x * p.dx * p.dx;
-            v[3] = 2.0f * d_x * p.dx * p.dy;
-            v[4] = d_x * p.dy * p.dy;
-            v[5] = dalpha * p.k;
-            v[6] = dk * p.k * (0.69314718f * lg2_approx(om));
-            v[7] = w * g0;
-            v[8] = w * g1;
-            v[9] = w * g2;
-            v[10] = w * gd;
-            float *dst = f.grad_acc + (int64_t)s_cidx[j] * kGradStride;
-            if (__popc(tm) <= direct_max) {  // few contributors: direct atomics beat the reduction
-                if (took) {
+        __syncthreads();
+        if (wlast <= lo) continue;
+        // entries [lo, lo + lim) precede the group's / warp's furthest last contributor
+        const int glim = min(nb, glast - lo), wlim = min(nb, wlast - lo);
+        bool dense = G == 1;
+        if (G > 1) {
+            int sum = 0, uni = 0;
+            const int nch = (wlim + 31) >> 5;
+            if (lane < nch) {
+                uint32_t u = 0;
 #pragma unroll
-                    for (int q = 0; q < 11; ++q)
-                        if (v[q] != 0.0f) atomicAdd(dst + q, v[q]);
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t cg = s_col[lane][TG::bit(warp, g)];
+                    sum += __popc(cg);
+                    u |= cg;
                 }
-                continue;
+                uni = __popc(u);
             }
 #pragma unroll
-            for (int q = 11; q < 16; ++q) v[q] = 0.f;
-            const float sum = warp_reduce16(v, lane);
-            const int idx = (lane >> 1) & 15;
-            if (!(lane & 1) && idx < 11 && sum != 0.0f) atomicAdd(dst + idx, sum);
+            for (int o = 4; o; o >>= 1) {
+                sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                uni += __shfl_xor_sync(0xffffffffu, uni, o);
+            }
+            // lanes 0..7 hold the totals; broadcast so the branch below is warp-uniform
+            dense = __shfl_sync(0xffffffffu, 2 * sum >= 5 * uni, 0);
+        }
+        // walk set bits from the highest entry below the limit down to entry 0
+        auto lowbits = [](int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); };
+        if (dense) {
+            auto col = [&](int cc) {
+                uint32_t u = 0;
+#pragma unroll
+                for (int g = 0; g < G; ++g) u |= s_col[cc][TG::bit(warp, g)];
+                return u;
+            };
+            int c = (wlim - 1) >> 5;
+            uint32_t bits = col(c) & lowbits(wlim - (c << 5));
+            while (true) {
+                while (!bits && c > 0) bits = col(--c);
+                if (!bits) break;
+                const int jb = 31 - __clz(bits);
+                bits &= ~(1u << jb);
+                pair(s_rec, s_cidx, lo, (c << 5) + jb, true, std::integral_constant<int, 32>());
+            }
+        } else {
+            int c = glim > 0 ? (glim - 1) >> 5 : -1;
+            uint32_t bits = c >= 0 ? s_col[c][my_bit] & lowbits(glim - (c << 5)) : 0u;
+            while (true) {
+                while (!bits && c > 0) bits = s_col[--c][my_bit];
+                if (!__any_sync(0xffffffffu, bits)) break;
+                const bool act = bits != 0;
+                const int jb = act ? 31 - __clz(bits) : 0;
+                bits &= ~(1u << jb);
+                pair(s_rec, s_cidx, lo, act ? (c << 5) + jb : 0, act, std::integral_constant<int, L>());
+            }
         }
     }
     if (STATS) {
@@ -244,6 +334,16 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         for (int o = 16; o; o >>= 1) p2 += __shfl_xor_sync(0xffffffffu, p2, o);
         if (lane == 0) atomicAdd(a.stats + 2, p2);
     }
+}
+
+int raster_groups();
+
+template <int G>
+static void launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
+    if (stats)
+        raster_bwd_kernel<true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+    else
+        raster_bwd_kernel<false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
 }
 
 int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, const float *d_depth,
@@ -270,10 +370,11 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, c
         return e ? atoi(e) : 2;
     }();
     a.direct_max = direct_max;
-    if (stats)
-        raster_bwd_kernel<true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else
-        raster_bwd_kernel<false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    switch (raster_groups()) {
+        case 1: launch_bwd_g<1>(a, f.n_tiles, stats != nullptr, st); break;
+        case 2: launch_bwd_g<2>(a, f.n_tiles, stats != nullptr, st); break;
+        default: launch_bwd_g<4>(a, f.n_tiles, stats != nullptr, st); break;
+    }
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -1,6 +1,7 @@
 // K4 raster_fwd: per-16x16-tile front-to-back compositing (_raster.pyx:74-155).
 //
-// One CTA (256 threads) per tile, one pixel per thread; a warp owns an 8x4 pixel block.
+// One CTA (256 threads) per tile, one pixel per thread; a warp owns an 8x4 pixel block,
+// split into G sub-blocks of 32/G lanes that walk their own entry lists (raster.cuh).
 // Tile-list records (64 B) are gathered into shared memory in batches of 256 with
 // cp.async double buffering.  Per batch, every warp builds a compacted list of the entries
 // whose ellipse actually reaches its 8x4 block (exact minimum of the conic over the block,
@@ -15,6 +16,8 @@
 // carry 1 - alpha) are handed over too.
 //
 // Roofline: FP32 + XU pipes, per evaluated pair ~27 FP32 FLOP + 2 XU.
+#include <stdlib.h>
+
 #include "raster.cuh"
 
 namespace bsr {
@@ -39,18 +42,21 @@ __device__ __noinline__ float2 unsafe_pair_fwd(const double *m64, float4 B, int 
     return make_float2(p.alpha, p.om);
 }
 
-template <bool STATS, bool CONTRIB>
+template <bool STATS, bool CONTRIB, int G>
 __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
+    using SB = SubBlock<G>;
+    using TG = TileGrid<G>;
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
-    __shared__ uint8_t s_list[BSR_BLOCK / 32][BSR_BLOCK];
+    __shared__ uint32_t s_col[BSR_BLOCK / 32][32];  // [chunk of 32 entries][tile sub-block]
     __shared__ int s_cnt[BSR_BLOCK];
     const FrameView &f = a.f;
     const int tile = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
-    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const int q = SB::group(lane);
+    const int px = wx0 + SB::px(lane), py = wy0 + SB::py(lane);
     const bool inside = px < f.W && py < f.H;
     const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
     const Record *rec = a.rec ? a.rec : f.rec;
@@ -58,7 +64,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
     const int start = (int)range.x, end = (int)range.y;
     constexpr bool want_contrib = CONTRIB;
     constexpr bool stats = STATS;
-    const uint32_t lt_mask = (1u << lane) - 1u;
+    const int my_bit = TG::bit(warp, q);
 
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
     int cnt = 0, last = 0, flag_at = -1;
@@ -81,6 +87,58 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
         cp_async_commit();
     };
 
+    // one (pixel, entry) pair of the front-to-back composite (_raster.pyx:101-123)
+    auto pair = [&](int b0, int buf, int j) -> bool {
+        bool took = false;
+        const int4 bd = s_rec[buf][j].d;
+        if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
+        const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
+        const bool unsafe = C.w < 0.f;
+        Pair p;
+        if (unsafe) {  // uniform per entry
+            const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
+            p.alpha = u.x;
+            p.om = u.y;
+        } else {
+            p = eval_pair(A, B, px - bd.x, py - bd.z);
+        }
+        bool ambiguous = false;
+        // rare path: alpha within 5% of the cutoff -> certify with the error bound
+        if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
+            const float rel = unsafe ? 8.0f * kEps : alpha_rel_err_pixel(A, B, p);
+            ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 4.0f * kEps * a.alpha_min;
+        }
+        if (!ambiguous && p.alpha >= a.alpha_min) {
+            const float one_m = __fsub_rn(1.0f, p.alpha);
+            const float Tn = __fmul_rn(T, one_m);
+            // relative error bound of T: sum over samples of
+            //   alpha/(1-alpha) * rel_err(alpha) + rounding
+            // (record_err_word: rel(alpha) <= Q / om)
+            const float rel = unsafe ? 8.0f * kEps : C.w * rcp_approx(fmaxf(p.om, 1e-30f));
+            const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * rcp_approx(fmaxf(one_m, 1e-30f));
+            if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
+                ambiguous = true;
+            } else {
+                const float w = __fmul_rn(p.alpha, T);
+                c0 = __fmaf_rn(w, C.x, c0);
+                c1 = __fmaf_rn(w, C.y, c1);
+                c2 = __fmaf_rn(w, C.z, c2);
+                dep = __fmaf_rn(w, B.w, dep);
+                T = Tn;
+                errT = errTn;
+                ++cnt;
+                last = b0 + j - start + 1;
+                took = true;
+                if (T < a.t_stop) done = true;
+            }
+        }
+        if (ambiguous) {
+            flag_at = b0 + j - start;
+            done = true;
+        }
+        return took;
+    };
+
     if (start < end) prefetch(start, 0);
     int buf = 0;
     for (int b0 = start; b0 < end; b0 += BSR_BLOCK, buf ^= 1) {
@@ -89,78 +147,78 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         if (__syncthreads_count(done) == BSR_BLOCK) break;
         const int nb = min(BSR_BLOCK, end - b0);
-        // ---- per-warp compacted list of entries reaching this warp's 8x4 block
-        int nl = 0;
-        if (!__all_sync(0xffffffffu, done)) {
-            for (int c0j = 0; c0j < nb; c0j += 32) {
-                const int j = c0j + lane;
-                bool hit = false;
-                if (j < nb) {
-                    const Record &r = s_rec[buf][j];
-                    hit = stats ? bbox_hits_rect(r.d, wx0, wx0 + 7, wy0, wy0 + 3)
-                                : ellipse_hits_rect(r.a, r.b, r.c, r.d, wx0, wx0 + 7, wy0, wy0 + 3, a.alpha_min);
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit) s_list[warp][nl + __popc(m & lt_mask)] = (uint8_t)j;
-                nl += __popc(m);
+        const int nch = (nb + 31) >> 5;
+        // ---- one thread per entry: which sub-blocks of the tile can it reach; transposed
+        //      per chunk of 32 entries into one bit column per sub-block
+        {
+            uint32_t m = 0;
+            if (t < nb) {
+                const Record &r = s_rec[buf][t];
+                m = entry_tile_mask<G, stats>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
             }
-            __syncwarp();
+            s_col[warp][lane] = warp_transpose32(m, lane);
         }
-        for (int i = 0; i < nl; ++i) {
-            if (__all_sync(0xffffffffu, done)) break;
-            const int j = s_list[warp][i];
-            bool took = false;
-            if (!done) {
-                const int4 bd = s_rec[buf][j].d;
-                if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-                const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
-                const bool unsafe = C.w < 0.f;
-                Pair p;
-                if (unsafe) {  // uniform per entry
-                    const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
-                    p.alpha = u.x;
-                    p.om = u.y;
-                } else {
-                    p = eval_pair(A, B, px - bd.x, py - bd.z);
+        __syncthreads();
+        // ---- this warp's groups: open (some pixel not finished) and how much their entry
+        //      sets overlap; groups that mostly share entries walk the union together
+        //      ("dense": one entry per warp-iteration), otherwise each group walks its own
+        const unsigned done_b = __ballot_sync(0xffffffffu, done);
+        const bool my_open = (done_b & SB::mask(q)) != SB::mask(q);
+        bool dense = G == 1;
+        if (G > 1) {
+            int sum = 0, uni = 0;
+            if (lane < nch) {
+                uint32_t u = 0;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t cg = s_col[lane][TG::bit(warp, g)];
+                    sum += __popc(cg);
+                    u |= cg;
                 }
-                bool ambiguous = false;
-                // rare path: alpha within 5% of the cutoff -> certify with the error bound
-                if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
-                    const float rel = unsafe ? 8.0f * kEps : alpha_rel_err_pixel(A, B, p);
-                    ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 4.0f * kEps * a.alpha_min;
-                }
-                if (!ambiguous && p.alpha >= a.alpha_min) {
-                    const float one_m = __fsub_rn(1.0f, p.alpha);
-                    const float Tn = __fmul_rn(T, one_m);
-                    // relative error bound of T: sum over samples of
-                    //   alpha/(1-alpha) * rel_err(alpha) + rounding
-                    // (record_err_word: rel(alpha) <= Q / om)
-                    const float rel = unsafe ? 8.0f * kEps : C.w * rcp_approx(fmaxf(p.om, 1e-30f));
-                    const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * rcp_approx(fmaxf(one_m, 1e-30f));
-                    if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
-                        ambiguous = true;
-                    } else {
-                        const float w = __fmul_rn(p.alpha, T);
-                        c0 = __fmaf_rn(w, C.x, c0);
-                        c1 = __fmaf_rn(w, C.y, c1);
-                        c2 = __fmaf_rn(w, C.z, c2);
-                        dep = __fmaf_rn(w, B.w, dep);
-                        T = Tn;
-                        errT = errTn;
-                        ++cnt;
-                        last = b0 + j - start + 1;
-                        took = true;
-                        if (T < a.t_stop) done = true;
-                    }
-                }
-                if (ambiguous) {
-                    flag_at = b0 + j - start;
-                    done = true;
+                uni = __popc(u);
+            }
+#pragma unroll
+            for (int o = 4; o; o >>= 1) {
+                sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                uni += __shfl_xor_sync(0xffffffffu, uni, o);
+            }
+            // lanes 0..7 hold the totals; broadcast so the branch below is warp-uniform
+            dense = __shfl_sync(0xffffffffu, 2 * sum >= 5 * uni, 0);  // >= 2.5 groups per entry on average
+        }
+        if (dense) {
+            int c = 0;
+            auto col = [&](int cc) {
+                uint32_t u = 0;
+#pragma unroll
+                for (int g = 0; g < G; ++g) u |= s_col[cc][TG::bit(warp, g)];
+                return u;
+            };
+            uint32_t bits = col(0);
+            while (true) {
+                while (!bits && c + 1 < nch) bits = col(++c);
+                if (!bits || __all_sync(0xffffffffu, done)) break;
+                const int j = (c << 5) + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const bool took = !done && pair(b0, buf, j);
+                if (want_contrib) {
+                    const unsigned bl = __ballot_sync(0xffffffffu, took);
+                    if (bl && lane == 0) atomicAdd(&s_cnt[j], __popc(bl));
                 }
             }
-            if (want_contrib) {
-                const unsigned ballot = __ballot_sync(0xffffffffu, took);
-                if (ballot && lane == 0) atomicAdd(&s_cnt[j], __popc(ballot));
+        } else {
+            int c = my_open ? 0 : nch;
+            uint32_t bits = my_open ? s_col[0][my_bit] : 0u;
+            while (true) {
+                while (!bits && c + 1 < nch) bits = s_col[++c][my_bit];
+                if (__all_sync(0xffffffffu, done || !bits)) break;
+                const bool act = bits != 0;
+                const int j = act ? (c << 5) + __ffs(bits) - 1 : 0;
+                bits &= bits - 1;
+                const bool took = act && !done && pair(b0, buf, j);
+                if (want_contrib) {
+                    const unsigned gb = __ballot_sync(0xffffffffu, took) & SB::mask(q);
+                    if (gb && lane == q * SB::lanes) atomicAdd(&s_cnt[j], __popc(gb));
+                }
             }
         }
         __syncthreads();
@@ -213,6 +271,29 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
     if (a.out.pixel_count) a.out.pixel_count[pix] = cnt;
 }
 
+// sub-warp groups per warp (1: 8x4, 2: 4x4, 4: 4x2 pixel sub-blocks); BSR_RASTER_G
+// overrides for A/B measurements
+int raster_groups() {
+    static const int g = [] {
+        const char *e = getenv("BSR_RASTER_G");
+        const int v = e ? atoi(e) : 4;
+        return (v == 1 || v == 2 || v == 4) ? v : 4;
+    }();
+    return g;
+}
+
+template <int G>
+static void launch_fwd_g(const RasterFwdArgs &a, int tiles, bool stats, bool contrib, cudaStream_t st) {
+    if (stats && contrib)
+        raster_fwd_kernel<true, true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+    else if (stats)
+        raster_fwd_kernel<true, false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+    else if (contrib)
+        raster_fwd_kernel<false, true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+    else
+        raster_fwd_kernel<false, false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+}
+
 int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg[3], float alpha_min,
                       float t_stop, const uint32_t *lists, const uint2 *ranges, const Record *rec,
                       unsigned long long *stats, cudaStream_t st) {
@@ -229,14 +310,12 @@ int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg
     a.ranges = ranges;
     a.rec = rec;
     a.stats = stats;
-    if (stats && out.contributions)
-        raster_fwd_kernel<true, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else if (stats)
-        raster_fwd_kernel<true, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else if (out.contributions)
-        raster_fwd_kernel<false, true><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
-    else
-        raster_fwd_kernel<false, false><<<f.n_tiles, BSR_BLOCK, 0, st>>>(a);
+    const bool contrib = out.contributions != nullptr, st_on = stats != nullptr;
+    switch (raster_groups()) {
+        case 1: launch_fwd_g<1>(a, f.n_tiles, st_on, contrib, st); break;
+        case 2: launch_fwd_g<2>(a, f.n_tiles, st_on, contrib, st); break;
+        default: launch_fwd_g<4>(a, f.n_tiles, st_on, contrib, st); break;
+    }
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
