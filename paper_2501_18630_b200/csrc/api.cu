@@ -69,18 +69,16 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
     Record r;
-    r.a = make_float4((float)(means[2 * k] - x0), (float)(means[2 * k + 1] - y0), (float)conics[3 * k],
-                      (float)conics[3 * k + 1]);
-    r.b = make_float4((float)conics[3 * k + 2], (float)opac[k], (float)betas[k], 0.f);
-    // r2 error coefficient as in preprocess.cu (extents from the conic's inverse)
+    // factored conic + r2 error coefficient as in preprocess.cu (extents from the conic's inverse)
     const double ca = conics[3 * k], cb = conics[3 * k + 1], cc = conics[3 * k + 2];
+    double l11, l21, l22;
+    const bool pd = conic_cholesky(ca, cb, cc, l11, l21, l22);
+    r.a = make_float4((float)(means[2 * k] - x0), (float)(means[2 * k + 1] - y0), (float)l11, (float)l21);
+    r.b = make_float4((float)l22, (float)opac[k], (float)betas[k], 0.f);
     const double det = ca * cc - cb * cb;
     const double ex = det > 0 ? sqrt(fabs(cc / det)) : 1e30, ey = det > 0 ? sqrt(fabs(ca / det)) : 1e30;
-    const double a = fabs(ca), b = fabs(cb), c = fabs(cc);
-    const double S = a * ex * ex + 2.0 * b * ex * ey + c * ey * ey;
-    const double kr = 5.9604644775390625e-08 * (8.0 * S + 3.0 * ((a * ex + b * ey) * (2.0 * ex + 3.0) +
-                                                                (b * ex + c * ey) * (2.0 * ey + 3.0))) * 1.5;
-    const bool unsafe = (float)kr > kUnsafeR2Err;
+    const double kr = pd ? chol_r2_error_bound(l11, l21, l22, ex + 2.0, ey + 2.0) : 1.0;
+    const bool unsafe = !pd || (float)kr > kUnsafeR2Err;
     r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
                       record_err_word(kr, (double)r.b.z, unsafe));
     double *d = rec64 + kRec64 * k;

@@ -20,19 +20,11 @@ struct PreArgs {
     FrameView f;
 };
 
-// Bound on |r2_fp32 - r2_exact| for any pixel of the footprint (r2 <= 1), accounting for
-// the fp32 rounding of the record (mean relative to the bounds corner, conic) and of the
-// r2 evaluation in eval_pair (raster.cuh):  eps * (8 S + 3 (GX + GY)) with
-//   S  = |a| ex^2 + 2|b| ex ey + |c| ey^2            (|terms| of the quadratic form)
-//   GX = (|a| ex + |b| ey)(2 ex + 3), GY = (|b| ex + |c| ey)(2 ey + 3)  (d r2 / d mean x
-//        the mean's representation error, |mean - corner| <= extent + 2)
-__device__ __forceinline__ double r2_error_bound(const Proj64 &p) {
-    const double ex = sqrt(p.c00), ey = sqrt(p.c11);
-    const double a = fabs(p.ca), b = fabs(p.cb), c = fabs(p.cc);
-    const double S = a * ex * ex + 2.0 * b * ex * ey + c * ey * ey;
-    const double GX = (a * ex + b * ey) * (2.0 * ex + 3.0);
-    const double GY = (b * ex + c * ey) * (2.0 * ey + 3.0);
-    return 5.9604644775390625e-08 * (8.0 * S + 3.0 * (GX + GY)) * 1.5;
+// Bound on |r2_fp32 - r2_exact| for any pixel of the footprint (bounds box: |dx| <= ex + 2,
+// |dy| <= ey + 2 around the mean, ex = sqrt(Sigma'_00)) of the factored evaluation in
+// eval_pair (raster.cuh chol_r2_error_bound).
+__device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, double l21, double l22) {
+    return chol_r2_error_bound(l11, l21, l22, sqrt(p.c00) + 2.0, sqrt(p.c11) + 2.0);
 }
 
 // Shared-memory staging of one CTA's 256 primitives: the parameter blocks are contiguous
@@ -150,10 +142,12 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
                                 vy * inv, vz * inv, rgb);
             const double o = sigmoid64((double)sm.op[tid]);
             const double beta = shape_to_exponent64((double)sm.shp[tid]);
-            r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)p.ca, (float)p.cb);
-            r.b = make_float4((float)p.cc, (float)o, (float)beta, (float)p.tz);
-            const float kr = (float)r2_error_bound(p);
-            unsafe = kr > kUnsafeR2Err;
+            double l11, l21, l22;
+            const bool pd = conic_cholesky(p.ca, p.cb, p.cc, l11, l21, l22);
+            r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)l11, (float)l21);
+            r.b = make_float4((float)l22, (float)o, (float)beta, (float)p.tz);
+            const float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
+            unsafe = !pd || kr > kUnsafeR2Err;
             r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
             m64[0] = p.mx;
             m64[1] = p.my;

@@ -20,7 +20,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 struct Pair {
-    float dx, dy, r2, x, om, k, alpha;
+    float dx, dy, u, w, r2, x, om, k, alpha;
 };
 
 // (1-x)^beta: two squarings for the Gaussian-like beta == 4 (no XU op); otherwise
@@ -33,16 +33,46 @@ __device__ __forceinline__ float beta_pow(float om, float beta) {
     return exp2f(__fmul_rn(beta, __log2f(om)));
 }
 
-// _raster.pyx:107-113:  r2 = a dx^2 + 2 b dx dy + c dy^2, x = clamp(r2, 0, 1),
-// kernel = (1 - x)^beta, alpha = o * kernel.  px_rel / py_rel are pixel coordinates
-// relative to the primitive's bounds corner (exact integers).
+// Cholesky factor of the conic Q = [[a, b], [b, c]] = L L^T, L = [[l11, 0], [l21, l22]]
+// (fp64, host and device): the record carries (l11, l21, l22) instead of (a, b, c), and
+//   r2 = a dx^2 + 2 b dx dy + c dy^2 = (l11 dx + l21 dy)^2 + (l22 dy)^2
+// is evaluated as a sum of two squares.  The conic form's terms are ~condition-number
+// times larger than r2 for elongated footprints and cancel; the factored form's error
+// grows only with the square root of the condition number (chol_r2_error_bound), so far
+// fewer primitives need the fp64 path.  Returns false if Q is not positive definite.
+__host__ __device__ inline bool conic_cholesky(double a, double b, double c, double &l11, double &l21,
+                                               double &l22) {
+    l11 = l21 = l22 = 0.0;
+    if (!(a > 0.0)) return false;
+    l11 = sqrt(a);
+    l21 = b / l11;
+    const double d = c - l21 * l21;
+    if (!(d > 0.0)) return false;
+    l22 = sqrt(d);
+    return true;
+}
+
+// Bound on |r2_fp32 - r2_exact| of eval_pair over a footprint |dx| <= X, |dy| <= Y with
+// the mean stored relative to the bounds corner (|rel| <= X), where it matters (r2 <= ~1,
+// so |u|, |w| <= ~1): rounding of the factors (eps U each) and of dx, dy (eps 2X, eps 2Y,
+// times |d r2 / d dx| <= 2 l11, |d r2 / d dy| <= 2 (|l21| + l22)), and of the evaluation
+// itself (u: eps (U + 1), w: eps, r2: 2 eps), U = l11 X + |l21| Y; safety factor 1.5.
+__host__ __device__ inline double chol_r2_error_bound(double l11, double l21, double l22, double X, double Y) {
+    const double U = l11 * X + fabs(l21) * Y;
+    return 5.9604644775390625e-08 * 1.5 * (4.0 * U + 8.0 + 4.0 * l11 * X + 4.0 * (fabs(l21) + l22) * Y);
+}
+
+// _raster.pyx:107-113:  r2 = a dx^2 + 2 b dx dy + c dy^2 (factored, see conic_cholesky),
+// x = clamp(r2, 0, 1), kernel = (1 - x)^beta, alpha = o * kernel.  px_rel / py_rel are
+// pixel coordinates relative to the primitive's bounds corner (exact integers); the
+// record holds A = (mean - corner, l11, l21), B.x = l22.
 __device__ __forceinline__ Pair eval_pair(const float4 A, const float4 B, int px_rel, int py_rel) {
     Pair p;
     p.dx = __fsub_rn((float)px_rel, A.x);
     p.dy = __fsub_rn((float)py_rel, A.y);
-    float t = __fmul_rn(B.x, __fmul_rn(p.dy, p.dy));
-    t = __fmaf_rn(__fmul_rn(__fmul_rn(2.0f, A.w), p.dx), p.dy, t);
-    p.r2 = __fmaf_rn(__fmul_rn(A.z, p.dx), p.dx, t);
+    p.u = __fmaf_rn(A.w, p.dy, __fmul_rn(A.z, p.dx));
+    p.w = __fmul_rn(B.x, p.dy);
+    p.r2 = __fmaf_rn(p.w, p.w, __fmul_rn(p.u, p.u));
     p.x = fminf(fmaxf(p.r2, 0.0f), 1.0f);
     p.om = __fsub_rn(1.0f, p.x);
     p.k = beta_pow(p.om, B.z);
@@ -71,6 +101,7 @@ __device__ __forceinline__ Pair eval_pair64(const double *m, const float4 B, int
     }
     p.dx = (float)dx;
     p.dy = (float)dy;
+    p.u = p.w = 0.f;  // factored terms: fp32 path only
     p.r2 = (float)r2;
     p.x = (float)x;
     p.om = (float)om;
@@ -107,46 +138,15 @@ __host__ __device__ inline float record_err_word(double kr, double beta, bool un
 }
 
 // Same bound with the r2 error evaluated at this pixel instead of the footprint maximum
-// (tighter; used on the rare alpha ~ alpha_min path):  |r2 error| <= eps (8 s + 3 (gx + gy)),
-// s = sum of |terms| of the quadratic form, g = |grad r2 / 2| x (|d| + |mean - corner| + 1).
+// (tighter; used on the rare alpha ~ alpha_min path), terms as in chol_r2_error_bound with
+// this pixel's u, w, dx, dy.
 __device__ __forceinline__ float alpha_rel_err_pixel(const float4 A, const float4 B, const Pair &p) {
-    const float s = fabsf(A.z * p.dx * p.dx) + fabsf(2.0f * A.w * p.dx * p.dy) + fabsf(B.x * p.dy * p.dy);
-    const float gx = fabsf(A.z * p.dx + A.w * p.dy) * (fabsf(p.dx) + fabsf(A.x) + 1.0f);
-    const float gy = fabsf(A.w * p.dx + B.x * p.dy) * (fabsf(p.dy) + fabsf(A.y) + 1.0f);
-    const float dr2 = 1.5f * kEps * (8.0f * s + 3.0f * (gx + gy));
+    const float au = fabsf(p.u), aw = fabsf(p.w);
+    const float U = fabsf(A.z * p.dx) + fabsf(A.w * p.dy);
+    const float gx = 2.0f * fabsf(A.z) * au * (fabsf(p.dx) + fabsf(A.x) + 1.0f);
+    const float gy = 2.0f * (fabsf(A.w) * au + fabsf(B.x) * aw) * (fabsf(p.dy) + fabsf(A.y) + 1.0f);
+    const float dr2 = 1.5f * kEps * (4.0f * au * (U + au + 1.0f) + 6.0f * aw * aw + 2.0f * fabsf(p.r2) + gx + gy + 1.0f);
     return B.z * dr2 / fmaxf(p.om, 1e-30f) + pow_rel_err(B.z);
-}
-
-// Does the ellipse r2 < 1 (+ fp32 slack) of a primitive touch the pixel-centre rectangle
-// [X0,X1] x [Y0,Y1]?  Exact minimum of the quadratic form over the rectangle (centre inside,
-// else the minimum over the four edges), conservative by the record's r2 error bound.
-__device__ __forceinline__ bool ellipse_hits_rect(const float4 A, const float4 B, const float4 C,
-                                                  const int4 D, int X0, int X1, int Y0, int Y1,
-                                                  float alpha_min) {
-    if (D.y < X0 || D.x > X1 || D.w < Y0 || D.z > Y1) return false;
-    const float mx = (float)D.x + A.x, my = (float)D.z + A.y;
-    if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
-    const float a = A.z, b = A.w, c = B.x;
-    // approximate reciprocals only perturb the edge minimiser (second-order in q)
-    const float ia = rcp_approx(a), ic = rcp_approx(c);
-    float q = 3.0e38f;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        // vertical edges x = X0 / X1
-        const float dx = (float)(e ? X1 : X0) - mx;
-        const float dy = fminf(fmaxf(my - b * dx * ic, (float)Y0), (float)Y1) - my;
-        q = fminf(q, a * dx * dx + 2.0f * b * dx * dy + c * dy * dy);
-        // horizontal edges y = Y0 / Y1
-        const float ey = (float)(e ? Y1 : Y0) - my;
-        const float ex = fminf(fmaxf(mx - b * ey * ia, (float)X0), (float)X1) - mx;
-        q = fminf(q, a * ex * ex + 2.0f * b * ex * ey + c * ey * ey);
-    }
-    // a sample can only pass alpha >= alpha_min where r2 < x_max = 1 - (alpha_min / o)^(1/beta)
-    // (o, beta as stored); relative slack 1e-4 covers the approximate lg2/ex2 and rounding
-    if (B.y < alpha_min) return false;
-    const float xmax = 1.0f - exp2f(__log2f(__fdividef(alpha_min, B.y)) * rcp_approx(B.z));
-    // r2 slack 4 kR with kR <= |Q| / beta (record_err_word)
-    return q < fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.04f * fabsf(C.w) * rcp_approx(B.z) + 1e-4f;
 }
 
 __device__ __forceinline__ bool bbox_hits_rect(const int4 D, int X0, int X1, int Y0, int Y1) {
@@ -179,13 +179,11 @@ struct SubBlock {
 // row 2 (v >> 1) + (q >> 1) [G = 4] / v >> 1.
 //
 // The test is exact per pixel row: for every pixel row y the ellipse {r2 <= xlim} (xlim =
-// the alpha cutoff plus the record's r2 error slack, as in ellipse_hits_rect) spans
-// dx in [(-b dy - sqrt(D)) / a, (-b dy + sqrt(D)) / a], D = a xlim - det dy^2; the span is
-// padded for fp32 rounding (the D cancellation costs at most ~3e-4 of the half width) and
-// clipped to the record bounds.  det = ac - b^2 of the record's fp32 conic is evaluated
-// with Kahan's FMA scheme (accurate to ~1.5 ulp of det even for needle-like footprints,
-// where the plain product difference cancels); fp32-unsafe records use the same spans
-// with their larger r2 slack.  Non-positive-definite fp32 conics and the pair-counting
+// x_max(o, beta) of the alpha cutoff, 1 - (alpha_min / o)^(1/beta), plus the record's r2
+// error slack) spans dx in [(-l21 dy - sqrt(R)) / l11, (-l21 dy + sqrt(R)) / l11],
+// R = xlim - (l22 dy)^2, in the factored form of the record; the span is padded for fp32
+// rounding and clipped to the record bounds.  fp32-unsafe records use the same spans
+// with their larger r2 slack; records without a positive factor and the pair-counting
 // variant (BBOX) use the bounds box.
 template <int G>
 struct TileGrid {
@@ -226,10 +224,8 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
     const int by0 = max(D.z - Y0, 0), by1 = min(D.w - Y0, BSR_TILE - 1);
     if (bx0 > bx1 || by0 > by1) return 0u;
     if (!BBOX && B.y < alpha_min) return 0u;
-    const float a = A.z, b = A.w, c = B.x;
-    const float bb = __fmul_rn(b, b);
-    const float det = __fadd_rn(__fmaf_rn(a, c, -bb), __fmaf_rn(-b, b, bb));  // Kahan 2x2
-    if (BBOX || !(det > 0.f && a > 0.f)) {
+    const float l11 = A.z, l21 = A.w, l22 = B.x;
+    if (BBOX || !(l11 > 0.f && l22 > 0.f)) {
         const uint32_t rb = row_bits<G>(bx0, bx1);
         uint32_t m = 0;
         for (int r = by0 / TG::h; r <= by1 / TG::h; ++r) m |= rb << (r * TG::cols);
@@ -237,20 +233,21 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
     }
     const float xmax = 1.0f - exp2f(__log2f(__fdividef(alpha_min, B.y)) * rcp_approx(B.z));
     const float xl = fminf(1.0f, xmax * 1.0001f + 1e-5f) + 4.04f * fabsf(C.w) * rcp_approx(B.z) + 1e-4f;
-    const float ia = rcp_approx(a), id = rcp_approx(det);
-    const float hy = sqrtf(xl * a * id) * 1.01f + 1e-3f;
-    // fp32 error of a row span: sqrt of the D cancellation (<= 3.5e-4 sqrt(xl / a), the span
-    // at dy = 0) plus a few ulp of the centre offset b dy / a
-    const float pad0 = 1e-3f * sqrtf(xl * ia) + 2e-3f;
+    const float sq = sqrtf(xl), il11 = rcp_approx(l11);
+    const float hy = sq * rcp_approx(l22) * 1.01f + 1e-3f;
+    // fp32 error of a row span: sqrt of the cancellation in xl - (l22 dy)^2 (<= 2.4e-4
+    // sqrt(xl) / l11, the span at w = 0) plus a few ulp of the centre offset l21 dy / l11
+    const float pad0 = 1e-3f * sq * il11 + 2e-3f;
     // mean relative to the tile origin (exact: small integers plus the record's offset)
     const float mx = (float)(D.x - X0) + A.x, my = (float)(D.z - Y0) + A.y;
     const int y0 = max(by0, (int)ceilf(my - hy)), y1 = min(by1, (int)floorf(my + hy));
     uint32_t m = 0;
     for (int y = y0; y <= y1; ++y) {
         const float dy = (float)y - my;
-        const float disc = fmaxf(a * xl - det * dy * dy, 0.f);
-        const float off = b * dy * ia;
-        const float half = sqrtf(disc) * ia * 1.001f + pad0 + 4e-7f * fabsf(off);
+        const float wy = l22 * dy;
+        const float rem = fmaxf(xl - wy * wy, 0.f);
+        const float off = l21 * dy * il11;
+        const float half = sqrtf(rem) * il11 * 1.001f + pad0 + 4e-7f * fabsf(off);
         const float cx = mx - off;
         const int x0 = max(bx0, (int)ceilf(cx - half)), x1 = min(bx1, (int)floorf(cx + half));
         if (x0 <= x1) m |= row_bits<G>(x0, x1) << ((y / TG::h) * TG::cols);

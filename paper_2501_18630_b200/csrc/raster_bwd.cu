@@ -186,8 +186,8 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
             gb = u.gb;
         } else {
             p = eval_pair(A, Bq, px - bd.x, py - bd.z);
-            ga = A.z * p.dx + A.w * p.dy;
-            gb = A.w * p.dx + Bq.x * p.dy;
+            ga = A.z * p.u;                 // a dx + b dy = l11 u
+            gb = A.w * p.u + Bq.x * p.w;    // b dx + c dy = l21 u + l22 w
         }
         const bool took = act && e < last && p.alpha >= a.alpha_min;
         const unsigned tm = __ballot_sync(0xffffffffu, took);
