@@ -125,54 +125,22 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     bool unsafe = false;
     double m64[kRec64];
     uint32_t tcount = 0;
+    Proj64 p;
     if (i < n) {
-        const float *pos = sm.pos + 3 * tid;
-        Proj64 p = project64(pos, sm.rot + 4 * tid, sm.ls + 3 * tid, args.cam);
+        p = project64(sm.pos + 3 * tid, sm.rot + 4 * tid, sm.ls + 3 * tid, args.cam);
         if (p.degenerate) raise_status(&f.ctr->status, BSR_ERR_DEGENERATE_QUAT);
-        if (p.visible) {
-            vis = true;
-            float rgb[3];
-            float vx = pos[0] - (float)args.cam.center[0], vy = pos[1] - (float)args.cam.center[1],
-                  vz = pos[2] - (float)args.cam.center[2];
-            const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
-            if constexpr (Tr::sh)
-                app_color32<CM>(app_a + 3 * Tr::K * tid, nullptr, nullptr, vx * inv, vy * inv, vz * inv, rgb);
-            else
-                app_color32<CM>(app_a + 3 * tid, app_b + 3 * Tr::M * tid, app_c + 3 * Tr::M * tid, vx * inv,
-                                vy * inv, vz * inv, rgb);
-            const double o = sigmoid64((double)sm.op[tid]);
-            const double beta = shape_to_exponent64((double)sm.shp[tid]);
-            double l11, l21, l22;
-            const bool pd = conic_cholesky(p.ca, p.cb, p.cc, l11, l21, l22);
-            r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)l11, (float)l21);
-            r.b = make_float4((float)l22, (float)o, (float)beta, (float)p.tz);
-            const float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
-            unsafe = !pd || kr > kUnsafeR2Err;
-            r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
-            m64[0] = p.mx;
-            m64[1] = p.my;
-            m64[2] = p.ca;
-            m64[3] = p.cb;
-            m64[4] = p.cc;
-            m64[5] = o;
-            m64[6] = beta;
-            m64[7] = p.tz;
-            r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
-            key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
-            key32 = (uint32_t)__float_as_int((float)p.tz);  // monotone rounding of tz
-            tcount = (uint32_t)((p.x1 / BSR_TILE - p.x0 / BSR_TILE + 1) *
-                                (p.y1 / BSR_TILE - p.y0 / BSR_TILE + 1));
-        }
+        vis = p.visible;
     }
-    // block-exclusive rank of visible primitives (source order preserved)
+    // block-exclusive rank of visible primitives (source order preserved); the block's
+    // aggregate is published as soon as visibility is known, and the look-back for the
+    // inclusive prefix runs only after the colour / record work below, by which time the
+    // predecessors have usually published theirs
     const uint32_t ballot = __ballot_sync(0xffffffffu, vis);
     const uint32_t local = __popc(ballot & ((1u << lane) - 1));
     if (lane == 0) s_warp[warp] = __popc(ballot);
-    // min depth key for the radix plan: max of the complement
-    const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
-    if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
     __syncthreads();
-    if (warp == 0) {  // block total -> aggregate, warp-parallel look-back -> prefix
+    uint32_t total = 0;
+    if (warp == 0) {
         const uint32_t mine = lane < BSR_BLOCK / 32 ? s_warp[lane] : 0u;
         uint32_t incl = mine;
 #pragma unroll
@@ -180,13 +148,49 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        total = __shfl_sync(0xffffffffu, incl, 31);
         if (lane < BSR_BLOCK / 32) s_warp[lane] = incl - mine;
+        if (lane == 0) st_release(f.pre_status + part, (part == 0 ? kFlagPrefix : kFlagAgg) | total);
+    }
+    if (vis) {
+        const float *pos = sm.pos + 3 * tid;
+        float rgb[3];
+        float vx = pos[0] - (float)args.cam.center[0], vy = pos[1] - (float)args.cam.center[1],
+              vz = pos[2] - (float)args.cam.center[2];
+        const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+        if constexpr (Tr::sh)
+            app_color32<CM>(app_a + 3 * Tr::K * tid, nullptr, nullptr, vx * inv, vy * inv, vz * inv, rgb);
+        else
+            app_color32<CM>(app_a + 3 * tid, app_b + 3 * Tr::M * tid, app_c + 3 * Tr::M * tid, vx * inv,
+                            vy * inv, vz * inv, rgb);
+        const double o = sigmoid64((double)sm.op[tid]);
+        const double beta = shape_to_exponent64((double)sm.shp[tid]);
+        double l11, l21, l22;
+        const bool pd = conic_cholesky(p.ca, p.cb, p.cc, l11, l21, l22);
+        r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)l11, (float)l21);
+        r.b = make_float4((float)l22, (float)o, (float)beta, (float)p.tz);
+        const float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
+        unsafe = !pd || kr > kUnsafeR2Err;
+        r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
+        m64[0] = p.mx;
+        m64[1] = p.my;
+        m64[2] = p.ca;
+        m64[3] = p.cb;
+        m64[4] = p.cc;
+        m64[5] = o;
+        m64[6] = beta;
+        m64[7] = p.tz;
+        r.d = make_int4(p.x0, p.x1, p.y0, p.y1);
+        key = (uint64_t)__double_as_longlong(p.tz);  // tz > 0.01: bits are monotonic
+        key32 = (uint32_t)__float_as_int((float)p.tz);  // monotone rounding of tz
+        tcount = (uint32_t)((p.x1 / BSR_TILE - p.x0 / BSR_TILE + 1) * (p.y1 / BSR_TILE - p.y0 / BSR_TILE + 1));
+    }
+    // min depth key for the radix plan: max of the complement
+    const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
+    if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
+    if (warp == 0) {  // warp-parallel look-back -> inclusive prefix
         uint32_t excl = 0;
-        if (part == 0) {
-            if (lane == 0) st_release(f.pre_status, kFlagPrefix | total);
-        } else {
-            if (lane == 0) st_release(f.pre_status + part, kFlagAgg | total);
+        if (part > 0) {
             excl = warp_lookback<uint32_t>(f.pre_status, part, 1, kFlagPrefix, kValueMask);
             if (lane == 0) st_release(f.pre_status + part, kFlagPrefix | (excl + total));
         }
