@@ -21,6 +21,7 @@
  *   mcmc.plan_relocation           mcmc.py:49-70           bsr_sample_live
  *   mcmc.apply_relocation          mcmc.py:86-106          bsr_apply_relocation
  *   mcmc.grow                      mcmc.py:108-146         bsr_sample_live + bsr_grow
+ *   sceneio.save/load_checkpoint   sceneio.py:467-564      bsr_checkpoint_pack / _unpack
  *
  * Conventions
  *   - Every pointer is DEVICE memory owned by the caller unless stated; the library
@@ -262,6 +263,15 @@ int bsr_grow(const float *src_params, const bsr_layout *src_layout, const float 
              const float *src_exp_avg_sq, float *dst_params, const bsr_layout *dst_layout,
              float *dst_exp_avg, float *dst_exp_avg_sq, const int64_t *sources, int64_t n_add,
              const int32_t *counts, double floor_, void *stream);
+
+/* ---- checkpoints (sceneio.save_checkpoint / load_checkpoint, sceneio.py:467-564) ------ */
+/* records: device (N, n_props) fp64, row-major (the PLY vertex block of the reference's
+ * checkpoint); property q of primitive i <-> flat[prop_start[q] + prop_stride[q] * i]
+ * (host tables, n_props <= 64).  unpack rounds to fp32; pack widens exactly. */
+int bsr_checkpoint_unpack(const double *records, int64_t n, int32_t n_props, const int64_t *prop_start,
+                          const int32_t *prop_stride, float *flat, void *stream);
+int bsr_checkpoint_pack(const float *flat, int64_t n, int32_t n_props, const int64_t *prop_start,
+                        const int32_t *prop_stride, double *records, void *stream);
 
 /* ---- parity / debug: export the binning of the last forward (synchronises) ---------- */
 /* order (V): compact index per depth rank (== np.argsort(depths, kind="stable"),

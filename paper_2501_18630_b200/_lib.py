@@ -130,6 +130,8 @@ EXPORTS = {
                                   c_void_p, c_uint64, c_void_p]),
     "bsr_apply_relocation": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_int64, c_void_p, c_double, c_void_p]),
+    "bsr_checkpoint_unpack": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "bsr_checkpoint_pack": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "bsr_grow": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                            c_void_p, c_int64, c_void_p, c_double, c_void_p]),
 }

@@ -105,5 +105,26 @@ def main():
     print("wrote", os.path.join(OUT, "train_aux.npz"), "dead", dead.size, "n_add", n_add)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def checkpoints():
+    """Reference-written checkpoints (sceneio.save_checkpoint) of fp32-valued parameters."""
+    import_reference()
+    from betasplat import sceneio
+    from betasplat.primitive import PrimitiveSet
+
+    for name, n, lobes, seed in (("ckpt_l2.ply", 37, 2, 41), ("ckpt_l0.ply", 5, 0, 42)):
+        rng = np.random.default_rng(seed)
+        prims = PrimitiveSet(positions=f32(rng.normal(0, 1, (n, 3))), opacity_raw=f32(rng.normal(0, 1, n)),
+                             rotations=f32(rng.normal(0, 1, (n, 4))), log_scales=f32(rng.normal(-3, 1, (n, 3))),
+                             shapes=f32(rng.normal(0, 1, n)), base_colors=f32(rng.normal(0, 1, (n, 3))),
+                             lobe_axes=f32(rng.normal(0, 1, (n, lobes, 3))),
+                             lobe_colors=f32(rng.normal(0, 1, (n, lobes, 3))))
+        sceneio.save_checkpoint(os.path.join(OUT, name), prims)
+    print("wrote checkpoints")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "checkpoints":
+    checkpoints()
