@@ -357,12 +357,9 @@ def kernel_launches_per_step(w):
     from paper_2501_18630_b200.rasterizer import frame_status
 
     cam = w["cams"][0]
-    tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
-    tile_passes = 1
-    while tile_passes < 4 and (tiles - 1) >= (1 << (8 * tile_passes)):
-        tile_passes += 1
-    # pre, depth sort (hist, plan, 4 passes, fp64 tie fixup), emit, tile sort, ranges, raster, replay
-    fwd = 1 + (2 + 4 + 1) + 2 + (2 + tile_passes) + 1 + 1 + 1
+    # pre, bin count (entries, big rects, scan), bin scatter (entries, big rects), per-tile sort,
+    # raster, replay
+    fwd = 1 + 3 + 2 + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
     per_view = fwd + 2 + 4  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain)
@@ -570,8 +567,11 @@ def main():
         V, E = info["visible"], info["entries"]
         hbm = {}
         hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80) / (stages["preprocess"] * 1e-3) / 1e9
-        hbm["depth_sort"] = (V * 12 * 2 * 7) / (stages["depth_sort"] * 1e-3) / 1e9
-        hbm["tile_sort"] = (E * 8 * 2 * 2) / (stages["tile_sort"] * 1e-3) / 1e9
+        # binning: count = V (tile count + rect, 20 B) + E 4-B atomics; scatter = V (20 B + key
+        # 4 B) + E (8-B entry + 4-B atomic); per-tile sort = E (8 B read + 4 B written)
+        hbm["bin_count"] = (V * 20 + E * 4) / (stages["bin_count"] * 1e-3) / 1e9
+        hbm["bin_scatter"] = (V * 24 + E * 12) / (stages["bin_scatter"] * 1e-3) / 1e9
+        hbm["tile_sort"] = (E * 12) / (stages["tile_sort"] * 1e-3) / 1e9
         if w["kind"] == "train":
             hbm["preprocess_bwd"] = V * (48 + 240 + 480) / (stages["preprocess_bwd"] * 1e-3) / 1e9
             cam0 = w["cams"][0]

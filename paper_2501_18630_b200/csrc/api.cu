@@ -10,9 +10,9 @@ namespace bsr {
 // kernel launchers (one per translation unit)
 int launch_preprocess(const bsr_scene &, const KCam &, const FrameView &, cudaStream_t);
 int launch_depth_sort(const FrameView &, cudaStream_t);
-int launch_emit(const FrameView &, cudaStream_t);
+int launch_bin_count(const FrameView &, cudaStream_t);
+int launch_bin_scatter(const FrameView &, cudaStream_t);
 int launch_tile_sort(const FrameView &, cudaStream_t);
-int launch_tile_ranges(const FrameView &, cudaStream_t);
 int launch_raster_fwd(const FrameView &, const bsr_outputs &, const float bg[3], float, float,
                       const uint32_t *, const uint2 *, const Record *, unsigned long long *,
                       cudaStream_t);
@@ -227,12 +227,11 @@ extern "C" int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, con
     BSR_CUDA_TRY(cudaMemsetAsync(frame, 0, f.zero_bytes, st));
     if ((rc = launch_preprocess(*scene, cam, f, st))) return rc;
     if ((rc = mark(prof, 1, st))) return rc;
-    if ((rc = launch_depth_sort(f, st))) return rc;
+    if ((rc = launch_bin_count(f, st))) return rc;
     if ((rc = mark(prof, 2, st))) return rc;
-    if ((rc = launch_emit(f, st))) return rc;
+    if ((rc = launch_bin_scatter(f, st))) return rc;
     if ((rc = mark(prof, 3, st))) return rc;
     if ((rc = launch_tile_sort(f, st))) return rc;
-    if ((rc = launch_tile_ranges(f, st))) return rc;
     if ((rc = mark(prof, 4, st))) return rc;
     if ((rc = launch_raster_fwd(f, *out, background, (float)kAlphaMin, (float)kTStop, nullptr, nullptr,
                                 nullptr, stats, st)))
@@ -430,12 +429,29 @@ extern "C" int bsr_debug_export(const void *frame, int64_t n, int32_t width, int
     Counters c;
     BSR_CUDA_TRY(cudaMemcpyAsync(&c, f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     BSR_CUDA_TRY(cudaStreamSynchronize(st));
-    if (order && c.visible)
+    if (order && c.visible) {
+        // the global depth order is not part of the per-frame binning (bin.cu sorts per
+        // tile); compute it here with the onesweep depth sort.  Its ping-pong buffers start
+        // from the keys / identity values preprocess wrote, which are saved in the gradient
+        // accumulator (zeroed by every backward before use) and restored afterwards.
+        uint32_t *save = reinterpret_cast<uint32_t *>(f.grad_acc);
+        BSR_CUDA_TRY(cudaMemcpyAsync(save, f.dkeys[0], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemcpyAsync(save + c.visible, f.dvals[0], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemsetAsync(f.depth_hist, 0, 4ull * kDepthPasses * 256, st));
+        BSR_CUDA_TRY(cudaMemsetAsync(f.depth_status, 0, 4ull * kDepthPasses * f.depth_parts * 256, st));
+        BSR_CUDA_TRY(cudaMemsetAsync(f.ctr->depth_ticket, 0, sizeof(c.depth_ticket), st));
+        BSR_CUDA_TRY(cudaMemsetAsync(f.ctr->depth_plan, 0, sizeof(c.depth_plan), st));
+        int rc = launch_depth_sort(f, st);
+        if (rc) return rc;
+        BSR_CUDA_TRY(cudaMemcpyAsync(&c, f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        BSR_CUDA_TRY(cudaStreamSynchronize(st));
         BSR_CUDA_TRY(cudaMemcpyAsync(order, f.dvals[c.depth_plan[kDepthPasses] & 1u], 4ull * c.visible,
                                      cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemcpyAsync(f.dkeys[0], save, 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemcpyAsync(f.dvals[0], save + c.visible, 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+    }
     if (lists && c.entries)
-        BSR_CUDA_TRY(cudaMemcpyAsync(lists, f.tvals[c.tile_plan[f.tile_passes] & 1u], 4ull * c.entries,
-                                     cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemcpyAsync(lists, f.lists, 4ull * c.entries, cudaMemcpyDeviceToDevice, st));
     if (ranges)
         BSR_CUDA_TRY(cudaMemcpyAsync(ranges, f.tile_ranges, 8ull * f.n_tiles, cudaMemcpyDeviceToDevice, st));
     if ((src_index || bounds) && c.visible)

@@ -1,176 +1,404 @@
-// K3b / K3d: tile binning (rasterizer.py:161-191).
+// K3: tile binning (rasterizer.py:83-85 _depth_order + :161-191 tile_bins).
 //
-// emit:   in depth-rank order r (perm from the depth sort), every primitive writes one
-//         (tile id, compact index) entry per tile of its bounds rectangle, row-major within
-//         the rectangle.  The exclusive scan of per-rank tile counts that places the
-//         entries is fused into the same kernel (single pass, 64-bit decoupled look-back),
-//         and the total E is checked against the caller's capacity (overflow -> status
-//         BSR_ERR_CAPACITY, nothing written, entries_needed reported for a retry).
-// ranges: after the stable tile sort, per-tile [start, end) from key boundaries
-//         (== np.bincount + cumsum offsets).
+// The reference sorts the visible primitives by depth (stable) and then stably sorts the
+// (tile, depth rank) entries by tile, so each tile's list is its primitives in global
+// depth order with source-index ties.  That order is a property of each tile alone, so
+// the B200 path builds it per tile instead of sorting twice globally:
+//
+//   bin_entries<COUNT>    every visible primitive adds one entry per tile of its bounds
+//                         rectangle to that tile's count (RED); warp-cooperative, so a
+//                         warp's 32 primitives' entries are spread over its lanes
+//   bin_big<COUNT>        rectangles of more than kBigRect tiles (near-plane primitives
+//                         cover whole frames), one CTA each
+//   bin_scan              one CTA: exclusive scan of the tile counts -> tile ranges, E,
+//                         capacity check (overflow -> BSR_ERR_CAPACITY, entries_needed)
+//   bin_entries<SCATTER>  each entry takes a slot in its tile (atomic cursor) and writes
+//   bin_big<SCATTER>      (fp32 depth key << 32 | compact index)
+//   tile_sort             one CTA per tile sorts its entries ascending by that 64-bit key
+//                         (bitonic, in shared memory up to kSortSmem entries, in place in
+//                         global memory beyond), then re-orders runs of equal fp32 keys by
+//                         (fp64 depth, compact index); writes the compact indices.
+//
+// fp32 rounding of the depth is monotone, so (fp32 key, then fp64 depth, then compact
+// index) is exactly the reference's order (compact index order == source order of the
+// visible primitives).  Nothing here needs a host synchronisation: counts and E live in
+// device memory, grids are sized by capacity with early exits.
 #include "frame.cuh"
 
 namespace bsr {
 
-constexpr uint32_t kBigRect = 64;  // rectangles with more tiles are emitted by a whole CTA
-constexpr unsigned long long kFlag64Agg = 1ull << 62;
-constexpr unsigned long long kFlag64Prefix = 2ull << 62;
-constexpr unsigned long long kValue64Mask = (1ull << 62) - 1;
+constexpr uint32_t kBigRect = 512;   // rectangles with more tiles are binned by a whole CTA
+constexpr int kSortSmem = 4096;      // entries sorted in shared memory (32 KB of u64)
 
-template <int kEmitItems>
-__global__ void __launch_bounds__(BSR_BLOCK) emit_kernel(FrameView f) {
-    constexpr int kEmitTile = BSR_BLOCK * kEmitItems;
-    __shared__ uint32_t s_part;
-    __shared__ unsigned long long s_warp[BSR_BLOCK / 32], s_excl;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    if (t == 0) s_part = atomicAdd(&f.ctr->emit_ticket, 1u);
-    __syncthreads();
+struct RectInfo {
+    int tx0, ty0, spanx;
+};
+
+__device__ __forceinline__ RectInfo rect_of(const FrameView &f, uint32_t c) {
+    const int4 bd = f.rec[c].d;
+    RectInfo r;
+    r.tx0 = bd.x / BSR_TILE;
+    r.ty0 = bd.z / BSR_TILE;
+    r.spanx = bd.y / BSR_TILE - r.tx0 + 1;
+    return r;
+}
+
+__device__ __forceinline__ bool over_capacity(const FrameView &f) {
+    return f.ctr->entries_needed > (unsigned long long)f.entry_cap;
+}
+
+// Warp-cooperative binning of compact primitives [32 w, 32 w + 32): lane l owns primitive
+// 32 w + l; the warp's entries (inclusive prefix `incl` over the lanes) are taken
+// round-robin by the lanes, each finding its entry's owner by a 5-step search over the
+// prefix.  COUNT: tile_cnt[t] += 1.  Otherwise: slot = tile_cur[t]++, write the entry.
+template <bool COUNT>
+__global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
     const uint32_t V = f.ctr->visible;
-    const int64_t part = s_part;
-    const int64_t base = part * kEmitTile;
-    if (base >= (int64_t)V) return;
-    const int64_t nparts = div_up(V, kEmitTile);
-    const uint32_t *perm = f.dvals[f.ctr->depth_plan[kDepthPasses] & 1u];
-    // blocked arrangement: thread t owns ranks base + t*ITEMS .. +ITEMS
-    uint32_t cidx[kEmitItems], cnt[kEmitItems];
-    unsigned long long tsum = 0;
-#pragma unroll
-    for (int i = 0; i < kEmitItems; ++i) {
-        const int64_t r = base + (int64_t)t * kEmitItems + i;
-        if (r < (int64_t)V) {
-            cidx[i] = perm[r];
-            cnt[i] = f.tile_count[cidx[i]];
-        } else {
-            cidx[i] = 0;
-            cnt[i] = 0;
+    if (!COUNT && over_capacity(f)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (BSR_BLOCK / 32);
+    for (int64_t w = (blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x) >> 5; w * 32 < (int64_t)V; w += nwarps) {
+        const uint32_t c = (uint32_t)(w * 32 + lane);
+        uint32_t cnt = 0;
+        RectInfo r{0, 0, 1};
+        uint64_t key = 0;
+        if (c < V) {
+            cnt = f.tile_count[c];
+            if (cnt > kBigRect) {  // a whole CTA takes it (bin_big_kernel)
+                if (COUNT) f.big[atomicAdd(&f.ctr->big_rects, 1u)] = make_uint2(c, cnt);
+                cnt = 0;
+            } else if (cnt) {
+                r = rect_of(f, c);
+                if (!COUNT) key = ((uint64_t)f.dkeys[0][c] << 32) | c;
+            }
         }
-        tsum += cnt[i];
-    }
-    // block exclusive scan of thread sums
-    unsigned long long x = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {  // block total -> aggregate, warp-parallel look-back -> prefix
-        const unsigned long long mine = lane < BSR_BLOCK / 32 ? s_warp[lane] : 0ull;
-        unsigned long long incl = mine;
+        uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        const unsigned long long run = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane < BSR_BLOCK / 32) s_warp[lane] = incl - mine;
-        unsigned long long excl = 0;
-        volatile unsigned long long *st = f.emit_status;
-        if (part == 0) {
-            if (lane == 0) {
-                __threadfence();
-                st[0] = kFlag64Prefix | run;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t e = base + lane;
+            // owner = number of lanes whose inclusive prefix is <= e
+            int lo = 0;
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + s - 1);
+                if (v <= e) lo += s;
             }
-        } else {
-            if (lane == 0) {
-                __threadfence();
-                st[part] = kFlag64Agg | run;
-            }
-            excl = warp_lookback<unsigned long long>(f.emit_status, part, 1, kFlag64Prefix, kValue64Mask);
-            if (lane == 0) {
-                __threadfence();
-                st[part] = kFlag64Prefix | (excl + run);
+            const int owner = min(lo, 31);
+            const uint32_t oin = __shfl_sync(0xffffffffu, incl, owner);
+            const uint32_t ocnt = __shfl_sync(0xffffffffu, cnt, owner);
+            const int tx0 = __shfl_sync(0xffffffffu, r.tx0, owner);
+            const int ty0 = __shfl_sync(0xffffffffu, r.ty0, owner);
+            const int spanx = __shfl_sync(0xffffffffu, r.spanx, owner);
+            const uint64_t okey = __shfl_sync(0xffffffffu, key, owner);
+            if (e >= total) continue;
+            const uint32_t local = e - (oin - ocnt);
+            const uint32_t row = local / (uint32_t)spanx;
+            const uint32_t t = (uint32_t)(ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(tx0 + (int)(local - row * spanx));
+            if (COUNT) {
+                atomicAdd(&f.tile_cnt[t], 1u);
+            } else {
+                const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
+                f.tent[f.tile_ranges[t].x + slot] = okey;
             }
         }
-        if (lane == 0) {
-            s_excl = excl;
-            if (part == nparts - 1) {
-                const unsigned long long total = excl + run;
-                f.ctr->entries_needed = total;
-                if (total > (unsigned long long)f.entry_cap) {
-                    f.ctr->entries = 0;
-                    raise_status(&f.ctr->status, BSR_ERR_CAPACITY);
-                } else {
-                    f.ctr->entries = (uint32_t)total;
+    }
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(BSR_BLOCK) bin_big_kernel(FrameView f) {
+    const uint32_t nbig = f.ctr->big_rects;
+    if (!COUNT && over_capacity(f)) return;
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const uint2 it = f.big[b];
+        const RectInfo r = rect_of(f, it.x);
+        const uint64_t key = ((uint64_t)f.dkeys[0][it.x] << 32) | it.x;
+        for (uint32_t j = threadIdx.x; j < it.y; j += BSR_BLOCK) {
+            const uint32_t row = j / (uint32_t)r.spanx;
+            const uint32_t t = (uint32_t)(r.ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(r.tx0 + (int)(j - row * r.spanx));
+            if (COUNT) {
+                atomicAdd(&f.tile_cnt[t], 1u);
+            } else {
+                const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
+                f.tent[f.tile_ranges[t].x + slot] = key;
+            }
+        }
+    }
+}
+
+// One CTA of 1024 threads: tile ranges from the counts (== np.bincount + cumsum offsets).
+__global__ void __launch_bounds__(1024) bin_scan_kernel(FrameView f) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ bool s_over;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int T = f.n_tiles;
+    const int per = (T + 1023) / 1024;
+    const int t0 = min(T, t * per), t1 = min(T, t0 + per);
+    unsigned long long mine = 0;
+    for (int i = t0; i < t1; ++i) mine += f.tile_cnt[i];
+    unsigned long long incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long v = s_w[lane];
+        unsigned long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        s_w[lane] = x - v;
+        if (lane == 31) {
+            f.ctr->entries_needed = x;
+            s_over = x > (unsigned long long)f.entry_cap;
+            if (s_over) {
+                f.ctr->entries = 0;
+                raise_status(&f.ctr->status, BSR_ERR_CAPACITY);
+            } else {
+                f.ctr->entries = (uint32_t)x;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long run = s_w[warp] + incl - mine;
+    const bool over = s_over;  // overflow: every tile empty (the caller retries larger)
+    for (int i = t0; i < t1; ++i) {
+        const uint32_t c = over ? 0u : f.tile_cnt[i];
+        f.tile_ranges[i] = over ? make_uint2(0u, 0u) : make_uint2((uint32_t)run, (uint32_t)(run + c));
+        run += c;
+    }
+}
+
+// Ascending bitonic sort of a[0, n) with virtual +inf padding to the next power of two
+// N: every compare-exchange keeps the smaller value at the lower index (first stage of
+// each merge compares i with its mirror, the rest are half-cleaners), so pairs whose upper
+// index is >= n are skipped.  All threads of the CTA call it.
+template <typename P, typename Sync>
+__device__ void bitonic_sort(P a, int n, int me, int nthreads, Sync sync) {
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int i = me; i < N / 2; i += nthreads) {
+            const int h = k >> 1;
+            const int lo = ((i & ~(h - 1)) << 1) | (i & (h - 1)), hi = lo ^ (k - 1);
+            if (hi < n) {
+                const uint64_t x = a[lo], y = a[hi];
+                if (y < x) {
+                    a[lo] = y;
+                    a[hi] = x;
                 }
             }
         }
+        sync();
+        for (int j = k >> 2; j >= 1; j >>= 1) {
+            for (int i = me; i < N / 2; i += nthreads) {
+                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+                if (hi < n) {
+                    const uint64_t x = a[lo], y = a[hi];
+                    if (y < x) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+            }
+            sync();
+        }
+    }
+}
+template <typename P>
+__device__ void bitonic_sort_block(P a, int n) {
+    bitonic_sort(a, n, (int)threadIdx.x, (int)blockDim.x, [] { __syncthreads(); });
+}
+template <typename P>
+__device__ void bitonic_sort_warp(P a, int n) {
+    bitonic_sort(a, n, (int)(threadIdx.x & 31), 32, [] { __syncwarp(); });
+}
+
+// Runs of equal fp32 keys: re-order by (fp64 depth, compact index); the thread at the
+// start of each run insertion-sorts it (runs are rare and short).
+template <typename P>
+__device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {
+    for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) {
+        const uint32_t ki = (uint32_t)(a[i] >> 32);
+        if ((uint32_t)(a[i + 1] >> 32) != ki || (i > 0 && (uint32_t)(a[i - 1] >> 32) == ki)) continue;
+        int j = i + 2;
+        while (j < n && (uint32_t)(a[j] >> 32) == ki) ++j;
+        for (int p = i + 1; p < j; ++p) {
+            const uint64_t vp = a[p];
+            const uint64_t dp = dkey64[(uint32_t)vp];
+            int q = p;
+            while (q > i) {
+                const uint64_t vq = a[q - 1];
+                const uint64_t dq = dkey64[(uint32_t)vq];
+                if (dq < dp || (dq == dp && (uint32_t)vq < (uint32_t)vp)) break;
+                a[q] = vq;
+                --q;
+            }
+            a[q] = vp;
+        }
     }
     __syncthreads();
-    unsigned long long off = s_excl + s_warp[warp] + (x - tsum);
-    const int tiles_x = f.tiles_x;
-#pragma unroll 1
-    for (int i = 0; i < kEmitItems; ++i) {
-        if (cnt[i] == 0) continue;
-        if (off + cnt[i] > (unsigned long long)f.entry_cap) return;  // overflow: caller retries
-        if (cnt[i] > kBigRect) {  // load balance: near-plane primitives cover whole frames
-            const uint32_t slot = atomicAdd(&f.ctr->big_emit, 1u);
-            f.big[slot] = make_uint4(cidx[i], (uint32_t)off, (uint32_t)(off >> 32), cnt[i]);
-            off += cnt[i];
+}
+
+// Per-tile order by the fp32 depth key.  Equal keys are re-ordered by fixup_ties anyway,
+// so the sort need not be stable: a bucket sort on the tile's key range (buckets ~ entries,
+// linear in the key bits), shared-memory atomics for the scatter, insertion sort inside
+// the (tiny) buckets; buckets of more than kMaxBucket entries (keys bunched in part of the
+// tile's range) get a warp each and a bitonic network.
+constexpr int kBuckets = 1024;
+constexpr int kMaxBucket = 16;  // larger buckets: one warp each, bitonic
+
+__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
+    __shared__ uint64_t s[kSortSmem];
+    __shared__ uint32_t s_start[kBuckets], s_cur[kBuckets];
+    __shared__ uint32_t s_kmin, s_kmax, s_big;
+    if (over_capacity(f)) return;
+    const uint2 rg = f.tile_ranges[blockIdx.x];
+    const int n = (int)(rg.y - rg.x);
+    if (n == 0) return;
+    const int t = threadIdx.x, lane = t & 31;
+    uint64_t *g = f.tent + rg.x;
+    uint32_t *out = f.lists + rg.x;
+    if (n > kSortSmem) {  // very crowded tile: the bitonic network in place in global memory
+        bitonic_sort_block(g, n);
+        fixup_ties(g, n, f.dkey64);
+        for (int i = t; i < n; i += BSR_BLOCK) out[i] = (uint32_t)g[i];
+        return;
+    }
+    if (n == 1) {
+        if (t == 0) out[0] = (uint32_t)g[0];
+        return;
+    }
+    // key range
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int i = t; i < n; i += BSR_BLOCK) {
+        const uint32_t k = (uint32_t)(g[i] >> 32);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (t == 0) {
+        s_kmin = 0xffffffffu;
+        s_kmax = 0u;
+        s_big = 0u;
+    }
+    int nb = 1;
+    while (nb < n && nb < kBuckets) nb <<= 1;
+    for (int b = t; b < nb; b += BSR_BLOCK) s_start[b] = 0u;
+    __syncthreads();
+    if (lane == 0) {
+        atomicMin(&s_kmin, kmin);
+        atomicMax(&s_kmax, kmax);
+    }
+    __syncthreads();
+    kmin = s_kmin;
+    const uint64_t span = (uint64_t)(s_kmax - kmin) + 1u;
+    auto bucket = [&](uint64_t e) { return (int)(((uint64_t)((uint32_t)(e >> 32) - kmin) * (uint64_t)nb) / span); };
+    for (int i = t; i < n; i += BSR_BLOCK) atomicAdd(&s_start[bucket(g[i])], 1u);
+    __syncthreads();
+    {
+        // exclusive scan of the bucket counts (nb <= 1024: 4 per thread)
+        uint32_t v[4], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int b = 4 * t + q;
+            v[q] = b < nb ? s_start[b] : 0u;
+            tot += v[q];
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        __shared__ uint32_t s_w[BSR_BLOCK / 32];
+        if (lane == 31) s_w[t >> 5] = incl;
+        __syncthreads();
+        uint32_t run = incl - tot;
+        for (int w = 0; w < (t >> 5); ++w) run += s_w[w];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int b = 4 * t + q;
+            if (b < nb) {
+                s_start[b] = run;
+                s_cur[b] = run;
+            }
+            run += v[q];
+        }
+    }
+    __syncthreads();
+    for (int i = t; i < n; i += BSR_BLOCK) {
+        const uint64_t e = g[i];
+        s[atomicAdd(&s_cur[bucket(e)], 1u)] = e;
+    }
+    __syncthreads();
+    // small buckets: insertion sort by one thread; large ones (keys bunched in the tile's
+    // range): queued, then a warp each runs a bitonic network on it
+    __shared__ uint32_t s_bigl[kBuckets];
+    for (int b = t; b < nb; b += BSR_BLOCK) {
+        const int lo = (int)s_start[b], hi = (int)s_cur[b];
+        if (hi - lo > kMaxBucket) {
+            s_bigl[atomicAdd(&s_big, 1u)] = (uint32_t)b;
             continue;
         }
-        const int4 bd = f.rec[cidx[i]].d;
-        const int tx0 = bd.x / BSR_TILE, tx1 = bd.y / BSR_TILE;
-        const int ty0 = bd.z / BSR_TILE, ty1 = bd.w / BSR_TILE;
-        uint32_t *kout = f.tkeys[0] + off;
-        uint32_t *vout = f.tvals[0] + off;
-        int j = 0;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx, ++j) {
-                kout[j] = (uint32_t)(ty * tiles_x + tx);
-                vout[j] = cidx[i];
+        for (int p = lo + 1; p < hi; ++p) {
+            const uint64_t x = s[p];
+            int q = p;
+            while (q > lo && s[q - 1] > x) {
+                s[q] = s[q - 1];
+                --q;
             }
-        off += cnt[i];
-    }
-}
-
-// Cooperative emission of the big rectangles queued by emit_kernel: one CTA per rectangle,
-// consecutive threads write consecutive (row-major) entries.
-__global__ void __launch_bounds__(BSR_BLOCK) emit_big_kernel(FrameView f) {
-    const uint32_t nbig = f.ctr->big_emit;
-    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
-        const uint4 it = f.big[b];
-        const int4 bd = f.rec[it.x].d;
-        const int tx0 = bd.x / BSR_TILE, ty0 = bd.z / BSR_TILE;
-        const uint32_t spanx = (uint32_t)(bd.y / BSR_TILE - tx0 + 1);
-        const unsigned long long off = (unsigned long long)it.y | ((unsigned long long)it.z << 32);
-        uint32_t *kout = f.tkeys[0] + off;
-        uint32_t *vout = f.tvals[0] + off;
-        for (uint32_t j = threadIdx.x; j < it.w; j += BSR_BLOCK) {
-            const uint32_t ty = ty0 + j / spanx, tx = tx0 + j % spanx;
-            kout[j] = ty * (uint32_t)f.tiles_x + tx;
-            vout[j] = it.x;
+            s[q] = x;
         }
     }
-}
-
-__global__ void tile_ranges_kernel(FrameView f) {
-    const uint32_t E = f.ctr->entries;
-    const uint32_t sel = f.ctr->tile_plan[f.tile_passes] & 1u;
-    const uint32_t *keys = f.tkeys[sel];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i];
-        if (i == 0 || keys[i - 1] != k) f.tile_ranges[k].x = i;
-        if (i == E - 1 || keys[i + 1] != k) f.tile_ranges[k].y = i + 1;
+    __syncthreads();
+    for (uint32_t k = t >> 5; k < s_big; k += BSR_BLOCK / 32) {
+        const int b = (int)s_bigl[k];
+        const int lo = (int)s_start[b];
+        bitonic_sort_warp(s + lo, (int)s_cur[b] - lo);
     }
+    __syncthreads();
+    fixup_ties(s, n, f.dkey64);
+    for (int i = t; i < n; i += BSR_BLOCK) out[i] = (uint32_t)s[i];
 }
 
-int launch_emit(const FrameView &f, cudaStream_t st) {
+static unsigned entry_blocks(const FrameView &f) {
+    return (unsigned)imin64(div_up(f.n, BSR_BLOCK), 148 * 16);
+}
+
+// counts -> ranges (profile stage "bin count")
+int launch_bin_count(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    if (f.depth_items == 4)
-        emit_kernel<4><<<(unsigned)div_up(f.n, BSR_BLOCK * 4), BSR_BLOCK, 0, st>>>(f);
-    else
-        emit_kernel<16><<<(unsigned)div_up(f.n, BSR_BLOCK * 16), BSR_BLOCK, 0, st>>>(f);
-    emit_big_kernel<<<148 * 4, BSR_BLOCK, 0, st>>>(f);
+    bin_entries_kernel<true><<<entry_blocks(f), BSR_BLOCK, 0, st>>>(f);
+    bin_big_kernel<true><<<148 * 2, BSR_BLOCK, 0, st>>>(f);
+    bin_scan_kernel<<<1, 1024, 0, st>>>(f);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
 
-int launch_tile_ranges(const FrameView &f, cudaStream_t st) {
-    if (f.entry_cap == 0) return BSR_OK;
-    const unsigned blocks = (unsigned)imin64(div_up(f.entry_cap, BSR_BLOCK), 148 * 16);
-    tile_ranges_kernel<<<blocks, BSR_BLOCK, 0, st>>>(f);
+// entries -> their tiles (profile stage "bin scatter")
+int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
+    if (f.n == 0) return BSR_OK;
+    bin_entries_kernel<false><<<entry_blocks(f), BSR_BLOCK, 0, st>>>(f);
+    bin_big_kernel<false><<<148 * 2, BSR_BLOCK, 0, st>>>(f);
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+// per-tile depth order (profile stage "tile sort")
+int launch_tile_sort(const FrameView &f, cudaStream_t st) {
+    if (f.n == 0 || f.n_tiles == 0) return BSR_OK;
+    tile_sort_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(f);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -24,27 +24,23 @@ struct Counters {
     uint32_t flagged;        // flagged pixels
     int32_t status;          // first device-side error
     uint32_t pre_ticket;     // preprocess partition ticket
-    uint32_t emit_ticket;
-    uint32_t depth_ticket[kDepthPasses];
-    uint32_t tile_ticket[4];
+    uint32_t big_rects;      // primitives whose tile rectangle is binned by a whole CTA
+    uint32_t depth_ticket[kDepthPasses];   // global depth sort (parity export only)
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
-    uint32_t big_emit;           // primitives whose tile rectangle is emitted cooperatively
     uint32_t depth_plan[kDepthPasses + 1];
-    uint32_t tile_plan[4 + 1];
-    uint32_t pad[6];
+    uint32_t pad[3];
 };
 
 struct FrameView {
     // --- zeroed every forward (one memset) ---
     Counters *ctr;
-    uint32_t *depth_hist;    // [4][256]
-    uint32_t *tile_hist;     // [4][256]
     uint32_t *pre_status;    // [ceil(N/256)]
-    uint32_t *depth_status;  // [4][ceil(N/4096)][256]
-    unsigned long long *emit_status;  // [ceil(N/4096)]
-    uint32_t *tile_status;   // [tile_passes][ceil(Ecap/4096)][256]
     uint2 *tile_ranges;      // [n_tiles] (start, end)
+    uint32_t *tile_cnt;      // [n_tiles] entries per tile
+    uint32_t *tile_cur;      // [n_tiles] scatter cursors
     // --- not zeroed ---
+    uint32_t *depth_hist;    // [4][256]                  global depth sort: parity export only,
+    uint32_t *depth_status;  // [4][ceil(N/4096)][256]     zeroed by bsr_debug_export
     Record *rec;             // [N] compact order
     uint32_t *src_of;        // [N] compact -> source index (batch.indices)
     double *rec64;           // [N][8] fp64 {mean x, y, conic a, b, c, opacity, beta, depth}:
@@ -54,9 +50,9 @@ struct FrameView {
     uint64_t *dkey64;        // [N] fp64 depth bits, compact order (tie fixup)
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched, compact order
-    uint4 *big;              // [N] (compact index, entry offset lo, hi, count) of big rects
-    uint32_t *tkeys[2];      // [Ecap] tile ids (ping-pong)
-    uint32_t *tvals[2];      // [Ecap] compact index (ping-pong)
+    uint2 *big;              // [N] (compact index, tile count) of big rectangles
+    uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | compact index), scattered per tile
+    uint32_t *lists;         // [Ecap] compact index per tile entry in depth order (tile_ranges)
     float *t_final;          // [H*W]
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
@@ -64,17 +60,11 @@ struct FrameView {
     float *grad_acc;         // [N][12] raster gradient accumulators (zeroed by backward)
     // --- sizes ---
     int64_t n, entry_cap;
-    int W, H, tiles_x, tiles_y, n_tiles, tile_passes;
-    int64_t pre_parts, depth_parts, tile_parts;
-    int depth_items, tile_items;  // sort_items() of the depth sort / emission and the tile sort
+    int W, H, tiles_x, tiles_y, n_tiles;
+    int64_t pre_parts, depth_parts;
+    int depth_items;  // sort_items() of the (parity-export) depth sort
     uint64_t zero_bytes, total_bytes;
 };
-
-inline int tile_key_passes(int n_tiles) {
-    int p = 1;
-    while (p < 4 && (uint64_t)(n_tiles - 1) >= (1ull << (8 * p))) ++p;
-    return p;
-}
 
 // Carve the frame.  base == nullptr computes sizes only.
 inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_cap) {
@@ -86,12 +76,9 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.tiles_x = (W + BSR_TILE - 1) / BSR_TILE;
     f.tiles_y = (H + BSR_TILE - 1) / BSR_TILE;
     f.n_tiles = f.tiles_x * f.tiles_y;
-    f.tile_passes = tile_key_passes(f.n_tiles);
     f.pre_parts = div_up(n > 0 ? n : 1, BSR_BLOCK);
     f.depth_items = sort_items(n);
-    f.tile_items = sort_items(entry_cap);
     f.depth_parts = div_up(n > 0 ? n : 1, (int64_t)BSR_BLOCK * f.depth_items);
-    f.tile_parts = div_up(entry_cap > 0 ? entry_cap : 1, (int64_t)BSR_BLOCK * f.tile_items);
     const int64_t npx = (int64_t)W * H;
     uint64_t off = 0;
     char *b = static_cast<char *>(base);
@@ -102,15 +89,14 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
         return p;
     };
     f.ctr = (Counters *)take(sizeof(Counters));
-    f.depth_hist = (uint32_t *)take(4ull * kDepthPasses * 256);
-    f.tile_hist = (uint32_t *)take(4ull * 4 * 256);
     f.pre_status = (uint32_t *)take(4ull * f.pre_parts);
-    f.depth_status = (uint32_t *)take(4ull * kDepthPasses * f.depth_parts * 256);
-    f.emit_status = (unsigned long long *)take(8ull * f.depth_parts);
-    f.tile_status = (uint32_t *)take(4ull * f.tile_passes * f.tile_parts * 256);
     f.tile_ranges = (uint2 *)take(8ull * f.n_tiles);
+    f.tile_cnt = (uint32_t *)take(4ull * f.n_tiles);
+    f.tile_cur = (uint32_t *)take(4ull * f.n_tiles);
     off = align_up(off, 256);
     f.zero_bytes = off;
+    f.depth_hist = (uint32_t *)take(4ull * kDepthPasses * 256);
+    f.depth_status = (uint32_t *)take(4ull * kDepthPasses * f.depth_parts * 256);
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
     f.src_of = (uint32_t *)take(4ull * n);
     f.rec64 = (double *)take(8ull * kRec64 * n);
@@ -120,11 +106,9 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.dvals[0] = (uint32_t *)take(4ull * n);
     f.dvals[1] = (uint32_t *)take(4ull * n);
     f.tile_count = (uint32_t *)take(4ull * n);
-    f.big = (uint4 *)take(16ull * n);
-    f.tkeys[0] = (uint32_t *)take(4ull * entry_cap);
-    f.tkeys[1] = (uint32_t *)take(4ull * entry_cap);
-    f.tvals[0] = (uint32_t *)take(4ull * entry_cap);
-    f.tvals[1] = (uint32_t *)take(4ull * entry_cap);
+    f.big = (uint2 *)take(8ull * n);
+    f.tent = (uint64_t *)take(8ull * entry_cap);
+    f.lists = (uint32_t *)take(4ull * entry_cap);
     f.t_final = (float *)take(4ull * npx);
     f.last = (uint32_t *)take(4ull * npx);
     f.flags = (uint2 *)take(8ull * npx);

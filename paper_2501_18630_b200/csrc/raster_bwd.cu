@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
     const int q = SB::group(lane), k = lane % L;
     const int px = wx0 + SB::px(lane), py = wy0 + SB::py(lane);
-    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint32_t *lists = a.lists ? a.lists : f.lists;
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x;

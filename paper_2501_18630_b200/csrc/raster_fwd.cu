@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
     const int q = SB::group(lane);
     const int px = wx0 + SB::px(lane), py = wy0 + SB::py(lane);
     const bool inside = px < f.W && py < f.H;
-    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint32_t *lists = a.lists ? a.lists : f.lists;
     const Record *rec = a.rec ? a.rec : f.rec;
     const uint2 range = (a.ranges ? a.ranges : f.tile_ranges)[tile];
     const int start = (int)range.x, end = (int)range.y;

@@ -148,7 +148,7 @@ template <typename P>
 __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplaySmem &sm) {
     const FrameView &f = a.f;
     const int t = threadIdx.x;
-    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint32_t *lists = a.lists ? a.lists : f.lists;
     const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
     const uint2 fl = f.flags[slot];
     const int64_t pix = fl.x;
@@ -242,7 +242,7 @@ template <typename P>
 __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplaySmem &sm) {
     const FrameView &f = a.f;
     const int t = threadIdx.x;
-    const uint32_t *lists = a.lists ? a.lists : f.tvals[f.ctr->tile_plan[f.tile_passes] & 1u];
+    const uint32_t *lists = a.lists ? a.lists : f.lists;
     const uint2 *ranges = a.ranges ? a.ranges : f.tile_ranges;
     const uint2 fl = f.flags[slot];
     const int64_t pix = fl.x;

@@ -1,11 +1,9 @@
 // K3a / K3c: hand-written onesweep LSD radix sort (stable), 8-bit digits.
 //
-// Used twice per frame:
-//   depth sort  64-bit keys = bits of fp64 camera z (> 0.01, so bit order == value order),
-//               values = compact index (ascending source index) -> stable sort reproduces
-//               np.argsort(depths, kind="stable") (rasterizer.py:83-85) bit-exactly;
-//   tile sort   32-bit keys = tile id, values = compact index, emitted in depth-rank order
-//               -> stable sort reproduces tile_bins' stable argsort (rasterizer.py:187).
+// The global depth order (np.argsort(depths, kind="stable"), rasterizer.py:83-85) for the
+// parity export: 32-bit keys = fp32-rounded camera z (monotone), values = compact index
+// (ascending source index), then the fp64 tie fixup below.  The per-frame binning does
+// not need it (bin.cu sorts each tile's entries by the same key).
 //
 // Fully device-driven (no host sync): the element count lives in device memory, one
 // histogram kernel computes every digit place at once, a 1-block plan kernel scans them,
@@ -314,24 +312,6 @@ int launch_depth_sort(const FrameView &f, cudaStream_t st) {
         BSR_LAUNCH_CHECK();
     }
     return BSR_OK;
-}
-
-int launch_tile_sort(const FrameView &f, cudaStream_t st) {
-    SortArgs<uint32_t> a;
-    a.keys[0] = f.tkeys[0];
-    a.keys[1] = f.tkeys[1];
-    a.vals[0] = f.tvals[0];
-    a.vals[1] = f.tvals[1];
-    a.count = &f.ctr->entries;
-    a.bias_inv = nullptr;
-    a.hist = f.tile_hist;
-    a.plan = f.ctr->tile_plan;
-    a.status = f.tile_status;
-    a.tickets = f.ctr->tile_ticket;
-    a.passes = f.tile_passes;
-    a.items = f.tile_items;
-    a.max_parts = f.tile_parts;
-    return launch_sort(a, f.entry_cap, st);
 }
 
 }  // namespace bsr

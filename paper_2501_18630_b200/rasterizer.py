@@ -342,7 +342,7 @@ class StageProfiler:
     the algorithmic pair counts the raster rooflines are computed from.  Events are
     per view, so a multi-view step needs no synchronisation until collect_step()."""
 
-    FWD = ("preprocess", "depth_sort", "emit", "tile_sort", "raster_fwd", "replay_fwd")
+    FWD = ("preprocess", "bin_count", "bin_scatter", "tile_sort", "raster_fwd", "replay_fwd")
     BWD = ("raster_bwd", "replay_bwd", "preprocess_bwd")
     EXTRA = ("loss", "adam")
 
