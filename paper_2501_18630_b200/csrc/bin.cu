@@ -255,25 +255,26 @@ __device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {
 // the (tiny) buckets; buckets of more than kMaxBucket entries (keys bunched in part of the
 // tile's range) get a warp each and a bitonic network.
 constexpr int kBuckets = 1024;
+constexpr int kSortBig = 16384;   // crowded tiles: 128 KB of dynamic shared memory
+constexpr int kBucketsBig = 4096;
 constexpr int kMaxBucket = 16;  // larger buckets: one warp each, bitonic
 
-__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
-    __shared__ uint64_t s[kSortSmem];
-    __shared__ uint32_t s_start[kBuckets], s_cur[kBuckets];
-    __shared__ uint32_t s_kmin, s_kmax, s_big;
-    if (over_capacity(f)) return;
-    const uint2 rg = f.tile_ranges[blockIdx.x];
+template <int NB>
+struct SortSmem {
+    uint32_t start[NB], cur[NB], bigl[NB];
+    uint32_t w[BSR_BLOCK / 32];
+    uint32_t kmin, kmax, big;
+};
+
+// Sort tile `tile`'s entries (n <= capacity of s) into f.lists; all threads of the CTA.
+template <int NB>
+__device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB> &sm) {
+    const uint2 rg = f.tile_ranges[tile];
     const int n = (int)(rg.y - rg.x);
     if (n == 0) return;
     const int t = threadIdx.x, lane = t & 31;
     uint64_t *g = f.tent + rg.x;
     uint32_t *out = f.lists + rg.x;
-    if (n > kSortSmem) {  // very crowded tile: the bitonic network in place in global memory
-        bitonic_sort_block(g, n);
-        fixup_ties(g, n, f.dkey64);
-        for (int i = t; i < n; i += BSR_BLOCK) out[i] = (uint32_t)g[i];
-        return;
-    }
     if (n == 1) {
         if (t == 0) out[0] = (uint32_t)g[0];
         return;
@@ -288,31 +289,36 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (t == 0) {
-        s_kmin = 0xffffffffu;
-        s_kmax = 0u;
-        s_big = 0u;
+        sm.kmin = 0xffffffffu;
+        sm.kmax = 0u;
+        sm.big = 0u;
     }
     int nb = 1;
-    while (nb < n && nb < kBuckets) nb <<= 1;
-    for (int b = t; b < nb; b += BSR_BLOCK) s_start[b] = 0u;
+    while (nb < n && nb < NB) nb <<= 1;
+    for (int b = t; b < nb; b += BSR_BLOCK) sm.start[b] = 0u;
     __syncthreads();
     if (lane == 0) {
-        atomicMin(&s_kmin, kmin);
-        atomicMax(&s_kmax, kmax);
+        atomicMin(&sm.kmin, kmin);
+        atomicMax(&sm.kmax, kmax);
     }
     __syncthreads();
-    kmin = s_kmin;
-    const uint64_t span = (uint64_t)(s_kmax - kmin) + 1u;
-    auto bucket = [&](uint64_t e) { return (int)(((uint64_t)((uint32_t)(e >> 32) - kmin) * (uint64_t)nb) / span); };
-    for (int i = t; i < n; i += BSR_BLOCK) atomicAdd(&s_start[bucket(g[i])], 1u);
+    kmin = sm.kmin;
+    // bucket = floor((key - kmin) * nb / span) in fp32: every step is monotone, so the bucket
+    // index never decreases with the key (which is all the bucket sort needs)
+    const float scale = (float)nb / ((float)(sm.kmax - kmin) + 1.0f);
+    auto bucket = [&](uint64_t e) {
+        return min(nb - 1, (int)((float)((uint32_t)(e >> 32) - kmin) * scale));
+    };
+    for (int i = t; i < n; i += BSR_BLOCK) atomicAdd(&sm.start[bucket(g[i])], 1u);
     __syncthreads();
     {
-        // exclusive scan of the bucket counts (nb <= 1024: 4 per thread)
-        uint32_t v[4], tot = 0;
+        // exclusive scan of the bucket counts (NB / 256 per thread)
+        constexpr int kPer = NB / BSR_BLOCK;
+        uint32_t v[kPer], tot = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int b = 4 * t + q;
-            v[q] = b < nb ? s_start[b] : 0u;
+        for (int q = 0; q < kPer; ++q) {
+            const int b = kPer * t + q;
+            v[q] = b < nb ? sm.start[b] : 0u;
             tot += v[q];
         }
         uint32_t incl = tot;
@@ -321,17 +327,16 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        __shared__ uint32_t s_w[BSR_BLOCK / 32];
-        if (lane == 31) s_w[t >> 5] = incl;
+        if (lane == 31) sm.w[t >> 5] = incl;
         __syncthreads();
         uint32_t run = incl - tot;
-        for (int w = 0; w < (t >> 5); ++w) run += s_w[w];
+        for (int w = 0; w < (t >> 5); ++w) run += sm.w[w];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int b = 4 * t + q;
+        for (int q = 0; q < kPer; ++q) {
+            const int b = kPer * t + q;
             if (b < nb) {
-                s_start[b] = run;
-                s_cur[b] = run;
+                sm.start[b] = run;
+                sm.cur[b] = run;
             }
             run += v[q];
         }
@@ -339,16 +344,15 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
     __syncthreads();
     for (int i = t; i < n; i += BSR_BLOCK) {
         const uint64_t e = g[i];
-        s[atomicAdd(&s_cur[bucket(e)], 1u)] = e;
+        s[atomicAdd(&sm.cur[bucket(e)], 1u)] = e;
     }
     __syncthreads();
     // small buckets: insertion sort by one thread; large ones (keys bunched in the tile's
     // range): queued, then a warp each runs a bitonic network on it
-    __shared__ uint32_t s_bigl[kBuckets];
     for (int b = t; b < nb; b += BSR_BLOCK) {
-        const int lo = (int)s_start[b], hi = (int)s_cur[b];
+        const int lo = (int)sm.start[b], hi = (int)sm.cur[b];
         if (hi - lo > kMaxBucket) {
-            s_bigl[atomicAdd(&s_big, 1u)] = (uint32_t)b;
+            sm.bigl[atomicAdd(&sm.big, 1u)] = (uint32_t)b;
             continue;
         }
         for (int p = lo + 1; p < hi; ++p) {
@@ -362,14 +366,51 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
         }
     }
     __syncthreads();
-    for (uint32_t k = t >> 5; k < s_big; k += BSR_BLOCK / 32) {
-        const int b = (int)s_bigl[k];
-        const int lo = (int)s_start[b];
-        bitonic_sort_warp(s + lo, (int)s_cur[b] - lo);
+    for (uint32_t k = t >> 5; k < sm.big; k += BSR_BLOCK / 32) {
+        const int b = (int)sm.bigl[k];
+        const int lo = (int)sm.start[b];
+        bitonic_sort_warp(s + lo, (int)sm.cur[b] - lo);
     }
     __syncthreads();
     fixup_ties(s, n, f.dkey64);
     for (int i = t; i < n; i += BSR_BLOCK) out[i] = (uint32_t)s[i];
+    __syncthreads();  // s / sm are reused by the next tile of a persistent CTA
+}
+
+// one CTA per tile with up to kSortSmem entries; bigger tiles are queued for the kernel below
+__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
+    __shared__ uint64_t s[kSortSmem];
+    __shared__ SortSmem<kBuckets> sm;
+    if (over_capacity(f)) return;
+    const uint2 rg = f.tile_ranges[blockIdx.x];
+    if (rg.y - rg.x > (uint32_t)kSortSmem) {
+        if (threadIdx.x == 0) f.big_tiles[atomicAdd(&f.ctr->big_tiles, 1u)] = blockIdx.x;
+        return;
+    }
+    sort_tile<kBuckets>(f, blockIdx.x, s, sm);
+}
+
+// crowded tiles (more than kSortSmem entries): up to kSortBig in dynamic shared memory,
+// beyond that the bitonic network in place in global memory
+__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_big_kernel(FrameView f) {
+    extern __shared__ __align__(16) uint64_t sb[];  // [kSortBig] entries, then the bucket arrays
+    SortSmem<kBucketsBig> &sm = *reinterpret_cast<SortSmem<kBucketsBig> *>(sb + kSortBig);
+    if (over_capacity(f)) return;
+    const uint32_t nbig = f.ctr->big_tiles;
+    for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
+        const int tile = (int)f.big_tiles[k];
+        const uint2 rg = f.tile_ranges[tile];
+        const int n = (int)(rg.y - rg.x);
+        if (n <= kSortBig) {
+            sort_tile<kBucketsBig>(f, tile, sb, sm);
+        } else {
+            uint64_t *g = f.tent + rg.x;
+            bitonic_sort_block(g, n);
+            fixup_ties(g, n, f.dkey64);
+            for (int i = threadIdx.x; i < n; i += BSR_BLOCK) f.lists[rg.x + i] = (uint32_t)g[i];
+            __syncthreads();
+        }
+    }
 }
 
 static unsigned entry_blocks(const FrameView &f) {
@@ -399,6 +440,13 @@ int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
 int launch_tile_sort(const FrameView &f, cudaStream_t st) {
     if (f.n == 0 || f.n_tiles == 0) return BSR_OK;
     tile_sort_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(f);
+    static bool attr = false;
+    const int smem = (int)(sizeof(uint64_t) * kSortBig + sizeof(SortSmem<kBucketsBig>));
+    if (!attr) {
+        BSR_CUDA_TRY(cudaFuncSetAttribute(tile_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    tile_sort_big_kernel<<<148, BSR_BLOCK, smem, st>>>(f);
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

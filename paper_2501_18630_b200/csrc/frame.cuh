@@ -25,10 +25,11 @@ struct Counters {
     int32_t status;          // first device-side error
     uint32_t pre_ticket;     // preprocess partition ticket
     uint32_t big_rects;      // primitives whose tile rectangle is binned by a whole CTA
+    uint32_t big_tiles;      // tiles sorted by the crowded-tile kernel
     uint32_t depth_ticket[kDepthPasses];   // global depth sort (parity export only)
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
     uint32_t depth_plan[kDepthPasses + 1];
-    uint32_t pad[3];
+    uint32_t pad[2];
 };
 
 struct FrameView {
@@ -51,6 +52,7 @@ struct FrameView {
     uint32_t *dvals[2];      // [N] compact index (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched, compact order
     uint2 *big;              // [N] (compact index, tile count) of big rectangles
+    uint32_t *big_tiles;     // [n_tiles] tiles with more entries than the shared-memory sort
     uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | compact index), scattered per tile
     uint32_t *lists;         // [Ecap] compact index per tile entry in depth order (tile_ranges)
     float *t_final;          // [H*W]
@@ -107,6 +109,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.dvals[1] = (uint32_t *)take(4ull * n);
     f.tile_count = (uint32_t *)take(4ull * n);
     f.big = (uint2 *)take(8ull * n);
+    f.big_tiles = (uint32_t *)take(4ull * f.n_tiles);
     f.tent = (uint64_t *)take(8ull * entry_cap);
     f.lists = (uint32_t *)take(4ull * entry_cap);
     f.t_final = (float *)take(4ull * npx);
