@@ -358,3 +358,22 @@ def test_spherical_beta_training_step(cuda):
         st.step()
     torch.cuda.synchronize()
     assert float(st.loss_values[0, 0]) < l0
+
+
+@pytest.mark.parametrize("n", [6000, 20000])
+def test_crowded_tile_binning(cuda, n):
+    """Tiles with more entries than the shared-memory sort (> 4096: 128 KB kernel; > 16384:
+    in-place network in global memory): lists, offsets and depth order stay bit-exact."""
+    rng = np.random.default_rng(50 + n)
+    scene = random_scene(rng, n, degree=0, spread=0.1, scale_range=(0.002, 0.01), opacity_range=(0.02, 0.1))
+    scene.positions[:, :2] += np.float32(0.1)  # inside one tile of the 48 x 48 view
+    _compare_forward(scene, toy_camera(48, 48), np.ones(3), cuda)
+
+
+def test_big_rectangles_binned_by_whole_ctas(cuda):
+    """Primitives whose bounds cover more than 512 tiles (bin_big_kernel) next to small ones."""
+    rng = np.random.default_rng(61)
+    scene = random_scene(rng, 400, degree=1, spread=0.8, scale_range=(0.01, 0.05))
+    scene.log_scales[:6] = np.log(np.float32(1.5))  # 6 huge footprints
+    scene.opacity_raw[:6] = np.float32(-3.0)
+    _compare_forward(scene, toy_camera(512, 384), np.ones(3), cuda)
