@@ -54,6 +54,7 @@ __device__ __forceinline__ void adam1(const AdamArgs &a, float &p, float g, floa
 // primitive.py), so one learning rate serves a whole float4.
 template <bool ALIGNED4>
 __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
+    pdl_wait();
     __shared__ float s_c[3];
     if (threadIdx.x == 0) {
         float c1 = a.inv_c1, c2 = a.inv_c2, ls = 0.f;
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
     }
 }
 
-__global__ void adam_bump_kernel(int64_t *step) { *step += 1; }
+__global__ void adam_bump_kernel(int64_t *step) {
+    pdl_wait(); *step += 1; }
 
 }  // namespace bsr
 
@@ -152,10 +154,10 @@ static int adam_impl(float *params, const float *grads, float *exp_avg, float *e
     bool aligned4 = true;
     for (int k = 0; k < n_groups - 1; ++k) aligned4 = aligned4 && (group_end[k] % 4 == 0);
     if (aligned4)
-        adam_kernel<true><<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
+        BSR_CUDA_TRY((pdl_launch(adam_kernel<true>, dim3(blocks), dim3(BSR_BLOCK), 0, (cudaStream_t)stream, a)));
     else
-        adam_kernel<false><<<blocks, BSR_BLOCK, 0, (cudaStream_t)stream>>>(a);
-    if (step_dev) adam_bump_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_dev);
+        BSR_CUDA_TRY((pdl_launch(adam_kernel<false>, dim3(blocks), dim3(BSR_BLOCK), 0, (cudaStream_t)stream, a)));
+    if (step_dev) BSR_CUDA_TRY((pdl_launch(adam_bump_kernel, dim3(1), dim3(1), 0, (cudaStream_t)stream, step_dev)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // C-ABI entry points of libbsr.so (declared in include/bsr.h): stream-ordered
 // orchestration of the kernels.  No allocation, no host sync except bsr_frame_status.
 #include <math.h>
@@ -33,6 +34,7 @@ constexpr double kAlphaMin = 1.0 / 255.0;  // rasterizer.py:28
 constexpr double kTStop = 1e-4;            // rasterizer.py:29
 
 __global__ void zero_acc_kernel(FrameView f) {
+    pdl_wait();
     const uint32_t V = f.ctr->visible;
     const int64_t n4 = (int64_t)V * kGradStride / 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
@@ -158,6 +160,16 @@ inline int mark(const bsr_profile *p, int i, cudaStream_t st) {
 
 using namespace bsr;
 
+namespace bsr {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("BSR_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+}  // namespace bsr
+
 static bool bad_camera(const bsr_camera *c) {
     return !c || c->width < 1 || c->height < 1 || !(c->fx > 0) || !(c->fy > 0);
 }
@@ -272,8 +284,7 @@ extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
     const KCam cam = make_kcam(*camera);
     int rc;
     if ((rc = mark(prof, 0, st))) return rc;
-    zero_acc_kernel<<<(unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8), BSR_BLOCK,
-                      0, st>>>(f);
+    BSR_CUDA_TRY((pdl_launch(zero_acc_kernel, dim3((unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8)), dim3(BSR_BLOCK), 0, st, f)));
     BSR_LAUNCH_CHECK();
     // fork: the fp64 replay of the flagged pixels runs beside the fp32 raster backward
     SideStream *ss = nullptr;

@@ -53,6 +53,7 @@ __device__ __forceinline__ bool over_capacity(const FrameView &f) {
 // prefix.  COUNT: tile_cnt[t] += 1.  Otherwise: slot = tile_cur[t]++, write the entry.
 template <bool COUNT>
 __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
+    pdl_wait();
     const uint32_t V = f.ctr->visible;
     if (!COUNT && over_capacity(f)) return;
     const int lane = threadIdx.x & 31;
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
 
 template <bool COUNT>
 __global__ void __launch_bounds__(BSR_BLOCK) bin_big_kernel(FrameView f) {
+    pdl_wait();
     const uint32_t nbig = f.ctr->big_rects;
     if (!COUNT && over_capacity(f)) return;
     for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
@@ -132,6 +134,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_big_kernel(FrameView f) {
 
 // One CTA of 1024 threads: tile ranges from the counts (== np.bincount + cumsum offsets).
 __global__ void __launch_bounds__(1024) bin_scan_kernel(FrameView f) {
+    pdl_wait();
     __shared__ unsigned long long s_w[32];
     __shared__ bool s_over;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -379,6 +382,7 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
 
 // one CTA per tile with up to kSortSmem entries; bigger tiles are queued for the kernel below
 __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
+    pdl_wait();
     __shared__ uint64_t s[kSortSmem];
     __shared__ SortSmem<kBuckets> sm;
     if (over_capacity(f)) return;
@@ -393,6 +397,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
 // crowded tiles (more than kSortSmem entries): up to kSortBig in dynamic shared memory,
 // beyond that the bitonic network in place in global memory
 __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_big_kernel(FrameView f) {
+    pdl_wait();
     extern __shared__ __align__(16) uint64_t sb[];  // [kSortBig] entries, then the bucket arrays
     SortSmem<kBucketsBig> &sm = *reinterpret_cast<SortSmem<kBucketsBig> *>(sb + kSortBig);
     if (over_capacity(f)) return;
@@ -420,9 +425,9 @@ static unsigned entry_blocks(const FrameView &f) {
 // counts -> ranges (profile stage "bin count")
 int launch_bin_count(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    bin_entries_kernel<true><<<entry_blocks(f), BSR_BLOCK, 0, st>>>(f);
-    bin_big_kernel<true><<<148 * 2, BSR_BLOCK, 0, st>>>(f);
-    bin_scan_kernel<<<1, 1024, 0, st>>>(f);
+    BSR_CUDA_TRY((pdl_launch(bin_entries_kernel<true>, dim3(entry_blocks(f)), dim3(BSR_BLOCK), 0, st, f)));
+    BSR_CUDA_TRY((pdl_launch(bin_big_kernel<true>, dim3(148 * 2), dim3(BSR_BLOCK), 0, st, f)));
+    BSR_CUDA_TRY((pdl_launch(bin_scan_kernel, dim3(1), dim3(1024), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -430,8 +435,8 @@ int launch_bin_count(const FrameView &f, cudaStream_t st) {
 // entries -> their tiles (profile stage "bin scatter")
 int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    bin_entries_kernel<false><<<entry_blocks(f), BSR_BLOCK, 0, st>>>(f);
-    bin_big_kernel<false><<<148 * 2, BSR_BLOCK, 0, st>>>(f);
+    BSR_CUDA_TRY((pdl_launch(bin_entries_kernel<false>, dim3(entry_blocks(f)), dim3(BSR_BLOCK), 0, st, f)));
+    BSR_CUDA_TRY((pdl_launch(bin_big_kernel<false>, dim3(148 * 2), dim3(BSR_BLOCK), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -439,14 +444,14 @@ int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
 // per-tile depth order (profile stage "tile sort")
 int launch_tile_sort(const FrameView &f, cudaStream_t st) {
     if (f.n == 0 || f.n_tiles == 0) return BSR_OK;
-    tile_sort_kernel<<<f.n_tiles, BSR_BLOCK, 0, st>>>(f);
+    BSR_CUDA_TRY((pdl_launch(tile_sort_kernel, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, f)));
     static bool attr = false;
     const int smem = (int)(sizeof(uint64_t) * kSortBig + sizeof(SortSmem<kBucketsBig>));
     if (!attr) {
         BSR_CUDA_TRY(cudaFuncSetAttribute(tile_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    tile_sort_big_kernel<<<148, BSR_BLOCK, smem, st>>>(f);
+    BSR_CUDA_TRY((pdl_launch(tile_sort_big_kernel, dim3(148), dim3(BSR_BLOCK), smem, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -196,6 +196,34 @@ __host__ __device__ inline uint64_t align_up(uint64_t a, uint64_t b) { return (a
 
 }  // namespace bsr
 
+namespace bsr {
+// ---- programmatic dependent launch (sm_90+): hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's grid is launched while
+// its predecessor in the stream drains (no launch gap between dependent kernels, also
+// inside captured CUDA graphs).  Every such kernel calls pdl_wait() before it touches
+// memory; griddepcontrol.wait returns once the predecessor grid has completed and its
+// writes are visible (immediately for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+bool pdl_enabled();  // api.cu (BSR_NO_PDL=1 disables, for A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+}  // namespace bsr
+
 #define BSR_CUDA_TRY(expr)                                      \
     do {                                                        \
         cudaError_t _e = (expr);                                \

@@ -53,6 +53,7 @@ struct HPair {
 };
 
 __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
+    pdl_wait();
     __shared__ float2 s_in[3][kIH][kIW];  // (a, b) per channel, zero outside the image
     __shared__ float2 s_hp[kIH][kTW], s_hq[kIH][kTW];
     __shared__ __align__(16) float s_hx[kIH][kTW];
@@ -211,6 +212,7 @@ __device__ __forceinline__ void loss_finish(const LossArgs &p) {
 }
 
 __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
+    pdl_wait();
     __shared__ float2 s_p[2][kIH][kIW];  // (d_mu, d_qa), double-buffered over channels
     __shared__ float s_x[2][kIH][kIW];   // d_qab
     __shared__ float2 s_hp[kIH][kTW];
@@ -364,8 +366,8 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     }
     for (int i = 0; i < 11; ++i) p.w[i] = (float)(w[i] / sum);
     dim3 grid((unsigned)div_up(width, kTW), (unsigned)div_up(height, kTH));
-    ssim_maps_kernel<<<grid, 256, 0, st>>>(p);
-    ssim_grad_kernel<<<grid, 256, 0, st>>>(p);
+    BSR_CUDA_TRY((pdl_launch(ssim_maps_kernel, dim3(grid), dim3(256), 0, st, p)));
+    BSR_CUDA_TRY((pdl_launch(ssim_grad_kernel, dim3(grid), dim3(256), 0, st, p)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -40,6 +40,7 @@ struct PreSmem {
 
 template <int CM>
 __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs args) {
+    pdl_wait();
     using Tr = AppTraits<CM>;
     const FrameView &f = args.f;
     extern __shared__ __align__(16) unsigned char pre_smem_raw[];
@@ -223,7 +224,7 @@ static int launch_pre_k(const PreArgs &a, unsigned blocks, cudaStream_t st) {
                                           (int)smem));
         attr = true;
     }
-    preprocess_fwd_kernel<CM><<<blocks, BSR_BLOCK, smem, st>>>(a);
+    BSR_CUDA_TRY((pdl_launch(preprocess_fwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), smem, st, a)));
     return BSR_OK;
 }
 

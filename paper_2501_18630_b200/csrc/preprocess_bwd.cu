@@ -168,6 +168,7 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
 
 template <int K>
 __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a) {
+    pdl_wait();
     const uint32_t V = a.f.ctr->visible;
     const uint32_t c = blockIdx.x * BSR_BLOCK + threadIdx.x;
     if (c >= V) return;
@@ -342,7 +343,7 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
     if (f.n == 0) return BSR_OK;
     PreBwdArgs a{sc, cam, f, g, screen_grad_norm};
     const unsigned blocks = (unsigned)div_up(f.n, BSR_BLOCK);
-#define BSR_PREBWD_LAUNCH(CM) preprocess_bwd_kernel<CM><<<blocks, BSR_BLOCK, 0, st>>>(a)
+#define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
     BSR_LAUNCH_CHECK();

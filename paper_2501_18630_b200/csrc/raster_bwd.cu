@@ -97,6 +97,7 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // state (T, behind colour) exactly unchanged and all 11 partials exactly 0.
 template <bool STATS, int G>
 __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
+    pdl_wait();
     using SB = SubBlock<G>;
     using TG = TileGrid<G>;
     constexpr int L = SB::lanes;
@@ -339,11 +340,12 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
 int raster_groups();
 
 template <int G>
-static void launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
+static int launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
     if (stats)
-        raster_bwd_kernel<true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else
-        raster_bwd_kernel<false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    return BSR_OK;
 }
 
 int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, const float *d_depth,
@@ -370,11 +372,13 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, c
         return e ? atoi(e) : 2;
     }();
     a.direct_max = direct_max;
+    int rc = BSR_OK;
     switch (raster_groups()) {
-        case 1: launch_bwd_g<1>(a, f.n_tiles, stats != nullptr, st); break;
-        case 2: launch_bwd_g<2>(a, f.n_tiles, stats != nullptr, st); break;
-        default: launch_bwd_g<4>(a, f.n_tiles, stats != nullptr, st); break;
+        case 1: rc = launch_bwd_g<1>(a, f.n_tiles, stats != nullptr, st); break;
+        case 2: rc = launch_bwd_g<2>(a, f.n_tiles, stats != nullptr, st); break;
+        default: rc = launch_bwd_g<4>(a, f.n_tiles, stats != nullptr, st); break;
     }
+    if (rc) return rc;
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

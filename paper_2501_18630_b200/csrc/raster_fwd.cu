@@ -44,6 +44,7 @@ __device__ __noinline__ float2 unsafe_pair_fwd(const double *m64, float4 B, int 
 
 template <bool STATS, bool CONTRIB, int G>
 __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
+    pdl_wait();
     using SB = SubBlock<G>;
     using TG = TileGrid<G>;
     __shared__ __align__(16) Record s_rec[2][BSR_BLOCK];
@@ -283,15 +284,16 @@ int raster_groups() {
 }
 
 template <int G>
-static void launch_fwd_g(const RasterFwdArgs &a, int tiles, bool stats, bool contrib, cudaStream_t st) {
+static int launch_fwd_g(const RasterFwdArgs &a, int tiles, bool stats, bool contrib, cudaStream_t st) {
     if (stats && contrib)
-        raster_fwd_kernel<true, true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<true, true, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (stats)
-        raster_fwd_kernel<true, false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<true, false, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (contrib)
-        raster_fwd_kernel<false, true, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, true, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else
-        raster_fwd_kernel<false, false, G><<<tiles, BSR_BLOCK, 0, st>>>(a);
+        BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, false, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    return BSR_OK;
 }
 
 int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg[3], float alpha_min,
@@ -311,11 +313,13 @@ int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg
     a.rec = rec;
     a.stats = stats;
     const bool contrib = out.contributions != nullptr, st_on = stats != nullptr;
+    int rc = BSR_OK;
     switch (raster_groups()) {
-        case 1: launch_fwd_g<1>(a, f.n_tiles, st_on, contrib, st); break;
-        case 2: launch_fwd_g<2>(a, f.n_tiles, st_on, contrib, st); break;
-        default: launch_fwd_g<4>(a, f.n_tiles, st_on, contrib, st); break;
+        case 1: rc = launch_fwd_g<1>(a, f.n_tiles, st_on, contrib, st); break;
+        case 2: rc = launch_fwd_g<2>(a, f.n_tiles, st_on, contrib, st); break;
+        default: rc = launch_fwd_g<4>(a, f.n_tiles, st_on, contrib, st); break;
     }
+    if (rc) return rc;
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -335,6 +335,7 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
 
 template <typename P>
 __global__ void __launch_bounds__(BSR_BLOCK) replay_fwd_kernel(ReplayArgs a, P prov) {
+    pdl_wait();
     __shared__ ReplaySmem sm;
     const uint32_t n = a.f.ctr->flagged;
     for (uint32_t slot = blockIdx.x; slot < n; slot += gridDim.x) {
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) replay_fwd_kernel(ReplayArgs a, P p
 
 template <typename P>
 __global__ void __launch_bounds__(BSR_BLOCK) replay_bwd_kernel(ReplayArgs a, P prov) {
+    pdl_wait();
     __shared__ ReplaySmem sm;
     const uint32_t n = a.f.ctr->flagged;
     for (uint32_t slot = blockIdx.x; slot < n; slot += gridDim.x) {
@@ -361,9 +363,9 @@ static unsigned replay_blocks(const FrameView &) {
 template <typename P>
 static int launch_replay(bool fwd, const ReplayArgs &a, const P &prov, cudaStream_t st) {
     if (fwd)
-        replay_fwd_kernel<P><<<replay_blocks(a.f), BSR_BLOCK, 0, st>>>(a, prov);
+        BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P>, dim3(replay_blocks(a.f)), dim3(BSR_BLOCK), 0, st, a, prov)));
     else
-        replay_bwd_kernel<P><<<replay_blocks(a.f), BSR_BLOCK, 0, st>>>(a, prov);
+        BSR_CUDA_TRY((pdl_launch(replay_bwd_kernel<P>, dim3(replay_blocks(a.f)), dim3(BSR_BLOCK), 0, st, a, prov)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
