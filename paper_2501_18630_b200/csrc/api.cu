@@ -33,13 +33,13 @@ int launch_preprocess_bwd(const bsr_scene &, const KCam &, const FrameView &, co
 constexpr double kAlphaMin = 1.0 / 255.0;  // rasterizer.py:28
 constexpr double kTStop = 1e-4;            // rasterizer.py:29
 
+// raster-gradient accumulators of the visible primitives (3 float4 each)
 __global__ void zero_acc_kernel(FrameView f) {
     pdl_wait();
-    const uint32_t V = f.ctr->visible;
-    const int64_t n4 = (int64_t)V * kGradStride / 4;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<float4 *>(f.grad_acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t n3 = f.n * (kGradStride / 4);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n3; q += (int64_t)gridDim.x * blockDim.x)
+        if (f.tile_count[q / (kGradStride / 4)])
+            reinterpret_cast<float4 *>(f.grad_acc)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // ---- core seam helpers ------------------------------------------------------------
@@ -66,7 +66,7 @@ inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
 
 __global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
                                  const double *opac, const double *betas, const double *colors,
-                                 const int32_t *bounds, Record *rec, uint32_t *src_of, double *rec64) {
+                                 const int32_t *bounds, Record *rec, double *rec64) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
@@ -94,7 +94,6 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     d[7] = 0.0;
     r.d = make_int4(x0, x1, y0, y1);
     rec[k] = r;
-    src_of[k] = (uint32_t)k;
 }
 
 __global__ void core_lists_kernel(const int64_t *offsets, const int64_t *lists, int64_t e,
@@ -323,8 +322,7 @@ static int core_prepare(const CoreView &c, int64_t v, const double *means, const
     BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
     if (v > 0)
         core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
-                                                                               colors, bounds, c.f.rec, c.f.src_of,
-                                                                               c.f.rec64);
+                                                                               colors, bounds, c.f.rec, c.f.rec64);
     const int64_t m = imax64(n_entries, c.f.n_tiles);
     core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
         offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);
@@ -415,19 +413,55 @@ extern "C" int bsr_core_backward(int64_t v, const double *means, const double *c
 }
 
 // ---- debug / parity export -----------------------------------------------------------
+// The frame indexes everything by source index; the export reports the reference's batch
+// (compact) indices: comp[i] = rank of visible primitive i among the visible ones.
 namespace bsr {
-__global__ void export_records_kernel(FrameView f, int32_t *src, int32_t *bounds) {
-    const uint32_t V = f.ctr->visible;
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= V) return;
-    const Record r = f.rec[c];
-    if (src) src[c] = (int32_t)f.src_of[c];
-    if (bounds) {
-        bounds[4 * c] = r.d.x;
-        bounds[4 * c + 1] = r.d.y;
-        bounds[4 * c + 2] = r.d.z;
-        bounds[4 * c + 3] = r.d.w;
+__global__ void __launch_bounds__(1024) export_compact_kernel(FrameView f, uint32_t *comp, int32_t *src,
+                                                               int32_t *bounds) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_carry;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < f.n; b0 += 1024) {
+        const int64_t i = b0 + t;
+        const uint32_t v = (i < f.n && f.tile_count[i]) ? 1u : 0u;
+        const uint32_t m = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) s_w[warp] = __popc(m);
+        __syncthreads();
+        uint32_t base = s_carry;
+        for (int w = 0; w < warp; ++w) base += s_w[w];
+        const uint32_t c = base + __popc(m & ((1u << lane) - 1u));
+        if (v) {
+            comp[i] = c;
+            if (src) src[c] = (int32_t)i;
+            if (bounds) {
+                const int4 d = f.rec[i].d;
+                bounds[4 * c] = d.x;
+                bounds[4 * c + 1] = d.y;
+                bounds[4 * c + 2] = d.z;
+                bounds[4 * c + 3] = d.w;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < 32; ++w) tot += s_w[w];
+            s_carry += tot;
+        }
+        __syncthreads();
     }
+}
+// depth-sort inputs in compact order: keys[c] = fp32 key of its source, vals[c] = source
+__global__ void export_keys_kernel(FrameView f, const uint32_t *comp) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= f.n || !f.tile_count[i]) return;
+    f.dkeys[1][comp[i]] = f.dkeys[0][i];
+    f.dvals[1][comp[i]] = (uint32_t)i;
+}
+__global__ void export_map_kernel(const uint32_t *comp, const uint32_t *in, int32_t *out, int64_t m) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < m) out[k] = (int32_t)comp[in[k]];
 }
 }  // namespace bsr
 
@@ -440,33 +474,39 @@ extern "C" int bsr_debug_export(const void *frame, int64_t n, int32_t width, int
     Counters c;
     BSR_CUDA_TRY(cudaMemcpyAsync(&c, f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     BSR_CUDA_TRY(cudaStreamSynchronize(st));
+    if (f.n == 0) return BSR_OK;
+    // scratch (the gradient accumulator is zeroed by every backward before use):
+    //   comp [N] | saved dkeys[0] [N] | sorted-order staging [N]
+    uint32_t *comp = reinterpret_cast<uint32_t *>(f.grad_acc);
+    uint32_t *saved = comp + f.n;
+    uint32_t *tmp = saved + f.n;
+    export_compact_kernel<<<1, 1024, 0, st>>>(f, comp, src_index, bounds);
+    BSR_LAUNCH_CHECK();
     if (order && c.visible) {
         // the global depth order is not part of the per-frame binning (bin.cu sorts per
-        // tile); compute it here with the onesweep depth sort.  Its ping-pong buffers start
-        // from the keys / identity values preprocess wrote, which are saved in the gradient
-        // accumulator (zeroed by every backward before use) and restored afterwards.
-        uint32_t *save = reinterpret_cast<uint32_t *>(f.grad_acc);
-        BSR_CUDA_TRY(cudaMemcpyAsync(save, f.dkeys[0], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
-        BSR_CUDA_TRY(cudaMemcpyAsync(save + c.visible, f.dvals[0], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        // tile); compute it here with the onesweep depth sort over the compact keys
+        BSR_CUDA_TRY(cudaMemcpyAsync(saved, f.dkeys[0], 4ull * f.n, cudaMemcpyDeviceToDevice, st));
+        export_keys_kernel<<<(unsigned)div_up(f.n, BSR_BLOCK), BSR_BLOCK, 0, st>>>(f, comp);
+        BSR_CUDA_TRY(cudaMemcpyAsync(f.dkeys[0], f.dkeys[1], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        BSR_CUDA_TRY(cudaMemcpyAsync(f.dvals[0], f.dvals[1], 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
         BSR_CUDA_TRY(cudaMemsetAsync(f.depth_hist, 0, 4ull * kDepthPasses * 256, st));
         BSR_CUDA_TRY(cudaMemsetAsync(f.depth_status, 0, 4ull * kDepthPasses * f.depth_parts * 256, st));
         BSR_CUDA_TRY(cudaMemsetAsync(f.ctr->depth_ticket, 0, sizeof(c.depth_ticket), st));
         BSR_CUDA_TRY(cudaMemsetAsync(f.ctr->depth_plan, 0, sizeof(c.depth_plan), st));
-        int rc = launch_depth_sort(f, st);
+        int rc = launch_depth_sort(f, st);  // values: source indices; fixup reads dkey64[source]
         if (rc) return rc;
         BSR_CUDA_TRY(cudaMemcpyAsync(&c, f.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         BSR_CUDA_TRY(cudaStreamSynchronize(st));
-        BSR_CUDA_TRY(cudaMemcpyAsync(order, f.dvals[c.depth_plan[kDepthPasses] & 1u], 4ull * c.visible,
+        BSR_CUDA_TRY(cudaMemcpyAsync(tmp, f.dvals[c.depth_plan[kDepthPasses] & 1u], 4ull * c.visible,
                                      cudaMemcpyDeviceToDevice, st));
-        BSR_CUDA_TRY(cudaMemcpyAsync(f.dkeys[0], save, 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
-        BSR_CUDA_TRY(cudaMemcpyAsync(f.dvals[0], save + c.visible, 4ull * c.visible, cudaMemcpyDeviceToDevice, st));
+        export_map_kernel<<<(unsigned)div_up(c.visible, BSR_BLOCK), BSR_BLOCK, 0, st>>>(comp, tmp, order, c.visible);
+        BSR_CUDA_TRY(cudaMemcpyAsync(f.dkeys[0], saved, 4ull * f.n, cudaMemcpyDeviceToDevice, st));
     }
     if (lists && c.entries)
-        BSR_CUDA_TRY(cudaMemcpyAsync(lists, f.lists, 4ull * c.entries, cudaMemcpyDeviceToDevice, st));
+        export_map_kernel<<<(unsigned)div_up(c.entries, BSR_BLOCK), BSR_BLOCK, 0, st>>>(comp, f.lists, lists,
+                                                                                       c.entries);
     if (ranges)
         BSR_CUDA_TRY(cudaMemcpyAsync(ranges, f.tile_ranges, 8ull * f.n_tiles, cudaMemcpyDeviceToDevice, st));
-    if ((src_index || bounds) && c.visible)
-        export_records_kernel<<<(unsigned)div_up(c.visible, BSR_BLOCK), BSR_BLOCK, 0, st>>>(f, src_index, bounds);
     BSR_LAUNCH_CHECK();
     BSR_CUDA_TRY(cudaStreamSynchronize(st));
     return BSR_OK;

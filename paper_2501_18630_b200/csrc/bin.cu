@@ -13,14 +13,14 @@
 //   bin_scan              one CTA: exclusive scan of the tile counts -> tile ranges, E,
 //                         capacity check (overflow -> BSR_ERR_CAPACITY, entries_needed)
 //   bin_entries<SCATTER>  each entry takes a slot in its tile (atomic cursor) and writes
-//   bin_big<SCATTER>      (fp32 depth key << 32 | compact index)
+//   bin_big<SCATTER>      (fp32 depth key << 32 | source index)
 //   tile_sort             one CTA per tile sorts its entries ascending by that 64-bit key
 //                         (bitonic, in shared memory up to kSortSmem entries, in place in
 //                         global memory beyond), then re-orders runs of equal fp32 keys by
-//                         (fp64 depth, compact index); writes the compact indices.
+//                         (fp64 depth, source index); writes the compact indices.
 //
 // fp32 rounding of the depth is monotone, so (fp32 key, then fp64 depth, then compact
-// index) is exactly the reference's order (compact index order == source order of the
+// index) is exactly the reference's order (source index order == source order of the
 // visible primitives).  Nothing here needs a host synchronisation: counts and E live in
 // device memory, grids are sized by capacity with early exits.
 #include "frame.cuh"
@@ -54,7 +54,7 @@ __device__ __forceinline__ bool over_capacity(const FrameView &f) {
 template <bool COUNT>
 __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
     pdl_wait();
-    const uint32_t V = f.ctr->visible;
+    const uint32_t V = (uint32_t)f.n;  // every primitive; culled ones have tile_count 0
     if (!COUNT && over_capacity(f)) return;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (BSR_BLOCK / 32);
@@ -226,7 +226,7 @@ __device__ void bitonic_sort_warp(P a, int n) {
     bitonic_sort(a, n, (int)(threadIdx.x & 31), 32, [] { __syncwarp(); });
 }
 
-// Runs of equal fp32 keys: re-order by (fp64 depth, compact index); the thread at the
+// Runs of equal fp32 keys: re-order by (fp64 depth, source index); the thread at the
 // start of each run insertion-sorts it (runs are rare and short).
 template <typename P>
 __device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {

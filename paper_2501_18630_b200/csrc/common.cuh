@@ -63,7 +63,7 @@ inline KCam make_kcam(const bsr_camera &c) {
 //   C: r, g, b, kR = bound on |r2(fp32) - r2(exact)| over the footprint (error analysis,
 //      raster.cuh); NEGATIVE kR marks an fp32-unsafe (ill-conditioned) primitive whose r2 /
 //      alpha the raster evaluates in fp64 from FrameView::rec64.  The source index lives
-//      in FrameView::src_of.
+//      is the record index itself (records are indexed by source index).
 //   D: x0, x1, y0, y1 (inclusive pixel bounds, primitive.py:252-262)
 struct __align__(16) Record {
     float4 a, b, c;

@@ -23,47 +23,44 @@ struct Counters {
     unsigned long long entries_needed;
     uint32_t flagged;        // flagged pixels
     int32_t status;          // first device-side error
-    uint32_t pre_ticket;     // preprocess partition ticket
     uint32_t big_rects;      // primitives whose tile rectangle is binned by a whole CTA
     uint32_t big_tiles;      // tiles sorted by the crowded-tile kernel
     uint32_t depth_ticket[kDepthPasses];   // global depth sort (parity export only)
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
     uint32_t depth_plan[kDepthPasses + 1];
-    uint32_t pad[2];
+    uint32_t pad[3];
 };
 
 struct FrameView {
     // --- zeroed every forward (one memset) ---
     Counters *ctr;
-    uint32_t *pre_status;    // [ceil(N/256)]
     uint2 *tile_ranges;      // [n_tiles] (start, end)
     uint32_t *tile_cnt;      // [n_tiles] entries per tile
     uint32_t *tile_cur;      // [n_tiles] scatter cursors
     // --- not zeroed ---
     uint32_t *depth_hist;    // [4][256]                  global depth sort: parity export only,
     uint32_t *depth_status;  // [4][ceil(N/4096)][256]     zeroed by bsr_debug_export
-    Record *rec;             // [N] compact order
-    uint32_t *src_of;        // [N] compact -> source index (batch.indices)
+    Record *rec;             // [N] by source index (valid where tile_count > 0)
     double *rec64;           // [N][8] fp64 {mean x, y, conic a, b, c, opacity, beta, depth}:
                              // the fp64 replay's geometry and the raster's path for fp32-unsafe
                              // primitives (Record.c.w < 0)
-    uint32_t *dkeys[2];      // [N] fp32-depth keys (ping-pong)
-    uint64_t *dkey64;        // [N] fp64 depth bits, compact order (tie fixup)
-    uint32_t *dvals[2];      // [N] compact index (ping-pong)
-    uint32_t *tile_count;    // [N] tiles touched, compact order
+    uint32_t *dkeys[2];      // [N] fp32-depth keys by source index ([1]: parity-export sort)
+    uint64_t *dkey64;        // [N] fp64 depth bits by source index (tie fixup)
+    uint32_t *dvals[2];      // [N] parity-export depth sort values (ping-pong)
+    uint32_t *tile_count;    // [N] tiles touched by source index, 0 = culled
     uint2 *big;              // [N] (compact index, tile count) of big rectangles
     uint32_t *big_tiles;     // [n_tiles] tiles with more entries than the shared-memory sort
-    uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | compact index), scattered per tile
-    uint32_t *lists;         // [Ecap] compact index per tile entry in depth order (tile_ranges)
+    uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | source index), scattered per tile
+    uint32_t *lists;         // [Ecap] source index per tile entry in depth order (tile_ranges)
     float *t_final;          // [H*W]
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
     double *replay_state;    // [H*W][6] raw(3), raw_depth, T, last  (fp64, flagged only)
-    float *grad_acc;         // [N][12] raster gradient accumulators (zeroed by backward)
+    float *grad_acc;         // [N][12] raster gradient accumulators by source index (zeroed by backward)
     // --- sizes ---
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles;
-    int64_t pre_parts, depth_parts;
+    int64_t depth_parts;
     int depth_items;  // sort_items() of the (parity-export) depth sort
     uint64_t zero_bytes, total_bytes;
 };
@@ -78,7 +75,6 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.tiles_x = (W + BSR_TILE - 1) / BSR_TILE;
     f.tiles_y = (H + BSR_TILE - 1) / BSR_TILE;
     f.n_tiles = f.tiles_x * f.tiles_y;
-    f.pre_parts = div_up(n > 0 ? n : 1, BSR_BLOCK);
     f.depth_items = sort_items(n);
     f.depth_parts = div_up(n > 0 ? n : 1, (int64_t)BSR_BLOCK * f.depth_items);
     const int64_t npx = (int64_t)W * H;
@@ -91,7 +87,6 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
         return p;
     };
     f.ctr = (Counters *)take(sizeof(Counters));
-    f.pre_status = (uint32_t *)take(4ull * f.pre_parts);
     f.tile_ranges = (uint2 *)take(8ull * f.n_tiles);
     f.tile_cnt = (uint32_t *)take(4ull * f.n_tiles);
     f.tile_cur = (uint32_t *)take(4ull * f.n_tiles);
@@ -100,7 +95,6 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.depth_hist = (uint32_t *)take(4ull * kDepthPasses * 256);
     f.depth_status = (uint32_t *)take(4ull * kDepthPasses * f.depth_parts * 256);
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
-    f.src_of = (uint32_t *)take(4ull * n);
     f.rec64 = (double *)take(8ull * kRec64 * n);
     f.dkeys[0] = (uint32_t *)take(4ull * n);
     f.dkeys[1] = (uint32_t *)take(4ull * n);

@@ -1,7 +1,8 @@
 // K1+K2 preprocess: fp64 EWA projection (primitive.py:221-277), SH colour
-// (appearance.py:235-261 via the SH adapter), opacity / Beta exponent, and an
-// order-preserving compaction of the visible subset (the reference's
-// ``idx = nonzero(vis)[keep]``) in ONE pass with decoupled look-back.
+// (appearance.py:235-261 via the SH adapter), opacity / Beta exponent.  Records are indexed
+// by the source index (culled primitives get tile_count 0): the reference's visible
+// subset ``idx = nonzero(vis)[keep]`` keeps source order, so every later stage can use
+// the source index as the batch index without a compaction pass.
 //
 // Compiled with -fmad=false: the fp64 integer outputs (bounds, depth keys) must follow
 // the reference's rounding, and replay.cu recomputes the same primitives bit-identically.
@@ -48,16 +49,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     float *app_a = sm.app;                                  // SH coeffs / SB base colours
     float *app_b = sm.app + BSR_BLOCK * (Tr::sh ? 0 : 3);   // SB lobe axes
     float *app_c = app_b + BSR_BLOCK * 3 * Tr::M;           // SB lobe colours
-    __shared__ uint32_t s_part, s_warp[BSR_BLOCK / 32], s_excl;
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ int s_bulk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = args.sc.n;
     const bsr_scene &sc = args.sc;
+    const int64_t part = blockIdx.x;
     if (tid == 0) {
-        const uint32_t part = atomicAdd(&f.ctr->pre_ticket, 1u);
-        s_part = part;
-        const int64_t base = (int64_t)part * BSR_BLOCK;
+        const int64_t base = part * BSR_BLOCK;
         const int64_t cnt = imin64(BSR_BLOCK, n - base);
         uintptr_t al = reinterpret_cast<uintptr_t>(sc.positions) | reinterpret_cast<uintptr_t>(sc.rotations) |
                        reinterpret_cast<uintptr_t>(sc.log_scales) | reinterpret_cast<uintptr_t>(sc.opacity_raw) |
@@ -91,7 +90,6 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         }
     }
     __syncthreads();
-    const int64_t part = s_part;
     const int64_t base = part * BSR_BLOCK;
     const int64_t i = base + tid;
     if (s_bulk) {
@@ -132,26 +130,12 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         if (p.degenerate) raise_status(&f.ctr->status, BSR_ERR_DEGENERATE_QUAT);
         vis = p.visible;
     }
-    // block-exclusive rank of visible primitives (source order preserved); the block's
-    // aggregate is published as soon as visibility is known, and the look-back for the
-    // inclusive prefix runs only after the colour / record work below, by which time the
-    // predecessors have usually published theirs
-    const uint32_t ballot = __ballot_sync(0xffffffffu, vis);
-    const uint32_t local = __popc(ballot & ((1u << lane) - 1));
-    if (lane == 0) s_warp[warp] = __popc(ballot);
-    __syncthreads();
-    uint32_t total = 0;
-    if (warp == 0) {
-        const uint32_t mine = lane < BSR_BLOCK / 32 ? s_warp[lane] : 0u;
-        uint32_t incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane < BSR_BLOCK / 32) s_warp[lane] = incl - mine;
-        if (lane == 0) st_release(f.pre_status + part, (part == 0 ? kFlagPrefix : kFlagAgg) | total);
+    // visible count (statistics / frame_status); records are indexed by the source index
+    // itself, so no compaction (and no cross-CTA dependency) is needed: the order of the
+    // visible subset the reference's ``batch.indices`` defines is the source order
+    {
+        const uint32_t ballot = __ballot_sync(0xffffffffu, vis);
+        if (lane == 0 && ballot) atomicAdd(&f.ctr->visible, (uint32_t)__popc(ballot));
     }
     if (vis) {
         const float *pos = sm.pos + 3 * tid;
@@ -189,29 +173,15 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     // min depth key for the radix plan: max of the complement
     const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
     if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
-    if (warp == 0) {  // warp-parallel look-back -> inclusive prefix
-        uint32_t excl = 0;
-        if (part > 0) {
-            excl = warp_lookback<uint32_t>(f.pre_status, part, 1, kFlagPrefix, kValueMask);
-            if (lane == 0) st_release(f.pre_status + part, kFlagPrefix | (excl + total));
-        }
-        if (lane == 0) {
-            s_excl = excl;
-            if (part == f.pre_parts - 1) f.ctr->visible = excl + total;
-        }
-    }
-    __syncthreads();
+    if (i < n) f.tile_count[i] = tcount;  // 0: culled
     if (vis) {
-        const uint32_t c = s_excl + s_warp[warp] + local;
+        const int64_t c = i;
         f.rec[c] = r;
-        f.src_of[c] = (uint32_t)i;
         double4 *d = reinterpret_cast<double4 *>(f.rec64 + kRec64 * (int64_t)c);
         d[0] = make_double4(m64[0], m64[1], m64[2], m64[3]);
         d[1] = make_double4(m64[4], m64[5], m64[6], m64[7]);
         f.dkeys[0][c] = key32;
         f.dkey64[c] = key;
-        f.dvals[0][c] = c;
-        f.tile_count[c] = tcount;
     }
 }
 
@@ -232,7 +202,7 @@ int launch_preprocess(const bsr_scene &sc, const KCam &cam, const FrameView &f, 
     if (sc.n == 0) return BSR_OK;
     PreArgs a{sc, cam, f};
     int rc = BSR_OK;
-    const unsigned blocks = (unsigned)f.pre_parts;
+    const unsigned blocks = (unsigned)div_up(sc.n, BSR_BLOCK);
 #define BSR_PRE_LAUNCH(CM) rc = launch_pre_k<CM>(a, blocks, st)
     BSR_DISPATCH_CM(sc, BSR_PRE_LAUNCH);
 #undef BSR_PRE_LAUNCH

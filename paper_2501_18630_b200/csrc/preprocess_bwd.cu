@@ -167,18 +167,14 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
 }
 
 template <int K>
-__global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a) {
-    pdl_wait();
-    const uint32_t V = a.f.ctr->visible;
-    const uint32_t c = blockIdx.x * BSR_BLOCK + threadIdx.x;
-    if (c >= V) return;
+__device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
     const float *acc = a.f.grad_acc + (int64_t)c * kGradStride;
     const float4 g0 = *reinterpret_cast<const float4 *>(acc);
     const float4 g1 = *reinterpret_cast<const float4 *>(acc + 4);
     const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
     const float dmx = g0.x, dmy = g0.y, dA = g0.z, dB = g0.w, dC = g1.x, d_o = g1.y, d_beta = g1.z;
     const float dr = g1.w, dg = g2.x, dbl = g2.y, dz = g2.z;
-    const int64_t i = a.f.src_of[c];
+    const int64_t i = c;
     const bsr_scene &sc = a.sc;
     const KCam &cam = a.cam;
 
@@ -338,11 +334,44 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
     if (a.screen_grad_norm) a.screen_grad_norm[i] = sqrtf(dmx * dmx + dmy * dmy);
 }
 
+// Each warp takes 64 consecutive source indices and runs the visible ones densely (32
+// per pass, ballot-compacted); culled primitives get no gradient (rasterizer.py:262-320
+// leaves them zero).
+constexpr int kPreBwdChunk = 64;
+
+template <int K>
+__global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = ((blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x) >> 5) * kPreBwdChunk;
+    if (c0 >= a.f.n) return;
+    uint32_t m[kPreBwdChunk / 32];
+    int tot = 0;
+#pragma unroll
+    for (int q = 0; q < kPreBwdChunk / 32; ++q) {
+        const int64_t c = c0 + 32 * q + lane;
+        m[q] = __ballot_sync(0xffffffffu, c < a.f.n && a.f.tile_count[c] != 0);
+        tot += __popc(m[q]);
+    }
+    for (int base = 0; base < tot; base += 32) {
+        int r = base + lane;
+        if (r >= tot) break;
+        int q = 0;
+#pragma unroll
+        for (int k = 0; k < kPreBwdChunk / 32 - 1; ++k)
+            if (q == k && r >= __popc(m[k])) {
+                r -= __popc(m[k]);
+                q = k + 1;
+            }
+        prebwd_one<K>(a, c0 + 32 * q + (int)__fns(m[q], 0, r + 1));
+    }
+}
+
 int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView &f,
                           const bsr_grads &g, float *screen_grad_norm, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
     PreBwdArgs a{sc, cam, f, g, screen_grad_norm};
-    const unsigned blocks = (unsigned)div_up(f.n, BSR_BLOCK);
+    const unsigned blocks = (unsigned)div_up(f.n, (int64_t)kPreBwdChunk * (BSR_BLOCK / 32));
 #define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs 
         }
         __syncthreads();
         if (want_contrib && t < nb && s_cnt[t]) {
-            atomicAdd(a.out.contributions + f.src_of[s_cidx[buf][t]], s_cnt[t]);
+            atomicAdd(a.out.contributions + s_cidx[buf][t], s_cnt[t]);
             s_cnt[t] = 0;
         }
     }

@@ -28,7 +28,6 @@ struct SceneProvider {
     bsr_scene sc;
     KCam cam;
     const Record *rec;
-    const uint32_t *src_of;
     const double *rec64;
     // fp64 geometry written by preprocess (project64, the same code and bits as the
     // reference restatement); only the colour is recomputed, for candidates
@@ -45,7 +44,7 @@ struct SceneProvider {
         e.o = d1.y;
         e.beta = d1.z;
         e.z = d1.w;
-        e.src = (int)src_of[c];
+        e.src = (int)c;
         return true;
     }
     // colour only for samples that pass the alpha cutoff (view dir as rasterizer.py:94-95)
@@ -385,7 +384,7 @@ int launch_replay_scene(bool fwd, const FrameView &f, const bsr_scene &sc, const
     a.d_depth = d_depth;
     a.mask_raw = true;
     int rc = BSR_OK;
-#define BSR_REPLAY_LAUNCH(CM) rc = launch_replay(fwd, a, SceneProvider<CM>{sc, cam, f.rec, f.src_of, f.rec64}, st)
+#define BSR_REPLAY_LAUNCH(CM) rc = launch_replay(fwd, a, SceneProvider<CM>{sc, cam, f.rec, f.rec64}, st)
     BSR_DISPATCH_CM(sc, BSR_REPLAY_LAUNCH);
 #undef BSR_REPLAY_LAUNCH
     return rc;
