@@ -130,7 +130,8 @@ def load_checkpoint(path, device="cuda") -> PrimitiveSet:
         raise CheckpointError(f"{path}: truncated vertex data")
     _lib.require_cuda()
     host = torch.frombuffer(bytearray(raw[:nbytes]), dtype=torch.float64) if nbytes else torch.zeros(0, dtype=torch.float64)
-    rec = host.pin_memory().to(device, non_blocking=True) if nbytes else host.to(device)
+    rec = (torch.empty(host.shape, dtype=host.dtype, pin_memory=True).copy_(host).to(device, non_blocking=True)
+           if nbytes else host.to(device))
     _, total = group_layout(n, shk, None if shk is not None else lobes)
     flat = torch.zeros(total, dtype=torch.float32, device=device)
     _lib.check(_lib.load().bsr_checkpoint_unpack(rec.data_ptr() if nbytes else None, n, len(names), st, sd,
