@@ -20,6 +20,10 @@
 
 #include "raster.cuh"
 
+#ifndef BSR_FWD_CTAS
+#define BSR_FWD_CTAS 4  // resident CTAs per SM the register budget targets
+#endif
+
 namespace bsr {
 
 struct RasterFwdArgs {
@@ -43,7 +47,7 @@ __device__ __noinline__ float2 unsafe_pair_fwd(const double *m64, float4 B, int 
 }
 
 template <bool STATS, bool CONTRIB, int G>
-__global__ void __launch_bounds__(BSR_BLOCK, 4) raster_fwd_kernel(RasterFwdArgs a) {
+__global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(RasterFwdArgs a) {
     pdl_wait();
     using SB = SubBlock<G>;
     using TG = TileGrid<G>;
