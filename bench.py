@@ -366,6 +366,9 @@ class BenchProfiler:
     def mark_adam(self, end=False):
         self.sp.mark_adam(end)
 
+    def mark_color(self, end=False):
+        self.sp.mark_color(end)
+
     def fwd(self, i):
         return self.sp.fwd(i)
 

@@ -141,6 +141,22 @@ int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float b
                  const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
                  const bsr_profile *profile, void *stream);
 
+/* Multi-view steps, SH colour: bsr_backward_deferred_color is bsr_backward except that
+ * the SH / view-direction part of the chain is not applied; drgb (device, float4 per
+ * primitive, 16-byte aligned) receives (dL/dr, dL/dg, dL/db, 0), zero where culled.
+ * bsr_color_grad_views then applies `views` such buffers ([views][N] float4, contiguous)
+ * at once: grads.sh += sum_v basis(dir_v) (x) d_rgb_v, grads.positions += sum_v the
+ * view-direction chain, dir_v = normalize(position - centers[v]) (host double[views][3]).
+ * Same gradients as per-view bsr_backward calls (appearance.py:264-318,
+ * rasterizer.py:287-289), with the coefficient gradients read and written once per step. */
+int bsr_backward_deferred_color(const bsr_scene *scene, const bsr_camera *camera,
+                                const float background[3], void *frame, uint64_t frame_bytes,
+                                int64_t entry_cap, const float *d_color, const float *d_depth,
+                                const bsr_grads *grads, float *screen_grad_norm,
+                                const bsr_profile *profile, float *drgb, void *stream);
+int bsr_color_grad_views(const bsr_scene *scene, const float *drgb, const double *centers,
+                         int32_t views, const bsr_grads *grads, void *stream);
+
 /* ---- core seam (backend.get_core(): forward_tiled / backward on depth-sorted input) -- */
 /* Inputs are DEVICE fp64 arrays exactly as the reference core receives them
  * (_raster.pyx:130-134): means (V,2), conics (V,3), opac (V,), betas (V,), colors (V,3),

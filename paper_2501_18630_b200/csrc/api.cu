@@ -28,7 +28,8 @@ int launch_replay_arrays(bool, const FrameView &, const double *, const double *
                          const uint2 *, const bsr_outputs &, const double bg[3], double, double,
                          const float *, cudaStream_t);
 int launch_preprocess_bwd(const bsr_scene &, const KCam &, const FrameView &, const bsr_grads &,
-                          float *, cudaStream_t);
+                          float *, float4 *, cudaStream_t);
+int launch_color_views(const bsr_scene &, const bsr_grads &, const float4 *, const double *, int, cudaStream_t);
 
 constexpr double kAlphaMin = 1.0 / 255.0;  // rasterizer.py:28
 constexpr double kTStop = 1e-4;            // rasterizer.py:29
@@ -269,13 +270,13 @@ extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *s
     return c.status;
 }
 
-extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
-                            const float background[3], void *frame, uint64_t frame_bytes,
-                            int64_t entry_cap, const float *d_color, const float *d_depth,
-                            const bsr_grads *grads, float *screen_grad_norm, const bsr_profile *prof,
-                            void *stream) {
+static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                         void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
+                         const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
+                         const bsr_profile *prof, float *drgb, void *stream) {
     if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || bad_grads(scene, grads))
         return BSR_ERR_BAD_ARG;
+    if (drgb && scene->color_model != BSR_COLOR_SH) return BSR_ERR_BAD_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
     if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
@@ -303,8 +304,36 @@ extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera,
     if ((rc = mark(prof, 1, st))) return rc;
     BSR_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));  // join
     if ((rc = mark(prof, 2, st))) return rc;
-    if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, st))) return rc;
+    if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, reinterpret_cast<float4 *>(drgb), st)))
+        return rc;
     return mark(prof, 3, st);
+}
+
+extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                            void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
+                            const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
+                            const bsr_profile *prof, void *stream) {
+    return backward_impl(scene, camera, background, frame, frame_bytes, entry_cap, d_color, d_depth, grads,
+                         screen_grad_norm, prof, nullptr, stream);
+}
+
+extern "C" int bsr_backward_deferred_color(const bsr_scene *scene, const bsr_camera *camera,
+                                           const float background[3], void *frame, uint64_t frame_bytes,
+                                           int64_t entry_cap, const float *d_color, const float *d_depth,
+                                           const bsr_grads *grads, float *screen_grad_norm,
+                                           const bsr_profile *prof, float *drgb, void *stream) {
+    if (!drgb || (reinterpret_cast<uintptr_t>(drgb) & 15)) return BSR_ERR_BAD_ARG;
+    return backward_impl(scene, camera, background, frame, frame_bytes, entry_cap, d_color, d_depth, grads,
+                         screen_grad_norm, prof, drgb, stream);
+}
+
+extern "C" int bsr_color_grad_views(const bsr_scene *scene, const float *drgb, const double *centers,
+                                    int32_t views, const bsr_grads *grads, void *stream) {
+    if (bad_scene(scene) || bad_grads(scene, grads) || scene->color_model != BSR_COLOR_SH || views < 0 ||
+        (views > 0 && (!drgb || !centers)) || (reinterpret_cast<uintptr_t>(drgb) & 15))
+        return BSR_ERR_BAD_ARG;
+    return launch_color_views(*scene, *grads, reinterpret_cast<const float4 *>(drgb), centers, views,
+                              (cudaStream_t)stream);
 }
 
 // ---- core seam ---------------------------------------------------------------------

@@ -19,6 +19,7 @@ struct PreBwdArgs {
     FrameView f;
     bsr_grads g;
     float *screen_grad_norm;
+    float4 *drgb;  // deferred colour chain: (dL/dr, dL/dg, dL/db, 0) per primitive, or nullptr
 };
 
 template <int K>
@@ -313,8 +314,11 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
             a.g.rotations[4 * i + 3] += (gz - dot * z) * iqn;
         }
     }
-    // ---- colour chain (SH or Spherical Beta) + view direction -> position
-    {
+    // ---- colour chain (SH or Spherical Beta) + view direction -> position; deferred for
+    //      multi-view steps (bsr_color_grad_views applies every view's chain at once)
+    if (a.drgb) {
+        a.drgb[i] = make_float4(dr, dg, dbl, 0.f);
+    } else {
         float vx = px - (float)cam.center[0], vy = py - (float)cam.center[1], vz = pz - (float)cam.center[2];
         const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
         const float ivn = 1.f / vn;
@@ -350,8 +354,10 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
 #pragma unroll
     for (int q = 0; q < kPreBwdChunk / 32; ++q) {
         const int64_t c = c0 + 32 * q + lane;
-        m[q] = __ballot_sync(0xffffffffu, c < a.f.n && a.f.tile_count[c] != 0);
+        const bool vis = c < a.f.n && a.f.tile_count[c] != 0;
+        m[q] = __ballot_sync(0xffffffffu, vis);
         tot += __popc(m[q]);
+        if (a.drgb && c < a.f.n && !vis) a.drgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (int base = 0; base < tot; base += 32) {
         int r = base + lane;
@@ -368,13 +374,108 @@ __global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a)
 }
 
 int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView &f,
-                          const bsr_grads &g, float *screen_grad_norm, cudaStream_t st) {
+                          const bsr_grads &g, float *screen_grad_norm, float4 *drgb, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    PreBwdArgs a{sc, cam, f, g, screen_grad_norm};
+    PreBwdArgs a{sc, cam, f, g, screen_grad_norm, drgb};
     const unsigned blocks = (unsigned)div_up(f.n, (int64_t)kPreBwdChunk * (BSR_BLOCK / 32));
 #define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
+// ---- deferred multi-view colour chain (SH colour) ---------------------------------------
+// For a step over several views the SH part of the chain is linear in each view's d rgb:
+//   d sh[k] = sum_v basis_k(dir_v) d_rgb_v,   d dir_v = dbasis(dir_v)^T (sh . d_rgb_v)
+// (appearance.py:264-318, rasterizer.py:287-289), so instead of a read-modify-write of
+// the 3K coefficient gradients per view, preprocess_bwd stores d_rgb_v (16 B) and this
+// kernel applies all views at once: SH coefficients read once, their gradients written
+// once.
+constexpr int kMaxViewsPerPass = 32;
+
+struct ColorViewsArgs {
+    bsr_scene sc;
+    bsr_grads g;
+    const float4 *drgb;  // [views][n]
+    int views;
+    float center[kMaxViewsPerPass][3];
+};
+
+template <int K>
+__global__ void __launch_bounds__(128) color_views_kernel(ColorViewsArgs a) {
+    pdl_wait();
+    const int64_t n = a.sc.n;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float px = a.sc.positions[3 * i], py = a.sc.positions[3 * i + 1], pz = a.sc.positions[3 * i + 2];
+    float sh[3 * K], dsh[3 * K];
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) {
+        sh[q] = __ldg(a.sc.sh + i * 3 * K + q);
+        dsh[q] = 0.f;
+    }
+    float dpx = 0.f, dpy = 0.f, dpz = 0.f;
+    bool any = false;
+    // the next view's d rgb is in flight while this view's chain is evaluated
+    float4 d_next = a.drgb[i];
+    for (int v = 0; v < a.views; ++v) {
+        const float4 d = d_next;
+        if (v + 1 < a.views) d_next = a.drgb[(int64_t)(v + 1) * n + i];
+        if (d.x == 0.f && d.y == 0.f && d.z == 0.f) continue;
+        any = true;
+        float vx = px - a.center[v][0], vy = py - a.center[v][1], vz = pz - a.center[v][2];
+        const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
+        const float ivn = 1.f / vn;
+        vx *= ivn;
+        vy *= ivn;
+        vz *= ivn;
+        float b[16], db[16][3];
+        sh_basis_and_grad<K>(vx, vy, vz, b, db);
+        float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            dsh[3 * k] += b[k] * d.x;
+            dsh[3 * k + 1] += b[k] * d.y;
+            dsh[3 * k + 2] += b[k] * d.z;
+            const float dbk = sh[3 * k] * d.x + sh[3 * k + 1] * d.y + sh[3 * k + 2] * d.z;
+            ddx += db[k][0] * dbk;
+            ddy += db[k][1] * dbk;
+            ddz += db[k][2] * dbk;
+        }
+        const float dd = ddx * vx + ddy * vy + ddz * vz;
+        dpx += (ddx - dd * vx) * ivn;
+        dpy += (ddy - dd * vy) * ivn;
+        dpz += (ddz - dd * vz) * ivn;
+    }
+    if (!any) return;
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) a.g.sh[i * 3 * K + q] += dsh[q];
+    a.g.positions[3 * i] += dpx;
+    a.g.positions[3 * i + 1] += dpy;
+    a.g.positions[3 * i + 2] += dpz;
+}
+
+int launch_color_views(const bsr_scene &sc, const bsr_grads &g, const float4 *drgb, const double *centers,
+                       int views, cudaStream_t st) {
+    if (sc.n == 0 || views == 0) return BSR_OK;
+    for (int v0 = 0; v0 < views; v0 += kMaxViewsPerPass) {
+        ColorViewsArgs a;
+        a.sc = sc;
+        a.g = g;
+        a.drgb = drgb + (int64_t)v0 * sc.n;
+        a.views = views - v0 < kMaxViewsPerPass ? views - v0 : kMaxViewsPerPass;
+        for (int v = 0; v < a.views; ++v)
+            for (int c = 0; c < 3; ++c) a.center[v][c] = (float)centers[3 * (v0 + v) + c];
+        const unsigned blocks = (unsigned)div_up(sc.n, 128);
+        switch (sc.sh_coeffs) {
+            case 1: BSR_CUDA_TRY((pdl_launch(color_views_kernel<1>, dim3(blocks), dim3(128), 0, st, a))); break;
+            case 4: BSR_CUDA_TRY((pdl_launch(color_views_kernel<4>, dim3(blocks), dim3(128), 0, st, a))); break;
+            case 9: BSR_CUDA_TRY((pdl_launch(color_views_kernel<9>, dim3(blocks), dim3(128), 0, st, a))); break;
+            case 16: BSR_CUDA_TRY((pdl_launch(color_views_kernel<16>, dim3(blocks), dim3(128), 0, st, a))); break;
+            default: return BSR_ERR_BAD_ARG;
+        }
+    }
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

@@ -196,20 +196,35 @@ def outputs_c(color=None, raw=None, alpha=None, trans=None, depth=None, pixel_co
 
 def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameState,
                  d_color: torch.Tensor, d_depth: torch.Tensor | None, grads: _lib.GradsC,
-                 screen_grad_norm: torch.Tensor | None = None, profile: _lib.ProfileC | None = None):
+                 screen_grad_norm: torch.Tensor | None = None, profile: _lib.ProfileC | None = None,
+                 drgb: torch.Tensor | None = None):
+    """bsr_backward; with ``drgb`` (float32 (N, 4), SH colour) the colour chain is deferred
+    into it (bsr_backward_deferred_color) for a later color_grad_views over all views."""
     lib = _lib.load()
     cam = _lib.camera_c(camera)
     if d_color.dtype != torch.float32 or not d_color.is_contiguous() or not d_color.is_cuda:
         raise ValueError("d_color must be a contiguous float32 CUDA tensor")
     if tuple(d_color.shape) != (camera.height, camera.width, 3):
         raise ValueError("d_color must be (H, W, 3)")
-    rc = lib.bsr_backward(ctypes.byref(scene), ctypes.byref(cam), _bg_arr(background),
-                          ctypes.c_void_p(frame.ptr()), frame.nbytes, frame.entry_cap,
-                          ctypes.c_void_p(d_color.data_ptr()),
-                          None if d_depth is None else ctypes.c_void_p(d_depth.data_ptr()),
-                          ctypes.byref(grads), _lib.ptr(screen_grad_norm),
-                          None if profile is None else ctypes.byref(profile), _stream())
+    args = (ctypes.byref(scene), ctypes.byref(cam), _bg_arr(background), ctypes.c_void_p(frame.ptr()),
+            frame.nbytes, frame.entry_cap, ctypes.c_void_p(d_color.data_ptr()),
+            None if d_depth is None else ctypes.c_void_p(d_depth.data_ptr()), ctypes.byref(grads),
+            _lib.ptr(screen_grad_norm), None if profile is None else ctypes.byref(profile))
+    if drgb is None:
+        rc = lib.bsr_backward(*args, _stream())
+    else:
+        rc = lib.bsr_backward_deferred_color(*args, ctypes.c_void_p(drgb.data_ptr()), _stream())
     _lib.check(rc, "bsr_backward")
+
+
+def color_grad_views(scene: _lib.SceneC, drgb: torch.Tensor, cameras, grads: _lib.GradsC):
+    """Apply the deferred colour chains of several views (bsr_color_grad_views): drgb is
+    (views, N, 4) float32 from backward_raw(..., drgb=drgb[v])."""
+    centers = np.ascontiguousarray(np.stack([np.asarray(c.center, np.float64) for c in cameras]))
+    rc = _lib.load().bsr_color_grad_views(ctypes.byref(scene), ctypes.c_void_p(drgb.data_ptr()),
+                                          centers.ctypes.data_as(ctypes.c_void_p), len(cameras),
+                                          ctypes.byref(grads), _stream())
+    _lib.check(rc, "bsr_color_grad_views")
 
 
 def grads_c(g: GradientBuffer) -> _lib.GradsC:
@@ -344,7 +359,7 @@ class StageProfiler:
 
     FWD = ("preprocess", "bin_count", "bin_scatter", "tile_sort", "raster_fwd", "replay_fwd")
     BWD = ("raster_bwd", "replay_bwd", "preprocess_bwd")
-    EXTRA = ("loss", "adam")
+    EXTRA = ("loss", "adam", "color_views")
 
     def __init__(self, n_views=1, device="cuda"):
         self.stats = torch.zeros(4, dtype=torch.int64, device=device)
@@ -368,6 +383,8 @@ class StageProfiler:
         self.loss_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                         for _ in range(n_views)]
         self.adam_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.color_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.used_color = False
         self.acc = {k: 0.0 for k in self.FWD + self.BWD + self.EXTRA}
         self.calls = {k: 0 for k in self.EXTRA}
         self.calls_fwd = 0
@@ -386,6 +403,11 @@ class StageProfiler:
         self.adam_ev[1 if end else 0].record()
         if end:
             self.used_adam = True
+
+    def mark_color(self, end=False):
+        self.color_ev[1 if end else 0].record()
+        if end:
+            self.used_color = True
 
     def fwd(self, view=0):
         self.used_fwd.add(view)
@@ -422,6 +444,10 @@ class StageProfiler:
         if self.used_adam:
             self.acc["adam"] += self.adam_ev[0].elapsed_time(self.adam_ev[1])
             self.calls["adam"] += 1
+        if self.used_color:
+            self.acc["color_views"] += self.color_ev[0].elapsed_time(self.color_ev[1])
+            self.calls["color_views"] += 1
+        self.used_color = False
         self.used_fwd.clear()
         self.used_bwd.clear()
         self.used_loss.clear()

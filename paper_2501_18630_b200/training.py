@@ -25,8 +25,8 @@ from . import _lib
 from .camera import Camera
 from .distributed import allreduce_grads
 from .primitive import GradientBuffer, PrimitiveSet
-from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, forward_raw, frame_status,
-                         grads_c, outputs_c)
+from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, color_grad_views, forward_raw,
+                         frame_status, grads_c, outputs_c)
 
 ADAM_BETA1 = 0.9  # training.py:31
 ADAM_BETA2 = 0.999  # training.py:32
@@ -324,7 +324,7 @@ class TrainStep:
 
     def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
                  lambda_ssim=0.2, process_group=None, cfg: TrainConfig | None = None, scene_scale=1.0,
-                 noise_rng=None):
+                 noise_rng=None, defer_color=True):
         """``cfg`` switches on the reference's full optimiser step (training.py:357-366):
         opacity / scale regularisers, the exponential position-lr schedule and the
         covariance-shaped position noise, all evaluated on the device from the device step
@@ -364,6 +364,12 @@ class TrainStep:
                                       d_image=torch.empty((h, w, 3), dtype=torch.float32, device=dev))
                 self.loss_ws[key] = LossWorkspace(w, h, dev)
         self.loss_values = torch.zeros((len(self.cameras), 3), dtype=torch.float64, device=dev)
+        # several views of an SH set: each view's backward defers its colour chain into
+        # drgb[v] and one kernel applies them all after the last view (the 3K coefficient
+        # gradients are read and written once per step instead of once per view)
+        self.drgb = None
+        if len(self.cameras) > 1 and prims.color_model == "sh" and defer_color:
+            self.drgb = torch.empty((len(self.cameras), prims.n, 4), dtype=torch.float32, device=dev)
         self.profile = None  # optional rasterizer.StageProfiler-like object with .fwd/.bwd
 
     def _frame(self, cam):
@@ -387,7 +393,14 @@ class TrainStep:
                 prof.mark_loss(i, end=True)
             self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
-                         profile=None if prof is None else prof.bwd(i))
+                         profile=None if prof is None else prof.bwd(i),
+                         drgb=None if self.drgb is None else self.drgb[i])
+        if self.drgb is not None:
+            if prof is not None and hasattr(prof, "mark_color"):
+                prof.mark_color()
+            color_grad_views(self.scene, self.drgb, self.cameras, self.gc)
+            if prof is not None and hasattr(prof, "mark_color"):
+                prof.mark_color(end=True)
         cfg = self.cfg
         if cfg is not None and self.rank0:  # direct regulariser terms, once per iteration
             regularizers_into(self.prims, self.grads, cfg.lambda_opacity, cfg.lambda_scale, self.loss_values[0])

@@ -377,3 +377,31 @@ def test_big_rectangles_binned_by_whole_ctas(cuda):
     scene.log_scales[:6] = np.log(np.float32(1.5))  # 6 huge footprints
     scene.opacity_raw[:6] = np.float32(-3.0)
     _compare_forward(scene, toy_camera(512, 384), np.ones(3), cuda)
+
+
+def test_multiview_deferred_colour_chain_matches_per_view(cuda):
+    """Several views of an SH set: the colour chain deferred into one kernel after the last
+    view (bsr_backward_deferred_color + bsr_color_grad_views) gives the gradients of the
+    per-view chain (bsr_backward per view) up to fp32 summation order."""
+    import torch
+
+    from paper_2501_18630_b200 import PrimitiveSet
+    from paper_2501_18630_b200.training import TrainStep, render_targets
+
+    rng = np.random.default_rng(71)
+    tgt = PrimitiveSet.from_scene(random_scene(rng, 500, degree=3))
+    cams = [toy_camera(64, 48, eye=(np.sin(a) * 4.0, 0.4 * np.cos(3 * a), -np.cos(a) * 4.0))
+            for a in (-0.5, 0.0, 0.3, 0.7)]
+    targets = render_targets(tgt, cams, np.ones(3))
+    scene = random_scene(np.random.default_rng(72), 400, degree=3)
+    a = TrainStep(PrimitiveSet.from_scene(scene), cams, targets, np.ones(3), defer_color=True)
+    b = TrainStep(PrimitiveSet.from_scene(scene), cams, targets, np.ones(3), defer_color=False)
+    assert a.drgb is not None and b.drgb is None
+    a.step(check=True, adam=False)
+    b.step(check=True, adam=False)
+    torch.cuda.synchronize()
+    for name in a.grads.groups:
+        ga, gb = getattr(a.grads, name), getattr(b.grads, name)
+        scale = max(float(gb.abs().max()), 1e-30)
+        torch.testing.assert_close(ga, gb, rtol=1e-4, atol=1e-6 * scale, msg=name)
+    np.testing.assert_allclose(a.loss_values.cpu().numpy(), b.loss_values.cpu().numpy(), rtol=1e-12)
