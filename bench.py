@@ -576,7 +576,9 @@ def main():
         rf = dict(raster_fwd=(pairs_f * FP32_FLOP_PER_PAIR_FWD, stages["raster_fwd"]))
         if w["kind"] == "train":
             rf["raster_bwd"] = (pairs_b * FP32_FLOP_PER_PAIR_BWD, stages["raster_bwd"])
-        dom = max(stages, key=lambda k: stages[k])
+        # dominant per-view stage (adam / color_views run once per multi-view step)
+        per_view = {k: v for k, v in stages.items() if k not in ("adam", "color_views")}
+        dom = max(per_view, key=lambda k: per_view[k])
         extra["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
         extra["pairs_per_view"] = {"fwd": pairs_f, "bwd": pairs_b, "contributions": contrib_f}
         extra["dominant_stage"] = dom
@@ -599,10 +601,17 @@ def main():
         hbm["bin_scatter"] = (V * 24 + E * 12) / (stages["bin_scatter"] * 1e-3) / 1e9
         hbm["tile_sort"] = (E * 12) / (stages["tile_sort"] * 1e-3) / 1e9
         if w["kind"] == "train":
-            hbm["preprocess_bwd"] = V * (48 + 240 + 480) / (stages["preprocess_bwd"] * 1e-3) / 1e9
+            # geometry chain + colour chain (768 B / visible primitive at SH-3); with the colour
+            # chain deferred to color_views: grad_acc 48 + geometry params 48 + their
+            # gradients read-modify-write 96 + d rgb 16
+            per_vis = 208 if stages.get("color_views", 0) > 0 else (48 + 240 + 480)
+            hbm["preprocess_bwd"] = V * per_vis / (stages["preprocess_bwd"] * 1e-3) / 1e9
             cam0 = w["cams"][0]
             if stages.get("loss", 0) > 0:
                 hbm["loss"] = 12 * 3 * cam0.width * cam0.height * 4 / (stages["loss"] * 1e-3) / 1e9
+            if stages.get("color_views", 0) > 0:  # once per step: SH rows read, gradients RMW
+                nv = len(w["cams"])
+                hbm["color_views"] = nscene * (12 * k3 * 3 + 16 * nv + 12) / (stages["color_views"] * 1e-3) / 1e9
             if stages.get("adam", 0) > 0:
                 hbm["adam"] = 28 * w["prims"].flat.numel() / (stages["adam"] * 1e-3) / 1e9
         extra["hbm_stage_gbs"] = {k: round(v, 1) for k, v in hbm.items()}
