@@ -405,3 +405,16 @@ def test_multiview_deferred_colour_chain_matches_per_view(cuda):
         scale = max(float(gb.abs().max()), 1e-30)
         torch.testing.assert_close(ga, gb, rtol=1e-4, atol=1e-6 * scale, msg=name)
     np.testing.assert_allclose(a.loss_values.cpu().numpy(), b.loss_values.cpu().numpy(), rtol=1e-12)
+
+
+def test_entry_capacity_overflow_retries(cuda):
+    """A frame whose tile-entry capacity is too small reports BSR_ERR_CAPACITY with the
+    entries needed; forward_raw grows the frame and the result is unchanged."""
+    from paper_2501_18630_b200 import rasterizer as rz
+
+    rng = np.random.default_rng(81)
+    scene = random_scene(rng, 300, degree=1)
+    cam = toy_camera(96, 64)
+    rz._ENTRY_CAP[(300, 96, 64)] = 16  # far below the E this scene needs
+    out, ref = _compare_forward(scene, cam, np.ones(3), cuda)
+    assert out.frame.entry_cap >= ref["E"] > 16
