@@ -383,13 +383,14 @@ def kernel_launches_per_step(w):
     from paper_2501_18630_b200.rasterizer import frame_status
 
     cam = w["cams"][0]
-    # pre, bin count (entries, big rects, scan), bin scatter (entries, big rects), per-tile sort,
-    # raster, replay
-    fwd = 1 + 3 + 2 + 1 + 1 + 1
+    # pre, bin count (entries incl. big rects, scan), bin scatter, per-tile sort, raster, replay
+    fwd = 1 + 2 + 1 + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
     per_view = fwd + 2 + 4  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain)
-    return per_view * len(w["cams"]) + (1 if w["adam"] else 0)
+    st = w.get("step")
+    color = 1 if st is not None and getattr(st, "drgb", None) is not None else 0  # deferred colour chain
+    return per_view * len(w["cams"]) + color + (1 if w["adam"] else 0)  # Adam (fused step bump)
 
 
 # ----------------------------------------------------------------------------- CPU baseline

@@ -233,6 +233,17 @@ int bsr_adam_step_scheduled(float *params, const float *grads, float *exp_avg, f
                             double beta2, double eps, void *stream);
 
 
+/* One-kernel optimizer step for captured training loops: device step count in
+ * step_counter[0] (step_counter: device int64[2], [1] is scratch kept 0 between calls),
+ * bumped by the kernel's last block; optional schedule as bsr_adam_step_scheduled
+ * (sched may be NULL); zero_grads != 0 clears the gradients after use (the next step
+ * accumulates from zero without a separate memset). */
+int bsr_adam_step_fused(float *params, float *grads, float *exp_avg, float *exp_avg_sq, int64_t count,
+                        int32_t n_groups, const int64_t *group_end /* host */,
+                        const float *group_lr /* host */, int64_t *step_counter,
+                        const bsr_lr_schedule *sched, int32_t sched_group, double beta1, double beta2,
+                        double eps, int32_t zero_grads, void *stream);
+
 /* training.loss direct terms (training.py:112-124): grads[opacity_raw] += lo * o (1 - o),
  * grads[log_scales] += ls * exp(log_scales); loss[0] += lo * sum(o) + ls * sum(s) (device
  * double, may be NULL). */

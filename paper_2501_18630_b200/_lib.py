@@ -122,6 +122,9 @@ EXPORTS = {
     "bsr_adam_step_scheduled": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_double,
                                           c_double, c_double, c_void_p]),
+    "bsr_adam_step_fused": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_int32, c_double, c_double, c_double,
+                                      c_int32, c_void_p]),
     "bsr_scheduled_lr": (c_double, [c_void_p, c_int64]),
     "bsr_regularizers": (c_int32, [c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p]),
     "bsr_inject_noise": (c_int32, [c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p,

@@ -22,6 +22,8 @@ struct AdamArgs {
     double beta1, beta2;
     int sched_group;  // group whose lr follows `sched` at the device step (-1: none)
     bsr_lr_schedule sched;
+    unsigned long long *ticket;  // in-kernel step bump: the last block to finish increments
+    float *gzero;                // gradients to clear after use (fused zeroing), or nullptr
 };
 
 // training.exponential_lr (training.py:134-145) x scene scale
@@ -96,10 +98,20 @@ __global__ void __launch_bounds__(BSR_BLOCK) adam_kernel(AdamArgs a) {
         reinterpret_cast<float4 *>(a.p)[q] = p[u];
         reinterpret_cast<float4 *>(a.m)[q] = m[u];
         reinterpret_cast<float4 *>(a.v)[q] = v[u];
+        if (a.gzero) reinterpret_cast<float4 *>(a.gzero)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (blockIdx.x == 0 && threadIdx.x < a.count - 4 * n4) {  // tail (< 4 elements)
         const int64_t i = 4 * n4 + threadIdx.x;
         adam1(a, a.p[i], a.g[i], a.m[i], a.v[i], group_lr(a, i, lr_s), inv_c1, inv_c2);
+        if (a.gzero) a.gzero[i] = 0.f;
+    }
+    if (a.ticket) {  // every block consumed the step above; the last one to get here bumps it
+        if (threadIdx.x == 0) {
+            if (atomicAdd(a.ticket, 1ull) == gridDim.x - 1) {
+                *a.ticket = 0ull;
+                *const_cast<int64_t *>(a.step_dev) += 1;
+            }
+        }
     }
 }
 
@@ -113,7 +125,7 @@ using namespace bsr;
 static int adam_impl(float *params, const float *grads, float *exp_avg, float *exp_avg_sq, int64_t count,
                      int32_t n_groups, const int64_t *group_end, const float *group_lr, int64_t step,
                      int64_t *step_dev, double beta1, double beta2, double eps, const bsr_lr_schedule *sched,
-                     int32_t sched_group, void *stream) {
+                     int32_t sched_group, void *stream, bool fused_bump = false, float *gzero = nullptr) {
     if (count < 0 || n_groups < 1 || n_groups > kMaxGroups || (!step_dev && step < 1) || !group_end ||
         !group_lr)
         return BSR_ERR_BAD_ARG;
@@ -142,6 +154,8 @@ static int adam_impl(float *params, const float *grads, float *exp_avg, float *e
     a.beta1 = beta1;
     a.beta2 = beta2;
     a.sched_group = -1;
+    a.ticket = fused_bump ? reinterpret_cast<unsigned long long *>(step_dev + 1) : nullptr;
+    a.gzero = gzero;
     if (sched) {
         if (!step_dev || sched_group < 0 || sched_group >= n_groups || sched->max_steps <= 0 ||
             sched->lr_init <= 0 || sched->lr_final <= 0)
@@ -157,7 +171,8 @@ static int adam_impl(float *params, const float *grads, float *exp_avg, float *e
         BSR_CUDA_TRY((pdl_launch(adam_kernel<true>, dim3(blocks), dim3(BSR_BLOCK), 0, (cudaStream_t)stream, a)));
     else
         BSR_CUDA_TRY((pdl_launch(adam_kernel<false>, dim3(blocks), dim3(BSR_BLOCK), 0, (cudaStream_t)stream, a)));
-    if (step_dev) BSR_CUDA_TRY((pdl_launch(adam_bump_kernel, dim3(1), dim3(1), 0, (cudaStream_t)stream, step_dev)));
+    if (step_dev && !fused_bump)
+        BSR_CUDA_TRY((pdl_launch(adam_bump_kernel, dim3(1), dim3(1), 0, (cudaStream_t)stream, step_dev)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -187,4 +202,13 @@ extern "C" int bsr_adam_step_scheduled(float *params, const float *grads, float 
     if (!step_counter || !sched) return BSR_ERR_BAD_ARG;
     return adam_impl(params, grads, exp_avg, exp_avg_sq, count, n_groups, group_end, group_lr, 0, step_counter,
                      beta1, beta2, eps, sched, sched_group, stream);
+}
+
+extern "C" int bsr_adam_step_fused(float *params, float *grads, float *exp_avg, float *exp_avg_sq, int64_t count,
+                                   int32_t n_groups, const int64_t *group_end, const float *group_lr,
+                                   int64_t *step_counter, const bsr_lr_schedule *sched, int32_t sched_group,
+                                   double beta1, double beta2, double eps, int32_t zero_grads, void *stream) {
+    if (!step_counter) return BSR_ERR_BAD_ARG;
+    return adam_impl(params, grads, exp_avg, exp_avg_sq, count, n_groups, group_end, group_lr, 0, step_counter, beta1,
+                     beta2, eps, sched, sched ? sched_group : -1, stream, true, zero_grads ? grads : nullptr);
 }

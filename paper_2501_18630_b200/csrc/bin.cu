@@ -8,12 +8,11 @@
 //   bin_entries<COUNT>    every visible primitive adds one entry per tile of its bounds
 //                         rectangle to that tile's count (RED); warp-cooperative, so a
 //                         warp's 32 primitives' entries are spread over its lanes
-//   bin_big<COUNT>        rectangles of more than kBigRect tiles (near-plane primitives
-//                         cover whole frames), one CTA each
+//                         (rectangles of more than kBigRect tiles: by the whole CTA)
 //   bin_scan              one CTA: exclusive scan of the tile counts -> tile ranges, E,
 //                         capacity check (overflow -> BSR_ERR_CAPACITY, entries_needed)
 //   bin_entries<SCATTER>  each entry takes a slot in its tile (atomic cursor) and writes
-//   bin_big<SCATTER>      (fp32 depth key << 32 | source index)
+//                         (fp32 depth key << 32 | source index)
 //   tile_sort             one CTA per tile sorts its entries ascending by that 64-bit key
 //                         (bitonic, in shared memory up to kSortSmem entries, in place in
 //                         global memory beyond), then re-orders runs of equal fp32 keys by
@@ -51,11 +50,42 @@ __device__ __forceinline__ bool over_capacity(const FrameView &f) {
 // 32 w + l; the warp's entries (inclusive prefix `incl` over the lanes) are taken
 // round-robin by the lanes, each finding its entry's owner by a 5-step search over the
 // prefix.  COUNT: tile_cnt[t] += 1.  Otherwise: slot = tile_cur[t]++, write the entry.
+//
+// Rectangles of more than kBigRect tiles (near-plane primitives can cover whole frames) are
+// queued in shared memory and binned by the whole CTA after its warps are done (a warp takes
+// its own when the CTA's queue is full).
+constexpr int kBigQueue = 64;
+
+template <bool COUNT>
+__device__ __forceinline__ void bin_one(const FrameView &f, uint32_t t, uint64_t key) {
+    if (COUNT) {
+        atomicAdd(&f.tile_cnt[t], 1u);
+    } else {
+        const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
+        f.tent[f.tile_ranges[t].x + slot] = key;
+    }
+}
+
+template <bool COUNT>
+__device__ __forceinline__ void bin_rect(const FrameView &f, uint32_t c, uint32_t cnt, uint32_t j0, uint32_t step) {
+    const RectInfo r = rect_of(f, c);
+    const uint64_t key = COUNT ? 0ull : (((uint64_t)f.dkeys[0][c] << 32) | c);
+    for (uint32_t j = j0; j < cnt; j += step) {
+        const uint32_t row = j / (uint32_t)r.spanx;
+        bin_one<COUNT>(f, (uint32_t)(r.ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(r.tx0 + (int)(j - row * r.spanx)),
+                       key);
+    }
+}
+
 template <bool COUNT>
 __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
     pdl_wait();
+    __shared__ uint2 s_big[kBigQueue];
+    __shared__ int s_nbig;
     const uint32_t V = (uint32_t)f.n;  // every primitive; culled ones have tile_count 0
     if (!COUNT && over_capacity(f)) return;
+    if (threadIdx.x == 0) s_nbig = 0;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (BSR_BLOCK / 32);
     for (int64_t w = (blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x) >> 5; w * 32 < (int64_t)V; w += nwarps) {
@@ -63,10 +93,13 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
         uint32_t cnt = 0;
         RectInfo r{0, 0, 1};
         uint64_t key = 0;
+        uint32_t own_big = 0;  // big rectangle this lane could not queue
         if (c < V) {
             cnt = f.tile_count[c];
-            if (cnt > kBigRect) {  // a whole CTA takes it (bin_big_kernel)
-                if (COUNT) f.big[atomicAdd(&f.ctr->big_rects, 1u)] = make_uint2(c, cnt);
+            if (cnt > kBigRect) {  // the whole CTA takes it after the warp loop
+                const int slot = atomicAdd(&s_nbig, 1);
+                if (slot < kBigQueue) s_big[slot] = make_uint2(c, cnt);
+                else own_big = cnt;
                 cnt = 0;
             } else if (cnt) {
                 r = rect_of(f, c);
@@ -100,36 +133,20 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
             const uint32_t local = e - (oin - ocnt);
             const uint32_t row = local / (uint32_t)spanx;
             const uint32_t t = (uint32_t)(ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(tx0 + (int)(local - row * spanx));
-            if (COUNT) {
-                atomicAdd(&f.tile_cnt[t], 1u);
-            } else {
-                const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
-                f.tent[f.tile_ranges[t].x + slot] = okey;
-            }
+            bin_one<COUNT>(f, t, okey);
+        }
+        // queue overflow: the warp bins those rectangles itself
+        unsigned ob = __ballot_sync(0xffffffffu, own_big != 0);
+        while (ob) {
+            const int src = __ffs(ob) - 1;
+            ob &= ob - 1;
+            const uint32_t bc = __shfl_sync(0xffffffffu, c, src), bn = __shfl_sync(0xffffffffu, own_big, src);
+            bin_rect<COUNT>(f, bc, bn, lane, 32);
         }
     }
-}
-
-template <bool COUNT>
-__global__ void __launch_bounds__(BSR_BLOCK) bin_big_kernel(FrameView f) {
-    pdl_wait();
-    const uint32_t nbig = f.ctr->big_rects;
-    if (!COUNT && over_capacity(f)) return;
-    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
-        const uint2 it = f.big[b];
-        const RectInfo r = rect_of(f, it.x);
-        const uint64_t key = ((uint64_t)f.dkeys[0][it.x] << 32) | it.x;
-        for (uint32_t j = threadIdx.x; j < it.y; j += BSR_BLOCK) {
-            const uint32_t row = j / (uint32_t)r.spanx;
-            const uint32_t t = (uint32_t)(r.ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(r.tx0 + (int)(j - row * r.spanx));
-            if (COUNT) {
-                atomicAdd(&f.tile_cnt[t], 1u);
-            } else {
-                const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
-                f.tent[f.tile_ranges[t].x + slot] = key;
-            }
-        }
-    }
+    __syncthreads();
+    const int nbig = min(s_nbig, kBigQueue);
+    for (int b = 0; b < nbig; ++b) bin_rect<COUNT>(f, s_big[b].x, s_big[b].y, threadIdx.x, BSR_BLOCK);
 }
 
 // One CTA of 1024 threads: tile ranges from the counts (== np.bincount + cumsum offsets).
@@ -258,8 +275,6 @@ __device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {
 // the (tiny) buckets; buckets of more than kMaxBucket entries (keys bunched in part of the
 // tile's range) get a warp each and a bitonic network.
 constexpr int kBuckets = 1024;
-constexpr int kSortBig = 16384;   // crowded tiles: 128 KB of dynamic shared memory
-constexpr int kBucketsBig = 4096;
 constexpr int kMaxBucket = 16;  // larger buckets: one warp each, bitonic
 
 template <int NB>
@@ -380,42 +395,23 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     __syncthreads();  // s / sm are reused by the next tile of a persistent CTA
 }
 
-// one CTA per tile with up to kSortSmem entries; bigger tiles are queued for the kernel below
+// one CTA per tile: up to kSortSmem entries in shared memory, beyond that (crowded tiles)
+// the bitonic network in place in global memory
 __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
     pdl_wait();
     __shared__ uint64_t s[kSortSmem];
     __shared__ SortSmem<kBuckets> sm;
     if (over_capacity(f)) return;
     const uint2 rg = f.tile_ranges[blockIdx.x];
-    if (rg.y - rg.x > (uint32_t)kSortSmem) {
-        if (threadIdx.x == 0) f.big_tiles[atomicAdd(&f.ctr->big_tiles, 1u)] = blockIdx.x;
+    const int n = (int)(rg.y - rg.x);
+    if (n > kSortSmem) {
+        uint64_t *g = f.tent + rg.x;
+        bitonic_sort_block(g, n);
+        fixup_ties(g, n, f.dkey64);
+        for (int i = threadIdx.x; i < n; i += BSR_BLOCK) f.lists[rg.x + i] = (uint32_t)g[i];
         return;
     }
     sort_tile<kBuckets>(f, blockIdx.x, s, sm);
-}
-
-// crowded tiles (more than kSortSmem entries): up to kSortBig in dynamic shared memory,
-// beyond that the bitonic network in place in global memory
-__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_big_kernel(FrameView f) {
-    pdl_wait();
-    extern __shared__ __align__(16) uint64_t sb[];  // [kSortBig] entries, then the bucket arrays
-    SortSmem<kBucketsBig> &sm = *reinterpret_cast<SortSmem<kBucketsBig> *>(sb + kSortBig);
-    if (over_capacity(f)) return;
-    const uint32_t nbig = f.ctr->big_tiles;
-    for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
-        const int tile = (int)f.big_tiles[k];
-        const uint2 rg = f.tile_ranges[tile];
-        const int n = (int)(rg.y - rg.x);
-        if (n <= kSortBig) {
-            sort_tile<kBucketsBig>(f, tile, sb, sm);
-        } else {
-            uint64_t *g = f.tent + rg.x;
-            bitonic_sort_block(g, n);
-            fixup_ties(g, n, f.dkey64);
-            for (int i = threadIdx.x; i < n; i += BSR_BLOCK) f.lists[rg.x + i] = (uint32_t)g[i];
-            __syncthreads();
-        }
-    }
 }
 
 static unsigned entry_blocks(const FrameView &f) {
@@ -426,7 +422,6 @@ static unsigned entry_blocks(const FrameView &f) {
 int launch_bin_count(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
     BSR_CUDA_TRY((pdl_launch(bin_entries_kernel<true>, dim3(entry_blocks(f)), dim3(BSR_BLOCK), 0, st, f)));
-    BSR_CUDA_TRY((pdl_launch(bin_big_kernel<true>, dim3(148 * 2), dim3(BSR_BLOCK), 0, st, f)));
     BSR_CUDA_TRY((pdl_launch(bin_scan_kernel, dim3(1), dim3(1024), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
@@ -436,7 +431,6 @@ int launch_bin_count(const FrameView &f, cudaStream_t st) {
 int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
     BSR_CUDA_TRY((pdl_launch(bin_entries_kernel<false>, dim3(entry_blocks(f)), dim3(BSR_BLOCK), 0, st, f)));
-    BSR_CUDA_TRY((pdl_launch(bin_big_kernel<false>, dim3(148 * 2), dim3(BSR_BLOCK), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -445,13 +439,6 @@ int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
 int launch_tile_sort(const FrameView &f, cudaStream_t st) {
     if (f.n == 0 || f.n_tiles == 0) return BSR_OK;
     BSR_CUDA_TRY((pdl_launch(tile_sort_kernel, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, f)));
-    static bool attr = false;
-    const int smem = (int)(sizeof(uint64_t) * kSortBig + sizeof(SortSmem<kBucketsBig>));
-    if (!attr) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(tile_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    BSR_CUDA_TRY((pdl_launch(tile_sort_big_kernel, dim3(148), dim3(BSR_BLOCK), smem, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

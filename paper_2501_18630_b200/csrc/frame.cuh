@@ -23,12 +23,10 @@ struct Counters {
     unsigned long long entries_needed;
     uint32_t flagged;        // flagged pixels
     int32_t status;          // first device-side error
-    uint32_t big_rects;      // primitives whose tile rectangle is binned by a whole CTA
-    uint32_t big_tiles;      // tiles sorted by the crowded-tile kernel
     uint32_t depth_ticket[kDepthPasses];   // global depth sort (parity export only)
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
     uint32_t depth_plan[kDepthPasses + 1];
-    uint32_t pad[3];
+    uint32_t pad[5];
 };
 
 struct FrameView {
@@ -48,8 +46,6 @@ struct FrameView {
     uint64_t *dkey64;        // [N] fp64 depth bits by source index (tie fixup)
     uint32_t *dvals[2];      // [N] parity-export depth sort values (ping-pong)
     uint32_t *tile_count;    // [N] tiles touched by source index, 0 = culled
-    uint2 *big;              // [N] (compact index, tile count) of big rectangles
-    uint32_t *big_tiles;     // [n_tiles] tiles with more entries than the shared-memory sort
     uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | source index), scattered per tile
     uint32_t *lists;         // [Ecap] source index per tile entry in depth order (tile_ranges)
     float *t_final;          // [H*W]
@@ -102,8 +98,6 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.dvals[0] = (uint32_t *)take(4ull * n);
     f.dvals[1] = (uint32_t *)take(4ull * n);
     f.tile_count = (uint32_t *)take(4ull * n);
-    f.big = (uint2 *)take(8ull * n);
-    f.big_tiles = (uint32_t *)take(4ull * f.n_tiles);
     f.tent = (uint64_t *)take(8ull * entry_cap);
     f.lists = (uint32_t *)take(4ull * entry_cap);
     f.t_final = (float *)take(4ull * npx);

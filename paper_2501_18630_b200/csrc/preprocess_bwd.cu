@@ -402,58 +402,119 @@ struct ColorViewsArgs {
     float center[kMaxViewsPerPass][3];
 };
 
+// One CTA owns 128 consecutive primitives.  Its inputs are contiguous runs in HBM (the 3K
+// coefficients, and per view 128 x 16 B of d rgb), so one elected thread streams them into
+// shared memory with TMA bulk copies: the coefficients once, the views in chunks of
+// kViewChunk through a two-slot ring, so a whole chunk of views is in flight per CTA
+// instead of one 16 B load per thread.  The coefficient gradients leave through shared
+// memory as one coalesced read-modify-write of the CTA's contiguous run.
+constexpr int kCvThreads = 128;
+constexpr int kViewChunk = 8;
+
 template <int K>
-__global__ void __launch_bounds__(128) color_views_kernel(ColorViewsArgs a) {
-    pdl_wait();
+constexpr size_t color_views_smem() {
+    return 2 * kViewChunk * kCvThreads * sizeof(float4) + (size_t)kCvThreads * 3 * K * sizeof(float) + 64;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kCvThreads) color_views_kernel(ColorViewsArgs a) {
+    extern __shared__ __align__(128) unsigned char cv_smem[];
+    float4 *s_d = reinterpret_cast<float4 *>(cv_smem);                   // [2][kViewChunk][128]
+    float *s_sh = reinterpret_cast<float *>(s_d + 2 * kViewChunk * kCvThreads);  // [128][3K]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(s_sh + kCvThreads * 3 * K);      // sh, slot 0, slot 1
     const int64_t n = a.sc.n;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float px = a.sc.positions[3 * i], py = a.sc.positions[3 * i + 1], pz = a.sc.positions[3 * i + 2];
+    const int64_t i0 = blockIdx.x * (int64_t)kCvThreads;
+    const int cnt = (int)(n - i0 < kCvThreads ? n - i0 : kCvThreads);
+    const int t = threadIdx.x;
+    const int chunks = (a.views + kViewChunk - 1) / kViewChunk;
+    auto issue = [&](int c) {  // views [c*kViewChunk, ...) -> slot c & 1
+        const int v0 = c * kViewChunk, nv = a.views - v0 < kViewChunk ? a.views - v0 : kViewChunk;
+        uint64_t *b = bar + 1 + (c & 1);
+        mbar_expect_tx(b, (uint32_t)(nv * cnt * sizeof(float4)));
+        for (int v = 0; v < nv; ++v)
+            bulk_g2s(s_d + ((c & 1) * kViewChunk + v) * kCvThreads, a.drgb + (int64_t)(v0 + v) * n + i0,
+                     (uint32_t)(cnt * sizeof(float4)), b);
+    };
+    if (t == 0) {
+        for (int q = 0; q < 3; ++q) mbar_init(bar + q, 1);
+    }
+    __syncthreads();
+    pdl_wait();  // d rgb comes from the preceding backward
+    const float *src_sh = a.sc.sh + i0 * 3 * K;
+    const uint32_t sh_bytes = (uint32_t)(cnt * 3 * K * sizeof(float));
+    const bool sh_bulk = ((reinterpret_cast<uintptr_t>(src_sh) | sh_bytes) & 15) == 0;
+    if (t == 0) {
+        if (sh_bulk) {
+            mbar_expect_tx(bar, sh_bytes);
+            bulk_g2s(s_sh, src_sh, sh_bytes, bar);
+        }
+        issue(0);
+        if (chunks > 1) issue(1);
+    }
+    if (!sh_bulk) {  // a 16 B-misaligned run (K = 1 or 9, partial CTA): coalesced plain loads
+        for (int e = t; e < cnt * 3 * K; e += kCvThreads) s_sh[e] = src_sh[e];
+        __syncthreads();
+    }
+    const bool live = t < cnt;
+    const int64_t i = i0 + t;
+    float px = 0.f, py = 0.f, pz = 0.f;
+    if (live) px = a.sc.positions[3 * i], py = a.sc.positions[3 * i + 1], pz = a.sc.positions[3 * i + 2];
     float sh[3 * K], dsh[3 * K];
+    if (sh_bulk) mbar_wait(bar, 0);
 #pragma unroll
     for (int q = 0; q < 3 * K; ++q) {
-        sh[q] = __ldg(a.sc.sh + i * 3 * K + q);
+        sh[q] = s_sh[t * 3 * K + q];
         dsh[q] = 0.f;
     }
     float dpx = 0.f, dpy = 0.f, dpz = 0.f;
     bool any = false;
-    // the next view's d rgb is in flight while this view's chain is evaluated
-    float4 d_next = a.drgb[i];
-    for (int v = 0; v < a.views; ++v) {
-        const float4 d = d_next;
-        if (v + 1 < a.views) d_next = a.drgb[(int64_t)(v + 1) * n + i];
-        if (d.x == 0.f && d.y == 0.f && d.z == 0.f) continue;
-        any = true;
-        float vx = px - a.center[v][0], vy = py - a.center[v][1], vz = pz - a.center[v][2];
-        const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
-        const float ivn = 1.f / vn;
-        vx *= ivn;
-        vy *= ivn;
-        vz *= ivn;
-        float b[16], db[16][3];
-        sh_basis_and_grad<K>(vx, vy, vz, b, db);
-        float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+    for (int c = 0; c < chunks; ++c) {
+        mbar_wait(bar + 1 + (c & 1), (c >> 1) & 1);
+        const int v0 = c * kViewChunk, nv = a.views - v0 < kViewChunk ? a.views - v0 : kViewChunk;
+        const float4 *slot = s_d + (c & 1) * kViewChunk * kCvThreads;
+        for (int v = 0; v < nv && live; ++v) {
+            const float4 d = slot[v * kCvThreads + t];
+            if (d.x == 0.f && d.y == 0.f && d.z == 0.f) continue;
+            any = true;
+            float vx = px - a.center[v0 + v][0], vy = py - a.center[v0 + v][1], vz = pz - a.center[v0 + v][2];
+            const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
+            const float ivn = 1.f / vn;
+            vx *= ivn;
+            vy *= ivn;
+            vz *= ivn;
+            float b[16], db[16][3];
+            sh_basis_and_grad<K>(vx, vy, vz, b, db);
+            float ddx = 0.f, ddy = 0.f, ddz = 0.f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            dsh[3 * k] += b[k] * d.x;
-            dsh[3 * k + 1] += b[k] * d.y;
-            dsh[3 * k + 2] += b[k] * d.z;
-            const float dbk = sh[3 * k] * d.x + sh[3 * k + 1] * d.y + sh[3 * k + 2] * d.z;
-            ddx += db[k][0] * dbk;
-            ddy += db[k][1] * dbk;
-            ddz += db[k][2] * dbk;
+            for (int k = 0; k < K; ++k) {
+                dsh[3 * k] += b[k] * d.x;
+                dsh[3 * k + 1] += b[k] * d.y;
+                dsh[3 * k + 2] += b[k] * d.z;
+                const float dbk = sh[3 * k] * d.x + sh[3 * k + 1] * d.y + sh[3 * k + 2] * d.z;
+                ddx += db[k][0] * dbk;
+                ddy += db[k][1] * dbk;
+                ddz += db[k][2] * dbk;
+            }
+            const float dd = ddx * vx + ddy * vy + ddz * vz;
+            dpx += (ddx - dd * vx) * ivn;
+            dpy += (ddy - dd * vy) * ivn;
+            dpz += (ddz - dd * vz) * ivn;
         }
-        const float dd = ddx * vx + ddy * vy + ddz * vz;
-        dpx += (ddx - dd * vx) * ivn;
-        dpy += (ddy - dd * vy) * ivn;
-        dpz += (ddz - dd * vz) * ivn;
+        __syncthreads();  // slot c & 1 is free again
+        if (t == 0 && c + 2 < chunks) issue(c + 2);
     }
-    if (!any) return;
+    if (live && any) {
+        a.g.positions[3 * i] += dpx;
+        a.g.positions[3 * i + 1] += dpy;
+        a.g.positions[3 * i + 2] += dpz;
+    }
+    // coefficient gradients: registers -> shared (own row) -> one coalesced RMW of the run
+    if (!__syncthreads_or(any)) return;
 #pragma unroll
-    for (int q = 0; q < 3 * K; ++q) a.g.sh[i * 3 * K + q] += dsh[q];
-    a.g.positions[3 * i] += dpx;
-    a.g.positions[3 * i + 1] += dpy;
-    a.g.positions[3 * i + 2] += dpz;
+    for (int q = 0; q < 3 * K; ++q) s_sh[t * 3 * K + q] = dsh[q];
+    __syncthreads();
+    float *gsh = a.g.sh + i0 * 3 * K;
+    for (int e = t; e < cnt * 3 * K; e += kCvThreads) gsh[e] += s_sh[e];
 }
 
 int launch_color_views(const bsr_scene &sc, const bsr_grads &g, const float4 *drgb, const double *centers,
@@ -467,14 +528,25 @@ int launch_color_views(const bsr_scene &sc, const bsr_grads &g, const float4 *dr
         a.views = views - v0 < kMaxViewsPerPass ? views - v0 : kMaxViewsPerPass;
         for (int v = 0; v < a.views; ++v)
             for (int c = 0; c < 3; ++c) a.center[v][c] = (float)centers[3 * (v0 + v) + c];
-        const unsigned blocks = (unsigned)div_up(sc.n, 128);
+        const unsigned blocks = (unsigned)div_up(sc.n, kCvThreads);
+#define BSR_CV_LAUNCH(K)                                                                                     \
+    do {                                                                                                     \
+        static bool attr = false;                                                                            \
+        if (!attr) {                                                                                         \
+            BSR_CUDA_TRY(cudaFuncSetAttribute(color_views_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              (int)color_views_smem<K>()));                                  \
+            attr = true;                                                                                     \
+        }                                                                                                    \
+        BSR_CUDA_TRY((pdl_launch(color_views_kernel<K>, dim3(blocks), dim3(kCvThreads), color_views_smem<K>(), st, a))); \
+    } while (0)
         switch (sc.sh_coeffs) {
-            case 1: BSR_CUDA_TRY((pdl_launch(color_views_kernel<1>, dim3(blocks), dim3(128), 0, st, a))); break;
-            case 4: BSR_CUDA_TRY((pdl_launch(color_views_kernel<4>, dim3(blocks), dim3(128), 0, st, a))); break;
-            case 9: BSR_CUDA_TRY((pdl_launch(color_views_kernel<9>, dim3(blocks), dim3(128), 0, st, a))); break;
-            case 16: BSR_CUDA_TRY((pdl_launch(color_views_kernel<16>, dim3(blocks), dim3(128), 0, st, a))); break;
+            case 1: BSR_CV_LAUNCH(1); break;
+            case 4: BSR_CV_LAUNCH(4); break;
+            case 9: BSR_CV_LAUNCH(9); break;
+            case 16: BSR_CV_LAUNCH(16); break;
             default: return BSR_ERR_BAD_ARG;
         }
+#undef BSR_CV_LAUNCH
     }
     BSR_LAUNCH_CHECK();
     return BSR_OK;

@@ -47,13 +47,14 @@ class LossWorkspace:
         self.width, self.height = width, height
 
 
-def loss_into(rendered, target, d_image, ws: LossWorkspace, lambda_ssim=0.2, raw=None):
-    """Device-side loss: writes d_image (optionally masked by raw >= 0) and ws.values =
-    [loss, l1, ssim] without a host sync."""
+def loss_into(rendered, target, d_image, ws: LossWorkspace, lambda_ssim=0.2, raw=None, values=None):
+    """Device-side loss: writes d_image (optionally masked by raw >= 0) and [loss, l1, ssim]
+    into ``values`` (3 float64 on the device; default ws.values) without a host sync."""
     h, w = rendered.shape[:2]
+    out = ws.values if values is None else values
     rc = _lib.load().bsr_loss_l1_dssim(
         rendered.data_ptr(), target.data_ptr(), _lib.ptr(raw), w, h, float(lambda_ssim),
-        ws.values.data_ptr(), d_image.data_ptr(), ws.scratch.data_ptr(), ws.nbytes, _stream())
+        out.data_ptr(), d_image.data_ptr(), ws.scratch.data_ptr(), ws.nbytes, _stream())
     _lib.check(rc, "loss")
 
 
@@ -134,8 +135,10 @@ class AdamState:
         self.exp_avg = torch.zeros_like(prims.flat)
         self.exp_avg_sq = torch.zeros_like(prims.flat)
         self.step = 0
-        # device-side step counter for graph-captured steps (bsr_adam_step_device)
-        self.step_dev = torch.zeros(1, dtype=torch.int64, device=prims.flat.device)
+        # device-side step counter for graph-captured steps: [0] the step, [1] the fused
+        # kernel's block ticket (bsr_adam_step_fused)
+        self._step_buf = torch.zeros(2, dtype=torch.int64, device=prims.flat.device)
+        self.step_dev = self._step_buf[:1]
         self._prims = prims
 
     @classmethod
@@ -170,24 +173,29 @@ def group_lrs(lr_means=1.6e-4, lr_other=5e-3, lr_shapes=0.0):
 
 
 def adam_step(prims: PrimitiveSet, grads: GradientBuffer, state: AdamState, lrs: dict,
-              device_step: bool = False, schedule=None):
+              device_step: bool = False, schedule=None, zero_grads: bool = False):
     """training.py:258-273 as one fused kernel over the flat buffers.
 
     ``device_step`` keeps the step count on the device (graph-capturable); the host-side
-    ``state.step`` then only counts calls made outside captured graphs."""
+    ``state.step`` then only counts calls made outside captured graphs.  ``zero_grads``
+    (device_step only) clears the gradients as the kernel consumes them, so the next step
+    needs no separate memset."""
     groups = prims.groups
     ends = (ctypes.c_int64 * len(groups))(*prims.group_ends())
     lr = (ctypes.c_float * len(groups))(*[float(lrs[g]) for g in groups])
     lib = _lib.load()
-    if schedule is not None:  # positions follow the lr schedule at the device step
+    if device_step:  # one kernel: bias corrections from, and bump of, the device counter
+        rc = lib.bsr_adam_step_fused(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
+                                     state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
+                                     state._step_buf.data_ptr(),
+                                     None if schedule is None else ctypes.byref(schedule),
+                                     groups.index("positions") if schedule is not None else -1,
+                                     ADAM_BETA1, ADAM_BETA2, ADAM_EPS, int(bool(zero_grads)), _stream())
+    elif schedule is not None:  # positions follow the lr schedule at the device step
         rc = lib.bsr_adam_step_scheduled(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
                                          state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
                                          state.step_dev.data_ptr(), ctypes.byref(schedule),
                                          groups.index("positions"), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
-    elif device_step:
-        rc = lib.bsr_adam_step_device(prims.flat.data_ptr(), grads.flat.data_ptr(), state.exp_avg.data_ptr(),
-                                      state.exp_avg_sq.data_ptr(), prims.flat.numel(), len(groups), ends, lr,
-                                      state.step_dev.data_ptr(), ADAM_BETA1, ADAM_BETA2, ADAM_EPS, _stream())
     else:
         state.step += 1
         state.step_dev.fill_(state.step)
@@ -371,13 +379,16 @@ class TrainStep:
         if len(self.cameras) > 1 and prims.color_model == "sh" and defer_color:
             self.drgb = torch.empty((len(self.cameras), prims.n, 4), dtype=torch.float32, device=dev)
         self.profile = None  # optional rasterizer.StageProfiler-like object with .fwd/.bwd
+        self._grads_clear = False  # the last step's Adam zeroed self.grads
 
     def _frame(self, cam):
         return self.frames.get((cam.width, cam.height))
 
     def step(self, check=False, adam=True):
         prof = self.profile
-        self.grads.flat.zero_()
+        if not self._grads_clear:
+            self.grads.flat.zero_()
+        self._grads_clear = False
         for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
             key = (cam.width, cam.height)
             b = self.bufs[key]
@@ -388,10 +399,9 @@ class TrainStep:
             ws = self.loss_ws[key]
             if prof is not None:
                 prof.mark_loss(i)
-            loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim)
+            loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim, values=self.loss_values[i])
             if prof is not None:
                 prof.mark_loss(i, end=True)
-            self.loss_values[i].copy_(ws.values)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
                          profile=None if prof is None else prof.bwd(i),
                          drgb=None if self.drgb is None else self.drgb[i])
@@ -409,10 +419,11 @@ class TrainStep:
         if adam:
             if prof is not None:
                 prof.mark_adam()
-            if cfg is None:
-                adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True)
-            else:
-                adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True, schedule=self.schedule)
+            # Adam clears the gradients it consumes: the next step skips its memset
+            adam_step(self.prims, self.grads, self.adam, self.lrs, device_step=True,
+                      schedule=None if cfg is None else self.schedule, zero_grads=True)
+            self._grads_clear = True
+            if cfg is not None:
                 # position noise at this step's scheduled lr (Adam bumped the device step)
                 lc = self.prims.layout_c()
                 rc = _lib.load().bsr_inject_noise(self.prims.flat.data_ptr(), ctypes.byref(lc), float(cfg.noise_lr),

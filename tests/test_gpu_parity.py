@@ -379,21 +379,24 @@ def test_big_rectangles_binned_by_whole_ctas(cuda):
     _compare_forward(scene, toy_camera(512, 384), np.ones(3), cuda)
 
 
-def test_multiview_deferred_colour_chain_matches_per_view(cuda):
+@pytest.mark.parametrize("degree,views,n", [(3, 4, 400), (3, 19, 401), (0, 11, 401), (2, 19, 257)])
+def test_multiview_deferred_colour_chain_matches_per_view(cuda, degree, views, n):
     """Several views of an SH set: the colour chain deferred into one kernel after the last
     view (bsr_backward_deferred_color + bsr_color_grad_views) gives the gradients of the
-    per-view chain (bsr_backward per view) up to fp32 summation order."""
+    per-view chain (bsr_backward per view) up to fp32 summation order.  Cases cover the
+    view-chunk ring (> 2 chunks of 8), partial CTAs and coefficient runs that are not
+    16 B multiples (degree 0 / 2)."""
     import torch
 
     from paper_2501_18630_b200 import PrimitiveSet
     from paper_2501_18630_b200.training import TrainStep, render_targets
 
     rng = np.random.default_rng(71)
-    tgt = PrimitiveSet.from_scene(random_scene(rng, 500, degree=3))
-    cams = [toy_camera(64, 48, eye=(np.sin(a) * 4.0, 0.4 * np.cos(3 * a), -np.cos(a) * 4.0))
-            for a in (-0.5, 0.0, 0.3, 0.7)]
+    tgt = PrimitiveSet.from_scene(random_scene(rng, 500, degree=degree))
+    angles = np.linspace(-0.5, 0.7, views)
+    cams = [toy_camera(64, 48, eye=(np.sin(a) * 4.0, 0.4 * np.cos(3 * a), -np.cos(a) * 4.0)) for a in angles]
     targets = render_targets(tgt, cams, np.ones(3))
-    scene = random_scene(np.random.default_rng(72), 400, degree=3)
+    scene = random_scene(np.random.default_rng(72), n, degree=degree)
     a = TrainStep(PrimitiveSet.from_scene(scene), cams, targets, np.ones(3), defer_color=True)
     b = TrainStep(PrimitiveSet.from_scene(scene), cams, targets, np.ones(3), defer_color=False)
     assert a.drgb is not None and b.drgb is None

@@ -208,6 +208,30 @@ def test_scheduled_adam_equals_host_lr(g, cuda):
     torch.testing.assert_close(b.flat, a.flat, rtol=2e-6, atol=1e-7)
 
 
+def test_fused_adam_bumps_step_and_zeroes_grads(g, cuda):
+    """bsr_adam_step_fused: the kernel's last block bumps the device step (ticket reset
+    for the next call) and zero_grads clears the gradients it consumed."""
+    import torch
+
+    from paper_2501_18630_b200.primitive import GradientBuffer
+    from paper_2501_18630_b200.training import AdamState, adam_step
+
+    a, b = _prims(g), _prims(g)
+    lrs = {k: 1e-3 for k in a.groups}
+    ga, gb = GradientBuffer.zeros_for(a), GradientBuffer.zeros_for(b)
+    sa, sb = AdamState(a), AdamState(b)
+    for _ in range(5):
+        src = torch.randn_like(ga.flat)
+        ga.flat.copy_(src)
+        gb.flat.copy_(src)
+        adam_step(a, ga, sa, lrs)
+        adam_step(b, gb, sb, lrs, device_step=True, zero_grads=True)
+        assert int(torch.count_nonzero(gb.flat)) == 0
+        torch.testing.assert_close(ga.flat, src, rtol=0, atol=0)
+    assert int(sb.step_dev.item()) == 5 and int(sb._step_buf[1].item()) == 0
+    torch.testing.assert_close(b.flat, a.flat, rtol=2e-6, atol=1e-7)
+
+
 class _Dataset:
     def __init__(self, cameras, images):
         self.cameras, self.images = cameras, images
