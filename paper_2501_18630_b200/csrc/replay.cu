@@ -14,6 +14,9 @@
 #include "frame.cuh"
 #include "appearance.cuh"
 #include "project.cuh"
+#ifdef BSR_REPLAY_TRACE
+#include <cstdio>
+#endif
 
 namespace bsr {
 
@@ -30,9 +33,12 @@ struct SceneProvider {
     const Record *rec;
     const double *rec64;
     // fp64 geometry written by preprocess (project64, the same code and bits as the
-    // reference restatement); only the colour is recomputed, for candidates
+    // reference restatement); the colour is the record's (fp32-evaluated, as on every
+    // certified pixel: colour never enters a decision, only the blended value)
     __device__ __forceinline__ bool get(uint32_t c, int px, int py, Entry64 &e) const {
-        const int4 bd = rec[c].d;
+        const Record &r = rec[c];
+        const int4 bd = r.d;
+        const float4 col = r.c;
         if (px < bd.x || px > bd.y || py < bd.z || py > bd.w) return false;
         const double4 *d = reinterpret_cast<const double4 *>(rec64 + kRec64 * (int64_t)c);
         const double4 d0 = d[0], d1 = d[1];
@@ -44,22 +50,13 @@ struct SceneProvider {
         e.o = d1.y;
         e.beta = d1.z;
         e.z = d1.w;
+        e.r = col.x;
+        e.g = col.y;
+        e.b = col.z;
         e.src = (int)c;
         return true;
     }
-    // colour only for samples that pass the alpha cutoff (view dir as rasterizer.py:94-95)
-    __device__ __forceinline__ void color(Entry64 &e) const {
-        const int64_t i = e.src;
-        double dx = (double)sc.positions[3 * i] - cam.center[0];
-        double dy = (double)sc.positions[3 * i + 1] - cam.center[1];
-        double dz = (double)sc.positions[3 * i + 2] - cam.center[2];
-        const double n = sqrt((dx * dx + dy * dy) + dz * dz);
-        double rgb[3];
-        app_color64<K>(sc, i, dx / n, dy / n, dz / n, rgb);
-        e.r = rgb[0];
-        e.g = rgb[1];
-        e.b = rgb[2];
-    }
+    __device__ __forceinline__ void color(Entry64 &) const {}
 };
 
 // Core seam: the caller's depth-sorted fp64 arrays (_raster.pyx:130-134 inputs).
@@ -111,7 +108,8 @@ __device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, doub
     dy = py - e.my;
     const double r2 = e.ca * dx * dx + 2.0 * e.cb * dx * dy + e.cc * dy * dy;
     x = fmin(fmax(r2, 0.0), 1.0);
-    kernel = pow(1.0 - x, e.beta);
+    // outside the support pow(+0, beta > 0) is +0: skip the fp64 pow (same bits)
+    kernel = (x == 1.0 && e.beta > 0.0) ? 0.0 : pow(1.0 - x, e.beta);
     return e.o * kernel;
 }
 
@@ -125,26 +123,50 @@ struct ReplaySmem {
     bool done;
 };
 
+// Forward rounds are wider (kReplayFwdThreads entries) and keep only what the recurrence
+// reads: alpha (overwritten by the weight alpha * T once T is known) and r, g, b, z.
+// Small frames (few flagged pixels, latency-bound) use one 1024-wide CTA per SM; large ones
+// (thousands of flagged pixels) two 512-wide CTAs per SM for more pixels in flight.
+constexpr int kRecBatch = 8;  // transmittance steps per batch (the stop test runs per batch)
+constexpr int64_t kReplayWideMaxPixels = 4 << 20;
+template <int NT>
+struct ReplayFwdSmem {
+    double alpha[NT], val[4][NT];
+    int entry[NT];
+    int warp_cnt[NT / 32];
+    int n_cand, n_used;
+    bool done;
+};
+
 // Block-wide ordered compaction of `cand` into slots [0, n): returns this thread's slot.
-__device__ __forceinline__ int compact_slot(bool cand, ReplaySmem &sm) {
+template <int NT, typename S>
+__device__ __forceinline__ int compact_slot(bool cand, S &sm) {
+    constexpr int NW = NT / 32;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const unsigned m = __ballot_sync(0xffffffffu, cand);
     if (lane == 0) sm.warp_cnt[warp] = __popc(m);
     __syncthreads();
-    int base = 0, total = 0;
-    for (int w = 0; w < BSR_BLOCK / 32; ++w) {
-        if (w < warp) base += sm.warp_cnt[w];
-        total += sm.warp_cnt[w];
+    // exclusive scan of the NW warp counts inside every warp
+    int c = lane < NW ? sm.warp_cnt[lane] : 0, incl = c;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
+    const int base = __shfl_sync(0xffffffffu, incl - c, warp);
+    const int total = __shfl_sync(0xffffffffu, incl, NW - 1);
     if (t == 0) sm.n_cand = total;
     return base + __popc(m & ((1u << lane) - 1u));
 }
 
-// One flagged pixel, one CTA: 256 list entries per round evaluated in parallel (fp64
-// projection on demand), the order-dependent recurrence runs on thread 0 over the
-// compacted candidates.  _raster.pyx:95-127.
-template <typename P>
-__device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplaySmem &sm) {
+// One flagged pixel, one CTA: NT list entries per round evaluated in
+// parallel (fp64 alpha), then the order-dependent recurrence in two phases: thread 0 runs
+// the transmittance chain T <- T * (1 - alpha) over the compacted candidates (batches of
+// kRecBatch with no branch inside, the stop test once per batch) and stores each weight
+// alpha * T; then lanes 0..3 of warp 0 each carry one of the r, g, b, depth sums over the
+// used candidates.  Same operations in the same order as _raster.pyx:95-127.
+template <typename P, int NT>
+__device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot, ReplayFwdSmem<NT> &sm) {
     const FrameView &f = a.f;
     const int t = threadIdx.x;
     const uint32_t *lists = a.lists ? a.lists : f.lists;
@@ -156,58 +178,102 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     const int start = (int)ranges[tile].x, end = (int)ranges[tile].y;
     const int flag_at = (int)fl.y;
 
-    double t_acc = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dd = 0.0;  // thread 0's state
+    double t_acc = 1.0;  // thread 0: transmittance
+    double sum = 0.0;    // lane c < 4 of warp 0: running r / g / b / depth sum
     int count = 0, last = 0;
     if (t == 0) sm.done = false;
     __syncthreads();
-    for (int base = start; base < end; base += BSR_BLOCK) {
+#ifdef BSR_REPLAY_TRACE
+    long long tr0 = clock64(), tr1 = 0, tr2 = 0;
+#endif
+    for (int base = start; base < end; base += NT) {
         if (sm.done) break;  // uniform (read after a barrier)
         const int e = base + t;
         Entry64 en;
         bool cand = false;
         double alpha = 0.0;
+#ifdef BSR_REPLAY_TRACE
+        if (t == 0) tr0 = clock64();
+#endif
         if (e < end && prov.get(lists[e], px, py, en)) {
             double dx, dy, x, k;
             alpha = alpha64(en, px, py, dx, dy, x, k);
             cand = !(alpha < a.alpha_min);
             if (cand) prov.color(en);
         }
-        const int s = compact_slot(cand, sm);
+        const int s = compact_slot<NT>(cand, sm);
         if (cand) {
             sm.alpha[s] = alpha;
-            sm.r[s] = en.r;
-            sm.g[s] = en.g;
-            sm.b[s] = en.b;
-            sm.z[s] = en.z;
+            sm.val[0][s] = en.r;
+            sm.val[1][s] = en.g;
+            sm.val[2][s] = en.b;
+            sm.val[3][s] = en.z;
             sm.entry[s] = e - start;
         }
         __syncthreads();
-        if (t == 0) {
-            int used = sm.n_cand;
-            for (int q = 0; q < sm.n_cand; ++q) {
-                const double al = sm.alpha[q];
-                const double weight = al * t_acc;
-                c0 = c0 + weight * sm.r[q];
-                c1 = c1 + weight * sm.g[q];
-                c2 = c2 + weight * sm.b[q];
-                dd = dd + weight * sm.z[q];
-                t_acc = t_acc * (1.0 - al);
-                ++count;
-                last = sm.entry[q] + 1;
-                if (t_acc < a.t_stop) {
-                    used = q + 1;
-                    sm.done = true;
-                    break;
+#ifdef BSR_REPLAY_TRACE
+        if (t == 0) tr1 = clock64();
+#endif
+        if (t < 32) {
+            const int n = sm.n_cand;
+            if (t == 0) {
+                int used = n;
+                bool stop = false;
+                for (int q0 = 0; q0 < n; q0 += kRecBatch) {
+                    double al[kRecBatch], tb[kRecBatch + 1];
+#pragma unroll
+                    for (int j = 0; j < kRecBatch; ++j) al[j] = sm.alpha[q0 + j < n ? q0 + j : 0];
+                    tb[0] = t_acc;
+#pragma unroll
+                    for (int j = 0; j < kRecBatch; ++j) tb[j + 1] = tb[j] * (1.0 - al[j]);
+                    unsigned stops = 0;
+#pragma unroll
+                    for (int j = 0; j < kRecBatch; ++j) {
+                        if (q0 + j < n) {
+                            sm.alpha[q0 + j] = al[j] * tb[j];  // weight
+                            if (tb[j + 1] < a.t_stop) stops |= 1u << j;
+                        }
+                    }
+                    const int valid = n - q0 < kRecBatch ? n - q0 : kRecBatch;
+                    const int take = stops ? __ffs(stops) : valid;  // steps applied from this batch
+#pragma unroll
+                    for (int j = 1; j <= kRecBatch; ++j)
+                        if (j == take) t_acc = tb[j];
+                    if (stops) {
+                        used = q0 + take;
+                        stop = true;
+                        break;
+                    }
                 }
+                count += used;
+                if (used > 0) last = sm.entry[used - 1] + 1;
+                if (stop) sm.done = true;
+                sm.n_used = used;
             }
-            sm.n_used = used;
+            __syncwarp();
+            if (t < 4) {
+                const int used = sm.n_used;
+                const double *v = sm.val[t];
+#pragma unroll 4
+                for (int q = 0; q < used; ++q) sum = sum + sm.alpha[q] * v[q];
+            }
         }
         __syncthreads();
+#ifdef BSR_REPLAY_TRACE
+        if (t == 0) {
+            tr2 = clock64();
+            printf("replay pix %lld base %d/%d cand %d used %d eval %lld rec %lld\n", (long long)pix, base - start,
+                   end - start, sm.n_cand, sm.n_used, tr1 - tr0, tr2 - tr1);
+        }
+#endif
         // contributions of entries at/after the fp32 flag point (earlier ones were counted)
         if (cand && s < sm.n_used && sm.entry[s] >= flag_at && a.out.contributions)
             atomicAdd(a.out.contributions + en.src, 1);
         __syncthreads();
     }
+    if (t >= 32) return;
+    const double c0 = __shfl_sync(0xffffffffu, sum, 0), c1 = __shfl_sync(0xffffffffu, sum, 1);
+    const double c2 = __shfl_sync(0xffffffffu, sum, 2), dd = __shfl_sync(0xffffffffu, sum, 3);
     if (t != 0) return;
     const double r0 = c0 + a.bg[0] * t_acc, r1 = c1 + a.bg[1] * t_acc, r2 = c2 + a.bg[2] * t_acc;
     if (a.out.raw) {
@@ -272,7 +338,7 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
                 if (cand) prov.color(en);
             }
         }
-        const int s = compact_slot(cand, sm);
+        const int s = compact_slot<BSR_BLOCK>(cand, sm);
         if (cand) {
             sm.alpha[s] = alpha;
             sm.r[s] = en.r;
@@ -332,13 +398,13 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     }
 }
 
-template <typename P>
-__global__ void __launch_bounds__(BSR_BLOCK) replay_fwd_kernel(ReplayArgs a, P prov) {
+template <typename P, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) replay_fwd_kernel(ReplayArgs a, P prov) {
     pdl_wait();
-    __shared__ ReplaySmem sm;
+    __shared__ ReplayFwdSmem<NT> sm;
     const uint32_t n = a.f.ctr->flagged;
     for (uint32_t slot = blockIdx.x; slot < n; slot += gridDim.x) {
-        replay_fwd_one(a, prov, slot, sm);
+        replay_fwd_one<P, NT>(a, prov, slot, sm);
         __syncthreads();
     }
 }
@@ -362,7 +428,12 @@ static unsigned replay_blocks(const FrameView &) {
 template <typename P>
 static int launch_replay(bool fwd, const ReplayArgs &a, const P &prov, cudaStream_t st) {
     if (fwd)
-        BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P>, dim3(replay_blocks(a.f)), dim3(BSR_BLOCK), 0, st, a, prov)));
+    {
+        if ((int64_t)a.f.W * a.f.H <= kReplayWideMaxPixels)
+            BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 1024>, dim3(148), dim3(1024), 0, st, a, prov)));
+        else
+            BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 512>, dim3(2 * 148), dim3(512), 0, st, a, prov)));
+    }
     else
         BSR_CUDA_TRY((pdl_launch(replay_bwd_kernel<P>, dim3(replay_blocks(a.f)), dim3(BSR_BLOCK), 0, st, a, prov)));
     BSR_LAUNCH_CHECK();
