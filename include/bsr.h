@@ -22,6 +22,8 @@
  *   mcmc.apply_relocation          mcmc.py:86-106          bsr_apply_relocation
  *   mcmc.grow                      mcmc.py:108-146         bsr_sample_live + bsr_grow
  *   sceneio.save/load_checkpoint   sceneio.py:467-564      bsr_checkpoint_pack / _unpack
+ *   compression.morton_keys/sort   compression.py:34-66    bsr_codec_sort
+ *   compression.pack / unpack      compression.py:141-250  bsr_codec_encode / _decode
  *
  * Conventions
  *   - Every pointer is DEVICE memory owned by the caller unless stated; the library
@@ -299,6 +301,38 @@ int bsr_checkpoint_unpack(const double *records, int64_t n, int32_t n_props, con
                           const int32_t *prop_stride, float *flat, void *stream);
 int bsr_checkpoint_pack(const float *flat, int64_t n, int32_t n_props, const int64_t *prop_start,
                         const int32_t *prop_stride, double *records, void *stream);
+
+/* ---- post-training codec (compression.py:34-250; docs/formats.md "Archives") ----------
+ * The device side of compression.pack / unpack; PNG encoding of the byte grids stays on
+ * the host (OpenCV, as sceneio.write_png / read_png).  Attribute group g holds channels
+ * [0, channels) of primitive i at flat[start + stride * i + c]; its codes occupy
+ * rows * cols * channels bytes (row-major grid, channel-interleaved, zero padding) at the
+ * running byte offset of the groups before it in `codes`; its min / max at the running
+ * channel offset in mins / maxs.  Position byte planes: planes[b][cell][axis] = byte b of
+ * the fp32 bits (4 x rows x cols x 3 bytes).  8-bit quantisation only (QUANT_BITS). */
+typedef struct {
+    int64_t start;
+    int32_t stride;
+    int32_t channels; /* 1..4 */
+} bsr_codec_group;
+
+size_t bsr_codec_scratch_bytes(int64_t n);
+/* compression.morton_keys + sort_primitives: keys_out (n, original order; may be NULL)
+ * and perm (n) = the stable argsort of the keys. */
+int bsr_codec_sort(const float *positions /* (n,3) */, int64_t n, uint64_t *keys_out, int64_t *perm,
+                   void *scratch, size_t scratch_bytes, void *stream);
+/* compression.pack minus the file I/O: grid cell j holds primitive perm[j] (perm NULL:
+ * j).  mins / maxs (device, one per channel) receive quantize_attribute's ranges; a
+ * non-finite value sets *status (device, may be NULL) to BSR_ERR_BAD_ARG. */
+int bsr_codec_encode(const float *flat, const float *positions, int64_t n, const int64_t *perm,
+                     int32_t n_groups, const bsr_codec_group *groups /* host */, int32_t rows,
+                     int32_t cols, uint8_t *planes, uint8_t *codes, double *mins, double *maxs,
+                     int32_t *status, void *scratch, size_t scratch_bytes, void *stream);
+/* compression.unpack minus the file I/O: fp32 positions from the planes (bit-exact), every
+ * group dequantised in fp64 (mins (1 - t) + maxs t, t = code / 255) and rounded to fp32. */
+int bsr_codec_decode(const uint8_t *planes, const uint8_t *codes, const double *mins, const double *maxs,
+                     int64_t n, int32_t n_groups, const bsr_codec_group *groups /* host */, int32_t rows,
+                     int32_t cols, float *flat, float *positions, void *stream);
 
 /* ---- parity / debug: export the binning of the last forward (synchronises) ---------- */
 /* order (V): compact index per depth rank (== np.argsort(depths, kind="stable"),

@@ -122,6 +122,12 @@ EXPORTS = {
     "bsr_adam_step_scheduled": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_double,
                                           c_double, c_double, c_void_p]),
+    "bsr_codec_scratch_bytes": (c_uint64, [c_int64]),
+    "bsr_codec_sort": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p]),
+    "bsr_codec_encode": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p]),
+    "bsr_codec_decode": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int32,
+                                   c_int32, c_void_p, c_void_p, c_void_p]),
     "bsr_adam_step_fused": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_int32, c_double, c_double, c_double,
                                       c_int32, c_void_p]),

@@ -15,23 +15,9 @@
 //
 // HBM roofline per pass: n * 2 * (sizeof(K) + 4) bytes.
 #include "frame.cuh"
+#include "sort.cuh"
 
 namespace bsr {
-
-template <typename K>
-struct SortArgs {
-    K *keys[2];
-    uint32_t *vals[2];
-    const uint32_t *count;            // device element count
-    const uint32_t *bias_inv;         // if non-null: bias = ~(*bias_inv) (min key)
-    uint32_t *hist;                   // [passes][256], zeroed; becomes exclusive offsets
-    uint32_t *plan;                   // [passes + 1]
-    uint32_t *status;                 // [passes][max_parts][256], zeroed
-    uint32_t *tickets;                // [passes], zeroed
-    int passes;
-    int items;                        // keys per thread (4 or 16), see sort_items()
-    int64_t max_parts;
-};
 
 template <typename K>
 __device__ __forceinline__ K sort_bias(const SortArgs<K> &a) {
@@ -259,6 +245,9 @@ int launch_sort(const SortArgs<K> &a, int64_t cap, cudaStream_t st) {
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
+
+template int launch_sort<uint32_t>(const SortArgs<uint32_t> &, int64_t, cudaStream_t);
+template int launch_sort<uint64_t>(const SortArgs<uint64_t> &, int64_t, cudaStream_t);
 
 // After sorting the fp32-rounded depths, primitives whose fp32 keys tie are re-ordered by
 // their exact fp64 depth (then compact index): rounding is monotone, so this yields exactly

@@ -7,7 +7,10 @@ from paper_2501_18630_b200 import PrimitiveSet
 from paper_2501_18630_b200.scenes import make_workload, target_scene
 from paper_2501_18630_b200.training import TrainStep, render_targets
 
-for n, w, h in ((1000, 64, 64), (10000, 256, 256), (100000, 800, 800)):
+SIZES = ((1000, 64, 64), (10000, 256, 256), (100000, 800, 800))
+if len(sys.argv) > 1:  # e.g. `tiny` -> the first size only, few replays (for ncu)
+    SIZES = SIZES[:1]
+for n, w, h in SIZES:
     wl = make_workload("c1", seed=0, n=n, width=w, height=h)
     prims = PrimitiveSet.from_scene(wl.scene)
     tgt = PrimitiveSet.from_scene(target_scene("c1", 1, n))
@@ -18,7 +21,7 @@ for n, w, h in ((1000, 64, 64), (10000, 256, 256), (100000, 800, 800)):
     for _ in range(10):
         st.replay()
     torch.cuda.synchronize()
-    K = 200
+    K = 200 if len(sys.argv) == 1 else 3
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(K):

@@ -126,5 +126,42 @@ def checkpoints():
     print("wrote checkpoints")
 
 
+def codec():
+    """Reference-written archives (compression.pack, compression.py:141-187) plus the keys,
+    permutation and unpacked values (compression.py:45-66, 190-250) they imply."""
+    import shutil
+
+    import_reference()
+    from betasplat import compression
+    from betasplat.primitive import PrimitiveSet
+
+    save = {}
+    cases = (("codec_l2", 777, 2, 51, True), ("codec_l0_keep", 50, 0, 52, False))
+    for name, n, lobes, seed, sort in cases:
+        rng = np.random.default_rng(seed)
+        pos = f32(rng.normal(0, 2, (n, 3)))
+        pos[n // 3] = pos[n // 5]  # a tie: the sort must stay stable
+        prims = PrimitiveSet(positions=pos, opacity_raw=f32(rng.normal(0, 1, n)),
+                             rotations=f32(rng.normal(0, 1, (n, 4))), log_scales=f32(rng.normal(-3, 1, (n, 3))),
+                             shapes=np.zeros(n) if lobes == 0 else f32(rng.normal(0, 1, n)),  # constant channel
+                             base_colors=f32(rng.normal(0, 1, (n, 3))),
+                             lobe_axes=f32(rng.normal(0, 1, (n, lobes, 3))),
+                             lobe_colors=f32(rng.normal(0, 1, (n, lobes, 3))))
+        for k, v in prims.parameters().items():
+            save[f"{name}_in_{k}"] = np.asarray(v, np.float64).copy()
+        save[f"{name}_keys"] = compression.morton_keys(prims.positions)
+        save[f"{name}_perm"] = compression.sort_primitives(prims)
+        out = os.path.join(OUT, name)
+        shutil.rmtree(out, ignore_errors=True)
+        compression.pack(prims, out, sort=sort)
+        back = compression.unpack(out)
+        for k, v in back.parameters().items():
+            save[f"{name}_out_{k}"] = np.asarray(v, np.float64).copy()
+    np.savez_compressed(os.path.join(OUT, "codec.npz"), **save)
+    print("wrote codec archives")
+
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "checkpoints":
     checkpoints()
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "codec":
+    codec()

@@ -13,7 +13,7 @@ from conftest import REPO
 
 def _header_symbols():
     txt = open(os.path.join(REPO, "include", "bsr.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|double|const char \*)\s*(bsr_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|double|size_t|const char \*)\s*(bsr_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol():
