@@ -205,19 +205,30 @@ def pack(prims: PrimitiveSet, out_dir, sort=True):
                 "attributes": {}, "position_planes": []}
     if sh:
         manifest["sh_coeffs"] = prims.k
+    jobs = []
     for b in range(4):
         name = f"positions_byte{b}.png"
-        write_png(os.path.join(out_dir, name), planes[b], PNG_LEVEL)
+        jobs.append((os.path.join(out_dir, name), planes[b]))
         manifest["position_planes"].append(name)
     for name, grid in codes.items():
         fn = f"{name}.png"
-        write_png(os.path.join(out_dir, fn), grid, PNG_LEVEL)
+        jobs.append((os.path.join(out_dir, fn), grid))
         mins, maxs = ranges[name]
         manifest["attributes"][name] = {"file": fn, "channels": 1 if grid.ndim == 2 else int(grid.shape[2]),
                                         "min": [float(v) for v in mins], "max": [float(v) for v in maxs]}
+    # the PNGs are independent deflate streams: encode them concurrently (OpenCV releases
+    # the GIL); the bytes are those of the serial loop
+    _parallel(lambda j: write_png(j[0], j[1], PNG_LEVEL), jobs)
     with open(os.path.join(out_dir, "manifest.json"), "w") as fh:
         json.dump(manifest, fh, indent=1, sort_keys=True)
     return manifest
+
+
+def _parallel(fn, items):
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(items), os.cpu_count() or 1) or 1) as ex:
+        return list(ex.map(fn, items))
 
 
 def unpack(archive_dir, device="cuda") -> PrimitiveSet:
@@ -235,9 +246,17 @@ def unpack(archive_dir, device="cuda") -> PrimitiveSet:
     shk = manifest.get("sh_coeffs")
     lobes = None if shk is not None else int(manifest["lobes"])
     cells = rows * cols
+    groups = attribute_groups(n, shk, lobes)
+    specs = []
+    for name, _, _, c in groups:
+        spec = manifest["attributes"].get(name)
+        if spec is None:
+            raise ArchiveError(f"manifest missing attribute {name}")
+        specs.append(spec)
+    files = list(manifest["position_planes"]) + [spec["file"] for spec in specs]
+    images = _parallel(lambda f: read_png(os.path.join(archive_dir, f)), files)
     planes = []
-    for name in manifest["position_planes"]:
-        g = read_png(os.path.join(archive_dir, name))
+    for name, g in zip(manifest["position_planes"], images):
         if g.shape[:2] != (rows, cols) or g.dtype != np.uint8:
             raise ArchiveError(f"{name}: unexpected plane shape or depth")
         if g.ndim != 3 or g.shape[2] != 3:
@@ -245,13 +264,8 @@ def unpack(archive_dir, device="cuda") -> PrimitiveSet:
         planes.append(g)
     if len(planes) != 4:
         raise ArchiveError("expected four position byte planes")
-    groups = attribute_groups(n, shk, lobes)
     blobs, mins, maxs = [np.stack(planes).reshape(-1)], [], []
-    for name, _, _, c in groups:
-        spec = manifest["attributes"].get(name)
-        if spec is None:
-            raise ArchiveError(f"manifest missing attribute {name}")
-        g = read_png(os.path.join(archive_dir, spec["file"]))
+    for (name, _, _, c), spec, g in zip(groups, specs, images[len(manifest["position_planes"]):]):
         got = 1 if g.ndim == 2 else g.shape[2]
         if got != spec["channels"] or spec["channels"] != c:
             raise ArchiveError(f"{name}: channel count mismatch")
