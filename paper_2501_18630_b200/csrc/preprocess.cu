@@ -29,9 +29,12 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, do
 }
 
 // Shared-memory staging of one CTA's 256 primitives: the parameter blocks are contiguous
-// per CTA, so one elected thread moves them with TMA bulk copies (cp.async.bulk +
-// mbarrier) while the other threads proceed; partial / misaligned blocks fall back to
-// cooperative loads.
+// per CTA, so one elected thread moves the geometry (48 B per primitive) with TMA bulk
+// copies (cp.async.bulk + mbarrier); partial / misaligned blocks fall back to cooperative
+// loads.  The appearance payload (192 B per primitive for SH-3) is needed only for visible
+// primitives: when at least half of the CTA is visible it comes in one more bulk copy,
+// otherwise each visible thread copies its own row with cp.async (wide views of large
+// scenes cull most primitives: config 3 keeps ~24%).
 // Appearance payload: SH -> sh[256][3K];  SB -> base[256][3] | axes[256][3M] | cols[256][3M]
 template <int CM>
 struct PreSmem {
@@ -49,15 +52,16 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     float *app_a = sm.app;                                  // SH coeffs / SB base colours
     float *app_b = sm.app + BSR_BLOCK * (Tr::sh ? 0 : 3);   // SB lobe axes
     float *app_c = app_b + BSR_BLOCK * 3 * Tr::M;           // SB lobe colours
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ __align__(8) uint64_t s_bar[2];  // geometry, appearance
     __shared__ int s_bulk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = args.sc.n;
     const bsr_scene &sc = args.sc;
     const int64_t part = blockIdx.x;
+    const int64_t base = part * BSR_BLOCK;
+    const int64_t cnt = imin64(BSR_BLOCK, n - base);
+    const float *app_src_a = Tr::sh ? sc.sh + 3 * Tr::K * base : sc.base_colors + 3 * base;
     if (tid == 0) {
-        const int64_t base = part * BSR_BLOCK;
-        const int64_t cnt = imin64(BSR_BLOCK, n - base);
         uintptr_t al = reinterpret_cast<uintptr_t>(sc.positions) | reinterpret_cast<uintptr_t>(sc.rotations) |
                        reinterpret_cast<uintptr_t>(sc.log_scales) | reinterpret_cast<uintptr_t>(sc.opacity_raw) |
                        reinterpret_cast<uintptr_t>(sc.shapes);
@@ -69,33 +73,23 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         const bool bulk = cnt == BSR_BLOCK && (al & 15) == 0;
         s_bulk = bulk;
         if (bulk) {
-            mbar_init(&s_bar, 1);
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
             const uint32_t b3 = BSR_BLOCK * 12, b4 = BSR_BLOCK * 16, b1 = BSR_BLOCK * 4;
-            const uint32_t bapp = BSR_BLOCK * 4 * Tr::floats;
-            mbar_expect_tx(&s_bar, 2 * b3 + b4 + 2 * b1 + bapp);
-            bulk_g2s(sm.pos, sc.positions + 3 * base, b3, &s_bar);
-            bulk_g2s(sm.rot, sc.rotations + 4 * base, b4, &s_bar);
-            bulk_g2s(sm.ls, sc.log_scales + 3 * base, b3, &s_bar);
-            bulk_g2s(sm.op, sc.opacity_raw + base, b1, &s_bar);
-            bulk_g2s(sm.shp, sc.shapes + base, b1, &s_bar);
-            if constexpr (Tr::sh) {
-                bulk_g2s(app_a, sc.sh + 3 * Tr::K * base, bapp, &s_bar);
-            } else {
-                bulk_g2s(app_a, sc.base_colors + 3 * base, b3, &s_bar);
-                if constexpr (Tr::M > 0) {
-                    bulk_g2s(app_b, sc.lobe_axes + 3 * Tr::M * base, b3 * Tr::M, &s_bar);
-                    bulk_g2s(app_c, sc.lobe_colors + 3 * Tr::M * base, b3 * Tr::M, &s_bar);
-                }
-            }
+            mbar_expect_tx(&s_bar[0], 2 * b3 + b4 + 2 * b1);
+            bulk_g2s(sm.pos, sc.positions + 3 * base, b3, &s_bar[0]);
+            bulk_g2s(sm.rot, sc.rotations + 4 * base, b4, &s_bar[0]);
+            bulk_g2s(sm.ls, sc.log_scales + 3 * base, b3, &s_bar[0]);
+            bulk_g2s(sm.op, sc.opacity_raw + base, b1, &s_bar[0]);
+            bulk_g2s(sm.shp, sc.shapes + base, b1, &s_bar[0]);
         }
     }
     __syncthreads();
-    const int64_t base = part * BSR_BLOCK;
     const int64_t i = base + tid;
-    if (s_bulk) {
-        mbar_wait(&s_bar, 0);
+    const bool bulk = s_bulk;
+    if (bulk) {
+        mbar_wait(&s_bar[0], 0);
     } else {
-        const int64_t cnt = imin64(BSR_BLOCK, n - base);
         for (int q = tid; q < cnt * 3; q += BSR_BLOCK) {
             sm.pos[q] = sc.positions[3 * base + q];
             sm.ls[q] = sc.log_scales[3 * base + q];
@@ -106,9 +100,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
             sm.shp[q] = sc.shapes[base + q];
         }
         if constexpr (Tr::sh) {
-            for (int q = tid; q < cnt * 3 * Tr::K; q += BSR_BLOCK) app_a[q] = sc.sh[3 * Tr::K * base + q];
+            for (int q = tid; q < cnt * 3 * Tr::K; q += BSR_BLOCK) app_a[q] = app_src_a[q];
         } else {
-            for (int q = tid; q < cnt * 3; q += BSR_BLOCK) app_a[q] = sc.base_colors[3 * base + q];
+            for (int q = tid; q < cnt * 3; q += BSR_BLOCK) app_a[q] = app_src_a[q];
             for (int q = tid; q < cnt * 3 * Tr::M; q += BSR_BLOCK) {
                 app_b[q] = sc.lobe_axes[3 * Tr::M * base + q];
                 app_c[q] = sc.lobe_colors[3 * Tr::M * base + q];
@@ -137,7 +131,44 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         const uint32_t ballot = __ballot_sync(0xffffffffu, vis);
         if (lane == 0 && ballot) atomicAdd(&f.ctr->visible, (uint32_t)__popc(ballot));
     }
+    // appearance payload of the visible primitives (the non-bulk path staged everything)
+    bool app_bulk = false;
+    if (bulk) {
+        const int nvis = __syncthreads_count(vis);
+        app_bulk = 2 * nvis >= BSR_BLOCK;
+        if (app_bulk) {
+            if (tid == 0) {
+                const uint32_t bapp = BSR_BLOCK * 4 * Tr::floats;
+                mbar_expect_tx(&s_bar[1], bapp);
+                if constexpr (Tr::sh) {
+                    bulk_g2s(app_a, app_src_a, bapp, &s_bar[1]);
+                } else {
+                    bulk_g2s(app_a, app_src_a, BSR_BLOCK * 12, &s_bar[1]);
+                    if constexpr (Tr::M > 0) {
+                        bulk_g2s(app_b, sc.lobe_axes + 3 * Tr::M * base, BSR_BLOCK * 12 * Tr::M, &s_bar[1]);
+                        bulk_g2s(app_c, sc.lobe_colors + 3 * Tr::M * base, BSR_BLOCK * 12 * Tr::M, &s_bar[1]);
+                    }
+                }
+            }
+        } else if (vis) {  // own row only; read back by this thread alone
+            constexpr int F = Tr::sh ? 3 * Tr::K : 3;
+            if constexpr (F % 4 == 0) {
+                for (int q = 0; q < F; q += 4) cp_async16(app_a + F * tid + q, app_src_a + F * tid + q);
+            } else {
+                for (int q = 0; q < F; ++q) cp_async4(app_a + F * tid + q, app_src_a + F * tid + q);
+            }
+            if constexpr (!Tr::sh) {
+                for (int q = 0; q < 3 * Tr::M; ++q) {
+                    cp_async4(app_b + 3 * Tr::M * tid + q, sc.lobe_axes + 3 * Tr::M * i + q);
+                    cp_async4(app_c + 3 * Tr::M * tid + q, sc.lobe_colors + 3 * Tr::M * i + q);
+                }
+            }
+            cp_async_commit();
+        }
+    }
     if (vis) {
+        if (app_bulk) mbar_wait(&s_bar[1], 0);
+        else if (bulk) cp_async_wait<0>();
         const float *pos = sm.pos + 3 * tid;
         float rgb[3];
         float vx = pos[0] - (float)args.cam.center[0], vy = pos[1] - (float)args.cam.center[1],
