@@ -104,7 +104,7 @@ def traffic(rep):
     for r in raw[2:]:
         b = float(r[cr].replace(",", "")) * scale.get(units[cr], 1) + \
             float(r[cw].replace(",", "")) * scale.get(units[cw], 1)
-        name = r[rk].split("(")[0].split(" ")[-1].split("<")[0].split("::")[-1].replace("_kernel", "")
+        name = r[rk].split("(")[0].split("<")[0].split(" ")[-1].split("::")[-1].replace("_kernel", "")
         per[name].append(b)
     return {k: sum(v) / len(v) for k, v in per.items()}
 

@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 CMD2="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --eager"
 $CMD2 > gpurun_out/fb_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-   -k 'regex:raster_(fwd|bwd)_kernel<\(bool\)0' -s 4 -c 2 -o gpurun_out/fb_raster_c1 $CMD2 > gpurun_out/fb_ncu2.log 2>&1
+   -k 'regex:raster_(fwd|bwd)_kernel<0' -s 4 -c 2 -o gpurun_out/fb_raster_c1 $CMD2 > gpurun_out/fb_ncu2.log 2>&1
 echo done
 for f in gpurun_out/fb_c*.json gpurun_out/fb_ref.json; do cut -c1-200 $f; done
