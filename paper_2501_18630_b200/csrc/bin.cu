@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(FrameView f) {
         }
         s_w[lane] = x - v;
         if (lane == 31) {
+            *f.vis_hint = f.ctr->visible;  // preprocess of the next forward reads it
             f.ctr->entries_needed = x;
             s_over = x > (unsigned long long)f.entry_cap;
             if (s_over) {

@@ -52,6 +52,8 @@ struct FrameView {
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
     double *replay_state;    // [H*W][6] raw(3), raw_depth, T, last  (fp64, flagged only)
+    uint32_t *vis_hint;      // visible count of the previous forward on this frame (a
+                             // scheduling hint for preprocess only: any value is safe)
     float *grad_acc;         // [N][12] raster gradient accumulators by source index (zeroed by backward)
     // --- sizes ---
     int64_t n, entry_cap;
@@ -88,6 +90,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.tile_cur = (uint32_t *)take(4ull * f.n_tiles);
     off = align_up(off, 256);
     f.zero_bytes = off;
+    f.vis_hint = (uint32_t *)take(4);
     f.depth_hist = (uint32_t *)take(4ull * kDepthPasses * 256);
     f.depth_status = (uint32_t *)take(4ull * kDepthPasses * f.depth_parts * 256);
     f.rec = (Record *)take(sizeof(Record) * (uint64_t)n);
