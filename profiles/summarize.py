@@ -47,6 +47,8 @@ def launches(path, skip_prefix=None):
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         name = d["Kernel Name"].split("(")[0]
+        if "spin_kernel" in name:  # torch.cuda._sleep of the stage-profiled eager steps
+            continue
         if skip_prefix and name.startswith(skip_prefix):
             name = "[torch] " + name
         v = float(d["Metric Value"].replace(",", "")) * _US.get(d["Metric Unit"], 1.0)

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/fb_c1.json 2> gpurun_out/fb_c1.err
 for C in c2 c3 c4; do
-  S=20; [ $C = c3 ] && S=10
+  S=20; [ $C = c2 ] && S=100; [ $C = c3 ] && S=10
   timeout 600 python bench.py --config $C --steps $S --warmup 5 --no-cpu-baseline > gpurun_out/fb_$C.json 2> gpurun_out/fb_$C.err
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/fb_ref.json 2> gpurun_out/fb_ref.err
