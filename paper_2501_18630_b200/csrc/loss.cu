@@ -145,10 +145,12 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
             const float a2 = 2.f * (qab - mu_a * mu_b) + C2;
             const float b1 = mu_a * mu_a + mu_b * mu_b + C1;
             const float b2 = (qa - mu_a * mu_a) + var_b + C2;
+            // one division: 1 / b1 = b2 ib, 1 / b2 = b1 ib
             const float ib = 1.f / (b1 * b2);
             const float sv = a1 * a2 * ib;
+            const float ib1 = b2 * ib, ib2 = b1 * ib;
             const int64_t o = (int64_t)c * p.H * p.W + (int64_t)y * p.W + x;
-            p.pq[o] = make_float2(2.f * mu_b * (a2 - a1) * ib - sv * (2.f * mu_a / b1 - 2.f * mu_a / b2), -sv / b2);
+            p.pq[o] = make_float2(2.f * mu_b * (a2 - a1) * ib - sv * (2.f * mu_a * (ib1 - ib2)), -sv * ib2);
             p.px[o] = 2.f * a1 * ib;
             s_sum += sv;
             const float2 ctr = s_in[c][kHalo + r0 + u][kHalo + tx];
