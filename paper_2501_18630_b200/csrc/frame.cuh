@@ -15,7 +15,10 @@ constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys
 constexpr int kRec64 = 8;                            // doubles per fp64 side record
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
 // primitives whose fp32 r2 error bound exceeds this are evaluated in fp64 by the raster
-constexpr float kUnsafeR2Err = 2.0e-5f;
+#ifndef BSR_UNSAFE_R2_ERR
+#define BSR_UNSAFE_R2_ERR 2.0e-5f
+#endif
+constexpr float kUnsafeR2Err = BSR_UNSAFE_R2_ERR;
 
 struct Counters {
     uint32_t visible;        // V
