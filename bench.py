@@ -162,7 +162,7 @@ def build_b200(cfg, rank, world, views_per_gpu):
     cams = rank_cameras(cfg, rank, world, views_per_gpu)
     bg = wl.background
     if cfg == "c2":
-        return dict(kind="render", prims=prims, cams=cams, bg=bg, scene=wl.scene)
+        return dict(kind="render", prims=prims, cams=cams, bg=bg, scene=wl.scene, world=world)
     tgt = PrimitiveSet.from_scene(target_scene(cfg, 1, n))
     targets = render_targets(tgt, cams, bg)
     del tgt
@@ -174,7 +174,7 @@ def build_b200(cfg, rank, world, views_per_gpu):
         pg = dist.group.WORLD
     step = TrainStep(prims, cams, targets, bg, process_group=pg)
     return dict(kind="train", prims=prims, cams=cams, bg=bg, step=step, targets=targets, scene=wl.scene,
-                adam=(cfg != "c4"))
+                adam=(cfg != "c4"), world=world)
 
 
 def run_step(w, prof=None):
@@ -203,6 +203,12 @@ def run_step(w, prof=None):
     return len(w["cams"])
 
 
+def capture_mode(w):
+    """Multi-rank steps capture the NCCL all-reduce: thread-local capture mode keeps the
+    process group's watchdog thread (event queries) from invalidating the capture."""
+    return "thread_local" if w.get("world", 1) > 1 else "global"
+
+
 def make_graph(w, prof=None, warmup=2):
     """Capture one whole step (all views, all kernels, all-reduce, Adam) in a CUDA graph."""
     import torch
@@ -214,7 +220,7 @@ def make_graph(w, prof=None, warmup=2):
             run_step(w, prof)
     torch.cuda.current_stream().wait_stream(side)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g, capture_error_mode=capture_mode(w)):
         run_step(w, prof)
     torch.cuda.synchronize()
     w["graph"] = g
@@ -291,7 +297,7 @@ def e2e_loop(w, steps, world):
     graphs = []
     for b in range(2):
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, capture_error_mode=capture_mode(w)):
             cur = torch.cuda.current_stream()
             cs.wait_stream(cur)
             with torch.cuda.stream(cs):

@@ -445,7 +445,8 @@ class TrainStep:
                 self.step(check=False, adam=adam)
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        mode = "thread_local" if self.pg is not None else "global"  # see bench.capture_mode
+        with torch.cuda.graph(self.graph, capture_error_mode=mode):
             self.step(check=False, adam=adam)
         return self.graph
 
