@@ -389,8 +389,8 @@ def kernel_launches_per_step(w):
     from paper_2501_18630_b200.rasterizer import frame_status
 
     cam = w["cams"][0]
-    # pre, bin count (entries incl. big rects, scan), bin scatter, per-tile sort, raster, replay
-    fwd = 1 + 2 + 1 + 1 + 1 + 1
+    # pre (+ tile counts), bin scan, bin scatter, per-tile sort, raster, replay
+    fwd = 1 + 1 + 1 + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
     per_view = fwd + 2 + 4  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain)

@@ -5,17 +5,17 @@
 // depth order with source-index ties.  That order is a property of each tile alone, so
 // the B200 path builds it per tile instead of sorting twice globally:
 //
-//   bin_entries<COUNT>    every visible primitive adds one entry per tile of its bounds
-//                         rectangle to that tile's count (RED); warp-cooperative, so a
-//                         warp's 32 primitives' entries are spread over its lanes
-//                         (rectangles of more than kBigRect tiles: by the whole CTA)
+//   (counts)              every visible primitive adds one per tile of its bounds
+//                         rectangle to that tile's count (RED), warp-cooperatively; done
+//                         at the end of preprocess (preprocess.cu), which has the rectangle
+//                         in registers (bin_entries<COUNT> is the standalone variant)
 //   bin_scan              one CTA: exclusive scan of the tile counts -> tile ranges, E,
 //                         capacity check (overflow -> BSR_ERR_CAPACITY, entries_needed)
 //   bin_entries<SCATTER>  each entry takes a slot in its tile (atomic cursor) and writes
 //                         (fp32 depth key << 32 | source index)
 //   tile_sort             one CTA per tile sorts its entries ascending by that 64-bit key
-//                         (bitonic, in shared memory up to kSortSmem entries, in place in
-//                         global memory beyond), then re-orders runs of equal fp32 keys by
+//                         (bucket sort in shared memory up to kSortSmem entries, bitonic in
+//                         place in global memory beyond), then re-orders runs of equal fp32 keys by
 //                         (fp64 depth, source index); writes the compact indices.
 //
 // fp32 rounding of the depth is monotone, so (fp32 key, then fp64 depth, then compact
@@ -420,9 +420,9 @@ static unsigned entry_blocks(const FrameView &f) {
 }
 
 // counts -> ranges (profile stage "bin count")
+// (the per-tile counts themselves are taken by preprocess, preprocess.cu)
 int launch_bin_count(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    BSR_CUDA_TRY((pdl_launch(bin_entries_kernel<true>, dim3(entry_blocks(f)), dim3(BSR_BLOCK), 0, st, f)));
     BSR_CUDA_TRY((pdl_launch(bin_scan_kernel, dim3(1), dim3(1024), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;

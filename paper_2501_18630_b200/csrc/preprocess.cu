@@ -40,6 +40,7 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, do
 // overlaps the projection (measured: config 2, 1M at 64% visible, 0.090 -> 0.080 ms; the
 // 3M / 6M configs are faster deferred: 0.256 -> 0.248 and 0.78 -> 0.68 ms).
 constexpr int64_t kEagerAppMaxN = 2 << 20;
+constexpr uint32_t kPreBigRect = 512;  // tile rectangles counted by the whole CTA
 // Appearance payload: SH -> sh[256][3K];  SB -> base[256][3] | axes[256][3M] | cols[256][3M]
 template <int CM>
 struct PreSmem {
@@ -218,6 +219,71 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     const uint32_t inv = __reduce_max_sync(0xffffffffu, vis ? ~key32 : 0u);
     if (lane == 0 && inv) atomicMax(&f.ctr->depth_key_max_inv, inv);
     if (i < n) f.tile_count[i] = tcount;  // 0: culled
+    // ---- tile_bins counts (rasterizer.py:161-191), fused here instead of a second pass
+    //      over the records: the warp's entries are spread over its lanes round-robin
+    //      (owner found by a search over the inclusive prefix), one RED per entry;
+    //      rectangles of more than kPreBigRect tiles are counted by the whole CTA at the end
+    {
+        __shared__ uint4 s_big[32];  // first tile, span x, tiles
+        __shared__ int s_nbig;
+        if (tid == 0) s_nbig = 0;
+        __syncthreads();
+        uint32_t cnt = tcount;
+        const int tx0 = vis ? p.x0 / BSR_TILE : 0, ty0 = vis ? p.y0 / BSR_TILE : 0;
+        const int spanx = vis ? p.x1 / BSR_TILE - tx0 + 1 : 1;
+        uint32_t own_big = 0;
+        if (cnt > kPreBigRect) {
+            const int slot = atomicAdd(&s_nbig, 1);
+            if (slot < 32) s_big[slot] = make_uint4((uint32_t)(ty0 * f.tiles_x + tx0), (uint32_t)spanx, cnt, 0u);
+            else own_big = cnt;
+            cnt = 0;
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t b = 0; b < total; b += 32) {
+            const uint32_t e = b + lane;
+            int lo = 0;
+#pragma unroll
+            for (int sft = 16; sft; sft >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + sft - 1);
+                if (v <= e) lo += sft;
+            }
+            const int owner = min(lo, 31);
+            const uint32_t oin = __shfl_sync(0xffffffffu, incl, owner);
+            const uint32_t ocnt = __shfl_sync(0xffffffffu, cnt, owner);
+            const int otx = __shfl_sync(0xffffffffu, tx0, owner), oty = __shfl_sync(0xffffffffu, ty0, owner);
+            const int osp = __shfl_sync(0xffffffffu, spanx, owner);
+            if (e >= total) continue;
+            const uint32_t local = e - (oin - ocnt), row = local / (uint32_t)osp;
+            atomicAdd(&f.tile_cnt[(uint32_t)(oty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)otx + (local - row * osp)], 1u);
+        }
+        unsigned ob = __ballot_sync(0xffffffffu, own_big != 0);  // queue overflow: the warp itself
+        while (ob) {
+            const int src = __ffs(ob) - 1;
+            ob &= ob - 1;
+            const uint32_t bn = __shfl_sync(0xffffffffu, own_big, src);
+            const int btx = __shfl_sync(0xffffffffu, tx0, src), bty = __shfl_sync(0xffffffffu, ty0, src);
+            const int bsp = __shfl_sync(0xffffffffu, spanx, src);
+            for (uint32_t j = lane; j < bn; j += 32) {
+                const uint32_t row = j / (uint32_t)bsp;
+                atomicAdd(&f.tile_cnt[(uint32_t)(bty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)btx + (j - row * bsp)], 1u);
+            }
+        }
+        __syncthreads();
+        const int nbig = min(s_nbig, 32);
+        for (int q = 0; q < nbig; ++q) {
+            const uint32_t t0 = s_big[q].x, bsp = s_big[q].y, bn = s_big[q].z;
+            for (uint32_t j = tid; j < bn; j += BSR_BLOCK) {
+                const uint32_t row = j / bsp;
+                atomicAdd(&f.tile_cnt[t0 + row * (uint32_t)f.tiles_x + (j - row * bsp)], 1u);
+            }
+        }
+    }
     if (vis) {
         const int64_t c = i;
         f.rec[c] = r;
