@@ -271,16 +271,26 @@ __device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {
 }
 
 // Per-tile order by the fp32 depth key.  Equal keys are re-ordered by fixup_ties anyway,
-// so the sort need not be stable: a bucket sort on the tile's key range (buckets ~ entries,
-// linear in the key bits), shared-memory atomics for the scatter, insertion sort inside
-// the (tiny) buckets; buckets of more than kMaxBucket entries (keys bunched in part of the
-// tile's range) get a warp each and a bitonic network.
+// so the sort need not be stable: a bucket sort on the tile's key range, shared-memory
+// atomics for the scatter, insertion sort inside the (tiny) buckets; buckets of more than
+// kMaxBucket entries get a warp each and a bitonic network.  The buckets are equi-depth
+// rather than equal-width: a coarse histogram (kCoarse bins, linear in the key) gives every
+// coarse bin a share of the nb fine buckets proportional to its entries, so the dense
+// depth clusters of crowded tiles are split finely instead of piling into a few big
+// buckets.  Every step of the mapping is monotone in the key.
 constexpr int kBuckets = 1024;
+constexpr int kCoarse = 256;
+constexpr int kEquiDepthMin = 1024;  // tiles with more entries get the coarse histogram
 constexpr int kMaxBucket = 16;  // larger buckets: one warp each, bitonic
+static_assert(kSortSmem / (kMaxBucket + 1) < 2 * kCoarse, "big-bucket list must fit in cbase / cnf");
 
 template <int NB>
 struct SortSmem {
-    uint32_t start[NB], cur[NB], bigl[NB];
+    uint32_t start[NB + kCoarse], cur[NB + kCoarse];
+    // cbase / cnf: coarse-bin fine-bucket base / count while bucketing; afterwards the
+    // same words hold the list of big buckets (at most kSortSmem / (kMaxBucket + 1) < 2 kCoarse)
+    uint32_t cbase[kCoarse], cnf[kCoarse];
+    __device__ uint32_t *bigl() { return cbase; }
     uint32_t w[BSR_BLOCK / 32];
     uint32_t kmin, kmax, big;
 };
@@ -314,7 +324,13 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     }
     int nb = 1;
     while (nb < n && nb < NB) nb <<= 1;
-    for (int b = t; b < nb; b += BSR_BLOCK) sm.start[b] = 0u;
+    // equal-width buckets for ordinary tiles (linear in the key); equi-depth for crowded ones
+    const bool eq = n > kEquiDepthMin;
+    const int nc = eq ? min(nb, kCoarse) : 1;
+    if (eq)
+        for (int b = t; b < nc; b += BSR_BLOCK) sm.cnf[b] = 0u;
+    else
+        for (int b = t; b < nb; b += BSR_BLOCK) sm.start[b] = 0u;
     __syncthreads();
     if (lane == 0) {
         atomicMin(&sm.kmin, kmin);
@@ -322,22 +338,66 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     }
     __syncthreads();
     kmin = sm.kmin;
-    // bucket = floor((key - kmin) * nb / span) in fp32: every step is monotone, so the bucket
-    // index never decreases with the key (which is all the bucket sort needs)
-    const float scale = (float)nb / ((float)(sm.kmax - kmin) + 1.0f);
+    // position t = (key - kmin) * bins / span in fp32 (monotone in the key)
+    const float cscale = (float)(eq ? nc : nb) / ((float)(sm.kmax - kmin) + 1.0f);
+    auto cpos = [&](uint64_t e) { return (float)((uint32_t)(e >> 32) - kmin) * cscale; };
+    auto cbin = [&](float tc) { return min(nc - 1, (int)tc); };
+    int nf = nb;
+    if (eq) {
+        for (int i = t; i < n; i += BSR_BLOCK) atomicAdd(&sm.cnf[cbin(cpos(g[i]))], 1u);
+        __syncthreads();
+        // fine buckets per coarse bin ~ its share of the entries (>= 1), exclusive prefix -> base
+        if (t < 32) {
+            constexpr int kPerC = kCoarse / 32;
+            uint32_t v[kPerC], tot = 0;
+#pragma unroll
+            for (int q = 0; q < kPerC; ++q) {
+                const int c = kPerC * t + q;
+                const uint32_t cnt = c < nc ? sm.cnf[c] : 0u;
+                v[q] = c < nc ? max(1u, (uint32_t)(((uint64_t)cnt * (uint32_t)nb + (uint32_t)n - 1) / (uint32_t)n)) : 0u;
+                tot += v[q];
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (t >= o) incl += y;
+            }
+            uint32_t run = incl - tot;
+#pragma unroll
+            for (int q = 0; q < kPerC; ++q) {
+                const int c = kPerC * t + q;
+                if (c < nc) {
+                    sm.cbase[c] = run;
+                    sm.cnf[c] = v[q];
+                }
+                run += v[q];
+            }
+            if (t == 31) sm.big = incl;  // total fine buckets (reset below)
+        }
+        __syncthreads();
+        nf = (int)sm.big;
+        for (int b = t; b < nf; b += BSR_BLOCK) sm.start[b] = 0u;
+        __syncthreads();
+        if (t == 0) sm.big = 0u;
+    }
     auto bucket = [&](uint64_t e) {
-        return min(nb - 1, (int)((float)((uint32_t)(e >> 32) - kmin) * scale));
+        const float tc = cpos(e);
+        if (!eq) return min(nb - 1, (int)tc);
+        const int c = cbin(tc);
+        const uint32_t k = sm.cnf[c];
+        return (int)sm.cbase[c] + min((int)k - 1, (int)(fminf(tc - (float)c, 0.99999994f) * (float)k));
     };
     for (int i = t; i < n; i += BSR_BLOCK) atomicAdd(&sm.start[bucket(g[i])], 1u);
     __syncthreads();
     {
-        // exclusive scan of the bucket counts (NB / 256 per thread)
-        constexpr int kPer = NB / BSR_BLOCK;
+        // exclusive scan of the fine bucket counts (up to (NB + kCoarse) / 256 per thread)
+        constexpr int kPer = (NB + kCoarse) / BSR_BLOCK;
         uint32_t v[kPer], tot = 0;
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int b = kPer * t + q;
-            v[q] = b < nb ? sm.start[b] : 0u;
+            v[q] = b < nf ? sm.start[b] : 0u;
             tot += v[q];
         }
         uint32_t incl = tot;
@@ -353,7 +413,7 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int b = kPer * t + q;
-            if (b < nb) {
+            if (b < nf) {
                 sm.start[b] = run;
                 sm.cur[b] = run;
             }
@@ -368,10 +428,10 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     __syncthreads();
     // small buckets: insertion sort by one thread; large ones (keys bunched in the tile's
     // range): queued, then a warp each runs a bitonic network on it
-    for (int b = t; b < nb; b += BSR_BLOCK) {
+    for (int b = t; b < nf; b += BSR_BLOCK) {
         const int lo = (int)sm.start[b], hi = (int)sm.cur[b];
         if (hi - lo > kMaxBucket) {
-            sm.bigl[atomicAdd(&sm.big, 1u)] = (uint32_t)b;
+            sm.bigl()[atomicAdd(&sm.big, 1u)] = (uint32_t)b;
             continue;
         }
         for (int p = lo + 1; p < hi; ++p) {
@@ -386,7 +446,7 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     }
     __syncthreads();
     for (uint32_t k = t >> 5; k < sm.big; k += BSR_BLOCK / 32) {
-        const int b = (int)sm.bigl[k];
+        const int b = (int)sm.bigl()[k];
         const int lo = (int)sm.start[b];
         bitonic_sort_warp(s + lo, (int)sm.cur[b] - lo);
     }
