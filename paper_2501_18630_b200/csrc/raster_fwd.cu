@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     constexpr bool stats = STATS;
     const int my_bit = TG::bit(warp, q);
 
-    float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;
+    float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;  // errT: absolute bound on T's error
     int cnt = 0, last = 0, flag_at = -1;
     uint32_t pairs = 0;
     bool done = !inside;
@@ -116,12 +116,15 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         if (!ambiguous && p.alpha >= a.alpha_min) {
             const float one_m = __fsub_rn(1.0f, p.alpha);
             const float Tn = __fmul_rn(T, one_m);
-            // relative error bound of T: sum over samples of
-            //   alpha/(1-alpha) * rel_err(alpha) + rounding
-            // (record_err_word: rel(alpha) <= Q / om)
-            const float rel = unsafe ? 8.0f * kEps : C.w * rcp_approx(fmaxf(p.om, 1e-30f));
-            const float errTn = errT + 2.5f * kEps + 1.01f * p.alpha * rel * rcp_approx(fmaxf(one_m, 1e-30f));
-            if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn * Tn + 4.0f * kEps * a.t_stop) {
+            // absolute error bound of T (T_c = T + dT, alpha_c = alpha + da):
+            //   dTn <= (1 - alpha) dT + T |da| + 2.5 eps Tn,
+            // |da| <= alpha Q / om (record_err_word); for beta = 4, alpha = o om^4, so
+            // alpha / om = o om^3 needs no reciprocal
+            const float da = unsafe ? 8.0f * kEps * p.alpha
+                                    : (B.z == 4.0f ? C.w * (B.y * (p.om * p.om * p.om))
+                                                   : p.alpha * C.w * rcp_approx(fmaxf(p.om, 1e-30f)));
+            const float errTn = one_m * errT + 1.01f * T * da + 2.5f * kEps * Tn;
+            if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn + 4.0f * kEps * a.t_stop) {
                 ambiguous = true;
             } else {
                 const float w = __fmul_rn(p.alpha, T);
