@@ -360,13 +360,18 @@ def test_spherical_beta_training_step(cuda):
     assert float(st.loss_values[0, 0]) < l0
 
 
-@pytest.mark.parametrize("n", [6000, 20000])
-def test_crowded_tile_binning(cuda, n):
-    """Tiles with more entries than the shared-memory sort (> 4096: 128 KB kernel; > 16384:
-    in-place network in global memory): lists, offsets and depth order stay bit-exact."""
-    rng = np.random.default_rng(50 + n)
+@pytest.mark.parametrize("n,bunched", [(2500, False), (2500, True), (6000, False), (20000, False)])
+def test_crowded_tile_binning(cuda, n, bunched):
+    """Crowded tiles: 1024 < n <= 4096 entries take the equi-depth bucket sort in shared
+    memory (also with depths bunched in a sliver of the tile's range plus far outliers),
+    > 4096 the in-place network in global memory; lists, offsets and depth order stay
+    bit-exact."""
+    rng = np.random.default_rng(50 + n + bunched)
     scene = random_scene(rng, n, degree=0, spread=0.1, scale_range=(0.002, 0.01), opacity_range=(0.02, 0.1))
     scene.positions[:, :2] += np.float32(0.1)  # inside one tile of the 48 x 48 view
+    if bunched:  # 95% of the depths within 1e-3 of each other, the rest spread over 2 units
+        far = rng.random(n) < 0.05
+        scene.positions[:, 2] = np.where(far, rng.uniform(-1.0, 1.0, n), rng.uniform(0.0, 1e-3, n)).astype(np.float32)
     _compare_forward(scene, toy_camera(48, 48), np.ones(3), cuda)
 
 
