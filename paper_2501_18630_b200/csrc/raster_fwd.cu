@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
     __shared__ uint32_t s_col[BSR_BLOCK / 32][32];  // [chunk of 32 entries][tile sub-block]
     __shared__ int s_cnt[BSR_BLOCK];
+    __shared__ int s_flag[BSR_BLOCK];  // entry where the pixel was handed to the fp64 replay (-1: none);
+                                       // written once, kept out of the pair loop's registers
     const FrameView &f = a.f;
     const int tile = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -72,10 +74,11 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     const int my_bit = TG::bit(warp, q);
 
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dep = 0.f, errT = 0.f;  // errT: absolute bound on T's error
-    int cnt = 0, last = 0, flag_at = -1;
+    int cnt = 0, last = 0;
     uint32_t pairs = 0;
     bool done = !inside;
     s_cnt[t] = 0;
+    s_flag[t] = -1;
 
     auto prefetch = [&](int b0, int buf) {
         const int e = b0 + t;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
             }
         }
         if (ambiguous) {
-            flag_at = b0 + j - start;
+            s_flag[t] = b0 + j - start;
             done = true;
         }
         return took;
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     }
     if (!inside) return;
     const int64_t pix = (int64_t)py * f.W + px;
+    const int flag_at = s_flag[t];
     if (flag_at >= 0) {
         const uint32_t slot = atomicAdd(&f.ctr->flagged, 1u);
         f.flags[slot] = make_uint2((uint32_t)pix, (uint32_t)flag_at);
