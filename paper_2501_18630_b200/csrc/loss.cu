@@ -13,12 +13,17 @@
 
 namespace bsr {
 
-// Tiles of 32 x 16 outputs with a 5-pixel halo.  The Gaussian blur runs on packed FP32
-// pairs (FFMA2, sm_100): the maps kernel blurs (a, b) and (a^2, b^2) as pairs and a*b as a
-// scalar; the gradient kernel blurs (d_mu, d_qa) as a pair and d_qab as a scalar.  Each
-// thread produces two adjacent outputs per pass so the loaded taps are reused.
-constexpr int kTW = 32, kTH = 16, kHalo = 5;
-constexpr int kIW = kTW + 2 * kHalo, kIH = kTH + 2 * kHalo;  // 42 x 26
+// Tiles of 32 x 32 outputs with a 5-pixel halo (42 x 42 inputs, rows padded to 44 so every
+// 4-pixel group is 16-byte aligned).  The Gaussian blur runs on packed FP32 pairs (FFMA2,
+// sm_100): the maps kernel blurs (a, b) and (a^2, b^2) as pairs and a*b as a scalar; the
+// gradient kernel blurs (d_mu, d_qa) as a pair and d_qab as a scalar.  Both passes produce
+// four adjacent outputs per work item from 14 taps (loaded as 16-byte vectors), so the
+// taps and the squares are reused four times; the 32 x 32 tile keeps the halo overhead of
+// the horizontal pass at 42 / 32 rows.
+constexpr int kTW = 32, kTH = 32, kHalo = 5;
+constexpr int kIW = kTW + 2 * kHalo, kIH = kTH + 2 * kHalo;  // 42 x 42
+constexpr int kIWP = 44;                                      // padded row (16-B aligned quads)
+constexpr int kQuads = kTW / 4;                               // 4-output items per row
 
 struct LossArgs {
     const float *a, *b, *raw;
@@ -46,32 +51,59 @@ __device__ __forceinline__ void cp_async_commit_l() { asm volatile("cp.async.com
 template <int N>
 __device__ __forceinline__ void cp_async_wait_l() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// horizontal pass of one row item: 12 consecutive input pairs -> 2 outputs
-struct HPair {
-    float2 p0, p1, q0, q1;
-    float x0, x1;
+// 14 consecutive float2 (7 x 16 B) / float (4 x 16 B, the last two unused) from shared memory
+__device__ __forceinline__ void load14(const float2 *src, float2 (&v)[14]) {
+    const float4 *q = reinterpret_cast<const float4 *>(src);
+#pragma unroll
+    for (int m = 0; m < 7; ++m) {
+        const float4 u = q[m];
+        v[2 * m] = make_float2(u.x, u.y);
+        v[2 * m + 1] = make_float2(u.z, u.w);
+    }
+}
+__device__ __forceinline__ void load14(const float *src, float (&v)[14]) {
+    const float4 *q = reinterpret_cast<const float4 *>(src);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const float4 u = q[m];
+        if (4 * m < 14) v[4 * m] = u.x;
+        if (4 * m + 1 < 14) v[4 * m + 1] = u.y;
+        if (4 * m + 2 < 14) v[4 * m + 2] = u.z;
+        if (4 * m + 3 < 14) v[4 * m + 3] = u.w;
+    }
+}
+
+struct MapsSmem {
+    float2 in[3][kIH][kIWP];  // (a, b) per channel, zero outside the image
+    float2 hp[kIH][kTW], hq[kIH][kTW];
+    float hx[kIH][kTW];
+    double red[2][8];
+};
+struct GradSmem {
+    float2 p[2][kIH][kIWP];  // (d_mu, d_qa), double-buffered over channels
+    float x[2][kIH][kIWP];   // d_qab
+    float2 hp[kIH][kTW];
+    float hx[kIH][kTW];
 };
 
-__global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
+__global__ void __launch_bounds__(256, 3) ssim_maps_kernel(LossArgs p) {
     pdl_wait();
-    __shared__ float2 s_in[3][kIH][kIW];  // (a, b) per channel, zero outside the image
-    __shared__ float2 s_hp[kIH][kTW], s_hq[kIH][kTW];
-    __shared__ __align__(16) float s_hx[kIH][kTW];
-    __shared__ double red[2][8];
+    extern __shared__ __align__(16) unsigned char loss_smem[];
+    MapsSmem &sm = *reinterpret_cast<MapsSmem *>(loss_smem);
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
     // rows of kIW pixels x 3 channels = 126 contiguous floats: two rows per pass
-    // (asynchronous copies: all 26 rows in flight at once, zero fill outside the image)
+    // (asynchronous copies: all rows in flight at once, zero fill outside the image)
     if (t < 2 * 3 * kIW) {
         const int half = t / (3 * kIW), q = t - half * 3 * kIW;
         const int c = q % 3, xx = q / 3, gx = x0 - kHalo + xx;
         const bool okx = gx >= 0 && gx < p.W;
-#pragma unroll
+#pragma unroll 3
         for (int r = half; r < kIH; r += 2) {
             const int gy = y0 - kHalo + r;
             const bool ok = okx && gy >= 0 && gy < p.H;
             const int64_t o = ok ? ((int64_t)gy * p.W + gx) * 3 + c : 0;
-            cp_async_zfill<4>(&s_in[c][r][xx].x, p.a + o, ok);
-            cp_async_zfill<4>(&s_in[c][r][xx].y, p.b + o, ok);
+            cp_async_zfill<4>(&sm.in[c][r][xx].x, p.a + o, ok);
+            cp_async_zfill<4>(&sm.in[c][r][xx].y, p.b + o, ok);
         }
     }
     cp_async_commit_l();
@@ -79,66 +111,77 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
     float w[11];
 #pragma unroll
     for (int k = 0; k < 11; ++k) w[k] = p.w[k];
-    const int tx = t & 31, r0 = 2 * (t >> 5);
+    const int tx = t & 31, r0 = 4 * (t >> 5);
     double s_sum = 0.0, l1_sum = 0.0;
     for (int c = 0; c < 3; ++c) {
         __syncthreads();
-        for (int it = t; it < kIH * (kTW / 2); it += 256) {
-            const int r = it >> 4, cp = it & 15;
-            float2 v[12], sq[12];
-            float xp[12];
+        // horizontal pass: item = (row, 4 adjacent outputs)
+        for (int it = t; it < kIH * kQuads; it += 256) {
+            const int r = it / kQuads, xb = 4 * (it - r * kQuads);
+            float2 v[14], sq[14];
+            float xp[14];
+            load14(&sm.in[c][r][xb], v);
 #pragma unroll
-            for (int k = 0; k < 12; ++k) {
-                v[k] = s_in[c][r][2 * cp + k];
+            for (int k = 0; k < 14; ++k) {
                 sq[k] = __fmul2_rn(v[k], v[k]);
                 xp[k] = v[k].x * v[k].y;
             }
-            float2 p0 = f2(0.f), p1 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f);
-            float xa = 0.f, xb = 0.f;
+            float2 P[4], Q[4];
+            float X[4];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                P[o] = f2(0.f);
+                Q[o] = f2(0.f);
+                X[o] = 0.f;
+            }
 #pragma unroll
             for (int k = 0; k < 11; ++k) {
                 const float2 wk = f2(w[k]);
-                p0 = __ffma2_rn(wk, v[k], p0);
-                p1 = __ffma2_rn(wk, v[k + 1], p1);
-                q0 = __ffma2_rn(wk, sq[k], q0);
-                q1 = __ffma2_rn(wk, sq[k + 1], q1);
-                xa = fmaf(w[k], xp[k], xa);
-                xb = fmaf(w[k], xp[k + 1], xb);
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    P[o] = __ffma2_rn(wk, v[k + o], P[o]);
+                    Q[o] = __ffma2_rn(wk, sq[k + o], Q[o]);
+                    X[o] = fmaf(w[k], xp[k + o], X[o]);
+                }
             }
-            s_hp[r][2 * cp] = p0;
-            s_hp[r][2 * cp + 1] = p1;
-            s_hq[r][2 * cp] = q0;
-            s_hq[r][2 * cp + 1] = q1;
-            reinterpret_cast<float2 *>(&s_hx[r][0])[cp] = make_float2(xa, xb);
+            float4 *hp = reinterpret_cast<float4 *>(&sm.hp[r][xb]);
+            float4 *hq = reinterpret_cast<float4 *>(&sm.hq[r][xb]);
+            hp[0] = make_float4(P[0].x, P[0].y, P[1].x, P[1].y);
+            hp[1] = make_float4(P[2].x, P[2].y, P[3].x, P[3].y);
+            hq[0] = make_float4(Q[0].x, Q[0].y, Q[1].x, Q[1].y);
+            hq[1] = make_float4(Q[2].x, Q[2].y, Q[3].x, Q[3].y);
+            *reinterpret_cast<float4 *>(&sm.hx[r][xb]) = make_float4(X[0], X[1], X[2], X[3]);
         }
         __syncthreads();
-        // vertical pass: column tx, output rows r0 and r0 + 1
-        float2 P0 = f2(0.f), P1 = f2(0.f), Q0 = f2(0.f), Q1 = f2(0.f);
-        float X0 = 0.f, X1 = 0.f;
+        // vertical pass: column tx, output rows r0 .. r0 + 3
+        float2 P[4], Q[4];
+        float X[4];
 #pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            const float2 hp = s_hp[r0 + k][tx], hq = s_hq[r0 + k][tx];
-            const float hx = s_hx[r0 + k][tx];
-            if (k < 11) {
-                const float2 wk = f2(w[k]);
-                P0 = __ffma2_rn(wk, hp, P0);
-                Q0 = __ffma2_rn(wk, hq, Q0);
-                X0 = fmaf(w[k], hx, X0);
-            }
-            if (k > 0) {
-                const float2 wk = f2(w[k - 1]);
-                P1 = __ffma2_rn(wk, hp, P1);
-                Q1 = __ffma2_rn(wk, hq, Q1);
-                X1 = fmaf(w[k - 1], hx, X1);
+        for (int u = 0; u < 4; ++u) {
+            P[u] = f2(0.f);
+            Q[u] = f2(0.f);
+            X[u] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+            const float2 hp = sm.hp[r0 + k][tx], hq = sm.hq[r0 + k][tx];
+            const float hx = sm.hx[r0 + k][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k - u >= 0 && k - u < 11) {
+                    const float2 wk = f2(w[k - u]);
+                    P[u] = __ffma2_rn(wk, hp, P[u]);
+                    Q[u] = __ffma2_rn(wk, hq, Q[u]);
+                    X[u] = fmaf(w[k - u], hx, X[u]);
+                }
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int x = x0 + tx, y = y0 + r0 + u;
             if (x >= p.W || y >= p.H) continue;
-            const float2 P = u ? P1 : P0, Q = u ? Q1 : Q0;
-            const float qab = u ? X1 : X0;
-            const float mu_a = P.x, mu_b = P.y, qa = Q.x, qb = Q.y;
+            const float mu_a = P[u].x, mu_b = P[u].y, qa = Q[u].x, qb = Q[u].y;
+            const float qab = X[u];
             const float C1 = 1e-4f, C2 = 9e-4f;
             const float var_b = qb - mu_b * mu_b;
             const float a1 = 2.f * mu_a * mu_b + C1;
@@ -153,7 +196,7 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
             p.pq[o] = make_float2(2.f * mu_b * (a2 - a1) * ib - sv * (2.f * mu_a * (ib1 - ib2)), -sv * ib2);
             p.px[o] = 2.f * a1 * ib;
             s_sum += sv;
-            const float2 ctr = s_in[c][kHalo + r0 + u][kHalo + tx];
+            const float2 ctr = sm.in[c][kHalo + r0 + u][kHalo + tx];
             l1_sum += fabsf(ctr.x - ctr.y);
         }
     }
@@ -164,15 +207,15 @@ __global__ void __launch_bounds__(256, 4) ssim_maps_kernel(LossArgs p) {
         l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
     }
     if ((t & 31) == 0) {
-        red[0][t >> 5] = s_sum;
-        red[1][t >> 5] = l1_sum;
+        sm.red[0][t >> 5] = s_sum;
+        sm.red[1][t >> 5] = l1_sum;
     }
     __syncthreads();
     if (t == 0) {  // per-block partials (no same-address atomics across 1e3+ blocks)
         double sv = 0, l = 0;
         for (int i = 0; i < 8; ++i) {
-            sv += red[0][i];
-            l += red[1][i];
+            sv += sm.red[0][i];
+            l += sm.red[1][i];
         }
         const int blk = blockIdx.y * gridDim.x + blockIdx.x;
         p.sums[blk] = sv;
@@ -213,12 +256,10 @@ __device__ __forceinline__ void loss_finish(const LossArgs &p) {
     }
 }
 
-__global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
+__global__ void __launch_bounds__(256, 3) ssim_grad_kernel(LossArgs p) {
     pdl_wait();
-    __shared__ float2 s_p[2][kIH][kIW];  // (d_mu, d_qa), double-buffered over channels
-    __shared__ float s_x[2][kIH][kIW];   // d_qab
-    __shared__ float2 s_hp[kIH][kTW];
-    __shared__ __align__(16) float s_hx[kIH][kTW];
+    extern __shared__ __align__(16) unsigned char loss_smem[];
+    GradSmem &sm = *reinterpret_cast<GradSmem *>(loss_smem);
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH, t = threadIdx.x;
     if (blockIdx.x == 0 && blockIdx.y == 0) loss_finish(p);
     const double n = 3.0 * p.W * p.H;
@@ -227,7 +268,7 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
     float w[11];
 #pragma unroll
     for (int k = 0; k < 11; ++k) w[k] = p.w[k];
-    const int tx = t & 31, r0 = 2 * (t >> 5);
+    const int tx = t & 31, r0 = 4 * (t >> 5);
     const int lrow = t / kIW, lcol = t - lrow * kIW;  // load mapping: 6 rows of 42 per pass
     const int64_t plane = (int64_t)p.H * p.W;
     auto load_plane = [&](int c, int buf) {
@@ -239,8 +280,8 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
                 const int gy = y0 - kHalo + r;
                 const bool ok = okx && gy >= 0 && gy < p.H;
                 const int64_t o = ok ? c * plane + (int64_t)gy * p.W + gx : 0;
-                cp_async_zfill<8>(&s_p[buf][r][lcol], p.pq + o, ok);
-                cp_async_zfill<4>(&s_x[buf][r][lcol], p.px + o, ok);
+                cp_async_zfill<8>(&sm.p[buf][r][lcol], p.pq + o, ok);
+                cp_async_zfill<4>(&sm.x[buf][r][lcol], p.px + o, ok);
             }
         }
         cp_async_commit_l();
@@ -249,9 +290,9 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
     for (int c = 0; c < 3; ++c) {
         const int buf = c & 1;
         // centre values for the epilogue, in flight during the blur
-        float av[2], bv[2], rv[2];
+        float av[4], bv[4], rv[4];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int x = x0 + tx, y = y0 + r0 + q;
             av[q] = bv[q] = 0.f;
             rv[q] = 1.f;
@@ -262,7 +303,7 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
                 if (p.raw) rv[q] = p.raw[o];
             }
         }
-        __syncthreads();  // buffer buf ^ 1 and s_hp / s_hx are free
+        __syncthreads();  // buffer buf ^ 1 and hp / hx are free
         if (c < 2) {
             load_plane(c + 1, buf ^ 1);
             cp_async_wait_l<1>();
@@ -270,52 +311,58 @@ __global__ void __launch_bounds__(256, 4) ssim_grad_kernel(LossArgs p) {
             cp_async_wait_l<0>();
         }
         __syncthreads();
-        for (int it = t; it < kIH * (kTW / 2); it += 256) {
-            const int r = it >> 4, cp = it & 15;
-            float2 v[12];
-            float u[12];
+        for (int it = t; it < kIH * kQuads; it += 256) {
+            const int r = it / kQuads, xb = 4 * (it - r * kQuads);
+            float2 v[14];
+            float u[14];
+            load14(&sm.p[buf][r][xb], v);
+            load14(&sm.x[buf][r][xb], u);
+            float2 P[4];
+            float X[4];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) {
-                v[k] = s_p[buf][r][2 * cp + k];
-                u[k] = s_x[buf][r][2 * cp + k];
+            for (int o = 0; o < 4; ++o) {
+                P[o] = f2(0.f);
+                X[o] = 0.f;
             }
-            float2 p0 = f2(0.f), p1 = f2(0.f);
-            float xa = 0.f, xb = 0.f;
 #pragma unroll
             for (int k = 0; k < 11; ++k) {
                 const float2 wk = f2(w[k]);
-                p0 = __ffma2_rn(wk, v[k], p0);
-                p1 = __ffma2_rn(wk, v[k + 1], p1);
-                xa = fmaf(w[k], u[k], xa);
-                xb = fmaf(w[k], u[k + 1], xb);
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    P[o] = __ffma2_rn(wk, v[k + o], P[o]);
+                    X[o] = fmaf(w[k], u[k + o], X[o]);
+                }
             }
-            s_hp[r][2 * cp] = p0;
-            s_hp[r][2 * cp + 1] = p1;
-            reinterpret_cast<float2 *>(&s_hx[r][0])[cp] = make_float2(xa, xb);
+            float4 *hp = reinterpret_cast<float4 *>(&sm.hp[r][xb]);
+            hp[0] = make_float4(P[0].x, P[0].y, P[1].x, P[1].y);
+            hp[1] = make_float4(P[2].x, P[2].y, P[3].x, P[3].y);
+            *reinterpret_cast<float4 *>(&sm.hx[r][xb]) = make_float4(X[0], X[1], X[2], X[3]);
         }
         __syncthreads();
-        float2 P0 = f2(0.f), P1 = f2(0.f);
-        float X0 = 0.f, X1 = 0.f;
+        float2 P[4];
+        float X[4];
 #pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            const float2 hp = s_hp[r0 + k][tx];
-            const float hx = s_hx[r0 + k][tx];
-            if (k < 11) {
-                P0 = __ffma2_rn(f2(w[k]), hp, P0);
-                X0 = fmaf(w[k], hx, X0);
-            }
-            if (k > 0) {
-                P1 = __ffma2_rn(f2(w[k - 1]), hp, P1);
-                X1 = fmaf(w[k - 1], hx, X1);
+        for (int q = 0; q < 4; ++q) {
+            P[q] = f2(0.f);
+            X[q] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+            const float2 hp = sm.hp[r0 + k][tx];
+            const float hx = sm.hx[r0 + k][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (k - q >= 0 && k - q < 11) {
+                    P[q] = __ffma2_rn(f2(w[k - q]), hp, P[q]);
+                    X[q] = fmaf(w[k - q], hx, X[q]);
+                }
             }
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int x = x0 + tx, y = y0 + r0 + q;
             if (x >= p.W || y >= p.H) continue;
-            const float2 P = q ? P1 : P0;
-            const float b2 = q ? X1 : X0;
-            const float grad = (P.x + 2.f * av[q] * P.y + bv[q] * b2) * inv_n;
+            const float grad = (P[q].x + 2.f * av[q] * P[q].y + bv[q] * X[q]) * inv_n;
             const float diff = av[q] - bv[q];
             const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
             float d = l1w * sgn - sw * grad;
@@ -368,8 +415,16 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     }
     for (int i = 0; i < 11; ++i) p.w[i] = (float)(w[i] / sum);
     dim3 grid((unsigned)div_up(width, kTW), (unsigned)div_up(height, kTH));
-    BSR_CUDA_TRY((pdl_launch(ssim_maps_kernel, dim3(grid), dim3(256), 0, st, p)));
-    BSR_CUDA_TRY((pdl_launch(ssim_grad_kernel, dim3(grid), dim3(256), 0, st, p)));
+    static bool attr = false;
+    if (!attr) {
+        BSR_CUDA_TRY(cudaFuncSetAttribute(ssim_maps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(MapsSmem)));
+        BSR_CUDA_TRY(cudaFuncSetAttribute(ssim_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(GradSmem)));
+        attr = true;
+    }
+    BSR_CUDA_TRY((pdl_launch(ssim_maps_kernel, dim3(grid), dim3(256), sizeof(MapsSmem), st, p)));
+    BSR_CUDA_TRY((pdl_launch(ssim_grad_kernel, dim3(grid), dim3(256), sizeof(GradSmem), st, p)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
