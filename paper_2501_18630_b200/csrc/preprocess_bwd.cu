@@ -342,12 +342,14 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
 // per pass, ballot-compacted); culled primitives get no gradient (rasterizer.py:262-320
 // leaves them zero).
 constexpr int kPreBwdChunk = 64;
+// 4-warp CTAs: small scenes (config 1: one wave) spread over more SMs
+constexpr int kPreBwdThreads = 128;
 
 template <int K>
-__global__ void __launch_bounds__(BSR_BLOCK) preprocess_bwd_kernel(PreBwdArgs a) {
+__global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(PreBwdArgs a) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
-    const int64_t c0 = ((blockIdx.x * (int64_t)BSR_BLOCK + threadIdx.x) >> 5) * kPreBwdChunk;
+    const int64_t c0 = ((blockIdx.x * (int64_t)kPreBwdThreads + threadIdx.x) >> 5) * kPreBwdChunk;
     if (c0 >= a.f.n) return;
     uint32_t m[kPreBwdChunk / 32];
     int tot = 0;
@@ -377,8 +379,8 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
                           const bsr_grads &g, float *screen_grad_norm, float4 *drgb, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
     PreBwdArgs a{sc, cam, f, g, screen_grad_norm, drgb};
-    const unsigned blocks = (unsigned)div_up(f.n, (int64_t)kPreBwdChunk * (BSR_BLOCK / 32));
-#define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), 0, st, a)))
+    const unsigned blocks = (unsigned)div_up(f.n, (int64_t)kPreBwdChunk * (kPreBwdThreads / 32));
+#define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
     BSR_LAUNCH_CHECK();
