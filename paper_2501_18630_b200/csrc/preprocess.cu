@@ -15,6 +15,12 @@
 
 namespace bsr {
 
+// CTA size NT: 4-warp CTAs (30 KB of staging each for SH-3, up to 7 CTAs per SM) for scenes
+// up to kPreSmallMaxN primitives -- small scenes (config 1: one wave) spread evenly over the
+// SMs; 8-warp CTAs above (measured: 1M / 3M configs 6% / 11% faster at 128 threads, the 6M
+// config 11% faster at 256)
+constexpr int64_t kPreSmallMaxN = 4 << 20;
+
 struct PreArgs {
     bsr_scene sc;
     KCam cam;
@@ -42,42 +48,42 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, do
 constexpr int64_t kEagerAppMaxN = 2 << 20;
 constexpr uint32_t kPreBigRect = 512;  // tile rectangles counted by the whole CTA
 // Appearance payload: SH -> sh[256][3K];  SB -> base[256][3] | axes[256][3M] | cols[256][3M]
-template <int CM>
+template <int CM, int kPreThreads>
 struct PreSmem {
-    float pos[BSR_BLOCK * 3], rot[BSR_BLOCK * 4], ls[BSR_BLOCK * 3], op[BSR_BLOCK], shp[BSR_BLOCK];
-    float app[BSR_BLOCK * AppTraits<CM>::floats];
+    float pos[kPreThreads * 3], rot[kPreThreads * 4], ls[kPreThreads * 3], op[kPreThreads], shp[kPreThreads];
+    float app[kPreThreads * AppTraits<CM>::floats];
 };
 
-template <int CM>
-__global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs args) {
+template <int CM, int kPreThreads>
+__global__ void __launch_bounds__(kPreThreads, 2) preprocess_fwd_kernel(PreArgs args) {
     pdl_wait();
     using Tr = AppTraits<CM>;
     const FrameView &f = args.f;
     extern __shared__ __align__(16) unsigned char pre_smem_raw[];
-    PreSmem<CM> &sm = *reinterpret_cast<PreSmem<CM> *>(pre_smem_raw);
+    PreSmem<CM, kPreThreads> &sm = *reinterpret_cast<PreSmem<CM, kPreThreads> *>(pre_smem_raw);
     float *app_a = sm.app;                                  // SH coeffs / SB base colours
-    float *app_b = sm.app + BSR_BLOCK * (Tr::sh ? 0 : 3);   // SB lobe axes
-    float *app_c = app_b + BSR_BLOCK * 3 * Tr::M;           // SB lobe colours
+    float *app_b = sm.app + kPreThreads * (Tr::sh ? 0 : 3);   // SB lobe axes
+    float *app_c = app_b + kPreThreads * 3 * Tr::M;           // SB lobe colours
     __shared__ __align__(8) uint64_t s_bar[2];  // geometry, appearance
     __shared__ int s_bulk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = args.sc.n;
     const bsr_scene &sc = args.sc;
     const int64_t part = blockIdx.x;
-    const int64_t base = part * BSR_BLOCK;
-    const int64_t cnt = imin64(BSR_BLOCK, n - base);
+    const int64_t base = part * kPreThreads;
+    const int64_t cnt = imin64(kPreThreads, n - base);
     const float *app_src_a = Tr::sh ? sc.sh + 3 * Tr::K * base : sc.base_colors + 3 * base;
     __shared__ int s_eager;
     auto issue_app = [&]() {  // one elected thread: the CTA's whole appearance block
-        const uint32_t bapp = BSR_BLOCK * 4 * Tr::floats;
+        const uint32_t bapp = kPreThreads * 4 * Tr::floats;
         mbar_expect_tx(&s_bar[1], bapp);
         if constexpr (Tr::sh) {
             bulk_g2s(app_a, app_src_a, bapp, &s_bar[1]);
         } else {
-            bulk_g2s(app_a, app_src_a, BSR_BLOCK * 12, &s_bar[1]);
+            bulk_g2s(app_a, app_src_a, kPreThreads * 12, &s_bar[1]);
             if constexpr (Tr::M > 0) {
-                bulk_g2s(app_b, sc.lobe_axes + 3 * Tr::M * base, BSR_BLOCK * 12 * Tr::M, &s_bar[1]);
-                bulk_g2s(app_c, sc.lobe_colors + 3 * Tr::M * base, BSR_BLOCK * 12 * Tr::M, &s_bar[1]);
+                bulk_g2s(app_b, sc.lobe_axes + 3 * Tr::M * base, kPreThreads * 12 * Tr::M, &s_bar[1]);
+                bulk_g2s(app_c, sc.lobe_colors + 3 * Tr::M * base, kPreThreads * 12 * Tr::M, &s_bar[1]);
             }
         }
     };
@@ -90,12 +96,12 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         else
             al |= reinterpret_cast<uintptr_t>(sc.base_colors) | reinterpret_cast<uintptr_t>(sc.lobe_axes) |
                   reinterpret_cast<uintptr_t>(sc.lobe_colors);
-        const bool bulk = cnt == BSR_BLOCK && (al & 15) == 0;
+        const bool bulk = cnt == kPreThreads && (al & 15) == 0;
         s_bulk = bulk;
         if (bulk) {
             mbar_init(&s_bar[0], 1);
             mbar_init(&s_bar[1], 1);
-            const uint32_t b3 = BSR_BLOCK * 12, b4 = BSR_BLOCK * 16, b1 = BSR_BLOCK * 4;
+            const uint32_t b3 = kPreThreads * 12, b4 = kPreThreads * 16, b1 = kPreThreads * 4;
             mbar_expect_tx(&s_bar[0], 2 * b3 + b4 + 2 * b1);
             bulk_g2s(sm.pos, sc.positions + 3 * base, b3, &s_bar[0]);
             bulk_g2s(sm.rot, sc.rotations + 4 * base, b4, &s_bar[0]);
@@ -113,20 +119,20 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     if (bulk) {
         mbar_wait(&s_bar[0], 0);
     } else {
-        for (int q = tid; q < cnt * 3; q += BSR_BLOCK) {
+        for (int q = tid; q < cnt * 3; q += kPreThreads) {
             sm.pos[q] = sc.positions[3 * base + q];
             sm.ls[q] = sc.log_scales[3 * base + q];
         }
-        for (int q = tid; q < cnt * 4; q += BSR_BLOCK) sm.rot[q] = sc.rotations[4 * base + q];
-        for (int q = tid; q < cnt; q += BSR_BLOCK) {
+        for (int q = tid; q < cnt * 4; q += kPreThreads) sm.rot[q] = sc.rotations[4 * base + q];
+        for (int q = tid; q < cnt; q += kPreThreads) {
             sm.op[q] = sc.opacity_raw[base + q];
             sm.shp[q] = sc.shapes[base + q];
         }
         if constexpr (Tr::sh) {
-            for (int q = tid; q < cnt * 3 * Tr::K; q += BSR_BLOCK) app_a[q] = app_src_a[q];
+            for (int q = tid; q < cnt * 3 * Tr::K; q += kPreThreads) app_a[q] = app_src_a[q];
         } else {
-            for (int q = tid; q < cnt * 3; q += BSR_BLOCK) app_a[q] = app_src_a[q];
-            for (int q = tid; q < cnt * 3 * Tr::M; q += BSR_BLOCK) {
+            for (int q = tid; q < cnt * 3; q += kPreThreads) app_a[q] = app_src_a[q];
+            for (int q = tid; q < cnt * 3 * Tr::M; q += kPreThreads) {
                 app_b[q] = sc.lobe_axes[3 * Tr::M * base + q];
                 app_c[q] = sc.lobe_colors[3 * Tr::M * base + q];
             }
@@ -160,7 +166,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         app_bulk = true;  // requested with the geometry
     } else if (bulk) {
         const int nvis = __syncthreads_count(vis);
-        app_bulk = 2 * nvis >= BSR_BLOCK;
+        app_bulk = 2 * nvis >= kPreThreads;
         if (app_bulk) {
             if (tid == 0) issue_app();
         } else if (vis) {  // own row only; read back by this thread alone
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
         const int nbig = min(s_nbig, 32);
         for (int q = 0; q < nbig; ++q) {
             const uint32_t t0 = s_big[q].x, bsp = s_big[q].y, bn = s_big[q].z;
-            for (uint32_t j = tid; j < bn; j += BSR_BLOCK) {
+            for (uint32_t j = tid; j < bn; j += kPreThreads) {
                 const uint32_t row = j / bsp;
                 atomicAdd(&f.tile_cnt[t0 + row * (uint32_t)f.tiles_x + (j - row * bsp)], 1u);
             }
@@ -295,16 +301,17 @@ __global__ void __launch_bounds__(BSR_BLOCK, 2) preprocess_fwd_kernel(PreArgs ar
     }
 }
 
-template <int CM>
-static int launch_pre_k(const PreArgs &a, unsigned blocks, cudaStream_t st) {
-    const size_t smem = sizeof(PreSmem<CM>);
+template <int CM, int NT>
+static int launch_pre_k(const PreArgs &a, cudaStream_t st) {
+    const size_t smem = sizeof(PreSmem<CM, NT>);
     static bool attr = false;
     if (!attr) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<CM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr = true;
     }
-    BSR_CUDA_TRY((pdl_launch(preprocess_fwd_kernel<CM>, dim3(blocks), dim3(BSR_BLOCK), smem, st, a)));
+    const unsigned blocks = (unsigned)div_up(a.sc.n, NT);
+    BSR_CUDA_TRY((pdl_launch(preprocess_fwd_kernel<CM, NT>, dim3(blocks), dim3(NT), smem, st, a)));
     return BSR_OK;
 }
 
@@ -312,8 +319,8 @@ int launch_preprocess(const bsr_scene &sc, const KCam &cam, const FrameView &f, 
     if (sc.n == 0) return BSR_OK;
     PreArgs a{sc, cam, f};
     int rc = BSR_OK;
-    const unsigned blocks = (unsigned)div_up(sc.n, BSR_BLOCK);
-#define BSR_PRE_LAUNCH(CM) rc = launch_pre_k<CM>(a, blocks, st)
+    const bool small = sc.n <= kPreSmallMaxN;
+#define BSR_PRE_LAUNCH(CM) rc = small ? launch_pre_k<CM, 128>(a, st) : launch_pre_k<CM, 256>(a, st)
     BSR_DISPATCH_CM(sc, BSR_PRE_LAUNCH);
 #undef BSR_PRE_LAUNCH
     if (rc) return rc;
