@@ -621,10 +621,13 @@ def main():
         info = frames[0].info
         V, E = info["visible"], info["entries"]
         hbm = {}
-        hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80) / (stages["preprocess"] * 1e-3) / 1e9
-        # binning: count = V (tile count + rect, 20 B) + E 4-B atomics; scatter = V (20 B + key
+        # preprocess: parameters (geometry 48 B + SH 12 K B), records 80 B per visible, and the
+        # per-tile counts (E 4-B REDs, taken here since the counting pass was fused in)
+        hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80 + E * 4) / (stages["preprocess"] * 1e-3) / 1e9
+        # binning: scan = T counts read + T ranges written (12 B); scatter = V (20 B + key
         # 4 B) + E (8-B entry + 4-B atomic); per-tile sort = E (8 B read + 4 B written)
-        hbm["bin_count"] = (V * 20 + E * 4) / (stages["bin_count"] * 1e-3) / 1e9
+        n_tiles = frames[0].info.get("tiles") or (-(-w["cams"][0].width // 16)) * (-(-w["cams"][0].height // 16))
+        hbm["bin_count"] = (n_tiles * 12) / (stages["bin_count"] * 1e-3) / 1e9
         hbm["bin_scatter"] = (V * 24 + E * 12) / (stages["bin_scatter"] * 1e-3) / 1e9
         hbm["tile_sort"] = (E * 12) / (stages["tile_sort"] * 1e-3) / 1e9
         if w["kind"] == "train":
