@@ -221,7 +221,7 @@ __device__ __forceinline__ uint32_t row_bits(int cx0, int cx1) {  // pixel colum
 
 template <int G, bool BBOX>
 __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4 B, const float4 C, const int4 D,
-                                                    int X0, int Y0, float alpha_min) {
+                                                    int X0, int Y0, float alpha_min, int part = 0, int K = 1) {
     using TG = TileGrid<G>;
     // bounds box clipped to the tile (tile-relative pixel coordinates)
     const int bx0 = max(D.x - X0, 0), bx1 = min(D.y - X0, BSR_TILE - 1);
@@ -230,6 +230,7 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
     if (!BBOX && B.y < alpha_min) return 0u;
     const float l11 = A.z, l21 = A.w, l22 = B.x;
     if (BBOX || !(l11 > 0.f && l22 > 0.f)) {
+        if (part) return 0u;  // part 0 covers the whole box
         const uint32_t rb = row_bits<G>(bx0, bx1);
         uint32_t m = 0;
         for (int r = by0 / TG::h; r <= by1 / TG::h; ++r) m |= rb << (r * TG::cols);
@@ -246,7 +247,7 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
     const float mx = (float)(D.x - X0) + A.x, my = (float)(D.z - Y0) + A.y;
     const int y0 = max(by0, (int)ceilf(my - hy)), y1 = min(by1, (int)floorf(my + hy));
     uint32_t m = 0;
-    for (int y = y0; y <= y1; ++y) {
+    for (int y = y0 + part; y <= y1; y += K) {  // rows part, part + K, ... of the span
         const float dy = (float)y - my;
         const float wy = l22 * dy;
         const float rem = fmaxf(xl - wy * wy, 0.f);
@@ -257,6 +258,42 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
         if (x0 <= x1) m |= row_bits<G>(x0, x1) << ((y / TG::h) * TG::cols);
     }
     return m;
+}
+
+// Sub-block masks of a batch's nb entries, transposed into s_col[chunk][sub-block] (bit
+// column per chunk of 32 entries).  With few entries (nb <= 128) K = 2..8 threads share an
+// entry, each taking every K-th pixel row of its span, so the mask phase does not wait on
+// single threads walking up to 16 rows; the parts are OR-combined (K | 32: an entry's
+// parts sit in one warp) and regathered per chunk through s_mask.  Chunks >= ceil(nb / 32)
+// of s_col are left untouched (never read).
+template <int G, bool BBOX>
+__device__ __forceinline__ void batch_masks(const Record *sr, int nb, int X0, int Y0, float alpha_min,
+                                            uint32_t *s_mask, uint32_t (*s_col)[32]) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int K = 1;
+    while (K < 8 && nb * K * 2 <= BSR_BLOCK) K <<= 1;
+    if (K == 1) {
+        uint32_t m = 0;
+        if (t < nb) {
+            const Record &r = sr[t];
+            m = entry_tile_mask<G, BBOX>(r.a, r.b, r.c, r.d, X0, Y0, alpha_min);
+        }
+        s_col[warp][lane] = warp_transpose32(m, lane);
+        return;
+    }
+    const int e = t / K, part = t - e * K;
+    uint32_t m = 0;
+    if (e < nb) {
+        const Record &r = sr[e];
+        m = entry_tile_mask<G, BBOX>(r.a, r.b, r.c, r.d, X0, Y0, alpha_min, part, K);
+    }
+    for (int o = 1; o < K; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+    if (part == 0 && e < nb) s_mask[e] = m;
+    __syncthreads();
+    if (warp < ((nb + 31) >> 5)) {
+        const int ee = 32 * warp + lane;
+        s_col[warp][lane] = warp_transpose32(ee < nb ? s_mask[ee] : 0u, lane);
+    }
 }
 
 }  // namespace bsr

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     __shared__ uint32_t s_cidx[2][BSR_BLOCK];
     __shared__ uint32_t s_col[BSR_BLOCK / 32][32];  // [chunk of 32 entries][tile sub-block]
     __shared__ int s_cnt[BSR_BLOCK];
+    __shared__ uint32_t s_mask[BSR_BLOCK];  // per-entry masks while several threads share an entry
     __shared__ int s_flag[BSR_BLOCK];  // entry where the pixel was handed to the fp64 replay (-1: none);
                                        // written once, kept out of the pair loop's registers
     const FrameView &f = a.f;
@@ -161,14 +162,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         const int nch = (nb + 31) >> 5;
         // ---- one thread per entry: which sub-blocks of the tile can it reach; transposed
         //      per chunk of 32 entries into one bit column per sub-block
-        {
-            uint32_t m = 0;
-            if (t < nb) {
-                const Record &r = s_rec[buf][t];
-                m = entry_tile_mask<G, stats>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
-            }
-            s_col[warp][lane] = warp_transpose32(m, lane);
-        }
+        batch_masks<G, stats>(s_rec[buf], nb, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min, s_mask, s_col);
         __syncthreads();
         // ---- this warp's groups: open (some pixel not finished) and how much their entry
         //      sets overlap; groups that mostly share entries walk the union together
