@@ -67,7 +67,7 @@ inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
 
 __global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
                                  const double *opac, const double *betas, const double *colors,
-                                 const int32_t *bounds, Record *rec, double *rec64) {
+                                 const int32_t *bounds, Record *rec, double *rec64, float4 *needle) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
@@ -82,6 +82,7 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     const double ex = det > 0 ? sqrt(fabs(cc / det)) : 1e30, ey = det > 0 ? sqrt(fabs(ca / det)) : 1e30;
     const double kr = pd ? chol_r2_error_bound(l11, l21, l22, ex + 2.0, ey + 2.0) : 1.0;
     const bool unsafe = !pd || (float)kr > kUnsafeR2Err;
+    if (unsafe) needle[k] = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);  // core seam: fp64 path
     r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
                       record_err_word(kr, (double)r.b.z, unsafe));
     double *d = rec64 + kRec64 * k;
@@ -351,7 +352,7 @@ static int core_prepare(const CoreView &c, int64_t v, const double *means, const
     BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
     if (v > 0)
         core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
-                                                                               colors, bounds, c.f.rec, c.f.rec64);
+                                                                               colors, bounds, c.f.rec, c.f.rec64, c.f.needle);
     const int64_t m = imax64(n_entries, c.f.n_tiles);
     core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
         offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);

@@ -55,6 +55,7 @@ struct FrameView {
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
     double *replay_state;    // [H*W][6] raw(3), raw_depth, T, last  (fp64, flagged only)
+    float4 *needle;          // [N] needle words of records with c.w < 0 (raster.cuh), NaN: fp64 path
     uint32_t *vis_hint;      // visible count of the previous forward on this frame (a
                              // scheduling hint for preprocess only: any value is safe)
     float *grad_acc;         // [N][12] raster gradient accumulators by source index (zeroed by backward)
@@ -111,6 +112,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.flags = (uint2 *)take(8ull * npx);
     f.replay_state = (double *)take(8ull * 6 * npx);
     f.grad_acc = (float *)take(4ull * kGradStride * n);
+    f.needle = (float4 *)take(16ull * n);
     f.total_bytes = align_up(off, 256);
     return f;
 }

@@ -205,8 +205,19 @@ __global__ void __launch_bounds__(kPreThreads, 2) preprocess_fwd_kernel(PreArgs 
         const bool pd = conic_cholesky(p.ca, p.cb, p.cc, l11, l21, l22);
         r.a = make_float4((float)(p.mx - p.x0), (float)(p.my - p.y0), (float)l11, (float)l21);
         r.b = make_float4((float)l22, (float)o, (float)beta, (float)p.tz);
-        const float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
+        float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
         unsafe = !pd || kr > kUnsafeR2Err;
+        if (unsafe) {  // needle (compensated fp32) if its bound allows, else the fp64 path
+            float4 nw = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+            if (pd) {
+                const float kn = (float)needle_r2_error_bound(l11, l21, sqrt(p.c00) + 2.0, sqrt(p.c11) + 2.0);
+                if (kn <= kUnsafeR2Err) {
+                    kr = kn;
+                    nw = needle_word(l11, l21, p.mx - p.x0, p.my - p.y0);
+                }
+            }
+            f.needle[i] = nw;
+        }
         r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
         m64[0] = p.mx;
         m64[1] = p.my;

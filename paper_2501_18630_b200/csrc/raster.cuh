@@ -66,6 +66,28 @@ __host__ __device__ inline double chol_r2_error_bound(double l11, double l21, do
     return 5.9604644775390625e-08 * 1.5 * (4.0 * U + 8.0 + 4.0 * l11 * X + 4.0 * (fabs(l21) + l22) * Y);
 }
 
+// Needles: primitives whose factored form still cancels (kR > kUnsafeR2Err: long thin
+// footprints, r2 ~ 1 where l11 dx and l21 dy are each ~ l21 / l22 >> 1) but whose conic is
+// positive definite.  They keep the fp32 path with compensated arithmetic: the frame's
+// needle word holds (t_hi, t_lo) = l21 / l11 and the low parts of the mean offsets, dx and
+// dy are formed exactly (TwoSum) as double-floats, and u = l11 (dx + t dy) is evaluated
+// with one fused rounding on a small quantity.  What remains is rounding of the small
+// terms themselves (bound below, X, Y the footprint half extents), so their decisions are
+// certified like any other record's instead of running the fp64 evaluation per pixel.
+__host__ __device__ inline double needle_r2_error_bound(double l11, double l21, double X, double Y) {
+    const double t = fabs(l21 / l11);
+    // |u| = l11 |s|, |w| <= 1 where it matters: du <= 4 eps |u| (s, l11, product), dw <= 3 eps |w|,
+    // r2 = fma(w, w, u u): dr2 <= 8 eps u^2 + 6 eps w^2 + 2 eps r2 <= 10 eps, plus the neglected
+    // second-order terms of the double-float parts (eps^2 t Y); safety factor 1.5
+    return 5.9604644775390625e-08 * 1.5 * (12.0 + 8.0 * 5.9604644775390625e-08 * l11 * (X + t * Y));
+}
+// side word of a needle: (t_hi, t_lo, rel_x_lo, rel_y_lo); fp64-path records: NaN
+__host__ __device__ inline float4 needle_word(double l11, double l21, double relx, double rely) {
+    const double t = l21 / l11;
+    const float th = (float)t, rx = (float)relx, ry = (float)rely;
+    return make_float4(th, (float)(t - (double)th), (float)(relx - (double)rx), (float)(rely - (double)ry));
+}
+
 // _raster.pyx:107-113:  r2 = a dx^2 + 2 b dx dy + c dy^2 (factored, see conic_cholesky),
 // x = clamp(r2, 0, 1), kernel = (1 - x)^beta, alpha = o * kernel.  px_rel / py_rel are
 // pixel coordinates relative to the primitive's bounds corner (exact integers); the
@@ -76,6 +98,36 @@ __device__ __forceinline__ Pair eval_pair(const float4 A, const float4 B, int px
     p.dy = __fsub_rn((float)py_rel, A.y);
     p.u = __fmaf_rn(A.w, p.dy, __fmul_rn(A.z, p.dx));
     p.w = __fmul_rn(B.x, p.dy);
+    p.r2 = __fmaf_rn(p.w, p.w, __fmul_rn(p.u, p.u));
+    p.x = fminf(fmaxf(p.r2, 0.0f), 1.0f);
+    p.om = __fsub_rn(1.0f, p.x);
+    p.k = beta_pow(p.om, B.z);
+    p.alpha = __fmul_rn(B.y, p.k);
+    return p;
+}
+
+// TwoSum: a + b = s + e exactly
+__device__ __forceinline__ float two_sum(float a, float b, float &e) {
+    const float s = __fadd_rn(a, b);
+    const float bb = __fsub_rn(s, a);
+    e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+    return s;
+}
+
+// Compensated evaluation of a needle record (N = its needle word); same outputs as eval_pair.
+__device__ __forceinline__ Pair eval_needle(const float4 A, const float4 B, const float4 N, int px_rel, int py_rel) {
+    Pair p;
+    float ex, ey;
+    const float dxh = two_sum((float)px_rel, -A.x, ex), dyh = two_sum((float)py_rel, -A.y, ey);
+    const float dxl = __fsub_rn(ex, N.z), dyl = __fsub_rn(ey, N.w);
+    // s = dx + t dy: the large parts cancel inside one fused rounding, the rest are small
+    const float s0 = __fmaf_rn(N.x, dyh, dxh);
+    const float corr = __fmaf_rn(N.x, dyl, __fmaf_rn(N.y, dyh, dxl));
+    const float sv = __fadd_rn(s0, corr);
+    p.dx = __fadd_rn(dxh, dxl);
+    p.dy = __fadd_rn(dyh, dyl);
+    p.u = __fmul_rn(A.z, sv);
+    p.w = __fmaf_rn(B.x, dyh, __fmul_rn(B.x, dyl));
     p.r2 = __fmaf_rn(p.w, p.w, __fmul_rn(p.u, p.u));
     p.x = fminf(fmaxf(p.r2, 0.0f), 1.0f);
     p.om = __fsub_rn(1.0f, p.x);

@@ -180,11 +180,18 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         if (STATS) pairs += (act && e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
         float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
         Pair p;
-        if (C.w < 0.f) {  // fp32-unsafe primitive
-            const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
-            p = u.p;
-            ga = u.ga;
-            gb = u.gb;
+        if (C.w < 0.f) {  // needle or fp64 primitive (uniform per entry)
+            const float4 N = f.needle[s_cidx[j]];
+            if (N.x == N.x) {  // needle: compensated fp32 (same bits as the forward)
+                p = eval_needle(A, Bq, N, px - bd.x, py - bd.z);
+                ga = A.z * p.u;
+                gb = A.w * p.u + Bq.x * p.w;
+            } else {
+                const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
+                p = u.p;
+                ga = u.ga;
+                gb = u.gb;
+            }
         } else {
             p = eval_pair(A, Bq, px - bd.x, py - bd.z);
             ga = A.z * p.u;                 // a dx + b dy = l11 u

@@ -102,19 +102,29 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         const int4 bd = s_rec[buf][j].d;
         if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
         const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
-        const bool unsafe = C.w < 0.f;
+        const bool unsafe = C.w < 0.f;  // needle or fp64 record (uniform per entry)
+        const float Q = fabsf(C.w);
+        bool fp64 = false;
         Pair p;
-        if (unsafe) {  // uniform per entry
-            const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
-            p.alpha = u.x;
-            p.om = u.y;
+        if (unsafe) {
+            const float4 N = f.needle[s_cidx[buf][j]];
+            if (N.x == N.x) {  // needle: compensated fp32
+                p = eval_needle(A, B, N, px - bd.x, py - bd.z);
+            } else {
+                fp64 = true;
+                const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
+                p.alpha = u.x;
+                p.om = u.y;
+            }
         } else {
             p = eval_pair(A, B, px - bd.x, py - bd.z);
         }
         bool ambiguous = false;
         // rare path: alpha within 5% of the cutoff -> certify with the error bound
         if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
-            const float rel = unsafe ? 8.0f * kEps : alpha_rel_err_pixel(A, B, p);
+            const float rel = fp64 ? 8.0f * kEps
+                                   : (unsafe ? Q * rcp_approx(fmaxf(p.om, 1e-30f)) * 1.01f
+                                             : alpha_rel_err_pixel(A, B, p));
             ambiguous = fabsf(p.alpha - a.alpha_min) <= 2.0f * rel * p.alpha + 4.0f * kEps * a.alpha_min;
         }
         if (!ambiguous && p.alpha >= a.alpha_min) {
@@ -124,9 +134,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
             //   dTn <= (1 - alpha) dT + T |da| + 2.5 eps Tn,
             // |da| <= alpha Q / om (record_err_word); for beta = 4, alpha = o om^4, so
             // alpha / om = o om^3 needs no reciprocal
-            const float da = unsafe ? 8.0f * kEps * p.alpha
-                                    : (B.z == 4.0f ? C.w * (B.y * (p.om * p.om * p.om))
-                                                   : p.alpha * C.w * rcp_approx(fmaxf(p.om, 1e-30f)));
+            const float da = fp64 ? 8.0f * kEps * p.alpha
+                                  : (B.z == 4.0f ? Q * (B.y * (p.om * p.om * p.om))
+                                                 : p.alpha * Q * rcp_approx(fmaxf(p.om, 1e-30f)));
             const float errTn = one_m * errT + 1.01f * T * da + 2.5f * kEps * Tn;
             if (p.alpha > 0.999f || fabsf(Tn - a.t_stop) <= 2.0f * errTn + 4.0f * kEps * a.t_stop) {
                 ambiguous = true;
