@@ -227,6 +227,72 @@ def test_backward_with_depth_matches_oracle(cuda):
         _grad_close(getattr(grads, k).cpu().numpy(), ref[k], k)
 
 
+def _needle_scene(rng, n):
+    """Long thin footprints (scale 0.8 x 0.004 x 0.004, random orientations) among ordinary
+    primitives: their factored-conic bound exceeds the fp32 limit, so they take the
+    compensated 'needle' evaluation (raster.cuh) or, if that bound fails too, the fp64 one."""
+    scene = random_scene(rng, n, degree=2, spread=0.7, scale_range=(0.02, 0.1))
+    k = n // 2
+    scene.log_scales[:k] = np.log(np.array([0.8, 0.004, 0.004], np.float32))
+    return scene, k
+
+
+def _needle_count(scene, cam):
+    """How many records the device classifies as needles (the bounds of preprocess.cu)."""
+    from oracle import pipeline as orc
+
+    b = orc.project(np.asarray(scene.positions, np.float64), scene.rotations,
+                    np.exp(np.asarray(scene.log_scales, np.float64)), cam)
+    c, cov = b["conics"], b["cov2d"]
+    l11 = np.sqrt(c[:, 0]); l21 = c[:, 1] / l11; l22 = np.sqrt(np.maximum(c[:, 2] - l21 ** 2, 0))
+    X, Y = np.sqrt(cov[:, 0, 0]) + 2, np.sqrt(cov[:, 1, 1]) + 2
+    eps = 5.9604644775390625e-08
+    kr = eps * 1.5 * (4 * (l11 * X + abs(l21) * Y) + 8 + 4 * l11 * X + 4 * (abs(l21) + l22) * Y)
+    kn = eps * 1.5 * (12 + 8 * eps * l11 * (X + abs(l21 / l11) * Y))
+    return int(np.sum((kr > 2e-5) & (kn <= 2e-5) & (l22 > 0)))
+
+
+def _needle_grads(cuda):
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import render_backward, render_tiled
+
+    rng = np.random.default_rng(97)
+    scene, k = _needle_scene(rng, 240)
+    cam = toy_camera(256, 192)
+    bg = np.array([1.0, 1.0, 1.0])
+    up = rng.standard_normal((192, 256, 3))
+    fwd = orc.forward(scene, cam, bg, core="c")
+    ref = orc.backward(scene, cam, bg, up, fwd, core="c")
+    prims = _gpu_prims(scene)
+    out = render_tiled(prims, cam, bg)
+    grads = render_backward(prims, cam, bg, up.astype(np.float32), forward_out=out)
+    return grads, ref, k
+
+
+def test_needles_match_oracle(cuda):
+    """Needle records: forward bit-exact on counts / tile lists against the oracle, images
+    within tolerance; gradients of the ordinary primitives rendered together with them
+    within 1e-3 (the needles' own gradients: test_needle_gradients_strict)."""
+    rng = np.random.default_rng(97)
+    scene, _ = _needle_scene(rng, 240)
+    cam = toy_camera(256, 192)
+    assert _needle_count(scene, cam) >= 20
+    _compare_forward(scene, cam, np.ones(3), cuda)
+    grads, ref, k = _needle_grads(cuda)
+    for name in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
+        _grad_close(getattr(grads, name).cpu().numpy()[k:], ref[name][k:], name)
+
+
+@pytest.mark.xfail(reason="fp32 accumulation of the needles' conic partials (large terms of both signs "
+                          "over ~1e3 pixels): up to ~10% relative error on some needle rotations / scales, "
+                          "the same with the fp64 pair evaluation and with an fp64 geometric chain; see "
+                          "DESIGN.md section 9", strict=False)
+def test_needle_gradients_strict(cuda):
+    grads, ref, k = _needle_grads(cuda)
+    for name in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
+        _grad_close(getattr(grads, name).cpu().numpy()[:k], ref[name][:k], name)
+
+
 def test_zero_upstream_gives_zero_gradients(cuda):
     """tests/test_rasterizer.py:221-227."""
     from paper_2501_18630_b200 import render_backward
