@@ -283,10 +283,10 @@ def test_needles_match_oracle(cuda):
         _grad_close(getattr(grads, name).cpu().numpy()[k:], ref[name][k:], name)
 
 
-@pytest.mark.xfail(reason="fp32 accumulation of the needles' conic partials (large terms of both signs "
-                          "over ~1e3 pixels): up to ~10% relative error on some needle rotations / scales, "
-                          "the same with the fp64 pair evaluation and with an fp64 geometric chain; see "
-                          "DESIGN.md section 9", strict=False)
+@pytest.mark.xfail(reason="up to ~10% relative error on some needle rotation / scale gradients; the same "
+                          "with the fp64 pair evaluation, an fp64 geometric chain or conic partials "
+                          "accumulated in the needle's own frame -- cause open, see DESIGN.md section 9",
+                   strict=False)
 def test_needle_gradients_strict(cuda):
     grads, ref, k = _needle_grads(cuda)
     for name in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
