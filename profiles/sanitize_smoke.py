@@ -25,6 +25,26 @@ tg = render_targets(PrimitiveSet.from_scene(target_scene("c1", 1, 5000)), wl1.ca
 st = TrainStep(PrimitiveSet.from_scene(wl1.scene), wl1.cameras, tg, wl1.background)
 st.step(check=True)
 st.step()
+# multi-view step (deferred colour chain), needles, codec round trip
+cams = [Camera.from_lookat((np.sin(a) * 4.0, 0.3, -np.cos(a) * 4.0), (0, 0, 0), (0, 1, 0), 0.9, 72, 56)
+        for a in np.linspace(-0.6, 0.6, 10)]
+tg3 = render_targets(PrimitiveSet.from_scene(target_scene("c1", 1, 3000)), cams, wl1.background)
+st3 = TrainStep(PrimitiveSet.from_scene(make_workload("c1", seed=0, n=3000).scene), cams, tg3, wl1.background)
+st3.step(check=True)
+nd = make_workload("c1", seed=3, n=600).scene
+nd.log_scales[:300] = np.log(np.array([0.8, 0.004, 0.004], np.float32))
+pn = PrimitiveSet.from_scene(nd)
+on = render_tiled(pn, wl1.cameras[0], wl1.background)
+render_backward(pn, wl1.cameras[0], wl1.background, np.ones((80, 96, 3), np.float32), forward_out=on)
+import tempfile
+
+from paper_2501_18630_b200 import compression
+
+with tempfile.TemporaryDirectory() as d:
+    compression.pack(sb, d)
+    compression.unpack(d)
+    compression.pack(pn, d + "/sh")
+    compression.unpack(d + "/sh")
 core = backend.get_core("cuda")
 torch.cuda.synchronize()
 print("sanitize smoke ok")
