@@ -55,7 +55,7 @@ struct PreSmem {
 };
 
 template <int CM, int kPreThreads>
-__global__ void __launch_bounds__(kPreThreads, 2) preprocess_fwd_kernel(PreArgs args) {
+__global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) preprocess_fwd_kernel(PreArgs args) {
     pdl_wait();
     using Tr = AppTraits<CM>;
     const FrameView &f = args.f;
