@@ -21,6 +21,10 @@
 
 #include "raster.cuh"
 
+#ifndef BSR_DENSE_X10
+#define BSR_DENSE_X10 30  // dense mode when groups share entries; backward: from 3 groups per entry (measured: config 4 raster bwd 4.27 -> 4.22 ms from 2.5; worse above 3.5)
+#endif
+
 namespace bsr {
 
 struct RasterBwdArgs {
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                 uni += __shfl_xor_sync(0xffffffffu, uni, o);
             }
             // lanes 0..7 hold the totals; broadcast so the branch below is warp-uniform
-            dense = __shfl_sync(0xffffffffu, 2 * sum >= 5 * uni, 0);
+            dense = __shfl_sync(0xffffffffu, 10 * sum >= BSR_DENSE_X10 * uni, 0);
         }
         // walk set bits from the highest entry below the limit down to entry 0
         auto lowbits = [](int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); };

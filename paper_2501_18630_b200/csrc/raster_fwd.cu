@@ -20,6 +20,10 @@
 
 #include "raster.cuh"
 
+#ifndef BSR_DENSE_X10
+#define BSR_DENSE_X10 40  // dense mode when groups share entries; forward: from 4 groups per entry (measured: config 4 raster fwd 2.76 -> 2.60 ms from 2.5)
+#endif
+
 #ifndef BSR_FWD_CTAS
 #define BSR_FWD_CTAS 4  // resident CTAs per SM the register budget targets
 #endif
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
                 uni += __shfl_xor_sync(0xffffffffu, uni, o);
             }
             // lanes 0..7 hold the totals; broadcast so the branch below is warp-uniform
-            dense = __shfl_sync(0xffffffffu, 2 * sum >= 5 * uni, 0);  // >= 2.5 groups per entry on average
+            dense = __shfl_sync(0xffffffffu, 10 * sum >= BSR_DENSE_X10 * uni, 0);
         }
         if (dense) {
             int c = 0;
