@@ -281,7 +281,10 @@ __device__ void fixup_ties(P a, int n, const uint64_t *dkey64) {
 constexpr int kBuckets = 1024;
 constexpr int kCoarse = 256;
 constexpr int kEquiDepthMin = 1024;  // tiles with more entries get the coarse histogram
-constexpr int kMaxBucket = 16;  // larger buckets: one warp each, bitonic
+#ifndef BSR_MAX_BUCKET
+#define BSR_MAX_BUCKET 16
+#endif
+constexpr int kMaxBucket = BSR_MAX_BUCKET;  // larger buckets: one warp each, bitonic
 static_assert(kSortSmem / (kMaxBucket + 1) < 2 * kCoarse, "big-bucket list must fit in cbase / cnf");
 
 template <int NB>
