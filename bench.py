@@ -307,8 +307,8 @@ def e2e_loop(w, steps, world):
                 else:  # previous frame's image
                     res_host[b ^ 1].copy_(stage[b ^ 1], non_blocking=True)
             if train:
-                for dst, src in zip(w["targets"], stage[b]):
-                    dst.copy_(src, non_blocking=True)
+                # graph b's step reads its targets straight from staging buffer b (no D2D copy)
+                w["step"].targets = list(stage[b])
                 run_step(w)
                 res_host[b].copy_(res_dev, non_blocking=True)  # the step's loss values
             else:
@@ -316,6 +316,8 @@ def e2e_loop(w, steps, world):
                 stage[b].copy_(res_dev, non_blocking=True)
             cur.wait_stream(cs)
         graphs.append(g)
+    if train:
+        w["step"].targets = list(w["targets"])
     for _ in range(10):  # first launches upload the graphs
         for g in graphs:
             g.replay()
