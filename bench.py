@@ -263,9 +263,9 @@ def e2e_loop(w, steps, world):
     none) and reads its result device->host (the loss values; the rendered image for
     config 2).  The step and its copies are captured together into two CUDA graphs
     (alternating staging buffers), the way a training / serving loop would pipeline them:
-    graph i uploads step i+1's inputs on a forked copy branch while step i computes
-    (one D2D moves the staged inputs into place), config 2 downloads frame i-1 while
-    frame i renders; the host reads step i-1's result before launching step i+1."""
+    graph i uploads step i+1's inputs into the other staging buffer on a forked copy
+    branch while step i reads its own, config 2 downloads frame i-1 while frame i
+    renders; the host reads step i-1's result before launching step i+1."""
     import torch
 
     main, cs = torch.cuda.current_stream(), torch.cuda.Stream()
