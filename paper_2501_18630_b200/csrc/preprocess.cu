@@ -41,11 +41,14 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, do
 // primitives: when at least half of the CTA is visible it comes in one more bulk copy,
 // otherwise each visible thread copies its own row with cp.async (wide views of large
 // scenes and mostly-culled CTAs).  When the previous forward on this frame kept at least
-// half of the primitives (FrameView::vis_hint) and the scene is at most kEagerAppMaxN, the
-// appearance block is requested together with the geometry instead, so its latency
-// overlaps the projection (measured: config 2, 1M at 64% visible, 0.090 -> 0.080 ms; the
-// 3M / 6M configs are faster deferred: 0.256 -> 0.248 and 0.78 -> 0.68 ms).
-constexpr int64_t kEagerAppMaxN = 2 << 20;
+// half of the primitives (FrameView::vis_hint) the appearance block is requested together
+// with the geometry instead, so its latency overlaps the projection (measured with the
+// current CTA sizes: config 2 0.090 -> 0.080 ms, config 3 0.251 -> 0.237, config 4 0.616 ->
+// 0.605; scripts/ab_eager.sh).
+#ifndef BSR_EAGER_APP_MAX_N
+#define BSR_EAGER_APP_MAX_N (1ll << 40)  // no size limit (build knob for A/B runs)
+#endif
+constexpr int64_t kEagerAppMaxN = BSR_EAGER_APP_MAX_N;
 constexpr uint32_t kPreBigRect = 512;  // tile rectangles counted by the whole CTA
 // Appearance payload: SH -> sh[256][3K];  SB -> base[256][3] | axes[256][3M] | cols[256][3M]
 template <int CM, int kPreThreads>
