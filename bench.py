@@ -25,9 +25,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -143,6 +141,8 @@ def rank_cameras(cfg, rank, world, views_per_gpu):
     if cfg == "c1":
         cams = orbit_cameras(world * views_per_gpu)
         return [cams[k] for k in partition_views(len(cams), world, rank)]
+    # the hemisphere cameras come from their own stream (scenes.camera_rng): the same views
+    # as the full-size workload that cpu_reference_step_fn renders
     if cfg == "c3":
         wl_cams = make_workload("c3", seed=0, n=16).cameras
         return [wl_cams[k] for k in partition_views(len(wl_cams), world, rank)]
@@ -395,7 +395,7 @@ def kernel_launches_per_step(w):
     fwd = 1 + 1 + 1 + 1 + 1 + 1
     if w["kind"] == "render":
         return fwd * len(w["cams"])
-    per_view = fwd + 2 + 4  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain)
+    per_view = fwd + 2 + 5  # + loss (maps, grad+finish) + backward (zero, raster, replay, chain, fp64 geometry chain)
     st = w.get("step")
     color = 1 if st is not None and getattr(st, "drgb", None) is not None else 0  # deferred colour chain
     return per_view * len(w["cams"]) + color + (1 if w["adam"] else 0)  # Adam (fused step bump)

@@ -222,6 +222,22 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: set it once per
+// (kernel, device) -- a process may drive several GPUs.  Each call site owns its flags.
+struct SmemAttrOnce {
+    bool done[64] = {};
+    template <typename... KArgs>
+    cudaError_t ensure(void (*kernel)(KArgs...), size_t bytes) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+        return e;
+    }
+};
 }  // namespace bsr
 
 #define BSR_CUDA_TRY(expr)                                      \

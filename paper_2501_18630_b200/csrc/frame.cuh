@@ -14,6 +14,7 @@ inline int sort_items(int64_t cap) { return cap <= kSmallSortCap ? 4 : 16; }
 constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
 constexpr int kRec64 = 8;                            // doubles per fp64 side record
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
+constexpr int kGrad64 = 6;                           // fp64 geometry accumulator doubles/primitive (5 used)
 // primitives whose fp32 r2 error bound exceeds this are evaluated in fp64 by the raster
 #ifndef BSR_UNSAFE_R2_ERR
 #define BSR_UNSAFE_R2_ERR 2.0e-5f
@@ -58,7 +59,13 @@ struct FrameView {
     float4 *needle;          // [N] needle words of records with c.w < 0 (raster.cuh), NaN: fp64 path
     uint32_t *vis_hint;      // visible count of the previous forward on this frame (a
                              // scheduling hint for preprocess only: any value is safe)
-    float *grad_acc;         // [N][12] raster gradient accumulators by source index (zeroed by backward)
+    float *grad_acc;         // [N][12] raster gradient accumulators by source index (zeroed by backward):
+                             // [0..4] geometry partials in the record's whitened frame (u, w) =
+                             // L^T (px - mean), Q = L L^T:  sum d_x (u, w, u^2, u w, w^2)
+                             // (d_x = dL/dr2), [5] d opacity, [6] d beta, [7..9] d rgb, [10] d z
+    double *grad64;          // [N][kGrad64] fp64 accumulators of the geometry partials (d mean2d x2,
+                             // d conic x3) of fp32-unsafe records (Record.c.w < 0): zeroed by
+                             // preprocess for those records, consumed and re-zeroed by preprocess_bwd
     // --- sizes ---
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles;
@@ -113,8 +120,23 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.replay_state = (double *)take(8ull * 6 * npx);
     f.grad_acc = (float *)take(4ull * kGradStride * n);
     f.needle = (float4 *)take(16ull * n);
+    f.grad64 = (double *)take(8ull * kGrad64 * n);
     f.total_bytes = align_up(off, 256);
     return f;
+}
+
+// fp64 geometry partials of an fp32-unsafe record (raster_bwd / replay_bwd): ill-conditioned
+// footprints (needles) carry gradients that are cancellation-heavy sums over many pixels
+// (d conic along the short axis is ~kappa times smaller than its xy components), so their
+// geometry partials are formed from the fp64 mean / conic and summed in fp64.
+__device__ __forceinline__ void add_geom64(double *g, double d_x, double dx, double dy, double ca, double cb,
+                                           double cc) {
+    const double ga = ca * dx + cb * dy, gb = cb * dx + cc * dy;
+    atomicAdd(g + 0, -2.0 * d_x * ga);
+    atomicAdd(g + 1, -2.0 * d_x * gb);
+    atomicAdd(g + 2, d_x * dx * dx);
+    atomicAdd(g + 3, 2.0 * d_x * dx * dy);
+    atomicAdd(g + 4, d_x * dy * dy);
 }
 
 }  // namespace bsr

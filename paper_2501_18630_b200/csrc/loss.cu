@@ -415,14 +415,9 @@ extern "C" int bsr_loss_l1_dssim(const float *rendered, const float *target, con
     }
     for (int i = 0; i < 11; ++i) p.w[i] = (float)(w[i] / sum);
     dim3 grid((unsigned)div_up(width, kTW), (unsigned)div_up(height, kTH));
-    static bool attr = false;
-    if (!attr) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(ssim_maps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(MapsSmem)));
-        BSR_CUDA_TRY(cudaFuncSetAttribute(ssim_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(GradSmem)));
-        attr = true;
-    }
+    static SmemAttrOnce attr_maps, attr_grad;
+    BSR_CUDA_TRY(attr_maps.ensure(ssim_maps_kernel, sizeof(MapsSmem)));
+    BSR_CUDA_TRY(attr_grad.ensure(ssim_grad_kernel, sizeof(GradSmem)));
     BSR_CUDA_TRY((pdl_launch(ssim_maps_kernel, dim3(grid), dim3(256), sizeof(MapsSmem), st, p)));
     BSR_CUDA_TRY((pdl_launch(ssim_grad_kernel, dim3(grid), dim3(256), sizeof(GradSmem), st, p)));
     BSR_LAUNCH_CHECK();

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
     float *app_c = app_b + kPreThreads * 3 * Tr::M;           // SB lobe colours
     __shared__ __align__(8) uint64_t s_bar[2];  // geometry, appearance
     __shared__ int s_bulk;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int64_t n = args.sc.n;
     const bsr_scene &sc = args.sc;
     const int64_t part = blockIdx.x;
@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
                 }
             }
             f.needle[i] = nw;
+            double2 *g64 = reinterpret_cast<double2 *>(f.grad64 + kGrad64 * (int64_t)i);
+            g64[0] = g64[1] = g64[2] = make_double2(0.0, 0.0);
         }
         r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
         m64[0] = p.mx;
@@ -318,12 +320,8 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
 template <int CM, int NT>
 static int launch_pre_k(const PreArgs &a, cudaStream_t st) {
     const size_t smem = sizeof(PreSmem<CM, NT>);
-    static bool attr = false;
-    if (!attr) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(preprocess_fwd_kernel<CM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    BSR_CUDA_TRY(attr.ensure(preprocess_fwd_kernel<CM, NT>, smem));
     const unsigned blocks = (unsigned)div_up(a.sc.n, NT);
     BSR_CUDA_TRY((pdl_launch(preprocess_fwd_kernel<CM, NT>, dim3(blocks), dim3(NT), smem, st, a)));
     return BSR_OK;

@@ -167,14 +167,138 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
     }
 }
 
+// Geometric chain of one primitive (primitive.py:302-367, project_backward +
+// _rotation_grad_to_quat), in fp64: from d mean2d and the symmetric d cov2d (already mapped
+// from the raster's conic partials) to the position / log-scale / rotation gradients.
+// Adds the log-scale and rotation gradients and returns d position (without the
+// view-direction part).  fp64 because the 3D covariance chain of an anisotropic primitive
+// cancels: a small-axis scale gradient is a ~kappa times smaller projection of xy-frame terms.
+template <typename T>
+__device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx, T dmy, T gm00, T gs01, T gm11,
+                                           float dz, float &dpx_out, float &dpy_out, float &dpz_out) {
+    const bsr_scene &sc = a.sc;
+    const KCam &cam = a.cam;
+    const T px = sc.positions[3 * i], py = sc.positions[3 * i + 1], pz = sc.positions[3 * i + 2];
+    T R[9];
+    for (int k = 0; k < 9; ++k) R[k] = (T)cam.R[k];
+    const T tx = R[0] * px + R[1] * py + R[2] * pz + (T)cam.t[0];
+    const T ty = R[3] * px + R[4] * py + R[5] * pz + (T)cam.t[1];
+    const T tz = R[6] * px + R[7] * py + R[8] * pz + (T)cam.t[2];
+    const T fx = (T)cam.fx, fy = (T)cam.fy;
+    const bool rot16 = ((reinterpret_cast<uintptr_t>(sc.rotations) | reinterpret_cast<uintptr_t>(a.g.rotations)) & 15) == 0;
+    float4 q4;
+    if (rot16) {
+        q4 = __ldg(reinterpret_cast<const float4 *>(sc.rotations) + i);
+    } else {
+        q4 = make_float4(sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2], sc.rotations[4 * i + 3]);
+    }
+    T qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
+    const T qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= qn;
+    qx /= qn;
+    qy /= qn;
+    qz /= qn;
+    const T one = 1, two = 2;
+    T Q[9] = {one - two * (qy * qy + qz * qz), two * (qx * qy - qw * qz), two * (qx * qz + qw * qy),
+              two * (qx * qy + qw * qz), one - two * (qx * qx + qz * qz), two * (qy * qz - qw * qx),
+              two * (qx * qz - qw * qy), two * (qy * qz + qw * qx), one - two * (qx * qx + qy * qy)};
+    T s2[3];
+    for (int k = 0; k < 3; ++k) {
+        const T s = exp((T)sc.log_scales[3 * i + k]);
+        s2[k] = s * s;
+    }
+    T Sig[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col)
+            Sig[3 * r + col] = Q[3 * r] * s2[0] * Q[3 * col] + Q[3 * r + 1] * s2[1] * Q[3 * col + 1] +
+                               Q[3 * r + 2] * s2[2] * Q[3 * col + 2];
+    const T itz = one / tz, itz2 = itz * itz;
+    const T J00 = fx * itz, J02 = -fx * tx * itz2, J11 = fy * itz, J12 = -fy * ty * itz2;
+    T Am[6];
+    for (int j = 0; j < 3; ++j) {
+        Am[j] = J00 * R[j] + J02 * R[6 + j];
+        Am[3 + j] = J11 * R[3 + j] + J12 * R[6 + j];
+    }
+    const T Gm[4] = {gm00, gs01, gs01, gm11};
+    // g_sigma = A^T g_m A (3x3)
+    T gS[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col) {
+            T v = 0;
+            for (int u = 0; u < 2; ++u)
+                for (int w = 0; w < 2; ++w) v += Am[3 * u + r] * Gm[2 * u + w] * Am[3 * w + col];
+            gS[3 * r + col] = v;
+        }
+    // g_a = 2 g_m A Sigma (2x3); g_jac = g_a R^T
+    T gA[6];
+    for (int u = 0; u < 2; ++u)
+        for (int j = 0; j < 3; ++j) {
+            T v = 0;
+            for (int w = 0; w < 2; ++w)
+                for (int k = 0; k < 3; ++k) v += Gm[2 * u + w] * Am[3 * w + k] * Sig[3 * k + j];
+            gA[3 * u + j] = two * v;
+        }
+    T gJ[6];
+    for (int u = 0; u < 2; ++u)
+        for (int j = 0; j < 3; ++j)
+            gJ[3 * u + j] = gA[3 * u] * R[3 * j] + gA[3 * u + 1] * R[3 * j + 1] + gA[3 * u + 2] * R[3 * j + 2];
+    // g_t = J^T d_mean + dJ/dt terms (primitive.py:328-337)
+    T gt0 = J00 * dmx, gt1 = J11 * dmy, gt2 = J02 * dmx + J12 * dmy;
+    gt0 += gJ[2] * (-fx * itz2);
+    gt1 += gJ[5] * (-fy * itz2);
+    gt2 += gJ[0] * (-fx * itz2) + gJ[2] * (two * fx * tx * itz2 * itz) + gJ[4] * (-fy * itz2) +
+           gJ[5] * (two * fy * ty * itz2 * itz);
+    gt2 += (T)dz;  // depth extension: z = t_z
+    dpx_out = (float)(gt0 * R[0] + gt1 * R[3] + gt2 * R[6]);
+    dpy_out = (float)(gt0 * R[1] + gt1 * R[4] + gt2 * R[7]);
+    dpz_out = (float)(gt0 * R[2] + gt1 * R[5] + gt2 * R[8]);
+    // Sigma = Q diag(s^2) Q^T: g_rot = 2 gS Q diag(s^2); g_d_i = (Q^T gS Q)_ii
+    T gR[9];
+    for (int r = 0; r < 3; ++r)
+        for (int col = 0; col < 3; ++col)
+            gR[3 * r + col] = two * (gS[3 * r] * Q[col] + gS[3 * r + 1] * Q[3 + col] + gS[3 * r + 2] * Q[6 + col]) * s2[col];
+    for (int k = 0; k < 3; ++k) {
+        T v = 0;
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) v += Q[3 * j + k] * gS[3 * j + l] * Q[3 * l + k];
+        a.g.log_scales[3 * i + k] += (float)(v * two * s2[k]);
+    }
+    // _rotation_grad_to_quat (primitive.py:348-367)
+    {
+        const T w = qw, x = qx, y = qy, z = qz;
+        const T *g = gR;
+        const T gw = two * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
+        const T gx = two * (y * g[1] + z * g[2] + y * g[3] - two * x * g[4] - w * g[5] + z * g[6] + w * g[7] - two * x * g[8]);
+        const T gy = two * (-two * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - two * y * g[8]);
+        const T gz = two * (-two * z * g[0] - w * g[1] + x * g[2] + w * g[3] - two * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
+        const T dot = gw * w + gx * x + gy * y + gz * z;
+        const T iqn = one / qn;
+        const float r0 = (float)((gw - dot * w) * iqn), r1 = (float)((gx - dot * x) * iqn);
+        const float r2 = (float)((gy - dot * y) * iqn), r3 = (float)((gz - dot * z) * iqn);
+        if (rot16) {
+            float4 *gr = reinterpret_cast<float4 *>(a.g.rotations) + i;
+            float4 gq = *gr;
+            gq.x += r0;
+            gq.y += r1;
+            gq.z += r2;
+            gq.w += r3;
+            *gr = gq;
+        } else {
+            a.g.rotations[4 * i] += r0;
+            a.g.rotations[4 * i + 1] += r1;
+            a.g.rotations[4 * i + 2] += r2;
+            a.g.rotations[4 * i + 3] += r3;
+        }
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
     const float *acc = a.f.grad_acc + (int64_t)c * kGradStride;
-    const float4 g0 = *reinterpret_cast<const float4 *>(acc);
     const float4 g1 = *reinterpret_cast<const float4 *>(acc + 4);
     const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
-    const float dmx = g0.x, dmy = g0.y, dA = g0.z, dB = g0.w, dC = g1.x, d_o = g1.y, d_beta = g1.z;
-    const float dr = g1.w, dg = g2.x, dbl = g2.y, dz = g2.z;
+    const float d_o = g1.y, d_beta = g1.z;
+    const float dr = g1.w, dg = g2.x, dbl = g2.y;
     const int64_t i = c;
     const bsr_scene &sc = a.sc;
     const KCam &cam = a.cam;
@@ -187,133 +311,9 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
     const float beta = 4.f * expf(fminf(fmaxf(bsh, -10.f), 10.f));
     if (fabsf(bsh) <= 10.f) a.g.shapes[i] += d_beta * beta;
 
-    // ---- recompute projection (fp32)
+    // ---- the geometric chain runs in fp64 in prebwd_geom_kernel (after this kernel)
+    float dpx = 0.f, dpy = 0.f, dpz = 0.f;
     const float px = sc.positions[3 * i], py = sc.positions[3 * i + 1], pz = sc.positions[3 * i + 2];
-    float R[9];
-    for (int k = 0; k < 9; ++k) R[k] = (float)cam.R[k];
-    const float tx = R[0] * px + R[1] * py + R[2] * pz + (float)cam.t[0];
-    const float ty = R[3] * px + R[4] * py + R[5] * pz + (float)cam.t[1];
-    const float tz = R[6] * px + R[7] * py + R[8] * pz + (float)cam.t[2];
-    const float fx = (float)cam.fx, fy = (float)cam.fy;
-    const bool rot16 = ((reinterpret_cast<uintptr_t>(sc.rotations) | reinterpret_cast<uintptr_t>(a.g.rotations)) & 15) == 0;
-    float4 q4;
-    if (rot16) {
-        q4 = __ldg(reinterpret_cast<const float4 *>(sc.rotations) + i);
-    } else {
-        q4 = make_float4(sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2], sc.rotations[4 * i + 3]);
-    }
-    float qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
-    const float qn = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-    qw /= qn;
-    qx /= qn;
-    qy /= qn;
-    qz /= qn;
-    float Q[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
-                  2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
-                  2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
-    float s2[3];
-    for (int k = 0; k < 3; ++k) {
-        const float s = expf(sc.log_scales[3 * i + k]);
-        s2[k] = s * s;
-    }
-    float Sig[9];
-    for (int r = 0; r < 3; ++r)
-        for (int col = 0; col < 3; ++col)
-            Sig[3 * r + col] = Q[3 * r] * s2[0] * Q[3 * col] + Q[3 * r + 1] * s2[1] * Q[3 * col + 1] +
-                               Q[3 * r + 2] * s2[2] * Q[3 * col + 2];
-    const float itz = 1.f / tz, itz2 = itz * itz;
-    const float J00 = fx * itz, J02 = -fx * tx * itz2, J11 = fy * itz, J12 = -fy * ty * itz2;
-    float Am[6];
-    for (int j = 0; j < 3; ++j) {
-        Am[j] = J00 * R[j] + J02 * R[6 + j];
-        Am[3 + j] = J11 * R[3 + j] + J12 * R[6 + j];
-    }
-    float AS[6];
-    for (int r = 0; r < 2; ++r)
-        for (int j = 0; j < 3; ++j)
-            AS[3 * r + j] = Am[3 * r] * Sig[j] + Am[3 * r + 1] * Sig[3 + j] + Am[3 * r + 2] * Sig[6 + j];
-    const float c00 = AS[0] * Am[0] + AS[1] * Am[1] + AS[2] * Am[2] + 0.3f;
-    const float c01 = AS[0] * Am[3] + AS[1] * Am[4] + AS[2] * Am[5];
-    const float c11 = AS[3] * Am[3] + AS[4] * Am[4] + AS[5] * Am[5] + 0.3f;
-    const float idet = 1.f / (c00 * c11 - c01 * c01);
-    const float ia = c11 * idet, ib = -c01 * idet, ic = c00 * idet;
-    // d cov2d = -Inv G Inv, G = [[dA, dB/2], [dB/2, dC]]
-    const float Gb = 0.5f * dB;
-    const float m00 = dA * ia + Gb * ib, m01 = dA * ib + Gb * ic;  // G Inv
-    const float m10 = Gb * ia + dC * ib, m11 = Gb * ib + dC * ic;
-    const float gm00 = -(ia * m00 + ib * m10), gm01 = -(ia * m01 + ib * m11);
-    const float gm10 = -(ib * m00 + ic * m10), gm11 = -(ib * m01 + ic * m11);
-    // symmetrise (project_backward g_m = (d + d^T)/2)
-    const float gs01 = 0.5f * (gm01 + gm10);
-    const float Gm[4] = {gm00, gs01, gs01, gm11};
-    // g_sigma = A^T g_m A (3x3)
-    float gS[9];
-    for (int r = 0; r < 3; ++r)
-        for (int col = 0; col < 3; ++col) {
-            float v = 0.f;
-            for (int u = 0; u < 2; ++u)
-                for (int w = 0; w < 2; ++w) v += Am[3 * u + r] * Gm[2 * u + w] * Am[3 * w + col];
-            gS[3 * r + col] = v;
-        }
-    // g_a = 2 g_m A Sigma (2x3); g_jac = g_a R^T
-    float gA[6];
-    for (int u = 0; u < 2; ++u)
-        for (int j = 0; j < 3; ++j) {
-            float v = 0.f;
-            for (int w = 0; w < 2; ++w)
-                for (int k = 0; k < 3; ++k) v += Gm[2 * u + w] * Am[3 * w + k] * Sig[3 * k + j];
-            gA[3 * u + j] = 2.f * v;
-        }
-    float gJ[6];
-    for (int u = 0; u < 2; ++u)
-        for (int j = 0; j < 3; ++j)
-            gJ[3 * u + j] = gA[3 * u] * R[3 * j] + gA[3 * u + 1] * R[3 * j + 1] + gA[3 * u + 2] * R[3 * j + 2];
-    // g_t = J^T d_mean + dJ/dt terms (primitive.py:328-337)
-    float gt0 = J00 * dmx, gt1 = J11 * dmy, gt2 = J02 * dmx + J12 * dmy;
-    gt0 += gJ[2] * (-fx * itz2);
-    gt1 += gJ[5] * (-fy * itz2);
-    gt2 += gJ[0] * (-fx * itz2) + gJ[2] * (2.f * fx * tx * itz2 * itz) + gJ[4] * (-fy * itz2) +
-           gJ[5] * (2.f * fy * ty * itz2 * itz);
-    gt2 += dz;  // depth extension: z = t_z
-    float dpx = gt0 * R[0] + gt1 * R[3] + gt2 * R[6];
-    float dpy = gt0 * R[1] + gt1 * R[4] + gt2 * R[7];
-    float dpz = gt0 * R[2] + gt1 * R[5] + gt2 * R[8];
-    // Sigma = Q diag(s^2) Q^T: g_rot = 2 gS Q diag(s^2); g_d_i = (Q^T gS Q)_ii
-    float gR[9];
-    for (int r = 0; r < 3; ++r)
-        for (int col = 0; col < 3; ++col)
-            gR[3 * r + col] = 2.f * (gS[3 * r] * Q[col] + gS[3 * r + 1] * Q[3 + col] + gS[3 * r + 2] * Q[6 + col]) * s2[col];
-    for (int k = 0; k < 3; ++k) {
-        float v = 0.f;
-        for (int j = 0; j < 3; ++j)
-            for (int l = 0; l < 3; ++l) v += Q[3 * j + k] * gS[3 * j + l] * Q[3 * l + k];
-        a.g.log_scales[3 * i + k] += v * 2.f * s2[k];
-    }
-    // _rotation_grad_to_quat (primitive.py:348-367)
-    {
-        const float w = qw, x = qx, y = qy, z = qz;
-        const float *g = gR;
-        const float gw = 2.f * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
-        const float gx = 2.f * (y * g[1] + z * g[2] + y * g[3] - 2.f * x * g[4] - w * g[5] + z * g[6] + w * g[7] - 2.f * x * g[8]);
-        const float gy = 2.f * (-2.f * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - 2.f * y * g[8]);
-        const float gz = 2.f * (-2.f * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2.f * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
-        const float dot = gw * w + gx * x + gy * y + gz * z;
-        const float iqn = 1.f / qn;
-        if (rot16) {
-            float4 *gr = reinterpret_cast<float4 *>(a.g.rotations) + i;
-            float4 gq = *gr;
-            gq.x += (gw - dot * w) * iqn;
-            gq.y += (gx - dot * x) * iqn;
-            gq.z += (gy - dot * y) * iqn;
-            gq.w += (gz - dot * z) * iqn;
-            *gr = gq;
-        } else {
-            a.g.rotations[4 * i] += (gw - dot * w) * iqn;
-            a.g.rotations[4 * i + 1] += (gx - dot * x) * iqn;
-            a.g.rotations[4 * i + 2] += (gy - dot * y) * iqn;
-            a.g.rotations[4 * i + 3] += (gz - dot * z) * iqn;
-        }
-    }
     // ---- colour chain (SH or Spherical Beta) + view direction -> position; deferred for
     //      multi-view steps (bsr_color_grad_views applies every view's chain at once)
     if (a.drgb) {
@@ -332,10 +332,11 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
         dpy += (ddy - dd * vy) * ivn;
         dpz += (ddz - dd * vz) * ivn;
     }
-    a.g.positions[3 * i] += dpx;
-    a.g.positions[3 * i + 1] += dpy;
-    a.g.positions[3 * i + 2] += dpz;
-    if (a.screen_grad_norm) a.screen_grad_norm[i] = sqrtf(dmx * dmx + dmy * dmy);
+    if (!a.drgb) {
+        a.g.positions[3 * i] += dpx;
+        a.g.positions[3 * i + 1] += dpy;
+        a.g.positions[3 * i + 2] += dpz;
+    }
 }
 
 // Each warp takes 64 consecutive source indices and runs the visible ones densely (32
@@ -346,7 +347,7 @@ constexpr int kPreBwdChunk = 64;
 constexpr int kPreBwdThreads = 128;
 
 template <int K>
-__global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(PreBwdArgs a) {
+__global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_constant__ const PreBwdArgs a) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t c0 = ((blockIdx.x * (int64_t)kPreBwdThreads + threadIdx.x) >> 5) * kPreBwdChunk;
@@ -375,6 +376,79 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(PreBwdAr
     }
 }
 
+// Geometric chain of every visible primitive, fp64 (geom_chain): the raster's geometry
+// partials are mapped to d mean2d / d cov2d with the record's factor L (whitened frame,
+// frame.cuh grad_acc):  d mean = -2 L M,  d cov2d = -Q G Q = -L H L^T  (Q = L L^T,
+// G = L^-T H L^-1 the conic gradient, rasterizer.py:302-312), so no inverse of the
+// ill-conditioned conic is formed.  fp32-unsafe records (Record.c.w < 0) carry xy-frame
+// conic partials summed in fp64 (grad64, cleared here) and use the fp64 conic.
+__device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) {
+    const FrameView &f = a.f;
+    const Record &r = f.rec[i];
+    const float4 ra = r.a, rb = r.b;
+    const float cw = r.c.w;
+    double dmx, dmy, gm00, gs01, gm11;
+    if (cw < 0.f) {
+        double2 *g2 = reinterpret_cast<double2 *>(f.grad64 + kGrad64 * i);
+        const double2 u0 = g2[0], u1 = g2[1], u2 = g2[2];
+        g2[0] = g2[1] = g2[2] = make_double2(0.0, 0.0);
+        const double *m64 = f.rec64 + kRec64 * i;
+        const double ia = m64[2], ib = m64[3], ic = m64[4];
+        const double dA = u1.x, Gb = 0.5 * u1.y, dC = u2.x;
+        dmx = u0.x;
+        dmy = u0.y;
+        const double m00 = dA * ia + Gb * ib, m01 = dA * ib + Gb * ic;  // G Q
+        const double m10 = Gb * ia + dC * ib, m11 = Gb * ib + dC * ic;
+        gm00 = -(ia * m00 + ib * m10);
+        gs01 = -0.5 * ((ia * m01 + ib * m11) + (ib * m00 + ic * m10));
+        gm11 = -(ib * m01 + ic * m11);
+    } else {
+        const float *acc = f.grad_acc + i * kGradStride;
+        const float4 g0 = *reinterpret_cast<const float4 *>(acc);
+        const double mu = g0.x, mw = g0.y, h00 = g0.z, h01 = g0.w, h11 = acc[4];
+        const double l11 = ra.z, l21 = ra.w, l22 = rb.x;
+        dmx = -2.0 * l11 * mu;
+        dmy = -2.0 * (l21 * mu + l22 * mw);
+        gm00 = -(l11 * l11 * h00);
+        gs01 = -(l11 * (h00 * l21 + h01 * l22));
+        gm11 = -((l21 * h00 + l22 * h01) * l21 + (l21 * h01 + l22 * h11) * l22);
+    }
+    const float dz = f.grad_acc[i * kGradStride + 10];
+    float dpx, dpy, dpz;
+    geom_chain<double>(a, i, dmx, dmy, gm00, gs01, gm11, dz, dpx, dpy, dpz);
+    a.g.positions[3 * i] += dpx;
+    a.g.positions[3 * i + 1] += dpy;
+    a.g.positions[3 * i + 2] += dpz;
+    if (a.screen_grad_norm) a.screen_grad_norm[i] = (float)sqrt(dmx * dmx + dmy * dmy);
+}
+
+__global__ void __launch_bounds__(kPreBwdThreads) prebwd_geom_kernel(__grid_constant__ const PreBwdArgs a) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = ((blockIdx.x * (int64_t)kPreBwdThreads + threadIdx.x) >> 5) * kPreBwdChunk;
+    if (c0 >= a.f.n) return;
+    uint32_t m[kPreBwdChunk / 32];
+    int tot = 0;
+#pragma unroll
+    for (int q = 0; q < kPreBwdChunk / 32; ++q) {
+        const int64_t c = c0 + 32 * q + lane;
+        m[q] = __ballot_sync(0xffffffffu, c < a.f.n && a.f.tile_count[c] != 0);
+        tot += __popc(m[q]);
+    }
+    for (int base = 0; base < tot; base += 32) {
+        int r = base + lane;
+        if (r >= tot) break;
+        int q = 0;
+#pragma unroll
+        for (int k = 0; k < kPreBwdChunk / 32 - 1; ++k)
+            if (q == k && r >= __popc(m[k])) {
+                r -= __popc(m[k]);
+                q = k + 1;
+            }
+        prebwd_geom_one(a, c0 + 32 * q + (int)__fns(m[q], 0, r + 1));
+    }
+}
+
 int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView &f,
                           const bsr_grads &g, float *screen_grad_norm, float4 *drgb, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
@@ -383,6 +457,7 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
 #define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
+    BSR_CUDA_TRY((pdl_launch(prebwd_geom_kernel, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -533,12 +608,8 @@ int launch_color_views(const bsr_scene &sc, const bsr_grads &g, const float4 *dr
         const unsigned blocks = (unsigned)div_up(sc.n, kCvThreads);
 #define BSR_CV_LAUNCH(K)                                                                                     \
     do {                                                                                                     \
-        static bool attr = false;                                                                            \
-        if (!attr) {                                                                                         \
-            BSR_CUDA_TRY(cudaFuncSetAttribute(color_views_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                              (int)color_views_smem<K>()));                                  \
-            attr = true;                                                                                     \
-        }                                                                                                    \
+        static SmemAttrOnce attr;                                                                            \
+        BSR_CUDA_TRY(attr.ensure(color_views_kernel<K>, color_views_smem<K>()));                             \
         BSR_CUDA_TRY((pdl_launch(color_views_kernel<K>, dim3(blocks), dim3(kCvThreads), color_views_smem<K>(), st, a))); \
     } while (0)
         switch (sc.sh_coeffs) {

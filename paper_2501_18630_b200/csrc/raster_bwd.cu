@@ -12,7 +12,7 @@
 //
 // Per batch each warp builds the compacted list of entries whose ellipse reaches its 8x4
 // block and that precede the warp's furthest last contributor, then walks it backwards.
-// Per pair the 11 partials (d mean2d x2, d conic x3, d opacity, d beta, d rgb x3, d z)
+// Per pair the 11 partials (geometry x5 in the whitened frame, d opacity, d beta, d rgb x3, d z)
 // are reduced across the warp with a 16-shuffle transpose reduction and added with one
 // warp-wide RED instruction per (warp, entry) into grad_acc[compact][12].
 #include <stdlib.h>
@@ -41,21 +41,19 @@ struct RasterBwdArgs {
     int direct_max;
 };
 
-// fp64 pair evaluation + the two conic-gradient terms for fp32-unsafe primitives; kept
-// out of line so the common fp32 path is not if-converted into predicated fp64 code.
-// Returned by value (no pointer arguments: those would force the caller's ga/gb into
-// local memory on the hot path).
-struct PairG {
-    Pair p;
-    float ga, gb;
-};
-__device__ __noinline__ PairG unsafe_pair_bwd(const double *m64, float4 B, int px, int py) {
-    const double dx = (double)px - m64[0], dy = (double)py - m64[1];
-    PairG r;
-    r.ga = (float)(m64[2] * dx + m64[3] * dy);
-    r.gb = (float)(m64[3] * dx + m64[4] * dy);
-    r.p = eval_pair64(m64, B, px, py);
-    return r;
+// fp64 pair evaluation for fp32-unsafe primitives; kept out of line so the common fp32
+// path is not if-converted into predicated fp64 code.
+__device__ __noinline__ Pair unsafe_pair_bwd(const double *m64, float4 B, int px, int py) {
+    return eval_pair64(m64, B, px, py);
+}
+
+// Geometry partials of an fp32-unsafe record in fp64 (frame.cuh add_geom64), out of line
+// like unsafe_pair_bwd: dx, dy from the fp64 side record, fp64 atomics into grad64.
+__device__ __noinline__ void unsafe_geom_bwd(double *grad64, const double *rec64, uint32_t c, float d_x, int px,
+                                             int py) {
+    const double *m64 = rec64 + kRec64 * (int64_t)c;
+    double *g = grad64 + (int64_t)kGrad64 * c;
+    add_geom64(g, (double)d_x, (double)px - m64[0], (double)py - m64[1], m64[2], m64[3], m64[4]);
 }
 
 // Transpose-reduce 16 values across the L lanes of a group (L = 32 / G): afterwards each
@@ -114,7 +112,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
-    const int q = SB::group(lane), k = lane % L;
+    const int q = SB::group(lane);
     const int px = wx0 + SB::px(lane), py = wy0 + SB::py(lane);
     const uint32_t *lists = a.lists ? a.lists : f.lists;
     const Record *rec = a.rec ? a.rec : f.rec;
@@ -182,31 +180,29 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         const int4 bd = s_rec[j].d;
         const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
         if (STATS) pairs += (act && e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-        float ga, gb;  // (a dx + b dy, b dx + c dy): fp64 for unsafe primitives
         Pair p;
         if (C.w < 0.f) {  // needle or fp64 primitive (uniform per entry)
             const float4 N = f.needle[s_cidx[j]];
-            if (N.x == N.x) {  // needle: compensated fp32 (same bits as the forward)
+            if (N.x == N.x)  // needle: compensated fp32 (same bits as the forward)
                 p = eval_needle(A, Bq, N, px - bd.x, py - bd.z);
-                ga = A.z * p.u;
-                gb = A.w * p.u + Bq.x * p.w;
-            } else {
-                const PairG u = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
-                p = u.p;
-                ga = u.ga;
-                gb = u.gb;
-            }
+            else
+                p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
         } else {
             p = eval_pair(A, Bq, px - bd.x, py - bd.z);
-            ga = A.z * p.u;                 // a dx + b dy = l11 u
-            gb = A.w * p.u + Bq.x * p.w;    // b dx + c dy = l21 u + l22 w
         }
         const bool took = act && e < last && p.alpha >= a.alpha_min;
         const unsigned tm = __ballot_sync(0xffffffffu, took);
         if (!tm) return;
         const float alpha = took ? p.alpha : 0.f;
         const float one_m = 1.0f - alpha;     // alpha <= 0.999 (forward flags larger)
-        T = took ? T * rcp_approx(one_m) : T;  // T_k
+        // T_k = T_{k+1} / (1 - alpha_k): rcp.approx plus one Newton step on the quotient, so the
+        // recovered transmittance is (nearly) correctly rounded and unbiased -- the front
+        // entries of a pixel recover T through every later entry, and a biased 1-ulp error per
+        // step would add up linearly over thousands of entries at config 4
+        const float rq = rcp_approx(one_m);
+        const float q0 = __fmul_rn(T, rq);
+        const float q1 = __fmaf_rn(__fmaf_rn(-q0, one_m, T), rq, q0);
+        T = took ? q1 : T;  // T_k
         const float w = alpha * T;
         float dalpha = T * (g0 * (C.x - B0) + g1 * (C.y - B1) + g2 * (C.z - B2) + gd * (Bq.w - BD));
         dalpha = took ? dalpha : 0.f;
@@ -221,11 +217,18 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         const float dk = dalpha * Bq.y;
         const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
         float v[16];
-        v[0] = -2.0f * d_x * ga;
-        v[1] = -2.0f * d_x * gb;
-        v[2] = d_x * p.dx * p.dx;
-        v[3] = 2.0f * d_x * p.dx * p.dy;
-        v[4] = d_x * p.dy * p.dy;
+        const bool geom64 = C.w < 0.f;  // fp32-unsafe record: geometry partials in fp64
+        if (geom64 && took) unsafe_geom_bwd(f.grad64, f.rec64, s_cidx[j], d_x, px, py);
+        // geometry partials in the record's whitened frame (frame.cuh grad_acc): the
+        // components of sum d_x (u, w)(u, w)^T do not cancel against each other the way the
+        // xy components of the conic gradient do for elongated footprints (preprocess_bwd
+        // maps them back: d mean = -2 L (.), d cov2d = -L (.) L^T, in fp64)
+        const float du = d_x * p.u, dw = d_x * p.w;
+        v[0] = geom64 ? 0.f : du;
+        v[1] = geom64 ? 0.f : dw;
+        v[2] = geom64 ? 0.f : du * p.u;
+        v[3] = geom64 ? 0.f : du * p.w;
+        v[4] = geom64 ? 0.f : dw * p.w;
         v[5] = dalpha * p.k;
         v[6] = dk * p.k * (0.69314718f * lg2_approx(om));
         v[7] = w * g0;
@@ -237,8 +240,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         int most = __popc(tm);
         if (GL < 32) {
             most = 0;
+            constexpr uint32_t gmask = GL >= 32 ? 0xffffffffu : ((1u << (GL & 31)) - 1u);
 #pragma unroll
-            for (int g = 0; g < 32 / GL; ++g) most = max(most, __popc(tm & (((1u << GL) - 1u) << (g * GL))));
+            for (int g = 0; g < 32 / GL; ++g) most = max(most, __popc(tm & (gmask << ((g * GL) & 31))));
         }
         if (most <= direct_max) {
             if (took) {

@@ -391,11 +391,17 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
                 double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
                 if (dkdx < -1e7) dkdx = -1e7;
                 const double d_x = d_kernel * dkdx;
-                atomicAdd(acc + 0, (float)(-d_x * 2.0 * (en.ca * dx + en.cb * dy)));
-                atomicAdd(acc + 1, (float)(-d_x * 2.0 * (en.cb * dx + en.cc * dy)));
-                atomicAdd(acc + 2, (float)(d_x * dx * dx));
-                atomicAdd(acc + 3, (float)(d_x * 2.0 * dx * dy));
-                atomicAdd(acc + 4, (float)(d_x * dy * dy));
+                if (f.rec[c].c.w < 0.f) {  // fp32-unsafe record: fp64 geometry accumulator
+                    add_geom64(f.grad64 + (int64_t)kGrad64 * c, d_x, dx, dy, en.ca, en.cb, en.cc);
+                } else {  // whitened frame of the record's factor (frame.cuh grad_acc)
+                    const Record &r = f.rec[c];
+                    const double u = (double)r.a.z * dx + (double)r.a.w * dy, w = (double)r.b.x * dy;
+                    atomicAdd(acc + 0, (float)(d_x * u));
+                    atomicAdd(acc + 1, (float)(d_x * w));
+                    atomicAdd(acc + 2, (float)(d_x * u * u));
+                    atomicAdd(acc + 3, (float)(d_x * u * w));
+                    atomicAdd(acc + 4, (float)(d_x * w * w));
+                }
             }
         }
         __syncthreads();

@@ -222,13 +222,9 @@ size_t sort_smem_bytes() {
 
 template <typename K, int ITEMS>
 static int launch_passes(const SortArgs<K> &a, int64_t cap, cudaStream_t st) {
-    static bool attr_set = false;  // idempotent attribute, safe to race
+    static SmemAttrOnce attr;
     const size_t smem = sort_smem_bytes<K, ITEMS>();
-    if (!attr_set) {
-        BSR_CUDA_TRY(cudaFuncSetAttribute(sort_pass_kernel<K, ITEMS>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
+    BSR_CUDA_TRY(attr.ensure(sort_pass_kernel<K, ITEMS>, smem));
     const unsigned parts = (unsigned)div_up(cap, BSR_BLOCK * ITEMS);
     for (int p = 0; p < a.passes; ++p) sort_pass_kernel<K, ITEMS><<<parts, BSR_BLOCK, smem, st>>>(a, p);
     return BSR_OK;

@@ -47,6 +47,14 @@ class DeviceRNG:
         self.offset += int(k)
         return o
 
+    def domain(self, name: str, size: int = 1 << 40) -> int:
+        """Base offset of a named counter range reserved once per stream (e.g. the
+        step-keyed noise of train(), whose counters must never meet the MCMC draws')."""
+        doms = self.__dict__.setdefault("_domains", {})
+        if name not in doms:
+            doms[name] = self.advance(size)
+        return doms[name]
+
 
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -185,13 +193,15 @@ def grow(prims: PrimitiveSet, budget: int, rng, adam_state=None, rate: float = G
     dev = prims.flat.device
     sources, counts = _sample(prims, dead_threshold, None, n_add, rng, "cannot grow: no live primitives")
     _, total = group_layout(n + n_add, prims.k, prims.lobes)
-    flat = torch.empty(total, dtype=torch.float32, device=dev)
+    # zeros, not empty: bsr_grow writes width * n floats per group and leaves the 16-byte
+    # alignment padding between groups alone; Adam runs over the whole flat range
+    flat = torch.zeros(total, dtype=torch.float32, device=dev)
     grown = PrimitiveSet.from_flat(n + n_add, prims.k, flat, prims.lobes)
     src_lc, dst_lc = prims.layout_c(), grown.layout_c()
     sm = sv = dm = dv = None
     if adam_state is not None:
         sm, sv = adam_state.exp_avg, adam_state.exp_avg_sq
-        dm, dv = torch.empty_like(flat), torch.empty_like(flat)
+        dm, dv = torch.zeros_like(flat), torch.zeros_like(flat)
     _lib.check(_lib.load().bsr_grow(
         prims.flat.data_ptr(), ctypes.byref(src_lc), _lib.ptr(sm), _lib.ptr(sv), flat.data_ptr(),
         ctypes.byref(dst_lc), _lib.ptr(dm), _lib.ptr(dv), sources.data_ptr(), n_add, counts.data_ptr(),

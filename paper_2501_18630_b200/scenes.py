@@ -4,13 +4,16 @@ No public dataset is named by BASELINE.json and the paper's scenes are not avail
 offline, so these generators stand in for them.  Every array is
 drawn in fp64 from ONE ``np.random.default_rng(seed)`` stream in a fixed order
 
-    means, log-scales, quaternions, opacity logits, SH DC, SH rest, [cameras]
+    means, log-scales, quaternions, opacity logits, SH DC, SH rest
 
 and rounded to fp32, so the GPU path and the fp64 oracle consume identical values.
 ``shapes`` are 0 (Beta exponent 4, the reference's "Gaussian-like" kernel, kernel.py:42-44).
 SH layout is (N, K, 3) with the DC row first (appearance.py:212-232).
 Cameras use the reference convention: horizontal fov, world up +y (toy.py:129-139);
 "upper hemisphere" = y > 0, rejecting y > 0.99 where ``from_lookat`` degenerates.
+Hemisphere cameras come from their own stream (``camera_rng(seed)``), so a workload's
+cameras do not depend on its primitive count: a reduced-size parity case, the bench's
+GPU arm and its CPU baseline all see the same views.
 """
 
 from __future__ import annotations
@@ -156,6 +159,11 @@ def hemisphere_eye(rng, radius):
             return radius * d
 
 
+def camera_rng(seed):
+    """The cameras' stream, independent of the scene arrays (and of N)."""
+    return np.random.default_rng([int(seed), 0x63616D])
+
+
 def scene_c0(seed=0, n=10_000):
     rng = np.random.default_rng(seed)
     pos = rng.uniform(-1.0, 1.0, (n, 3))
@@ -212,18 +220,21 @@ def make_workload(name: str, seed: int = 0, n: int | None = None, views: int | N
         cams = [Camera.from_lookat((0, 0, 4), (0, 0, 0), up, np.deg2rad(60.0), w, h)]
         return Workload(name, scene, cams, train=True, target_seed=seed + 1)
     if name == "c2":
-        scene, rng = scene_c2(seed, n or 1_000_000)
+        scene, _ = scene_c2(seed, n or 1_000_000)
+        rng = camera_rng(seed)
         w, h = width or 1920, height or 1080
         cams = [Camera.from_lookat(hemisphere_eye(rng, 8.0), (0, 0, 0), up, np.deg2rad(50.0), w, h)]
         return Workload(name, scene, cams)
     if name == "c3":
-        scene, rng = scene_c2(seed, n or 3_000_000)
+        scene, _ = scene_c2(seed, n or 3_000_000)
+        rng = camera_rng(seed)
         w, h = width or 1600, height or 1067
         cams = [Camera.from_lookat(hemisphere_eye(rng, 8.0), (0, 0, 0), up, np.deg2rad(50.0), w, h)
                 for _ in range(views or 32)]
         return Workload(name, scene, cams, train=True, target_seed=seed + 1)
     if name == "c4":
-        scene, rng = scene_c4(seed, n or 6_000_000)
+        scene, _ = scene_c4(seed, n or 6_000_000)
+        rng = camera_rng(seed)
         w, h = width or 3840, height or 2160
         cams = [Camera.from_lookat(hemisphere_eye(rng, 3.0), (0, 0, 0), up, np.deg2rad(70.0), w, h)]
         return Workload(name, scene, cams, train=True, target_seed=None)

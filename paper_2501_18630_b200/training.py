@@ -311,7 +311,9 @@ def inject_noise(prims: PrimitiveSet, cfg: TrainConfig, position_lr, rng, step_c
     eta = None
     seed = offset = 0
     if isinstance(rng, DeviceRNG):
-        seed, offset = rng.seed, rng.advance(1 << 32) if step_counter is None else 0
+        seed = rng.seed
+        # step-keyed draws live in their own reserved counter range (never the MCMC draws')
+        offset = rng.advance(1 << 32) if step_counter is None else rng.domain("noise")
     else:
         eta = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((n, 3)), dtype=np.float32)).to(
             prims.flat.device)

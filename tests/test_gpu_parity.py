@@ -283,11 +283,9 @@ def test_needles_match_oracle(cuda):
         _grad_close(getattr(grads, name).cpu().numpy()[k:], ref[name][k:], name)
 
 
-@pytest.mark.xfail(reason="up to ~10% relative error on some needle rotation / scale gradients; the same "
-                          "with the fp64 pair evaluation, an fp64 geometric chain or conic partials "
-                          "accumulated in the needle's own frame -- cause open, see DESIGN.md section 9",
-                   strict=False)
 def test_needle_gradients_strict(cuda):
+    """The needles' own gradients within 1e-3 (their geometry partials are summed in fp64
+    and their chain runs in fp64: DESIGN.md section 3, 'Gradients')."""
     grads, ref, k = _needle_grads(cuda)
     for name in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"):
         _grad_close(getattr(grads, name).cpu().numpy()[:k], ref[name][:k], name)
