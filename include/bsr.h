@@ -137,6 +137,14 @@ int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float ba
                 const bsr_profile *profile, void *stream);
 /* Synchronises `stream`, then reports counters / device-side errors of the last forward. */
 int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream);
+/* Asynchronous status (no sync): enqueues on `stream` a copy of the frame's counters into
+ * caller-owned host memory `snapshot` of bsr_frame_snapshot_bytes() bytes (pinned, so the
+ * copy is truly asynchronous); once the stream has passed that point (e.g. an event
+ * recorded after the call has completed) bsr_frame_snapshot_decode() reports what
+ * bsr_frame_status() would have.  Lets render_tiled skip the per-call stream sync. */
+int bsr_frame_snapshot_bytes(uint64_t *bytes);
+int bsr_frame_status_async(const void *frame, void *snapshot, void *stream);
+int bsr_frame_snapshot_decode(const void *snapshot, bsr_frame_info *info);
 /* d_color: (H,W,3) dL/d color (clamped image); d_depth: (H,W) or NULL. */
 int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                  void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,

@@ -94,6 +94,9 @@ EXPORTS = {
     "bsr_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
                               c_void_p, c_void_p]),
     "bsr_frame_status": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "bsr_frame_snapshot_bytes": (c_int32, [c_void_p]),
+    "bsr_frame_status_async": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "bsr_frame_snapshot_decode": (c_int32, [c_void_p, c_void_p]),
     "bsr_backward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "bsr_backward_deferred_color": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64,

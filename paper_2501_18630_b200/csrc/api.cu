@@ -289,6 +289,31 @@ extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *s
     return c.status;
 }
 
+extern "C" int bsr_frame_snapshot_bytes(uint64_t *bytes) {
+    if (!bytes) return BSR_ERR_BAD_ARG;
+    *bytes = sizeof(Counters);
+    return BSR_OK;
+}
+
+extern "C" int bsr_frame_status_async(const void *frame, void *snapshot, void *stream) {
+    if (!frame || !snapshot) return BSR_ERR_BAD_ARG;
+    BSR_CUDA_TRY(cudaMemcpyAsync(snapshot, frame, sizeof(Counters), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    return BSR_OK;
+}
+
+extern "C" int bsr_frame_snapshot_decode(const void *snapshot, bsr_frame_info *info) {
+    if (!snapshot || !info) return BSR_ERR_BAD_ARG;
+    Counters c;
+    memcpy(&c, snapshot, sizeof(Counters));
+    info->visible = c.visible;
+    info->entries = c.entries;
+    info->entries_needed = (int64_t)c.entries_needed;
+    info->flagged_pixels = c.flagged;
+    info->status = c.status;
+    info->reserved = 0;
+    return c.status;
+}
+
 static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                          void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
                          const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,

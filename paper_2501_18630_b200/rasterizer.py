@@ -35,12 +35,17 @@ ALPHA_MIN = 1.0 / 255.0  # rasterizer.py:28
 T_STOP = 1e-4  # rasterizer.py:29
 TILE_SIZE = 16  # rasterizer.py:30
 
-_ENTRY_CAP: dict = {}  # (n, W, H) -> last entry capacity that sufficed
+_ENTRY_CAP: dict = {}  # (n, W, H) -> entry capacity to allocate (last that sufficed, or a grown guess)
+_VERIFIED: set = set()  # shapes whose capacity was verified by a synchronous check
 
 
-@dataclass
+@dataclass(eq=False)
 class FrameState:
-    """Saved forward state in a device buffer owned by torch's caching allocator."""
+    """Saved forward state in a device buffer owned by torch's caching allocator.
+
+    ``pending`` holds an asynchronous status check (pinned counter snapshot + the event
+    after which it is valid) of a forward that was not synchronised; ``check()`` resolves
+    it (waiting for that event) and raises on a device-side error or capacity overflow."""
 
     buf: torch.Tensor
     nbytes: int
@@ -49,9 +54,62 @@ class FrameState:
     width: int
     height: int
     info: dict = field(default_factory=dict)
+    pending: tuple | None = None
 
     def ptr(self):
         return self.buf.data_ptr()
+
+    def ready(self) -> bool:
+        return self.pending is None or self.pending[1].query()
+
+    def check(self) -> dict:
+        """Resolve a pending asynchronous status (blocks until that forward finished)."""
+        if self.pending is not None:
+            snap, ev = self.pending
+            ev.synchronize()
+            self.pending = None
+            info = _lib.FrameInfoC()
+            st = _lib.load().bsr_frame_snapshot_decode(ctypes.c_void_p(snap.data_ptr()), ctypes.byref(info))
+            self.info = dict(visible=info.visible, entries=info.entries, entries_needed=info.entries_needed,
+                             flagged_pixels=info.flagged_pixels, status=info.status)
+            if st == _lib.BSR_ERR_CAPACITY:
+                key = (self.n, self.width, self.height)
+                _ENTRY_CAP[key] = int(min(2**31 - 1, info.entries_needed * 1.25 + 1024))
+                _VERIFIED.discard(key)  # the next call re-verifies synchronously
+                raise _lib.CapacityError(info.entries_needed)
+            _lib.check(st, "forward")
+        return self.info
+
+
+_SNAPSHOT_BYTES = None
+_PENDING: list = []  # frames with unresolved asynchronous status checks (oldest first)
+
+
+def _snapshot_bytes():
+    global _SNAPSHOT_BYTES
+    if _SNAPSHOT_BYTES is None:
+        out = ctypes.c_uint64()
+        _lib.check(_lib.load().bsr_frame_snapshot_bytes(ctypes.byref(out)), "snapshot")
+        _SNAPSHOT_BYTES = int(out.value)
+    return _SNAPSHOT_BYTES
+
+
+def _queue_status(frame: FrameState):
+    """Enqueue the frame's status copy into pinned memory (no sync) and remember it."""
+    snap = torch.empty(_snapshot_bytes(), dtype=torch.uint8, pin_memory=True)
+    _lib.check(_lib.load().bsr_frame_status_async(ctypes.c_void_p(frame.ptr()), ctypes.c_void_p(snap.data_ptr()),
+                                                  _stream()), "frame_status_async")
+    ev = torch.cuda.Event()
+    ev.record()
+    frame.pending = (snap, ev)
+    _PENDING.append(frame)
+
+
+def check_pending(block: bool = False):
+    """Resolve the asynchronous status checks of earlier un-synchronised forwards that have
+    completed (all of them with ``block``); raises the first error found."""
+    while _PENDING and (block or _PENDING[0].ready()):
+        _PENDING.pop(0).check()
 
 
 @dataclass
@@ -132,6 +190,10 @@ def new_frame(n, width, height, entry_cap, device=None) -> FrameState:
 
 
 def frame_status(frame: FrameState, raise_on_error=True) -> dict:
+    """Synchronous status of the frame's last forward (supersedes a pending async check)."""
+    frame.pending = None
+    if frame in _PENDING:
+        _PENDING.remove(frame)
     info = _lib.FrameInfoC()
     st = _lib.load().bsr_frame_status(ctypes.c_void_p(frame.ptr()), ctypes.byref(info), _stream())
     frame.info = dict(visible=info.visible, entries=info.entries, entries_needed=info.entries_needed,
@@ -151,31 +213,42 @@ def initial_entry_cap(n, width, height) -> int:
 
 
 def forward_raw(scene: _lib.SceneC, camera: Camera, background, outputs: _lib.OutputsC,
-                frame: FrameState | None = None, check: bool = True,
+                frame: FrameState | None = None, check: bool | str = True,
                 contrib: torch.Tensor | None = None, profile: _lib.ProfileC | None = None) -> FrameState:
     """Run bsr_forward; on capacity overflow grow the entry capacity and retry.
 
     ``contrib`` is the tensor behind ``outputs.contributions`` (accumulated by the
     kernels), cleared before a retry.  With ``check=False`` no host sync happens; call
-    frame_status() later (the bench hot loop does this after the timed region).
+    frame_status() later (the bench hot loop does this after the timed region).  With
+    ``check="async"`` a shape whose entry capacity is already known is not synchronised:
+    the status is copied asynchronously and resolved by check_pending() / frame.check()
+    (a fresh capacity guess is still verified synchronously once).
     """
     _lib.require_cuda()
     lib = _lib.load()
     cam = _lib.camera_c(camera)
     bg = _bg_arr(background)
     n, w, h = int(scene.n), int(camera.width), int(camera.height)
+    if check == "async" and (n, w, h) not in _VERIFIED:
+        check = True  # no verified capacity for this shape yet
     while True:
         if frame is None or frame.n != n or frame.width != w or frame.height != h:
             frame = new_frame(n, w, h, initial_entry_cap(n, w, h))
-            check = True  # a fresh capacity guess is always verified once
+            if check is not True and (n, w, h) not in _VERIFIED:
+                check = True  # a fresh capacity guess is always verified once
         rc = lib.bsr_forward(ctypes.byref(scene), ctypes.byref(cam), bg, ctypes.c_void_p(frame.ptr()),
                              frame.nbytes, frame.entry_cap, ctypes.byref(outputs),
                              None if profile is None else ctypes.byref(profile), _stream())
         _lib.check(rc, "bsr_forward")
+        if check == "async":
+            _queue_status(frame)
+            return frame
         if not check:
             return frame
         try:
             frame_status(frame)
+            _ENTRY_CAP.setdefault((n, w, h), frame.entry_cap)
+            _VERIFIED.add((n, w, h))  # this capacity is verified
             return frame
         except _lib.CapacityError as e:
             cap = int(min(2**31 - 1, e.needed * 1.25 + 1024))
@@ -245,10 +318,17 @@ def _check_core(core):
         raise ValueError(f"unknown backend {core!r} (this package provides only 'cuda')")
 
 
-def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, core=None) -> RenderOutput:
-    """rasterizer.py:194-211 on the B200."""
+def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, core=None,
+                 sync: bool = False) -> RenderOutput:
+    """rasterizer.py:194-211 on the B200.
+
+    Asynchronous like any torch op: once a (N, W, H) shape has a verified tile-entry
+    capacity the call does not synchronise the stream; its status (device-side errors,
+    capacity overflow) is copied asynchronously and raised by a later call
+    (check_pending) or by ``out.frame.check()``.  ``sync=True`` checks before returning."""
     _check_core(core)
     _lib.require_cuda()
+    check_pending()
     dev = prims.flat.device
     h, w = camera.height, camera.width
     color = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
@@ -264,7 +344,8 @@ def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, 
         return RenderOutput(torch.clamp_min(raw, 0.0), torch.zeros_like(alpha), contrib.long(), raw,
                             torch.ones_like(alpha), torch.zeros_like(alpha), torch.zeros_like(count), None)
     out = outputs_c(color, raw, alpha, trans, depth, count, contrib)
-    frame = forward_raw(_prims_scene_c(prims), camera, background, out, contrib=contrib)
+    frame = forward_raw(_prims_scene_c(prims), camera, background, out, contrib=contrib,
+                        check=True if sync else "async")
     return RenderOutput(color, alpha, contrib.long(), raw, trans, depth, count, frame)
 
 

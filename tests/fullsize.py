@@ -67,7 +67,7 @@ def compare_forward(out, ref, check_bins=True):
         nz = np.diff(off) > 0
         ok = ok and np.array_equal(dbg["ranges"][nz, 0], off[:-1][nz])
         rep["bins_equal"] = bool(ok)
-    rep["flagged_pixels"] = int(out.frame.info.get("flagged_pixels", -1)) if out.frame is not None else 0
+    rep["flagged_pixels"] = int(out.frame.check().get("flagged_pixels", -1)) if out.frame is not None else 0
     return rep
 
 

@@ -490,3 +490,114 @@ def test_entry_capacity_overflow_retries(cuda):
     rz._ENTRY_CAP[(300, 96, 64)] = 16  # far below the E this scene needs
     out, ref = _compare_forward(scene, cam, np.ones(3), cuda)
     assert out.frame.entry_cap >= ref["E"] > 16
+
+
+def test_render_masked_matches_oracle(cuda):
+    """rasterizer.py:214-227: render the primitives whose shape passes the predicate;
+    contributions stay aligned with the full set (oracle on the kept subset)."""
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import rasterizer as rz
+
+    rng = np.random.default_rng(90)
+    scene = random_scene(rng, 300, degree=2)
+    cam = toy_camera(80, 64)
+    bg = np.array([1.0, 0.5, 0.25])
+    pred = lambda b: b < np.float32(0.2)  # noqa: E731
+    out = rz.render_masked(_gpu_prims(scene), cam, bg, pred)
+    keep = np.nonzero(pred(scene.shapes))[0]
+    assert 0 < keep.size < 300
+    ref = orc.forward(scene.take(keep), cam, bg, core="c")
+    assert np.abs(out.color.cpu().numpy() - ref["color"]).max() <= IMG_TOL
+    full = np.zeros(300, np.int64)
+    full[keep] = ref["contributions"]
+    np.testing.assert_array_equal(out.contributions.cpu().numpy(), full)
+    nothing = rz.render_masked(_gpu_prims(scene), cam, bg, lambda b: np.zeros(b.shape, bool))
+    np.testing.assert_array_equal(nothing.color.cpu().numpy(), np.broadcast_to(bg.astype(np.float32), (64, 80, 3)))
+
+
+def test_rasterize_autograd_matches_render_backward_and_oracle(cuda):
+    """The torch.autograd entry (north star: PyTorch calling CUDA): gradients of
+    sum(color * up) + sum(depth * upd) w.r.t. every input tensor equal render_backward's
+    and the oracle's."""
+    import torch
+
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import rasterize
+
+    rng = np.random.default_rng(91)
+    scene = random_scene(rng, 200, degree=3)
+    cam = toy_camera(72, 56)
+    bg = np.array([0.3, 0.6, 0.9])
+    up = rng.standard_normal((56, 72, 3))
+    upd = rng.standard_normal((56, 72))
+    leaves = [torch.tensor(np.asarray(getattr(scene, k)), device="cuda", requires_grad=True)
+              for k in ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh")]
+    color, alpha, depth = rasterize(*leaves, cam, bg)
+    fwd = orc.forward(scene, cam, bg, core="c")
+    assert np.abs(color.detach().cpu().numpy() - fwd["color"]).max() <= IMG_TOL
+    assert np.abs(alpha.cpu().numpy() - fwd["alpha"]).max() <= IMG_TOL
+    loss = (color * torch.tensor(up, dtype=torch.float32, device="cuda")).sum() + \
+        (depth * torch.tensor(upd, dtype=torch.float32, device="cuda")).sum()
+    loss.backward()
+    ref = orc.backward(scene, cam, bg, up, fwd, core="c", d_depth=upd)
+    for name, t in zip(("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh"), leaves):
+        _grad_close(t.grad.cpu().numpy(), ref[name], name)
+
+
+def test_render_tiled_async_status(cuda):
+    """render_tiled does not synchronise once a shape's entry capacity is verified; a later
+    overflow (scene grew) is reported by the asynchronous status check, and the next call
+    re-verifies with a grown frame."""
+    from paper_2501_18630_b200 import _lib
+    from paper_2501_18630_b200 import rasterizer as rz
+
+    rng = np.random.default_rng(92)
+    scene = random_scene(rng, 500, degree=1)
+    cam = toy_camera(96, 80)
+    prims = _gpu_prims(scene)
+    a = rz.render_tiled(prims, cam, np.ones(3))  # first call: synchronous check
+    assert a.frame.pending is None
+    b = rz.render_tiled(prims, cam, np.ones(3))  # verified shape: asynchronous
+    assert b.frame.pending is not None
+    info = b.frame.check()
+    assert info["status"] == 0 and info["entries"] == a.frame.info["entries"]
+    np.testing.assert_array_equal(a.color.cpu().numpy(), b.color.cpu().numpy())
+    key = (500, 96, 80)
+    rz._ENTRY_CAP[key] = 8  # pretend the verified capacity became too small
+    c = rz.render_tiled(prims, cam, np.ones(3))
+    with pytest.raises(_lib.CapacityError):
+        rz.check_pending(block=True)
+    assert key not in rz._VERIFIED and rz._ENTRY_CAP[key] >= info["entries"]
+    d = rz.render_tiled(prims, cam, np.ones(3))  # re-verified synchronously, correct again
+    assert d.frame.pending is None
+    np.testing.assert_array_equal(a.color.cpu().numpy(), d.color.cpu().numpy())
+    del c
+
+
+def test_compat_drop_in_returns_reference_types(cuda):
+    """compat.render_tiled / render_backward / render_masked: numpy in (a Spherical-Beta
+    reference-layout set and an SH set), numpy fp64 / int64 out with the reference's
+    field names, values equal to the device path's and the oracle's."""
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import compat
+    from paper_2501_18630_b200.scenes import sb_random_scene
+
+    rng = np.random.default_rng(93)
+    cam = toy_camera(64, 48)
+    bg = np.ones(3)
+    for scene in (sb_random_scene(rng, 120).astype(np.float64), random_scene(rng, 120, degree=2)):
+        out = compat.render_tiled(scene, cam, bg)
+        assert out.color.dtype == np.float64 and out.contributions.dtype == np.int64
+        ref = orc.forward(scene, cam, bg, core="c")
+        np.testing.assert_array_equal(out.contributions, ref["contributions"])
+        assert np.abs(out.color - ref["color"]).max() <= IMG_TOL
+        assert np.abs(out.alpha - (1.0 - out.transmittance)).max() == 0.0
+        up = rng.standard_normal((48, 64, 3))
+        g = compat.render_backward(scene, cam, bg, up, forward_out=out)
+        g2 = compat.render_backward(scene, cam, bg, up)  # recomputes the forward
+        gref = orc.backward(scene, cam, bg, up, ref, core="c")
+        for name, arr in g.parameters().items():
+            _grad_close(arr, gref[name], name)
+            _grad_close(getattr(g2, name), gref[name], name)
+        m = compat.render_masked(scene, cam, bg, lambda b: b > 0)
+        assert m.contributions.shape == (120,)
