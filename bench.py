@@ -3,20 +3,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4]
     python bench.py --impl reference ...      (the reference's CPU implementation)
 
-Default workload (N=1): BASELINE config 1 -- one training step = forward render of
-N=100k SH-3 Gaussians at 800x800 + 0.8 L1 + 0.2 D-SSIM loss + backward + Adam, all on the
-device through libbsr.so.  With N>1 (torchrun, NCCL) every rank trains on its own view of
-the same scene (weak scaling: one 800x800 view per GPU per step) and the flat per-Gaussian
-gradient buffer is all-reduced before Adam.  --config c3 runs the 32-view batch of
-config 3 split across ranks (strong scaling), c2 the 1080p forward render, c4 the 4K
-stress forward + backward.
+Default workload at N=1: BASELINE config 4, the largest single-GPU config -- one step =
+forward render of N=6M SH-3 Gaussians at 3840x2160 + 0.8 L1 + 0.2 D-SSIM against the seed-1
+target set's render + the full backward, all on the device through libbsr.so; config 1
+(100k, 800x800, + Adam) is measured after it and nested under "secondary".  At N>1 the
+default is config 3: the 32-view batch (3M Gaussians, 1600x1067) split 32/N across ranks
+(one process per GPU, NCCL all-reduce of the flat gradient buffer, then Adam; strong
+scaling).  `--gpus N` without a torchrun environment relaunches itself under
+torch.distributed.run with N local ranks.  --config c1|c2|c3|c4 picks a workload.
 
-Timing: W warm-up steps, then K steps each timed with CUDA events on the launching
-stream (L2 flushed with a 256 MiB write between steps, outside the events), bracketed by
-barrier + synchronize, max over ranks.  Stage times / pair counts for the roofline come
-from libbsr's caller-owned events and device counters recorded inside the same timed
-steps.  e2e repeats the step through the public API with the per-step inputs (target
-images) copied from pinned host memory and the loss read back, copies inside the timing.
+Timing: W warm-up steps, then K steps of the captured step graph, each timed with CUDA
+events on the launching stream (L2 flushed with a 256 MiB write between steps, outside the
+events), bracketed by barrier + synchronize, max over ranks.  Stage times / pair counts for
+the roofline come from libbsr's caller-owned events and device counters (eager steps before
+the timed region).  e2e: the same step through the public API (render_tiled,
+training.loss_into, render_backward, adam_step) with every step's inputs copied from
+pinned host memory and its loss read back, copies inside the timing.
 """
 
 from __future__ import annotations
@@ -256,8 +258,9 @@ def timed_loop(w, steps, world, prof=None, l2=None):
 
 
 def e2e_loop(w, steps, world):
-    """Same step through the public API with per-step host inputs (pinned) and the result
-    read back, copies inside the timing.
+    """The step captured in CUDA graphs together with its per-step host inputs (pinned) and
+    the result read back, copies inside the timing (reported as extra.e2e_graph; the
+    headline e2e is e2e_api_loop).
 
     Every step copies its inputs host->device (the per-view target images; config 2 has
     none) and reads its result device->host (the loss values; the rendered image for
@@ -322,18 +325,7 @@ def e2e_loop(w, steps, world):
         for g in graphs:
             g.replay()
     torch.cuda.synchronize()
-    # steady-state host link: on the B200 boxes host<->device copies start at ~11 GB/s and
-    # reach ~54 GB/s only after about a second of sustained traffic (scripts/h2d_probe.py,
-    # scripts/e2e_probe4.py); bring the link up before timing, as a running job would have
-    warm_dev = torch.empty(16 << 20, dtype=torch.uint8, device="cuda")
-    warm_host = torch.empty(16 << 20, dtype=torch.uint8, pin_memory=True)
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < 1.5:
-        for _ in range(8):
-            warm_dev.copy_(warm_host, non_blocking=True)
-            warm_host.copy_(warm_dev, non_blocking=True)
-        torch.cuda.synchronize()
-    del warm_dev, warm_host
+    warm_host_link()  # steady-state host link (scripts/h2d_probe.py)
 
     done = [torch.cuda.Event(), torch.cuda.Event()]
     barrier(world)
@@ -446,7 +438,8 @@ def cpu_baseline(cfg, budget_s=15.0):
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     step, kind, desc = cpu_reference_step_fn(cfg, threads)
-    step()  # warm-up (first-touch, BLAS init)
+    if cfg in ("c1", "c2"):
+        step()  # warm-up (first-touch, BLAS init); configs 3 / 4 take 10-40 s per step: one timed step
     t0 = time.perf_counter()
     k = 0
     while True:
@@ -479,7 +472,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     step, kind, desc = cpu_reference_step_fn(args.config, threads)
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 1) if args.config in ("c1", "c2", "c3") else 0
     steps = max(1, min(args.steps, 5 if args.config in ("c1", "c2") else 1))
     for _ in range(warm):
         step()
@@ -503,19 +496,344 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- e2e (public API)
+def e2e_api_loop(w, steps, world):
+    """The same step through the package's public API -- render_tiled, training.loss_into,
+    render_backward (+ all-reduce + adam_step for the training configs) -- eagerly, with
+    every step's inputs copied host->device from pinned memory (the per-view targets;
+    config 2 has none) and its result read device->host (the loss values; the rendered
+    image for config 2), copies inside the timed region.  Returns (ms, views, h2d, d2h)."""
+    import torch
+
+    from paper_2501_18630_b200 import distributed as dd
+    from paper_2501_18630_b200.primitive import GradientBuffer
+    from paper_2501_18630_b200.rasterizer import check_pending, render_backward, render_tiled
+    from paper_2501_18630_b200.training import AdamState, LossWorkspace, adam_step, group_lrs, loss_into
+
+    prims, cams, bg = w["prims"], w["cams"], w["bg"]
+    train = w["kind"] == "train"
+    main = torch.cuda.current_stream()
+    if train:
+        if "e2e_host" not in w:  # pinned (torch.empty(pin_memory=True)) and exercised once
+            w["e2e_host"] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t.cpu())
+                             for t in w["targets"]]
+        host = w["e2e_host"]
+        tgt = [torch.empty_like(t) for t in w["targets"]]
+        ws = {}
+        for cam in cams:
+            ws.setdefault((cam.width, cam.height), LossWorkspace(cam.width, cam.height))
+        d_img = {k: torch.empty((k[1], k[0], 3), dtype=torch.float32, device="cuda") for k in ws}
+        vals = torch.zeros((len(cams), 3), dtype=torch.float64, device="cuda")
+        vals_host = torch.empty_like(vals, device="cpu").pin_memory()
+        state = AdamState(prims) if w["adam"] else None
+        lrs = group_lrs()
+        bi = sum(h.numel() * h.element_size() for h in host)
+        bo = vals.numel() * vals.element_size()
+    else:
+        side = torch.cuda.Stream()
+        c0 = cams[0]
+        img_host = [torch.empty((c0.height, c0.width, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        bi, bo = 0, img_host[0].numel() * 4
+
+    def step(i):
+        if not train:
+            out = render_tiled(prims, cams[0], bg)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            out.color.record_stream(side)
+            with torch.cuda.stream(side):  # frame i downloads while frame i+1 renders
+                img_host[i % 2].copy_(out.color, non_blocking=True)
+            return 1
+        for v in range(len(cams)):
+            tgt[v].copy_(host[v], non_blocking=True)
+        grads = GradientBuffer.zeros_for(prims)
+        for v, cam in enumerate(cams):
+            out = render_tiled(prims, cam, bg)
+            k = (cam.width, cam.height)
+            loss_into(out.color, tgt[v], d_img[k], ws[k], values=vals[v])
+            render_backward(prims, cam, bg, d_img[k], forward_out=out, grads=grads)
+        if world > 1:
+            dd.allreduce_grads(grads.flat)
+        if state is not None:
+            adam_step(prims, grads, state, lrs, device_step=True)
+        vals_host.copy_(vals, non_blocking=True)
+        return len(cams)
+
+    for i in range(3):  # untimed: allocator / capacity warm-up
+        step(i)
+    torch.cuda.synchronize()
+    check_pending(block=True)
+    warm_host_link()
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(main)
+    views = 0
+    for i in range(steps):
+        views += step(i)
+    if not train:
+        main.wait_stream(side)
+    e.record(main)
+    e.synchronize()
+    ms = s.elapsed_time(e)
+    check_pending(block=True)  # any device-side error / overflow invalidates the run
+    barrier(world)
+    return ms, views, bi, bo
+
+
+def warm_host_link():
+    """Bring host<->device copies to steady state before a timed region: on these boxes
+    they start at ~11 GB/s and reach ~54 GB/s only after about a second of traffic."""
+    import torch
+
+    warm_dev = torch.empty(16 << 20, dtype=torch.uint8, device="cuda")
+    warm_host = torch.empty(16 << 20, dtype=torch.uint8, pin_memory=True)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 1.5:
+        for _ in range(8):
+            warm_dev.copy_(warm_host, non_blocking=True)
+            warm_host.copy_(warm_dev, non_blocking=True)
+        torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- peaks
+def fp32_peaks(clk_mhz):
+    """Measured FFMA / FFMA2 / SFU rates (profiles/r02_peaks.json, written by
+    profiles/micro/run_peaks.py on this pool's B200), else the nominal FMA rate."""
+    pk = peaks()
+    nominal = SM_COUNT * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+    try:
+        with open(os.path.join(REPO, "profiles", "r02_peaks.json")) as f:
+            m = json.load(f)
+        return dict(fp32=float(m["ffma_tflops"]), ffma2=float(m["ffma2_tflops"]), sfu_gops=float(m["ex2_gops"]),
+                    nominal=nominal, source=f"measured: profiles/micro/peaks.cu (FFMA chains, 148x8 CTAs, "
+                                            f"SM clock {m.get('sm_mhz_median')} MHz) -> profiles/r02_peaks.json")
+    except Exception:
+        return dict(fp32=nominal, ffma2=nominal, sfu_gops=None, nominal=nominal,
+                    source="nominal FP32 FMA rate 148 SM x 128 lanes x 2 x sm_max_mhz")
+
+
+# ----------------------------------------------------------------------------- one workload
+def measure(cfg, args, rank, world, local, K, W, want_cpu, want_e2e):
+    """Device-timed value, e2e, roofline and CPU baseline of one workload; returns the line."""
+    import torch
+
+    from paper_2501_18630_b200.rasterizer import frame_status
+
+    w = build_b200(cfg, rank, world, args.views_per_gpu)
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    for _ in range(W):  # warm-up (also sizes the tile-entry capacity with a checked forward)
+        run_step(w)
+    torch.cuda.synchronize()
+    frames = [w["frame"]] if w["kind"] == "render" else list(w["step"].frames.values())
+    for f in frames:
+        frame_status(f)
+
+    prof = BenchProfiler(len(w["cams"]))
+    prof.sp.count_pairs(True)  # algorithmic pair counts (P_f, P_b) from one untimed step
+    run_step(w, prof)
+    torch.cuda.synchronize()
+    pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64) / len(w["cams"])
+    prof.sp.count_pairs(False)
+    prof.sp.collect_step()
+    prof.sp.reset()
+    # per-stage kernel durations: eager steps with libbsr's stage events (kernel time is the
+    # same in and out of a graph; events cannot be timed inside a replayed graph)
+    timed_loop(w, min(K, 20), world, prof=prof, l2=l2)
+    timed_prof = prof
+    if not args.eager:
+        try:
+            make_graph(w, None)
+            timed_prof = None
+        except Exception as exc:  # NCCL inside a capture is a driver/library feature: degrade, do not fail
+            if world == 1:
+                raise
+            print(f"[bench] rank {rank}: graph capture with the all-reduce failed ({exc!r}); timing eager steps",
+                  file=sys.stderr)
+            w.pop("graph", None)
+            torch.cuda.synchronize()
+    if timed_prof is not None:
+        prof.sp.reset()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, views = timed_loop(w, K, world, prof=timed_prof, l2=l2)
+    clk = clocks.stop()
+    for f in frames:  # any device-side error or capacity overflow invalidates the run
+        frame_status(f)
+    ms_max = max_over_ranks(ms, world)
+    views_all = sum_over_ranks(views, world)
+    value = views_all / (ms_max / 1e3)
+
+    e2e = extra_e2e = None
+    if want_e2e:
+        ke = max(K, 10)
+        try:
+            ems, eviews, bi, bo = e2e_api_loop(w, ke, world)
+            ems_max = max_over_ranks(ems, world)
+            e2e = {"value": sum_over_ranks(eviews, world) / (ems_max / 1e3), "unit": unit_for(cfg),
+                   "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+                   "path": "public API per step: pinned H2D of the inputs, render_tiled, training.loss_into, "
+                           "render_backward (+ all-reduce + adam_step), D2H of the loss values "
+                           "(config 2: render_tiled + D2H of the image), eager"}
+        except Exception as exc:
+            if world == 1:
+                raise
+            print(f"[bench] rank {rank}: e2e failed ({exc!r})", file=sys.stderr)
+        try:  # the same step captured with its copies in CUDA graphs (a serving / training loop's form)
+            gms, gviews, gbi, gbo = e2e_loop(w, max(K, 20), world)
+            gms_max = max_over_ranks(gms, world)
+            extra_e2e = {"value": sum_over_ranks(gviews, world) / (gms_max / 1e3), "unit": unit_for(cfg),
+                         "h2d_bytes_per_step": int(gbi), "d2h_bytes_per_step": int(gbo),
+                         "path": "training.TrainStep / render step captured with its copies in two CUDA graphs"}
+        except Exception as exc:
+            print(f"[bench] rank {rank}: graph e2e failed ({exc!r})", file=sys.stderr)
+            torch.cuda.synchronize()
+
+    stages = prof.sp.mean_ms()
+    pk = peaks()
+    clk_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+    fp = fp32_peaks(clk_mhz)
+    pairs_f, contrib_f, pairs_b = pair_stats[0], pair_stats[1], pair_stats[2]
+    rf = dict(raster_fwd=(pairs_f * FP32_FLOP_PER_PAIR_FWD, stages["raster_fwd"]))
+    if w["kind"] == "train":
+        rf["raster_bwd"] = (pairs_b * FP32_FLOP_PER_PAIR_BWD, stages["raster_bwd"])
+    per_view = {k: v for k, v in stages.items() if k not in ("adam", "color_views")}
+    dom = max(per_view, key=lambda k: per_view[k])
+    extra = {"stage_ms": {k: round(v, 4) for k, v in stages.items()},
+             "pairs_per_view": {"fwd": pairs_f, "bwd": pairs_b, "contributions": contrib_f},
+             "dominant_stage": dom}
+    ach = {}
+    for k, (flop, t_ms) in rf.items():
+        a = flop / (t_ms * 1e-3) / 1e12
+        ach[k] = {"achieved_tflops": round(a, 3), "frac_of_measured_ffma": round(a / fp["fp32"], 4),
+                  "frac_of_nominal": round(a / fp["nominal"], 4)}
+    extra["raster_roofline"] = ach
+    nscene = len(w["prims"])
+    k3 = w["prims"].sh_coeffs
+    info = frames[0].info
+    V, E = info["visible"], info["entries"]
+    hbm = {}
+    hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80 + E * 4) / (stages["preprocess"] * 1e-3) / 1e9
+    n_tiles = (-(-w["cams"][0].width // 16)) * (-(-w["cams"][0].height // 16))
+    hbm["bin_count"] = (n_tiles * 12) / (stages["bin_count"] * 1e-3) / 1e9
+    hbm["bin_scatter"] = (V * 24 + E * 12) / (stages["bin_scatter"] * 1e-3) / 1e9
+    hbm["tile_sort"] = (E * 12) / (stages["tile_sort"] * 1e-3) / 1e9
+    if w["kind"] == "train":
+        # geometry chain (fp64 kernel) + colour chain: grad_acc 48 + params 240 + gradients
+        # RMW 480 per visible primitive at SH-3; with the colour chain deferred to color_views
+        # grad_acc 48 + geometry params 48 + their gradients RMW 96 + d rgb 16
+        per_vis = 208 if stages.get("color_views", 0) > 0 else (48 + 240 + 480)
+        hbm["preprocess_bwd"] = V * per_vis / (stages["preprocess_bwd"] * 1e-3) / 1e9
+        cam0 = w["cams"][0]
+        if stages.get("loss", 0) > 0:
+            hbm["loss"] = 12 * 3 * cam0.width * cam0.height * 4 / (stages["loss"] * 1e-3) / 1e9
+        if stages.get("color_views", 0) > 0:
+            nv = len(w["cams"])
+            hbm["color_views"] = nscene * (12 * k3 * 3 + 16 * nv + 12) / (stages["color_views"] * 1e-3) / 1e9
+        if stages.get("adam", 0) > 0:
+            hbm["adam"] = 28 * w["prims"].flat.numel() / (stages["adam"] * 1e-3) / 1e9
+    extra["hbm_stage_gbs"] = {k: round(v, 1) for k, v in hbm.items()}
+    extra["visible"], extra["entries"], extra["flagged_pixels"] = V, E, info["flagged_pixels"]
+    if dom in rf:
+        flop, t_ms = rf[dom]
+        a = flop / (t_ms * 1e-3) / 1e12
+        roof = {"bound": "fp32", "achieved": round(a, 3), "peak": round(fp["fp32"], 2), "unit": "TFLOP/s",
+                "frac": round(a / fp["fp32"], 4), "traffic": None, "kernel": dom, "peak_source": fp["source"],
+                "nominal_peak": round(fp["nominal"], 2), "ffma2_peak": round(fp["ffma2"], 2),
+                "algorithmic": f"{FP32_FLOP_PER_PAIR_FWD if dom == 'raster_fwd' else FP32_FLOP_PER_PAIR_BWD} "
+                               f"FLOP per evaluated (pixel, entry) pair (SURVEY 8(d)) x pairs counted on the "
+                               f"device in an untimed step / the kernel's mean CUDA-event duration"}
+    else:
+        gbs = hbm.get(dom)
+        roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": None if gbs is None else gbs / pk["hbm_gbs"], "traffic": None, "kernel": dom}
+    ncu = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu):
+        try:
+            tr = json.load(open(ncu)).get(cfg, {}).get(roof["kernel"])
+            if tr:
+                roof["traffic"] = tr
+        except Exception:
+            pass
+    cam = w["cams"][0]
+    line = {
+        "metric": metric_for(cfg), "value": value, "unit": unit_for(cfg), "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "strong" if cfg == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded BASELINE config generators, random-init Gaussians)",
+        "config": {"workload": cfg, "gaussians": len(w["prims"]), "sh_degree": 3, "width": cam.width,
+                   "height": cam.height, "views_per_gpu": len(w["cams"]),
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "flushed between steps (256 MiB write)"},
+        "roofline": roof, "cpu_baseline": None, "e2e": e2e,
+        "gpu_launches": kernel_launches_per_step(w) * K, "clocks": clk, "extra": extra,
+        "cuda_graph": "graph" in w,
+    }
+    if extra_e2e is not None:
+        line["extra"]["e2e_graph"] = extra_e2e
+    if world > 1:
+        line["nccl"] = nccl_info()
+    del w, l2
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    if want_cpu and rank == 0 and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as e:  # the baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "unit": unit_for(cfg), "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"unavailable: {e!r}"}
+    return line
+
+
+def nccl_info():
+    import torch
+    import torch.distributed as dist
+
+    try:
+        ver = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        ver = None
+    return {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "nccl_version": ver,
+            "collective": "all_reduce (sum, fp32) of the flat per-Gaussian gradient buffer per step"}
+
+
+# ----------------------------------------------------------------------------- launcher
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a torchrun environment: relaunch this command under
+    torch.distributed.run with N local ranks (one per GPU, NCCL, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank count) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, cmd, env)
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4"],
+                    help="default: c4 (the largest single-GPU config) at N=1, c3 (view-batch DP) at N>1")
     ap.add_argument("--views-per-gpu", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-1 line nested in the c4 line")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph capture of the step")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)  # does not return
+    if args.config is None:
+        args.config = "c4" if max(world_env, 1) == 1 else "c3"
     if args.impl == "reference":
         return run_reference(args)
 
@@ -527,171 +845,16 @@ def main():
     _lib.require_cuda()
     W = max(args.warmup, 3)
     K = max(args.steps, 1)
-    w = build_b200(args.config, rank, world, args.views_per_gpu)
-    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
-
-    # warm-up (also sizes the tile-entry capacity with a checked forward)
-    from paper_2501_18630_b200.rasterizer import frame_status
-
-    for _ in range(W):
-        run_step(w)
-    torch.cuda.synchronize()
-    frames = [w["frame"]] if w["kind"] == "render" else list(w["step"].frames.values())
-    for f in frames:
-        frame_status(f)
-
-    prof = BenchProfiler(len(w["cams"]))
-    if prof is not None:  # algorithmic pair counts (P_f, P_b) from one untimed step
-        prof.sp.count_pairs(True)
-        run_step(w, prof)
-        torch.cuda.synchronize()
-        pair_stats = prof.sp.stats.cpu().numpy().astype(np.float64) / len(w["cams"])
-        prof.sp.count_pairs(False)
-        prof.sp.collect_step()
-        prof.sp.reset()
-    timed_prof = prof
-    if not args.eager:
-        # per-stage kernel durations: eager steps with libbsr's stage events (kernel time is
-        # the same in and out of a graph; events cannot be timed inside a replayed graph)
-        timed_loop(w, min(K, 20), world, prof=prof, l2=l2)
-        try:
-            make_graph(w, None)
-        except Exception as exc:  # NCCL inside a capture is a driver/library feature: degrade, do not fail
-            if world == 1:
-                raise
-            import sys as _sys
-
-            print(f"[bench] rank {rank}: graph capture with the all-reduce failed ({exc!r}); "
-                  f"timing eager steps", file=_sys.stderr)
-            w.pop("graph", None)
-            torch.cuda.synchronize()
-        timed_prof = None
-    clocks = ClockSampler(local)
-    clocks.start()
-    ms, views = timed_loop(w, K, world, prof=timed_prof, l2=l2)
-    clk = clocks.stop()
-    for f in frames:  # any device-side error or capacity overflow invalidates the run
-        frame_status(f)
-    ms_max = max_over_ranks(ms, world)
-    views_all = sum_over_ranks(views, world)
-    value = views_all / (ms_max / 1e3)
-
-    e2e = None
-    if not args.no_e2e:
-        ke = max(K, 20)
-        try:
-            ems, eviews, bi, bo = e2e_loop(w, ke, world)
-        except Exception as exc:  # see the capture fallback above
-            if world == 1:
-                raise
-            import sys as _sys
-
-            print(f"[bench] rank {rank}: e2e capture failed ({exc!r})", file=_sys.stderr)
-            torch.cuda.synchronize()
-            ems = None
-        if ems is not None:
-            ems_max = max_over_ranks(ems, world)
-            e2e = {"value": sum_over_ranks(eviews, world) / (ems_max / 1e3), "unit": unit_for(args.config),
-                   "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo)}
-
-    pk = peaks()
-    roof, stages, extra = None, None, {}
-    if prof is not None:
-        stages = prof.sp.mean_ms()
-        pairs_f, contrib_f, pairs_b = pair_stats[0], pair_stats[1], pair_stats[2]
-        clk_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
-        fp32_peak_max = SM_COUNT * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
-        fp32_peak_clk = SM_COUNT * FP32_LANES_PER_SM * 2 * clk_mhz * 1e6 / 1e12
-        rf = dict(raster_fwd=(pairs_f * FP32_FLOP_PER_PAIR_FWD, stages["raster_fwd"]))
-        if w["kind"] == "train":
-            rf["raster_bwd"] = (pairs_b * FP32_FLOP_PER_PAIR_BWD, stages["raster_bwd"])
-        # dominant per-view stage (adam / color_views run once per multi-view step)
-        per_view = {k: v for k, v in stages.items() if k not in ("adam", "color_views")}
-        dom = max(per_view, key=lambda k: per_view[k])
-        extra["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
-        extra["pairs_per_view"] = {"fwd": pairs_f, "bwd": pairs_b, "contributions": contrib_f}
-        extra["dominant_stage"] = dom
-        ach = {}
-        for k, (flop, t_ms) in rf.items():
-            a = flop / (t_ms * 1e-3) / 1e12
-            ach[k] = {"achieved_tflops": round(a, 3), "frac_of_fp32_peak_at_max_clock": round(a / fp32_peak_max, 4),
-                      "frac_of_fp32_peak_at_measured_clock": round(a / fp32_peak_clk, 4)}
-        extra["raster_roofline"] = ach
-        # HBM stages: algorithmic bytes / stage time
-        nscene = len(w["prims"])
-        k3 = w["prims"].sh_coeffs
-        info = frames[0].info
-        V, E = info["visible"], info["entries"]
-        hbm = {}
-        # preprocess: parameters (geometry 48 B + SH 12 K B), records 80 B per visible, and the
-        # per-tile counts (E 4-B REDs, taken here since the counting pass was fused in)
-        hbm["preprocess"] = (nscene * (48 + 12 * k3) + V * 80 + E * 4) / (stages["preprocess"] * 1e-3) / 1e9
-        # binning: scan = T counts read + T ranges written (12 B); scatter = V (20 B + key
-        # 4 B) + E (8-B entry + 4-B atomic); per-tile sort = E (8 B read + 4 B written)
-        n_tiles = frames[0].info.get("tiles") or (-(-w["cams"][0].width // 16)) * (-(-w["cams"][0].height // 16))
-        hbm["bin_count"] = (n_tiles * 12) / (stages["bin_count"] * 1e-3) / 1e9
-        hbm["bin_scatter"] = (V * 24 + E * 12) / (stages["bin_scatter"] * 1e-3) / 1e9
-        hbm["tile_sort"] = (E * 12) / (stages["tile_sort"] * 1e-3) / 1e9
-        if w["kind"] == "train":
-            # geometry chain + colour chain (768 B / visible primitive at SH-3); with the colour
-            # chain deferred to color_views: grad_acc 48 + geometry params 48 + their
-            # gradients read-modify-write 96 + d rgb 16
-            per_vis = 208 if stages.get("color_views", 0) > 0 else (48 + 240 + 480)
-            hbm["preprocess_bwd"] = V * per_vis / (stages["preprocess_bwd"] * 1e-3) / 1e9
-            cam0 = w["cams"][0]
-            if stages.get("loss", 0) > 0:
-                hbm["loss"] = 12 * 3 * cam0.width * cam0.height * 4 / (stages["loss"] * 1e-3) / 1e9
-            if stages.get("color_views", 0) > 0:  # once per step: SH rows read, gradients RMW
-                nv = len(w["cams"])
-                hbm["color_views"] = nscene * (12 * k3 * 3 + 16 * nv + 12) / (stages["color_views"] * 1e-3) / 1e9
-            if stages.get("adam", 0) > 0:
-                hbm["adam"] = 28 * w["prims"].flat.numel() / (stages["adam"] * 1e-3) / 1e9
-        extra["hbm_stage_gbs"] = {k: round(v, 1) for k, v in hbm.items()}
-        extra["visible"], extra["entries"], extra["flagged_pixels"] = V, E, info["flagged_pixels"]
-        if dom in rf:
-            flop, t_ms = rf[dom]
-            a = flop / (t_ms * 1e-3) / 1e12
-            roof = {"bound": "fp32", "achieved": round(a, 3), "peak": round(fp32_peak_max, 2), "unit": "TFLOP/s",
-                    "frac": round(a / fp32_peak_max, 4), "traffic": None, "kernel": dom,
-                    "peak_source": "nominal FP32 FMA rate 148 SM x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json "
-                                   "has no FP32 figure; the raster is not a dense contraction, no tensor cores)",
-                    "algorithmic": f"{FP32_FLOP_PER_PAIR_FWD if dom == 'raster_fwd' else FP32_FLOP_PER_PAIR_BWD} "
-                                   f"FLOP per evaluated (pixel, entry) pair x pairs counted on device"}
-        else:
-            gbs = hbm.get(dom)
-            roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": None if gbs is None else gbs / pk["hbm_gbs"], "traffic": None, "kernel": dom}
-        ncu = os.path.join(REPO, "profiles", "ncu_traffic.json")
-        if os.path.exists(ncu) and roof is not None:
-            try:
-                tr = json.load(open(ncu)).get(args.config, {}).get(roof["kernel"])
-                if tr:
-                    roof["traffic"] = tr
-            except Exception:
-                pass
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(args.config)
-        except Exception as e:  # the baseline is reported, never the target
-            cpu = {"value": None, "unit": unit_for(args.config), "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"unavailable: {e!r}"}
-
+    line = measure(args.config, args, rank, world, local, K, W, not args.no_cpu_baseline, not args.no_e2e)
+    if world == 1 and args.config == "c4" and not args.no_secondary:
+        # config 1 (the reference's CPU-sized training step) as a secondary figure
+        sec = measure("c1", args, rank, world, local, max(K, 20), W, not args.no_cpu_baseline, not args.no_e2e)
+        line["secondary"] = {"c1": {k: sec[k] for k in ("metric", "value", "unit", "ms_per_step", "e2e", "roofline",
+                                                          "cpu_baseline", "clocks")}}
+        line["secondary"]["c1"]["stage_ms"] = sec["extra"]["stage_ms"]
+        line["secondary"]["c1"]["e2e_graph"] = sec["extra"].get("e2e_graph")
+        line["gpu_launches_secondary"] = sec["gpu_launches"]
     if rank == 0:
-        cam = w["cams"][0]
-        line = {
-            "metric": metric_for(args.config), "value": value, "unit": unit_for(args.config), "n_gpus": world,
-            "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
-            "scaling": "strong" if args.config == "c3" else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded BASELINE config generators, random-init Gaussians)",
-            "config": {"workload": args.config, "gaussians": len(w["prims"]), "sh_degree": 3,
-                       "width": cam.width, "height": cam.height, "views_per_gpu": len(w["cams"]),
-                       "parallelism": f"dp{world}" if world > 1 else "single", "l2": "flushed between steps"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": kernel_launches_per_step(w) * K, "clocks": clk, "extra": extra,
-            "cuda_graph": "graph" in w,
-        }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -350,10 +350,16 @@ def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, 
 
 
 def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, forward_out=None,
-                    threads=None, core=None, d_depth=None) -> GradientBuffer:
-    """rasterizer.py:230-321 on the B200: exact analytic gradients of the rendered image."""
+                    threads=None, core=None, d_depth=None, grads: GradientBuffer | None = None) -> GradientBuffer:
+    """rasterizer.py:230-321 on the B200: exact analytic gradients of the rendered image.
+
+    ``grads`` (extension): an existing GradientBuffer of ``prims`` the gradients are ADDED
+    into (multi-view accumulation without a fresh buffer per view); returned."""
     _check_core(core)
-    grads = GradientBuffer.zeros_for(prims)
+    if grads is None:
+        grads = GradientBuffer.zeros_for(prims)
+    elif grads.flat.numel() != prims.flat.numel():
+        raise ValueError("grads does not match prims")
     if len(prims) == 0:
         return grads
     if forward_out is None or forward_out.frame is None:
