@@ -68,7 +68,7 @@ inline CoreView carve_core(void *base, int64_t v, int W, int H, int64_t e) {
 __global__ void core_pack_kernel(int64_t v, const double *means, const double *conics,
                                  const double *opac, const double *betas, const double *colors,
                                  const int32_t *bounds, Record *rec, double *rec64, float4 *needle,
-                                 double *grad64) {
+                                 double *side64) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
     const int x0 = bounds[4 * k], x1 = bounds[4 * k + 1], y0 = bounds[4 * k + 2], y1 = bounds[4 * k + 3];
@@ -83,9 +83,15 @@ __global__ void core_pack_kernel(int64_t v, const double *means, const double *c
     const double ex = det > 0 ? sqrt(fabs(cc / det)) : 1e30, ey = det > 0 ? sqrt(fabs(ca / det)) : 1e30;
     const double kr = pd ? chol_r2_error_bound(l11, l21, l22, ex + 2.0, ey + 2.0) : 1.0;
     const bool unsafe = !pd || (float)kr > kUnsafeR2Err;
-    if (unsafe) {  // core seam: fp64 path, fp64 geometry gradients
-        needle[k] = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
-        for (int q = 0; q < kGrad64; ++q) grad64[kGrad64 * k + q] = 0.0;
+    if (unsafe) {  // core seam: fp64 path (its factor, or zeroed xy-frame fp64 accumulators)
+        needle[k] = make_float4(__int_as_float(0x7fc00000), pd ? 1.f : 0.f, 0.f, 0.f);
+        double *s64 = side64 + kSide64 * k;
+        for (int q = 0; q < kSide64; ++q) s64[q] = 0.0;
+        if (pd) {
+            s64[0] = l11;
+            s64[1] = l21;
+            s64[2] = l22;
+        }
     }
     r.c = make_float4((float)colors[3 * k], (float)colors[3 * k + 1], (float)colors[3 * k + 2],
                       record_err_word(kr, (double)r.b.z, unsafe));
@@ -109,22 +115,20 @@ __global__ void core_lists_kernel(const int64_t *offsets, const int64_t *lists, 
     if (i < n_tiles) ranges[i] = make_uint2((uint32_t)offsets[i], (uint32_t)offsets[i + 1]);
 }
 
-__global__ void core_unpack_kernel(int64_t v, const float *acc, const Record *rec, const double *grad64,
-                                   float *d_means, float *d_conics, float *d_opac, float *d_betas,
-                                   float *d_colors) {
+__global__ void core_unpack_kernel(FrameView f, int64_t v, float *d_means, float *d_conics, float *d_opac,
+                                   float *d_betas, float *d_colors) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= v) return;
-    const float *g = acc + k * kGradStride;
-    const Record r = rec[k];
-    if (r.c.w < 0.f) {  // fp32-unsafe record: xy-frame partials summed in fp64 (add_geom64)
-        const double *g64 = grad64 + kGrad64 * k;
+    const float *g = f.grad_acc + k * kGradStride;
+    double l11, l21, l22;
+    if (!record_factor64(f, (uint32_t)k, l11, l21, l22)) {  // xy-frame partials summed in fp64
+        const double *g64 = f.side64 + kSide64 * k;
         d_means[2 * k] = (float)g64[0];
         d_means[2 * k + 1] = (float)g64[1];
         d_conics[3 * k] = (float)g64[2];
         d_conics[3 * k + 1] = (float)g64[3];
         d_conics[3 * k + 2] = (float)g64[4];
     } else {  // whitened-frame partials (frame.cuh grad_acc): d mean = -2 L M, G = L^-T H L^-1
-        const double l11 = r.a.z, l21 = r.a.w, l22 = r.b.x;
         const double mu = g[0], mw = g[1], h00 = g[2], h01 = g[3], h11 = g[4];
         d_means[2 * k] = (float)(-2.0 * l11 * mu);
         d_means[2 * k + 1] = (float)(-2.0 * (l21 * mu + l22 * mw));
@@ -395,7 +399,7 @@ static int core_prepare(const CoreView &c, int64_t v, const double *means, const
     BSR_CUDA_TRY(cudaMemsetAsync(c.f.ctr, 0, c.f.zero_bytes, st));
     if (v > 0)
         core_pack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, means, conics, opac, betas,
-                                                                               colors, bounds, c.f.rec, c.f.rec64, c.f.needle, c.f.grad64);
+                                                                               colors, bounds, c.f.rec, c.f.rec64, c.f.needle, c.f.side64);
     const int64_t m = imax64(n_entries, c.f.n_tiles);
     core_lists_kernel<<<(unsigned)div_up(imax64(m, 1), BSR_BLOCK), BSR_BLOCK, 0, st>>>(
         offsets, lists, n_entries, c.f.n_tiles, c.lists, c.ranges);
@@ -478,8 +482,7 @@ extern "C" int bsr_core_backward(int64_t v, const double *means, const double *c
                                    none, background, alpha_min, t_stop, d_raw, st)))
         return rc;
     if (v > 0)
-        core_unpack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(v, c.f.grad_acc, c.f.rec, c.f.grad64, d_means,
-                                                                                 d_conics, d_opac, d_betas,
+        core_unpack_kernel<<<(unsigned)div_up(v, BSR_BLOCK), BSR_BLOCK, 0, st>>>(c.f, v, d_means, d_conics, d_opac, d_betas,
                                                                                  d_colors);
     BSR_LAUNCH_CHECK();
     return BSR_OK;

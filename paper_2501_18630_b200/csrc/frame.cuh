@@ -14,7 +14,7 @@ inline int sort_items(int64_t cap) { return cap <= kSmallSortCap ? 4 : 16; }
 constexpr int kDepthPasses = 4;                      // 32-bit (fp32-depth) keys + fp64 fixup
 constexpr int kRec64 = 8;                            // doubles per fp64 side record
 constexpr int kGradStride = 12;                      // raster grad accumulator floats/primitive
-constexpr int kGrad64 = 6;                           // fp64 geometry accumulator doubles/primitive (5 used)
+constexpr int kSide64 = 6;                           // fp64 side doubles per primitive (FrameView::side64)
 // primitives whose fp32 r2 error bound exceeds this are evaluated in fp64 by the raster
 #ifndef BSR_UNSAFE_R2_ERR
 #define BSR_UNSAFE_R2_ERR 2.0e-5f
@@ -63,9 +63,12 @@ struct FrameView {
                              // [0..4] geometry partials in the record's whitened frame (u, w) =
                              // L^T (px - mean), Q = L L^T:  sum d_x (u, w, u^2, u w, w^2)
                              // (d_x = dL/dr2), [5] d opacity, [6] d beta, [7..9] d rgb, [10] d z
-    double *grad64;          // [N][kGrad64] fp64 accumulators of the geometry partials (d mean2d x2,
-                             // d conic x3) of fp32-unsafe records (Record.c.w < 0): zeroed by
-                             // preprocess for those records, consumed and re-zeroed by preprocess_bwd
+    double *side64;          // [N][kSide64] fp64 side data of fp32-unsafe records (Record.c.w < 0) that
+                             // take the fp64 path (needle word .x NaN): with a positive-definite
+                             // conic (needle word .y == 1) [0..2] = its fp64 factor (l11, l21,
+                             // l22); without one (.y == 0) [0..4] = xy-frame geometry partials
+                             // summed in fp64 (add_geom64; zeroed by preprocess, re-zeroed when
+                             // preprocess_bwd consumes them)
     // --- sizes ---
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles;
@@ -120,15 +123,15 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.replay_state = (double *)take(8ull * 6 * npx);
     f.grad_acc = (float *)take(4ull * kGradStride * n);
     f.needle = (float4 *)take(16ull * n);
-    f.grad64 = (double *)take(8ull * kGrad64 * n);
+    f.side64 = (double *)take(8ull * kSide64 * n);
     f.total_bytes = align_up(off, 256);
     return f;
 }
 
-// fp64 geometry partials of an fp32-unsafe record (raster_bwd / replay_bwd): ill-conditioned
-// footprints (needles) carry gradients that are cancellation-heavy sums over many pixels
-// (d conic along the short axis is ~kappa times smaller than its xy components), so their
-// geometry partials are formed from the fp64 mean / conic and summed in fp64.
+// xy-frame geometry partials summed in fp64 (raster_bwd / replay_bwd) for the records that
+// have no usable factor (fp64-path records whose conic is not positive definite in fp64):
+// without a whitened frame their conic gradient's short-axis part is a cancellation of
+// large xy terms, so it is formed from the fp64 mean / conic and summed in fp64.
 __device__ __forceinline__ void add_geom64(double *g, double d_x, double dx, double dy, double ca, double cb,
                                            double cc) {
     const double ga = ca * dx + cb * dy, gb = cb * dx + cc * dy;

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
         float kr = pd ? (float)r2_error_bound(p, l11, l21, l22) : 1.0f;
         unsafe = !pd || kr > kUnsafeR2Err;
         if (unsafe) {  // needle (compensated fp32) if its bound allows, else the fp64 path
-            float4 nw = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+            float4 nw = make_float4(__int_as_float(0x7fc00000), pd ? 1.f : 0.f, 0.f, 0.f);
             if (pd) {
                 const float kn = (float)needle_r2_error_bound(l11, l21, sqrt(p.c00) + 2.0, sqrt(p.c11) + 2.0);
                 if (kn <= kUnsafeR2Err) {
@@ -220,8 +220,12 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
                 }
             }
             f.needle[i] = nw;
-            double2 *g64 = reinterpret_cast<double2 *>(f.grad64 + kGrad64 * (int64_t)i);
-            g64[0] = g64[1] = g64[2] = make_double2(0.0, 0.0);
+            if (nw.x != nw.x) {  // fp64 path: its factor, or zeroed xy-frame fp64 accumulators
+                double2 *s64 = reinterpret_cast<double2 *>(f.side64 + kSide64 * (int64_t)i);
+                s64[0] = make_double2(pd ? l11 : 0.0, pd ? l21 : 0.0);
+                s64[1] = make_double2(pd ? l22 : 0.0, 0.0);
+                s64[2] = make_double2(0.0, 0.0);
+            }
         }
         r.c = make_float4(rgb[0], rgb[1], rgb[2], record_err_word(kr, (double)r.b.z, unsafe));
         m64[0] = p.mx;

@@ -10,6 +10,7 @@
 // HBM roofline: V * (48 B grad_acc + 240 B params read + 240 B grads RMW) at SH-3.
 #include "appearance.cuh"
 #include "frame.cuh"
+#include "raster.cuh"
 
 namespace bsr {
 
@@ -380,16 +381,24 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_c
 // partials are mapped to d mean2d / d cov2d with the record's factor L (whitened frame,
 // frame.cuh grad_acc):  d mean = -2 L M,  d cov2d = -Q G Q = -L H L^T  (Q = L L^T,
 // G = L^-T H L^-1 the conic gradient, rasterizer.py:302-312), so no inverse of the
-// ill-conditioned conic is formed.  fp32-unsafe records (Record.c.w < 0) carry xy-frame
-// conic partials summed in fp64 (grad64, cleared here) and use the fp64 conic.
+// ill-conditioned conic is formed (the factor of each record class: raster.cuh
+// record_factor64).  fp64-path records without a factor carry xy-frame conic partials
+// summed in fp64 (side64, cleared here) and use the fp64 conic.
 __device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) {
     const FrameView &f = a.f;
-    const Record &r = f.rec[i];
-    const float4 ra = r.a, rb = r.b;
-    const float cw = r.c.w;
     double dmx, dmy, gm00, gs01, gm11;
-    if (cw < 0.f) {
-        double2 *g2 = reinterpret_cast<double2 *>(f.grad64 + kGrad64 * i);
+    double l11, l21, l22;
+    if (record_factor64(f, (uint32_t)i, l11, l21, l22)) {
+        const float *acc = f.grad_acc + i * kGradStride;
+        const float4 g0 = *reinterpret_cast<const float4 *>(acc);
+        const double mu = g0.x, mw = g0.y, h00 = g0.z, h01 = g0.w, h11 = acc[4];
+        dmx = -2.0 * l11 * mu;
+        dmy = -2.0 * (l21 * mu + l22 * mw);
+        gm00 = -(l11 * l11 * h00);
+        gs01 = -(l11 * (h00 * l21 + h01 * l22));
+        gm11 = -((l21 * h00 + l22 * h01) * l21 + (l21 * h01 + l22 * h11) * l22);
+    } else {  // no factor: xy-frame conic partials summed in fp64, fp64 conic
+        double2 *g2 = reinterpret_cast<double2 *>(f.side64 + kSide64 * i);
         const double2 u0 = g2[0], u1 = g2[1], u2 = g2[2];
         g2[0] = g2[1] = g2[2] = make_double2(0.0, 0.0);
         const double *m64 = f.rec64 + kRec64 * i;
@@ -402,16 +411,6 @@ __device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) 
         gm00 = -(ia * m00 + ib * m10);
         gs01 = -0.5 * ((ia * m01 + ib * m11) + (ib * m00 + ic * m10));
         gm11 = -(ib * m01 + ic * m11);
-    } else {
-        const float *acc = f.grad_acc + i * kGradStride;
-        const float4 g0 = *reinterpret_cast<const float4 *>(acc);
-        const double mu = g0.x, mw = g0.y, h00 = g0.z, h01 = g0.w, h11 = acc[4];
-        const double l11 = ra.z, l21 = ra.w, l22 = rb.x;
-        dmx = -2.0 * l11 * mu;
-        dmy = -2.0 * (l21 * mu + l22 * mw);
-        gm00 = -(l11 * l11 * h00);
-        gs01 = -(l11 * (h00 * l21 + h01 * l22));
-        gm11 = -((l21 * h00 + l22 * h01) * l21 + (l21 * h01 + l22 * h11) * l22);
     }
     const float dz = f.grad_acc[i * kGradStride + 10];
     float dpx, dpy, dpz;

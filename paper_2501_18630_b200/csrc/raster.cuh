@@ -81,7 +81,8 @@ __host__ __device__ inline double needle_r2_error_bound(double l11, double l21, 
     // second-order terms of the double-float parts (eps^2 t Y); safety factor 1.5
     return 5.9604644775390625e-08 * 1.5 * (12.0 + 8.0 * 5.9604644775390625e-08 * l11 * (X + t * Y));
 }
-// side word of a needle: (t_hi, t_lo, rel_x_lo, rel_y_lo); fp64-path records: NaN
+// side word of a needle: (t_hi, t_lo, rel_x_lo, rel_y_lo); fp64-path records: (NaN, 1 if the
+// fp64 conic has a factor (stored in side64) else 0, 0, 0)
 __host__ __device__ inline float4 needle_word(double l11, double l21, double relx, double rely) {
     const double t = l21 / l11;
     const float th = (float)t, rx = (float)relx, ry = (float)rely;
@@ -112,6 +113,39 @@ __device__ __forceinline__ float two_sum(float a, float b, float &e) {
     const float bb = __fsub_rn(s, a);
     e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
     return s;
+}
+
+// The factor L (fp64) that the raster's whitened geometry partials of record c refer to
+// (frame.cuh grad_acc: u = l11 dx + l21 dy, w = l22 dy):
+//   fp32-safe records: the record's (l11, l21, l22);
+//   needles: (l11, l11 t, l22) with t = t_hi + t_lo of the needle word (eval_needle's u);
+//   fp64-path records with a positive-definite conic: the fp64 factor in side64;
+// returns false for fp64-path records without one (xy-frame fp64 partials, add_geom64).
+__device__ __forceinline__ bool record_factor64(const FrameView &f, uint32_t c, double &l11, double &l21,
+                                                double &l22) {
+    const Record &r = f.rec[c];
+    const float4 ra = r.a, rb = r.b;
+    if (!(r.c.w < 0.f)) {
+        l11 = ra.z;
+        l21 = ra.w;
+        l22 = rb.x;
+        return true;
+    }
+    const float4 N = f.needle[c];
+    if (N.x == N.x) {
+        l11 = ra.z;
+        l21 = (double)ra.z * ((double)N.x + (double)N.y);
+        l22 = rb.x;
+        return true;
+    }
+    if (N.y != 0.f) {
+        const double *s = f.side64 + (int64_t)kSide64 * c;
+        l11 = s[0];
+        l21 = s[1];
+        l22 = s[2];
+        return true;
+    }
+    return false;
 }
 
 // Compensated evaluation of a needle record (N = its needle word); same outputs as eval_pair.

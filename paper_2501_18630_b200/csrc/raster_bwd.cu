@@ -42,18 +42,48 @@ struct RasterBwdArgs {
 };
 
 // fp64 pair evaluation for fp32-unsafe primitives; kept out of line so the common fp32
-// path is not if-converted into predicated fp64 code.
-__device__ __noinline__ Pair unsafe_pair_bwd(const double *m64, float4 B, int px, int py) {
-    return eval_pair64(m64, B, px, py);
+// path is not if-converted into predicated fp64 code.  With the record's fp64 factor
+// (side64, positive-definite conic) the whitened coordinates u, w are formed in fp64 too.
+__device__ __noinline__ Pair unsafe_pair_bwd(const double *m64, const double *s64, bool has_factor, float4 B,
+                                             int px, int py) {
+    Pair p = eval_pair64(m64, B, px, py);
+    if (has_factor) {
+        const double dx = (double)px - m64[0], dy = (double)py - m64[1];
+        p.u = (float)(s64[0] * dx + s64[1] * dy);
+        p.w = (float)(s64[2] * dy);
+    }
+    return p;
 }
 
-// Geometry partials of an fp32-unsafe record in fp64 (frame.cuh add_geom64), out of line
-// like unsafe_pair_bwd: dx, dy from the fp64 side record, fp64 atomics into grad64.
-__device__ __noinline__ void unsafe_geom_bwd(double *grad64, const double *rec64, uint32_t c, float d_x, int px,
-                                             int py) {
-    const double *m64 = rec64 + kRec64 * (int64_t)c;
-    double *g = grad64 + (int64_t)kGrad64 * c;
-    add_geom64(g, (double)d_x, (double)px - m64[0], (double)py - m64[1], m64[2], m64[3], m64[4]);
+// xy-frame geometry partials in fp64 (frame.cuh add_geom64) of fp64-path records without a
+// factor (conic not positive definite in fp64 -- practically never met), out of line like
+// unsafe_pair_bwd.  Called by the whole warp when any lane took such a pair; the entry is
+// uniform within each group of GL lanes, so the five partials are summed over the group in
+// fp64 with shuffles and its first lane adds them.
+template <int GL>
+__device__ __noinline__ void unsafe_geom_bwd(double *side64, const double *rec64, uint32_t c, float d_x, int px,
+                                             int py, bool mine, unsigned gmask_any) {
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (mine) {
+        const double *m64 = rec64 + kRec64 * (int64_t)c;
+        const double dx = (double)px - m64[0], dy = (double)py - m64[1], dxx = (double)d_x;
+        v[0] = -2.0 * dxx * (m64[2] * dx + m64[3] * dy);
+        v[1] = -2.0 * dxx * (m64[3] * dx + m64[4] * dy);
+        v[2] = dxx * dx * dx;
+        v[3] = 2.0 * dxx * dx * dy;
+        v[4] = dxx * dy * dy;
+    }
+#pragma unroll
+    for (int o = GL / 2; o >= 1; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    const int lane = threadIdx.x & 31;
+    if ((lane % GL) == 0 && ((gmask_any >> lane) & 1u)) {
+        double *g = side64 + (int64_t)kSide64 * c;
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (v[q] != 0.0) atomicAdd(g + q, v[q]);
+    }
 }
 
 // Transpose-reduce 16 values across the L lanes of a group (L = 32 / G): afterwards each
@@ -181,12 +211,17 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
         if (STATS) pairs += (act && e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
         Pair p;
+        bool geom64 = false;  // fp64-path record without a factor: xy-frame fp64 partials
         if (C.w < 0.f) {  // needle or fp64 primitive (uniform per entry)
-            const float4 N = f.needle[s_cidx[j]];
-            if (N.x == N.x)  // needle: compensated fp32 (same bits as the forward)
+            const uint32_t c = s_cidx[j];
+            const float4 N = f.needle[c];
+            if (N.x == N.x) {  // needle: compensated fp32 (same bits as the forward)
                 p = eval_needle(A, Bq, N, px - bd.x, py - bd.z);
-            else
-                p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)s_cidx[j], Bq, px, py);
+            } else {
+                p = unsafe_pair_bwd(f.rec64 + kRec64 * (int64_t)c, f.side64 + (int64_t)kSide64 * c, N.y != 0.f,
+                                    Bq, px, py);
+                geom64 = N.y == 0.f;
+            }
         } else {
             p = eval_pair(A, Bq, px - bd.x, py - bd.z);
         }
@@ -217,12 +252,24 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         const float dk = dalpha * Bq.y;
         const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
         float v[16];
-        const bool geom64 = C.w < 0.f;  // fp32-unsafe record: geometry partials in fp64
-        if (geom64 && took) unsafe_geom_bwd(f.grad64, f.rec64, s_cidx[j], d_x, px, py);
-        // geometry partials in the record's whitened frame (frame.cuh grad_acc): the
-        // components of sum d_x (u, w)(u, w)^T do not cancel against each other the way the
-        // xy components of the conic gradient do for elongated footprints (preprocess_bwd
-        // maps them back: d mean = -2 L (.), d cov2d = -L (.) L^T, in fp64)
+        {
+            const unsigned um = __ballot_sync(0xffffffffu, geom64 && took);
+            if (um) {
+                // group-leader lanes whose group has a contributing lane
+                unsigned lead = 0u;
+#pragma unroll
+                for (int g = 0; g < 32 / GL; ++g) {
+                    constexpr uint32_t gm = GL >= 32 ? 0xffffffffu : ((1u << (GL & 31)) - 1u);
+                    if (um & (gm << ((g * GL) & 31))) lead |= 1u << ((g * GL) & 31);
+                }
+                unsafe_geom_bwd<GL>(f.side64, f.rec64, s_cidx[j], d_x, px, py, geom64 && took, lead);
+            }
+        }
+        // geometry partials in the record's whitened frame (frame.cuh grad_acc, factor L of
+        // raster.cuh record_factor64): the components of sum d_x (u, w)(u, w)^T do not cancel
+        // against each other the way the xy components of the conic gradient do for
+        // elongated footprints (preprocess_bwd maps them back in fp64: d mean = -2 L (.),
+        // d cov2d = -L (.) L^T)
         const float du = d_x * p.u, dw = d_x * p.w;
         v[0] = geom64 ? 0.f : du;
         v[1] = geom64 ? 0.f : dw;

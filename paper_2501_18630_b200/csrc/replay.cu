@@ -16,6 +16,7 @@
 #include "frame.cuh"
 #include "appearance.cuh"
 #include "project.cuh"
+#include "raster.cuh"
 #ifdef BSR_REPLAY_TRACE
 #include <cstdio>
 #endif
@@ -391,11 +392,11 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
                 double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
                 if (dkdx < -1e7) dkdx = -1e7;
                 const double d_x = d_kernel * dkdx;
-                if (f.rec[c].c.w < 0.f) {  // fp32-unsafe record: fp64 geometry accumulator
-                    add_geom64(f.grad64 + (int64_t)kGrad64 * c, d_x, dx, dy, en.ca, en.cb, en.cc);
+                double l11, l21, l22;
+                if (!record_factor64(f, c, l11, l21, l22)) {  // no factor: xy-frame fp64 partials
+                    add_geom64(f.side64 + (int64_t)kSide64 * c, d_x, dx, dy, en.ca, en.cb, en.cc);
                 } else {  // whitened frame of the record's factor (frame.cuh grad_acc)
-                    const Record &r = f.rec[c];
-                    const double u = (double)r.a.z * dx + (double)r.a.w * dy, w = (double)r.b.x * dy;
+                    const double u = l11 * dx + l21 * dy, w = l22 * dy;
                     atomicAdd(acc + 0, (float)(d_x * u));
                     atomicAdd(acc + 1, (float)(d_x * w));
                     atomicAdd(acc + 2, (float)(d_x * u * u));
