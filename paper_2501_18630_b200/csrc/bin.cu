@@ -22,6 +22,8 @@
 // index) is exactly the reference's order (source index order == source order of the
 // visible primitives).  Nothing here needs a host synchronisation: counts and E live in
 // device memory, grids are sized by capacity with early exits.
+#include <algorithm>
+
 #include "frame.cuh"
 
 namespace bsr {
@@ -150,38 +152,34 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
 }
 
 // One CTA of 1024 threads: tile ranges from the counts (== np.bincount + cumsum offsets).
-__global__ void __launch_bounds__(1024) bin_scan_kernel(FrameView f) {
+// The counts stream through in chunks of 4096 (one uint4 per thread, coalesced), each
+// chunk is block-scanned (warp shuffles + one word per warp in shared memory) and its
+// ranges written back coalesced; a running total carries across chunks.
+constexpr int kScanThreads = 1024, kScanChunk = 4 * kScanThreads;
+__global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
     pdl_wait();
     __shared__ unsigned long long s_w[32];
-    __shared__ bool s_over;
+    __shared__ unsigned long long s_total, s_chunk;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int T = f.n_tiles;
-    const int per = (T + 1023) / 1024;
-    const int t0 = min(T, t * per), t1 = min(T, t0 + per);
+    const bool vec = (T & 3) == 0;  // uint4 / 2 x uint4 accesses stay aligned
+    // pass 1: the total (capacity check before any range is written), 64-bit
     unsigned long long mine = 0;
-    for (int i = t0; i < t1; ++i) mine += f.tile_cnt[i];
-    unsigned long long incl = mine;
+    for (int i = 4 * t; i < T; i += kScanChunk)
+        for (int k = 0; k < 4; ++k) mine += i + k < T ? f.tile_cnt[i + k] : 0u;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) s_w[warp] = mine;
     __syncthreads();
     if (warp == 0) {
-        const unsigned long long v = s_w[lane];
-        unsigned long long x = v;
+        unsigned long long x = s_w[lane];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        s_w[lane] = x - v;
-        if (lane == 31) {
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) {
+            s_total = x;
             *f.vis_hint = f.ctr->visible;  // preprocess of the next forward reads it
             f.ctr->entries_needed = x;
-            s_over = x > (unsigned long long)f.entry_cap;
-            if (s_over) {
+            if (x > (unsigned long long)f.entry_cap) {
                 f.ctr->entries = 0;
                 raise_status(&f.ctr->status, BSR_ERR_CAPACITY);
             } else {
@@ -190,12 +188,59 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(FrameView f) {
         }
     }
     __syncthreads();
-    unsigned long long run = s_w[warp] + incl - mine;
-    const bool over = s_over;  // overflow: every tile empty (the caller retries larger)
-    for (int i = t0; i < t1; ++i) {
-        const uint32_t c = over ? 0u : f.tile_cnt[i];
-        f.tile_ranges[i] = over ? make_uint2(0u, 0u) : make_uint2((uint32_t)run, (uint32_t)(run + c));
-        run += c;
+    const bool over = s_total > (unsigned long long)f.entry_cap;  // every tile empty: the caller retries larger
+    // pass 2: exclusive scan chunk by chunk (E <= entry_cap < 2^31 when not over)
+    unsigned long long carry = 0;
+    for (int base = 0; base < T; base += kScanChunk) {
+        const int i = base + 4 * t;
+        uint32_t c[4];
+        if (vec && i < T) {
+            const uint4 c4 = *reinterpret_cast<const uint4 *>(f.tile_cnt + i);
+            c[0] = c4.x;
+            c[1] = c4.y;
+            c[2] = c4.z;
+            c[3] = c4.w;
+        } else {
+            for (int k = 0; k < 4; ++k) c[k] = i + k < T ? f.tile_cnt[i + k] : 0u;
+        }
+        const uint32_t sum = c[0] + c[1] + c[2] + c[3];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        __syncthreads();  // s_w / s_chunk of the previous chunk are consumed
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long v = s_w[lane];
+            unsigned long long x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            s_w[lane] = x - v;  // exclusive warp offsets
+            if (lane == 31) s_chunk = x;
+        }
+        __syncthreads();
+        unsigned long long run = carry + s_w[warp] + (incl - sum);
+        uint2 r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            r[k] = over ? make_uint2(0u, 0u) : make_uint2((uint32_t)run, (uint32_t)(run + c[k]));
+            run += c[k];
+        }
+        if (vec && i < T) {
+            uint4 *dst = reinterpret_cast<uint4 *>(f.tile_ranges + i);
+            dst[0] = make_uint4(r[0].x, r[0].y, r[1].x, r[1].y);
+            dst[1] = make_uint4(r[2].x, r[2].y, r[3].x, r[3].y);
+        } else {
+            for (int k = 0; k < 4; ++k)
+                if (i + k < T) f.tile_ranges[i + k] = r[k];
+        }
+        carry += s_chunk;
     }
 }
 
@@ -293,7 +338,10 @@ struct SortSmem {
     // cbase / cnf: coarse-bin fine-bucket base / count while bucketing; afterwards the
     // same words hold the list of big buckets (at most kSortSmem / (kMaxBucket + 1) < 2 kCoarse)
     uint32_t cbase[kCoarse], cnf[kCoarse];
-    __device__ uint32_t *bigl() { return cbase; }
+    // the crowded-tile variant (NB = kBigBuckets) can have up to kBigSortSmem / (kMaxBucket + 1)
+    // big buckets: its own list
+    uint32_t bigbuf[NB >= 4096 ? 1280 : 1];
+    __device__ uint32_t *bigl() { return NB >= 4096 ? bigbuf : cbase; }
     uint32_t w[BSR_BLOCK / 32];
     uint32_t kmin, kmax, big;
 };
@@ -459,23 +507,51 @@ __device__ void sort_tile(const FrameView &f, int tile, uint64_t *s, SortSmem<NB
     __syncthreads();  // s / sm are reused by the next tile of a persistent CTA
 }
 
-// one CTA per tile: up to kSortSmem entries in shared memory, beyond that (crowded tiles)
-// the bitonic network in place in global memory
+// one CTA per tile: up to kSortSmem entries in shared memory; crowded tiles are left to
+// tile_sort_big_kernel
 __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
     pdl_wait();
     __shared__ uint64_t s[kSortSmem];
     __shared__ SortSmem<kBuckets> sm;
     if (over_capacity(f)) return;
     const uint2 rg = f.tile_ranges[blockIdx.x];
-    const int n = (int)(rg.y - rg.x);
-    if (n > kSortSmem) {
+    if ((int)(rg.y - rg.x) > kSortSmem) return;
+    sort_tile<kBuckets>(f, blockIdx.x, s, sm);
+}
+
+// Crowded tiles (more than kSortSmem entries; config 4's dense cluster reaches ~4200):
+// the same bucket sort with kBigSortSmem entries in dynamic shared memory and 4x the fine
+// buckets, the tiles taken grid-stride by kBigSortCtas CTAs (the crowded tiles are known
+// on the device only); beyond kBigSortSmem the in-place bitonic network in global memory.
+constexpr int kBigSortSmem = 20480;  // 160 KB of u64 keys
+constexpr int kBigBuckets = 4096;
+constexpr int kBigSortCtas = 148;
+static_assert(kBigSortSmem / (kMaxBucket + 1) < 1280, "big-bucket list bound (SortSmem::bigbuf)");
+
+struct BigSortSmem {
+    uint64_t s[kBigSortSmem];
+    SortSmem<kBigBuckets> sm;
+};
+
+__global__ void __launch_bounds__(BSR_BLOCK) tile_sort_big_kernel(FrameView f) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char big_smem[];
+    BigSortSmem &b = *reinterpret_cast<BigSortSmem *>(big_smem);
+    if (over_capacity(f)) return;
+    for (int tile = blockIdx.x; tile < f.n_tiles; tile += gridDim.x) {
+        const uint2 rg = f.tile_ranges[tile];
+        const int n = (int)(rg.y - rg.x);
+        if (n <= kSortSmem) continue;
+        if (n <= kBigSortSmem) {
+            sort_tile<kBigBuckets>(f, tile, b.s, b.sm);
+            continue;
+        }
         uint64_t *g = f.tent + rg.x;
         bitonic_sort_block(g, n);
         fixup_ties(g, n, f.dkey64);
         for (int i = threadIdx.x; i < n; i += BSR_BLOCK) f.lists[rg.x + i] = (uint32_t)g[i];
-        return;
+        __syncthreads();
     }
-    sort_tile<kBuckets>(f, blockIdx.x, s, sm);
 }
 
 static unsigned entry_blocks(const FrameView &f) {
@@ -486,7 +562,7 @@ static unsigned entry_blocks(const FrameView &f) {
 // (the per-tile counts themselves are taken by preprocess, preprocess.cu)
 int launch_bin_count(const FrameView &f, cudaStream_t st) {
     if (f.n == 0) return BSR_OK;
-    BSR_CUDA_TRY((pdl_launch(bin_scan_kernel, dim3(1), dim3(1024), 0, st, f)));
+    BSR_CUDA_TRY((pdl_launch(bin_scan_kernel, dim3(1), dim3(kScanThreads), 0, st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
@@ -503,6 +579,10 @@ int launch_bin_scatter(const FrameView &f, cudaStream_t st) {
 int launch_tile_sort(const FrameView &f, cudaStream_t st) {
     if (f.n == 0 || f.n_tiles == 0) return BSR_OK;
     BSR_CUDA_TRY((pdl_launch(tile_sort_kernel, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, f)));
+    static SmemAttrOnce attr;
+    BSR_CUDA_TRY(attr.ensure(tile_sort_big_kernel, sizeof(BigSortSmem)));
+    BSR_CUDA_TRY((pdl_launch(tile_sort_big_kernel, dim3((unsigned)std::min(f.n_tiles, kBigSortCtas)), dim3(BSR_BLOCK),
+                             sizeof(BigSortSmem), st, f)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }

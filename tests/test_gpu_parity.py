@@ -424,11 +424,13 @@ def test_spherical_beta_training_step(cuda):
     assert float(st.loss_values[0, 0]) < l0
 
 
-@pytest.mark.parametrize("n,bunched", [(2500, False), (2500, True), (6000, False), (20000, False)])
+@pytest.mark.parametrize("n,bunched", [(2500, False), (2500, True), (6000, False), (6000, True), (20000, False),
+                                       (30000, False)])
 def test_crowded_tile_binning(cuda, n, bunched):
     """Crowded tiles: 1024 < n <= 4096 entries take the equi-depth bucket sort in shared
     memory (also with depths bunched in a sliver of the tile's range plus far outliers),
-    > 4096 the in-place network in global memory; lists, offsets and depth order stay
+    4096 < n <= 20480 the same sort in 160 KB of dynamic shared memory (tile_sort_big_kernel),
+    beyond that the in-place network in global memory; lists, offsets and depth order stay
     bit-exact."""
     rng = np.random.default_rng(50 + n + bunched)
     scene = random_scene(rng, n, degree=0, spread=0.1, scale_range=(0.002, 0.01), opacity_range=(0.02, 0.1))
