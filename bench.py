@@ -596,6 +596,37 @@ def warm_host_link():
         torch.cuda.synchronize()
 
 
+def deterministic_cost(w, reps=3):
+    """Device time of one view's backward in the default mode vs the deterministic mode
+    (bsr_backward_deterministic: fixed-point accumulation, two raster passes), on the
+    step's own frame and upstream gradient (extra.deterministic_backward)."""
+    import torch
+
+    from paper_2501_18630_b200.rasterizer import backward_raw, det_workspace
+
+    st = w.get("step")
+    if st is None:
+        return None
+    cam = w["cams"][0]
+    key = (cam.width, cam.height)
+    frame, d_img = st.frames[key], st.bufs[key]["d_image"]
+    ws = det_workspace(len(w["prims"]))
+    out = {}
+    for name, det in (("default_ms", None), ("deterministic_ms", ws)):
+        backward_raw(st.scene, cam, w["bg"], frame, d_img, None, st.gc, det_ws=det)  # warm
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            backward_raw(st.scene, cam, w["bg"], frame, d_img, None, st.gc, det_ws=det)
+        e.record()
+        e.synchronize()
+        out[name] = round(s.elapsed_time(e) / reps, 4)
+    st.grads.flat.zero_()
+    st._grads_clear = True
+    del ws
+    return out
+
+
 # ----------------------------------------------------------------------------- peaks
 def fp32_peaks(clk_mhz):
     """Measured FFMA / FFMA2 / SFU rates (profiles/r02_peaks.json, written by
@@ -772,6 +803,11 @@ def measure(cfg, args, rank, world, local, K, W, want_cpu, want_e2e):
     }
     if extra_e2e is not None:
         line["extra"]["e2e_graph"] = extra_e2e
+    if w["kind"] == "train" and world == 1:
+        try:
+            line["extra"]["deterministic_backward"] = deterministic_cost(w)
+        except Exception as exc:
+            print(f"[bench] deterministic timing failed ({exc!r})", file=sys.stderr)
     if world > 1:
         line["nccl"] = nccl_info()
     del w, l2

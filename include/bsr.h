@@ -145,6 +145,18 @@ int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream);
 int bsr_frame_snapshot_bytes(uint64_t *bytes);
 int bsr_frame_status_async(const void *frame, void *snapshot, void *stream);
 int bsr_frame_snapshot_decode(const void *snapshot, bsr_frame_info *info);
+/* Deterministic backward (the reference's bitwise determinism for a fixed input,
+ * SPEC.md:334, _raster.pyx:273-286): the same gradients as bsr_backward, but every
+ * per-primitive partial is summed as a 64-bit fixed-point integer (two passes: magnitude
+ * bound, then the sums), so results are bitwise identical run to run whatever order the
+ * device's atomics land in.  det_ws: caller-owned device workspace of
+ * bsr_det_workspace_bytes(n) bytes, 256-byte aligned.  drgb: as bsr_backward_deferred_color
+ * (SH colour, multi-view), or NULL for the full chain. */
+int bsr_det_workspace_bytes(int64_t n, uint64_t *bytes);
+int bsr_backward_deterministic(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                               void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
+                               const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
+                               float *drgb, void *det_ws, uint64_t det_ws_bytes, void *stream);
 /* d_color: (H,W,3) dL/d color (clamped image); d_depth: (H,W) or NULL. */
 int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                  void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,

@@ -102,6 +102,10 @@ EXPORTS = {
     "bsr_backward_deferred_color": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64,
                                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_void_p]),
+    "bsr_det_workspace_bytes": (c_int32, [c_int64, c_void_p]),
+    "bsr_backward_deterministic": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
+                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_uint64,
+                                             c_void_p]),
     "bsr_color_grad_views": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "bsr_core_scratch_bytes": (c_int32, [c_int64, c_int32, c_int32, c_int64, c_void_p]),
     "bsr_core_forward_tiled": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -318,10 +318,30 @@ extern "C" int bsr_frame_snapshot_decode(const void *snapshot, bsr_frame_info *i
     return c.status;
 }
 
+// Deterministic mode: fixed-point sums -> grad_acc (float) / side64 (the xy-frame fp64
+// partials of fp64-path records without a factor), for every visible primitive.
+__global__ void det_finalize_kernel(FrameView f) {
+    pdl_wait();
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < f.n; c += (int64_t)gridDim.x * blockDim.x) {
+        if (!f.tile_count[c]) continue;
+        double l11, l21, l22;
+        const bool factor = record_factor64(f, (uint32_t)c, l11, l21, l22);
+        for (int k = 0; k < 11; ++k) {
+            const int64_t q = (int64_t)kDetSlots * c + k;
+            const uint32_t b = f.det.bound[q];
+            const double v = b ? ldexp((double)(long long)f.det.acc[q], det_exp(b) - 38) : 0.0;
+            if (k < 5 && !factor)
+                f.side64[kSide64 * c + k] = v;
+            else
+                f.grad_acc[kGradStride * c + k] = (float)v;
+        }
+    }
+}
+
 static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                          void *frame, uint64_t frame_bytes, int64_t entry_cap, const float *d_color,
                          const float *d_depth, const bsr_grads *grads, float *screen_grad_norm,
-                         const bsr_profile *prof, float *drgb, void *stream) {
+                         const bsr_profile *prof, float *drgb, void *stream, void *det_ws = nullptr) {
     if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || bad_grads(scene, grads))
         return BSR_ERR_BAD_ARG;
     if (drgb && scene->color_model != BSR_COLOR_SH) return BSR_ERR_BAD_ARG;
@@ -334,6 +354,33 @@ static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const
     if ((rc = mark(prof, 0, st))) return rc;
     BSR_CUDA_TRY((pdl_launch(zero_acc_kernel, dim3((unsigned)imin64(div_up(f.n * kGradStride / 4, BSR_BLOCK), 148 * 8)), dim3(BSR_BLOCK), 0, st, f)));
     BSR_LAUNCH_CHECK();
+    const double bg64_[3] = {background[0], background[1], background[2]};
+    if (det_ws) {
+        // deterministic mode (frame.cuh DetAcc): bound pass, fixed-point pass, finalize;
+        // replay and raster run in sequence on the caller's stream
+        bsr_outputs none_;
+        memset(&none_, 0, sizeof(none_));
+        FrameView fd = f;
+        fd.det.bound = static_cast<uint32_t *>(det_ws);
+        fd.det.acc = reinterpret_cast<unsigned long long *>(
+            static_cast<char *>(det_ws) + align_up(4ull * kDetSlots * f.n, 256));
+        BSR_CUDA_TRY(cudaMemsetAsync(det_ws, 0, align_up(4ull * kDetSlots * f.n, 256) + 8ull * kDetSlots * f.n, st));
+        for (int mode = 1; mode <= 2; ++mode) {
+            fd.det.mode = mode;
+            if ((rc = launch_replay_scene(false, fd, *scene, cam, none_, bg64_, kAlphaMin, kTStop, d_color, d_depth, st)))
+                return rc;
+            if ((rc = launch_raster_bwd(fd, d_color, true, d_depth, background, (float)kAlphaMin, nullptr, nullptr,
+                                        nullptr, nullptr, st)))
+                return rc;
+        }
+        BSR_CUDA_TRY((pdl_launch(det_finalize_kernel, dim3(148 * 8), dim3(BSR_BLOCK), 0, st, fd)));
+        BSR_LAUNCH_CHECK();
+        if ((rc = mark(prof, 1, st))) return rc;
+        if ((rc = mark(prof, 2, st))) return rc;
+        if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, reinterpret_cast<float4 *>(drgb), st)))
+            return rc;
+        return mark(prof, 3, st);
+    }
     // fork: the fp64 replay of the flagged pixels runs beside the fp32 raster backward
     SideStream *ss = nullptr;
     if ((rc = side_stream(&ss))) return rc;
@@ -355,6 +402,25 @@ static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const
     if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, reinterpret_cast<float4 *>(drgb), st)))
         return rc;
     return mark(prof, 3, st);
+}
+
+extern "C" int bsr_det_workspace_bytes(int64_t n, uint64_t *bytes) {
+    if (!bytes || n < 0) return BSR_ERR_BAD_ARG;
+    *bytes = align_up(4ull * kDetSlots * (uint64_t)n, 256) + 8ull * kDetSlots * (uint64_t)n;
+    return BSR_OK;
+}
+
+extern "C" int bsr_backward_deterministic(const bsr_scene *scene, const bsr_camera *camera,
+                                          const float background[3], void *frame, uint64_t frame_bytes,
+                                          int64_t entry_cap, const float *d_color, const float *d_depth,
+                                          const bsr_grads *grads, float *screen_grad_norm, float *drgb,
+                                          void *det_ws, uint64_t det_ws_bytes, void *stream) {
+    uint64_t need = 0;
+    if (!det_ws || bsr_det_workspace_bytes(scene ? scene->n : 0, &need) || det_ws_bytes < need ||
+        (reinterpret_cast<uintptr_t>(det_ws) & 255) || (drgb && (reinterpret_cast<uintptr_t>(drgb) & 15)))
+        return BSR_ERR_BAD_ARG;
+    return backward_impl(scene, camera, background, frame, frame_bytes, entry_cap, d_color, d_depth, grads,
+                         screen_grad_norm, nullptr, drgb, stream, det_ws);
 }
 
 extern "C" int bsr_backward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],

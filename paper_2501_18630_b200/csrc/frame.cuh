@@ -33,6 +33,35 @@ struct Counters {
     uint32_t pad[5];
 };
 
+// Deterministic accumulation of the backward's per-primitive partials
+// (bsr_backward_deterministic): float atomics land in a run-dependent order and their sums
+// differ in the last bits, so in this mode every value is added as a 64-bit fixed-point
+// integer (integer addition is associative: the sum does not depend on the order).  Pass 1
+// (mode 1) records per primitive and slot the largest magnitude that will be added
+// (atomicMax on the float bits, itself order-independent); pass 2 (mode 2) recomputes the
+// same values and adds round(v * 2^(38 - e)), e = exponent of that bound, so every term is
+// below 2^39 in magnitude and up to 2^24 terms fit in 63 bits with a resolution of
+// bound * 2^-39; a finalize kernel converts the sums back (det_finalize in api.cu).
+constexpr int kDetSlots = 12;  // grad_acc's 11 slots (fp64-path xy partials reuse 0..4)
+struct DetAcc {
+    int mode;                  // 0: off (float / fp64 atomics), 1: bound pass, 2: fixed-point pass
+    uint32_t *bound;           // [N][kDetSlots] float bits of max |value|
+    unsigned long long *acc;   // [N][kDetSlots] fixed-point sums (two's complement)
+};
+
+__device__ __forceinline__ int det_exp(uint32_t bound_bits) { return (int)((bound_bits >> 23) & 0xff) - 127; }
+
+__device__ __forceinline__ void det_add(const DetAcc &d, uint32_t c, int slot, double v) {
+    const int64_t k = (int64_t)kDetSlots * c + slot;
+    if (d.mode == 1) {
+        const float av = fabsf((float)v);
+        if (av > 0.f) atomicMax(d.bound + k, __float_as_uint(av));
+    } else if (v != 0.0) {
+        const long long qv = __double2ll_rn(ldexp(v, 38 - det_exp(d.bound[k])));
+        atomicAdd(d.acc + k, (unsigned long long)qv);
+    }
+}
+
 struct FrameView {
     // --- zeroed every forward (one memset) ---
     Counters *ctr;
@@ -69,6 +98,7 @@ struct FrameView {
                              // l22); without one (.y == 0) [0..4] = xy-frame geometry partials
                              // summed in fp64 (add_geom64; zeroed by preprocess, re-zeroed when
                              // preprocess_bwd consumes them)
+    DetAcc det;              // deterministic-backward workspace (mode 0 outside bsr_backward_deterministic)
     // --- sizes ---
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles;
@@ -82,6 +112,9 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     FrameView f;
     f.n = n;
     f.entry_cap = entry_cap;
+    f.det.mode = 0;
+    f.det.bound = nullptr;
+    f.det.acc = nullptr;
     f.W = W;
     f.H = H;
     f.tiles_x = (W + BSR_TILE - 1) / BSR_TILE;
@@ -132,14 +165,16 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
 // have no usable factor (fp64-path records whose conic is not positive definite in fp64):
 // without a whitened frame their conic gradient's short-axis part is a cancellation of
 // large xy terms, so it is formed from the fp64 mean / conic and summed in fp64.
-__device__ __forceinline__ void add_geom64(double *g, double d_x, double dx, double dy, double ca, double cb,
-                                           double cc) {
+__device__ __forceinline__ void add_geom64(const FrameView &f, uint32_t c, double d_x, double dx, double dy,
+                                           double ca, double cb, double cc) {
     const double ga = ca * dx + cb * dy, gb = cb * dx + cc * dy;
-    atomicAdd(g + 0, -2.0 * d_x * ga);
-    atomicAdd(g + 1, -2.0 * d_x * gb);
-    atomicAdd(g + 2, d_x * dx * dx);
-    atomicAdd(g + 3, 2.0 * d_x * dx * dy);
-    atomicAdd(g + 4, d_x * dy * dy);
+    const double v[5] = {-2.0 * d_x * ga, -2.0 * d_x * gb, d_x * dx * dx, 2.0 * d_x * dx * dy, d_x * dy * dy};
+    if (f.det.mode) {
+        for (int q = 0; q < 5; ++q) det_add(f.det, c, q, v[q]);
+        return;
+    }
+    double *g = f.side64 + (int64_t)kSide64 * c;
+    for (int q = 0; q < 5; ++q) atomicAdd(g + q, v[q]);
 }
 
 }  // namespace bsr

@@ -61,8 +61,8 @@ __device__ __noinline__ Pair unsafe_pair_bwd(const double *m64, const double *s6
 // uniform within each group of GL lanes, so the five partials are summed over the group in
 // fp64 with shuffles and its first lane adds them.
 template <int GL>
-__device__ __noinline__ void unsafe_geom_bwd(double *side64, const double *rec64, uint32_t c, float d_x, int px,
-                                             int py, bool mine, unsigned gmask_any) {
+__device__ __noinline__ void unsafe_geom_bwd(double *side64, const double *rec64, DetAcc det, uint32_t c, float d_x,
+                                             int px, int py, bool mine, unsigned gmask_any) {
     double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (mine) {
         const double *m64 = rec64 + kRec64 * (int64_t)c;
@@ -81,8 +81,13 @@ __device__ __noinline__ void unsafe_geom_bwd(double *side64, const double *rec64
     if ((lane % GL) == 0 && ((gmask_any >> lane) & 1u)) {
         double *g = side64 + (int64_t)kSide64 * c;
 #pragma unroll
-        for (int q = 0; q < 5; ++q)
-            if (v[q] != 0.0) atomicAdd(g + q, v[q]);
+        for (int q = 0; q < 5; ++q) {
+            if (v[q] == 0.0) continue;
+            if (det.mode)
+                det_add(det, c, q, v[q]);
+            else
+                atomicAdd(g + q, v[q]);
+        }
     }
 }
 
@@ -127,7 +132,9 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // lane that does not take the pair (outside its last contributor, alpha < alpha_min, or
 // its group's list exhausted) runs it with alpha = 0 and dL/dalpha = 0, which leaves its
 // state (T, behind colour) exactly unchanged and all 11 partials exactly 0.
-template <bool STATS, int G>
+// DET: 0 float atomics into grad_acc; 1 / 2 the deterministic bound / fixed-point passes
+// (frame.cuh DetAcc) -- the same values, added through det_add.
+template <bool STATS, int G, int DET>
 __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
     pdl_wait();
     using SB = SubBlock<G>;
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                     constexpr uint32_t gm = GL >= 32 ? 0xffffffffu : ((1u << (GL & 31)) - 1u);
                     if (um & (gm << ((g * GL) & 31))) lead |= 1u << ((g * GL) & 31);
                 }
-                unsafe_geom_bwd<GL>(f.side64, f.rec64, s_cidx[j], d_x, px, py, geom64 && took, lead);
+                unsafe_geom_bwd<GL>(f.side64, f.rec64, f.det, s_cidx[j], d_x, px, py, geom64 && took, lead);
             }
         }
         // geometry partials in the record's whitened frame (frame.cuh grad_acc, factor L of
@@ -282,7 +289,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         v[8] = w * g1;
         v[9] = w * g2;
         v[10] = w * gd;
-        float *dst = f.grad_acc + (int64_t)s_cidx[j] * kGradStride;
+        const uint32_t cj = s_cidx[j];
+        float *dst = f.grad_acc + (int64_t)cj * kGradStride;
+        auto acc = [&](int k, float val) {
+            if (DET == 0)
+                atomicAdd(dst + k, val);
+            else
+                det_add(f.det, cj, k, (double)val);
+        };
         // few contributors: direct atomics beat the reduction
         int most = __popc(tm);
         if (GL < 32) {
@@ -295,7 +309,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
             if (took) {
 #pragma unroll
                 for (int qq = 0; qq < 11; ++qq)
-                    if (v[qq] != 0.0f) atomicAdd(dst + qq, v[qq]);
+                    if (v[qq] != 0.0f) acc(qq, v[qq]);
             }
             return;
         }
@@ -305,10 +319,10 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         group_reduce16<GL>(v, lane, r0, r1);
         const int idx = reduce_index<GL>(lane % GL);
         if (GL == 32) {
-            if (!(lane & 1) && idx < 11 && r0 != 0.0f) atomicAdd(dst + idx, r0);
+            if (!(lane & 1) && idx < 11 && r0 != 0.0f) acc(idx, r0);
         } else {
-            if (idx < 11 && r0 != 0.0f) atomicAdd(dst + idx, r0);
-            if (GL == 8 && idx + 1 < 11 && r1 != 0.0f) atomicAdd(dst + idx + 1, r1);
+            if (idx < 11 && r0 != 0.0f) acc(idx, r0);
+            if (GL == 8 && idx + 1 < 11 && r1 != 0.0f) acc(idx + 1, r1);
         }
     };
 
@@ -404,9 +418,13 @@ int raster_groups();
 template <int G>
 static int launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
     if (stats)
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G, 0>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    else if (a.f.det.mode == 1)
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 1>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    else if (a.f.det.mode == 2)
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 2>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 0>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     return BSR_OK;
 }
 

@@ -380,28 +380,37 @@ __device__ void replay_bwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
             const double g_dot_behind = g0 * behind0 + g1 * behind1 + g2 * behind2;
             double d_alpha = g_dot_col * my_t - g_dot_behind / (1.0 - alpha);
             d_alpha = d_alpha + (gd * en.z * my_t - gd * behindd / (1.0 - alpha));
+            // partial -> slot of primitive c: float atomics, or the deterministic fixed-point
+            // accumulator (frame.cuh DetAcc); the float rounding of the value is the same in
+            // both, so both modes sum the same terms
             float *acc = f.grad_acc + (int64_t)c * kGradStride;
-            atomicAdd(acc + 7, (float)(weight * g0));
-            atomicAdd(acc + 8, (float)(weight * g1));
-            atomicAdd(acc + 9, (float)(weight * g2));
-            atomicAdd(acc + 10, (float)(weight * gd));
-            atomicAdd(acc + 5, (float)(d_alpha * kernel));
+            auto add = [&](int slot, double v) {
+                if (f.det.mode)
+                    det_add(f.det, c, slot, (double)(float)v);
+                else
+                    atomicAdd(acc + slot, (float)v);
+            };
+            add(7, weight * g0);
+            add(8, weight * g1);
+            add(9, weight * g2);
+            add(10, weight * gd);
+            add(5, d_alpha * kernel);
             const double d_kernel = d_alpha * en.o;
             if (x < 1.0) {
-                atomicAdd(acc + 6, (float)(d_kernel * kernel * log(1.0 - x)));
+                add(6, d_kernel * kernel * log(1.0 - x));
                 double dkdx = -en.beta * pow(1.0 - x, en.beta - 1.0);
                 if (dkdx < -1e7) dkdx = -1e7;
                 const double d_x = d_kernel * dkdx;
                 double l11, l21, l22;
                 if (!record_factor64(f, c, l11, l21, l22)) {  // no factor: xy-frame fp64 partials
-                    add_geom64(f.side64 + (int64_t)kSide64 * c, d_x, dx, dy, en.ca, en.cb, en.cc);
+                    add_geom64(f, c, d_x, dx, dy, en.ca, en.cb, en.cc);
                 } else {  // whitened frame of the record's factor (frame.cuh grad_acc)
                     const double u = l11 * dx + l21 * dy, w = l22 * dy;
-                    atomicAdd(acc + 0, (float)(d_x * u));
-                    atomicAdd(acc + 1, (float)(d_x * w));
-                    atomicAdd(acc + 2, (float)(d_x * u * u));
-                    atomicAdd(acc + 3, (float)(d_x * u * w));
-                    atomicAdd(acc + 4, (float)(d_x * w * w));
+                    add(0, d_x * u);
+                    add(1, d_x * w);
+                    add(2, d_x * u * u);
+                    add(3, d_x * u * w);
+                    add(4, d_x * w * w);
                 }
             }
         }

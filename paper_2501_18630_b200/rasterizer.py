@@ -267,12 +267,21 @@ def outputs_c(color=None, raw=None, alpha=None, trans=None, depth=None, pixel_co
     return o
 
 
+def det_workspace(n: int, device=None) -> torch.Tensor:
+    """Device workspace of bsr_backward_deterministic for n primitives (256-byte aligned)."""
+    out = ctypes.c_uint64()
+    _lib.check(_lib.load().bsr_det_workspace_bytes(int(n), ctypes.byref(out)), "det_workspace")
+    return torch.empty(max(int(out.value), 1), dtype=torch.uint8, device=device or "cuda")
+
+
 def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameState,
                  d_color: torch.Tensor, d_depth: torch.Tensor | None, grads: _lib.GradsC,
                  screen_grad_norm: torch.Tensor | None = None, profile: _lib.ProfileC | None = None,
-                 drgb: torch.Tensor | None = None):
+                 drgb: torch.Tensor | None = None, det_ws: torch.Tensor | None = None):
     """bsr_backward; with ``drgb`` (float32 (N, 4), SH colour) the colour chain is deferred
-    into it (bsr_backward_deferred_color) for a later color_grad_views over all views."""
+    into it (bsr_backward_deferred_color) for a later color_grad_views over all views.  With
+    ``det_ws`` (det_workspace) the deterministic backward (bsr_backward_deterministic):
+    bitwise identical gradients run to run."""
     lib = _lib.load()
     cam = _lib.camera_c(camera)
     if d_color.dtype != torch.float32 or not d_color.is_contiguous() or not d_color.is_cuda:
@@ -283,7 +292,10 @@ def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameSta
             frame.nbytes, frame.entry_cap, ctypes.c_void_p(d_color.data_ptr()),
             None if d_depth is None else ctypes.c_void_p(d_depth.data_ptr()), ctypes.byref(grads),
             _lib.ptr(screen_grad_norm), None if profile is None else ctypes.byref(profile))
-    if drgb is None:
+    if det_ws is not None:
+        rc = lib.bsr_backward_deterministic(*args[:10], _lib.ptr(drgb), ctypes.c_void_p(det_ws.data_ptr()),
+                                            det_ws.numel(), _stream())
+    elif drgb is None:
         rc = lib.bsr_backward(*args, _stream())
     else:
         rc = lib.bsr_backward_deferred_color(*args, ctypes.c_void_p(drgb.data_ptr()), _stream())
@@ -350,11 +362,15 @@ def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, 
 
 
 def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, forward_out=None,
-                    threads=None, core=None, d_depth=None, grads: GradientBuffer | None = None) -> GradientBuffer:
+                    threads=None, core=None, d_depth=None, grads: GradientBuffer | None = None,
+                    deterministic: bool = False) -> GradientBuffer:
     """rasterizer.py:230-321 on the B200: exact analytic gradients of the rendered image.
 
     ``grads`` (extension): an existing GradientBuffer of ``prims`` the gradients are ADDED
-    into (multi-view accumulation without a fresh buffer per view); returned."""
+    into (multi-view accumulation without a fresh buffer per view); returned.
+    ``deterministic``: bitwise-reproducible gradients (the reference's contract for a fixed
+    input) via fixed-point accumulation (bsr_backward_deterministic), at about
+    twice the raster-backward cost."""
     _check_core(core)
     if grads is None:
         grads = GradientBuffer.zeros_for(prims)
@@ -369,7 +385,8 @@ def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, fo
     if d_depth is not None:
         d_depth = torch.as_tensor(d_depth, dtype=torch.float32, device=dev).contiguous()
     backward_raw(_prims_scene_c(prims), camera, background, forward_out.frame, d_color, d_depth,
-                 grads_c(grads), grads.screen_grad_norm)
+                 grads_c(grads), grads.screen_grad_norm,
+                 det_ws=det_workspace(len(prims), dev) if deterministic else None)
     return grads
 
 

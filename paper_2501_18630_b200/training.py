@@ -25,7 +25,7 @@ from . import _lib
 from .camera import Camera
 from .distributed import allreduce_grads
 from .primitive import GradientBuffer, PrimitiveSet
-from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, color_grad_views, forward_raw,
+from .rasterizer import (FrameState, _bg_arr, _prims_scene_c, backward_raw, color_grad_views, det_workspace, forward_raw,
                          frame_status, grads_c, outputs_c)
 
 ADAM_BETA1 = 0.9  # training.py:31
@@ -334,12 +334,14 @@ class TrainStep:
 
     def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
                  lambda_ssim=0.2, process_group=None, cfg: TrainConfig | None = None, scene_scale=1.0,
-                 noise_rng=None, defer_color=True):
+                 noise_rng=None, defer_color=True, deterministic=False):
         """``cfg`` switches on the reference's full optimiser step (training.py:357-366):
         opacity / scale regularisers, the exponential position-lr schedule and the
         covariance-shaped position noise, all evaluated on the device from the device step
         counter (graph-capturable).  Without it the step is the BASELINE configs' (L1 +
-        D-SSIM, constant group learning rates, no noise)."""
+        D-SSIM, constant group learning rates, no noise).  ``deterministic`` runs every
+        view's backward in the fixed-point mode (bsr_backward_deterministic): the whole step,
+        Adam included, is bitwise reproducible on one GPU."""
         self.prims = prims
         self.cfg = cfg
         self.scene_scale = float(scene_scale)
@@ -380,6 +382,7 @@ class TrainStep:
         self.drgb = None
         if len(self.cameras) > 1 and prims.color_model == "sh" and defer_color:
             self.drgb = torch.empty((len(self.cameras), prims.n, 4), dtype=torch.float32, device=dev)
+        self.det_ws = det_workspace(prims.n, dev) if deterministic else None
         self.profile = None  # optional rasterizer.StageProfiler-like object with .fwd/.bwd
         self._grads_clear = False  # the last step's Adam zeroed self.grads
 
@@ -406,7 +409,7 @@ class TrainStep:
                 prof.mark_loss(i, end=True)
             backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
                          profile=None if prof is None else prof.bwd(i),
-                         drgb=None if self.drgb is None else self.drgb[i])
+                         drgb=None if self.drgb is None else self.drgb[i], det_ws=self.det_ws)
         if self.drgb is not None:
             if prof is not None and hasattr(prof, "mark_color"):
                 prof.mark_color()

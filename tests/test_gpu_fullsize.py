@@ -26,3 +26,28 @@ def test_full_size_parity(cuda, cfg, view, bwd):
     assert fok, msg
     if bwd:
         assert gok, msg
+
+
+def test_full_size_deterministic_backward_c1(cuda):
+    """Config 1 at full size in the deterministic mode: bitwise identical gradients in two
+    runs, and the parity bar against the oracle."""
+    import numpy as np
+    import torch
+
+    import fullsize
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import PrimitiveSet, render_backward, render_tiled
+    from paper_2501_18630_b200.scenes import make_workload
+
+    wl = make_workload("c1", seed=0)
+    cam, bg = wl.cameras[0], wl.background
+    prims = PrimitiveSet.from_scene(wl.scene)
+    out = render_tiled(prims, cam, bg)
+    ref = orc.forward(wl.scene, cam, bg, core="c")
+    up = fullsize.upstream("c1", 100_000, cam, bg, out, ref["raw"])
+    g1 = render_backward(prims, cam, bg, up, forward_out=out, deterministic=True)
+    g2 = render_backward(prims, cam, bg, up, forward_out=out, deterministic=True)
+    assert torch.equal(g1.flat.view(torch.int32), g2.flat.view(torch.int32))
+    ref_g = orc.backward(wl.scene, cam, bg, up.astype(np.float64), ref, core="c")
+    rep = fullsize.compare_grads(g1, ref_g)
+    assert fullsize.grads_ok(rep), rep
