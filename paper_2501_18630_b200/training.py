@@ -334,14 +334,17 @@ class TrainStep:
 
     def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
                  lambda_ssim=0.2, process_group=None, cfg: TrainConfig | None = None, scene_scale=1.0,
-                 noise_rng=None, defer_color=True, deterministic=False):
+                 noise_rng=None, defer_color=True, deterministic=False, shard_optimizer=True):
         """``cfg`` switches on the reference's full optimiser step (training.py:357-366):
         opacity / scale regularisers, the exponential position-lr schedule and the
         covariance-shaped position noise, all evaluated on the device from the device step
         counter (graph-capturable).  Without it the step is the BASELINE configs' (L1 +
         D-SSIM, constant group learning rates, no noise).  ``deterministic`` runs every
         view's backward in the fixed-point mode (bsr_backward_deterministic): the whole step,
-        Adam included, is bitwise reproducible on one GPU."""
+        Adam included, is bitwise reproducible on one GPU.  With a ``process_group`` the
+        exchange is reduce-scatter -> Adam on this rank's shard -> all-gather
+        (distributed.ShardedOptimizer) unless ``shard_optimizer`` is False (all-reduce +
+        replicated Adam)."""
         self.prims = prims
         self.cfg = cfg
         self.scene_scale = float(scene_scale)
@@ -360,8 +363,16 @@ class TrainStep:
         self.lrs = lrs or (group_lrs() if prims.color_model == "sh" else sb_group_lrs())
         self.lambda_ssim = lambda_ssim
         self.pg = process_group
-        self.grads = GradientBuffer.zeros_for(prims)
-        self.adam = AdamState(prims)
+        self.sharded = None
+        if process_group is not None and shard_optimizer:
+            from .distributed import ShardedOptimizer
+
+            self.sharded = ShardedOptimizer(prims, GradientBuffer, process_group)
+            self.grads = self.sharded.grads
+            self.adam = self.sharded  # exp_avg / exp_avg_sq / step_dev of this rank's shard
+        else:
+            self.grads = GradientBuffer.zeros_for(prims)
+            self.adam = AdamState(prims)
         self.scene = _prims_scene_c(prims)
         self.gc = grads_c(self.grads)
         dev = prims.flat.device
@@ -419,6 +430,25 @@ class TrainStep:
         cfg = self.cfg
         if cfg is not None and self.rank0:  # direct regulariser terms, once per iteration
             regularizers_into(self.prims, self.grads, cfg.lambda_opacity, cfg.lambda_scale, self.loss_values[0])
+        if self.sharded is not None:  # reduce-scatter -> sharded Adam -> all-gather (distributed.py)
+            if prof is not None:
+                prof.mark_adam()
+            sh = self.sharded
+            sh.reduce_scatter()
+            if adam:
+                _sharded_adam(sh, self.lrs, None if cfg is None else self.schedule)
+                sh.all_gather()
+            sh.gbuf.zero_()  # the next step accumulates from zero
+            self._grads_clear = True
+            if adam and cfg is not None:
+                lc = self.prims.layout_c()
+                rc = _lib.load().bsr_inject_noise(self.prims.flat.data_ptr(), ctypes.byref(lc), float(cfg.noise_lr),
+                                                  0.0, ctypes.byref(self.schedule), sh.step_dev.data_ptr(),
+                                                  None, self.noise_rng.seed, self.noise_offset, None, _stream())
+                _lib.check(rc, "inject_noise")
+            if prof is not None:
+                prof.mark_adam(end=True)
+            return self.loss_values
         if self.pg is not None:  # the one exchange step of view-batch DP (distributed.py)
             allreduce_grads(self.grads.flat, group=self.pg)
         if adam:
@@ -463,6 +493,23 @@ class TrainStep:
         """Host-side check of every frame's device status (capacity / errors)."""
         for f in self.frames.values():
             frame_status(f)
+
+
+def _sharded_adam(sh, lrs: dict, schedule=None):
+    """The fused Adam kernel on this rank's shard (distributed.ShardedOptimizer): shard
+    pointers, the global group ends shifted into shard coordinates, the device step counter
+    bumped by the kernel (graph-capturable)."""
+    groups = sh.prims.groups
+    ends = (ctypes.c_int64 * len(groups))(*sh.shard_group_ends())
+    lr = (ctypes.c_float * len(groups))(*[float(lrs[g]) for g in groups])
+    p = sh.pbuf[sh.lo: sh.lo + sh.shard]
+    rc = _lib.load().bsr_adam_step_fused(p.data_ptr(), sh.gshard.data_ptr(), sh.exp_avg.data_ptr(),
+                                         sh.exp_avg_sq.data_ptr(), sh.shard, len(groups), ends, lr,
+                                         sh._step_buf.data_ptr(),
+                                         None if schedule is None else ctypes.byref(schedule),
+                                         groups.index("positions") if schedule is not None else -1,
+                                         ADAM_BETA1, ADAM_BETA2, ADAM_EPS, 0, _stream())
+    _lib.check(rc, "adam (shard)")
 
 
 def render_targets(target_prims: PrimitiveSet, cameras, background):
