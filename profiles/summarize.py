@@ -27,6 +27,10 @@ RAW_METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_execut
                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
                "sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+               "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+               "smsp__issue_active.avg.pct_of_peak_sustained_active",
                "sm__inst_executed_pipe_xu.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
                "gpu__time_duration.sum"]
 
