@@ -518,7 +518,11 @@ def e2e_api_loop(w, steps, world):
             w["e2e_host"] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t.cpu())
                              for t in w["targets"]]
         host = w["e2e_host"]
-        tgt = [torch.empty_like(t) for t in w["targets"]]
+        # two device copies of the targets: step i+1's upload (copy stream) overlaps step i
+        tgt2 = [[torch.empty_like(t) for t in w["targets"]] for _ in range(2)]
+        cs = torch.cuda.Stream()
+        up_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        used_ev = [torch.cuda.Event(), torch.cuda.Event()]
         ws = {}
         for cam in cams:
             ws.setdefault((cam.width, cam.height), LossWorkspace(cam.width, cam.height))
@@ -545,8 +549,19 @@ def e2e_api_loop(w, steps, world):
             with torch.cuda.stream(side):  # frame i downloads while frame i+1 renders
                 img_host[i % 2].copy_(out.color, non_blocking=True)
             return 1
-        for v in range(len(cams)):
-            tgt[v].copy_(host[v], non_blocking=True)
+        b = i % 2
+        if i == 0:  # the first step's inputs (later ones were prefetched by the previous step)
+            with torch.cuda.stream(cs):
+                for v in range(len(cams)):
+                    tgt2[0][v].copy_(host[v], non_blocking=True)
+                up_ev[0].record(cs)
+        with torch.cuda.stream(cs):  # prefetch step i+1's inputs once step i-1 released the buffer
+            cs.wait_event(used_ev[b ^ 1])
+            for v in range(len(cams)):
+                tgt2[b ^ 1][v].copy_(host[v], non_blocking=True)
+            up_ev[b ^ 1].record(cs)
+        main.wait_event(up_ev[b])
+        tgt = tgt2[b]
         grads = GradientBuffer.zeros_for(prims)
         for v, cam in enumerate(cams):
             out = render_tiled(prims, cam, bg)
@@ -557,12 +572,16 @@ def e2e_api_loop(w, steps, world):
             dd.allreduce_grads(grads.flat)
         if state is not None:
             adam_step(prims, grads, state, lrs, device_step=True)
+        used_ev[b].record(main)
         vals_host.copy_(vals, non_blocking=True)
         return len(cams)
 
     for i in range(3):  # untimed: allocator / capacity warm-up
         step(i)
     torch.cuda.synchronize()
+    if train:  # the timed loop starts from step 0 again (no upload in flight)
+        for ev in used_ev:
+            ev.record(main)
     check_pending(block=True)
     warm_host_link()
     barrier(world)
@@ -571,8 +590,7 @@ def e2e_api_loop(w, steps, world):
     views = 0
     for i in range(steps):
         views += step(i)
-    if not train:
-        main.wait_stream(side)
+    main.wait_stream(side if not train else cs)  # the last prefetch / download is part of the run
     e.record(main)
     e.synchronize()
     ms = s.elapsed_time(e)
@@ -704,9 +722,11 @@ def measure(cfg, args, rank, world, local, K, W, want_cpu, want_e2e):
             ems_max = max_over_ranks(ems, world)
             e2e = {"value": sum_over_ranks(eviews, world) / (ems_max / 1e3), "unit": unit_for(cfg),
                    "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
-                   "path": "public API per step: pinned H2D of the inputs, render_tiled, training.loss_into, "
-                           "render_backward (+ all-reduce + adam_step), D2H of the loss values "
-                           "(config 2: render_tiled + D2H of the image), eager"}
+                   "path": "public API per step: render_tiled, training.loss_into, render_backward "
+                           "(+ all-reduce + adam_step), eager; each step's inputs copied H2D from pinned "
+                           "memory on a copy stream while the previous step computes (double-buffered), "
+                           "the loss values read back D2H (config 2: render_tiled + the image D2H on a "
+                           "side stream)"}
         except Exception as exc:
             if world == 1:
                 raise
