@@ -81,6 +81,8 @@ struct FrameView {
     uint32_t *tile_count;    // [N] tiles touched by source index, 0 = culled
     uint64_t *tent;          // [Ecap] (fp32 depth key << 32 | source index), scattered per tile
     uint32_t *lists;         // [Ecap] source index per tile entry in depth order (tile_ranges)
+    uint32_t *emask;         // [Ecap] sub-block occupancy mask of every tile entry the forward raster
+                             // reached (raster.cuh entry_tile_mask), reused by the backward
     float *t_final;          // [H*W]
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
@@ -150,6 +152,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.tile_count = (uint32_t *)take(4ull * n);
     f.tent = (uint64_t *)take(8ull * entry_cap);
     f.lists = (uint32_t *)take(4ull * entry_cap);
+    f.emask = (uint32_t *)take(4ull * entry_cap);
     f.t_final = (float *)take(4ull * npx);
     f.last = (uint32_t *)take(4ull * npx);
     f.flags = (uint2 *)take(8ull * npx);

@@ -193,19 +193,26 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
     } else {
         q4 = make_float4(sc.rotations[4 * i], sc.rotations[4 * i + 1], sc.rotations[4 * i + 2], sc.rotations[4 * i + 3]);
     }
+    // The chain's inputs (1 / |q|, exp(log_scale), 1 / t_z) come from fp32 transcendentals
+    // refined by one fp64 Newton step where a quotient feeds a cancellation (relative
+    // error <= ~1e-7 on an input is the fp32 parameters' own precision); the linear
+    // algebra below, where the cancellations happen, runs in T.  fp64 division, sqrt and
+    // exp sequences dominated the latency of the fp64 variant.
     T qw = q4.x, qx = q4.y, qy = q4.z, qz = q4.w;
-    const T qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-    qw /= qn;
-    qx /= qn;
-    qy /= qn;
-    qz /= qn;
+    const T qq = qw * qw + qx * qx + qy * qy + qz * qz;
+    T iqn = (T)rsqrtf((float)qq);
+    iqn = iqn * ((T)1.5 - (T)0.5 * qq * iqn * iqn);  // Newton step on 1 / sqrt(qq)
+    qw *= iqn;
+    qx *= iqn;
+    qy *= iqn;
+    qz *= iqn;
     const T one = 1, two = 2;
     T Q[9] = {one - two * (qy * qy + qz * qz), two * (qx * qy - qw * qz), two * (qx * qz + qw * qy),
               two * (qx * qy + qw * qz), one - two * (qx * qx + qz * qz), two * (qy * qz - qw * qx),
               two * (qx * qz - qw * qy), two * (qy * qz + qw * qx), one - two * (qx * qx + qy * qy)};
     T s2[3];
     for (int k = 0; k < 3; ++k) {
-        const T s = exp((T)sc.log_scales[3 * i + k]);
+        const T s = (T)expf(sc.log_scales[3 * i + k]);
         s2[k] = s * s;
     }
     T Sig[9];
@@ -213,7 +220,9 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
         for (int col = 0; col < 3; ++col)
             Sig[3 * r + col] = Q[3 * r] * s2[0] * Q[3 * col] + Q[3 * r + 1] * s2[1] * Q[3 * col + 1] +
                                Q[3 * r + 2] * s2[2] * Q[3 * col + 2];
-    const T itz = one / tz, itz2 = itz * itz;
+    T itz = (T)(1.0f / (float)tz);
+    itz = itz * (two - tz * itz);  // Newton step on 1 / t_z
+    const T itz2 = itz * itz;
     const T J00 = fx * itz, J02 = -fx * tx * itz2, J11 = fy * itz, J12 = -fy * ty * itz2;
     T Am[6];
     for (int j = 0; j < 3; ++j) {
@@ -273,7 +282,6 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
         const T gy = two * (-two * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - two * y * g[8]);
         const T gz = two * (-two * z * g[0] - w * g[1] + x * g[2] + w * g[3] - two * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
         const T dot = gw * w + gx * x + gy * y + gz * z;
-        const T iqn = one / qn;
         const float r0 = (float)((gw - dot * w) * iqn), r1 = (float)((gx - dot * x) * iqn);
         const float r2 = (float)((gy - dot * y) * iqn), r3 = (float)((gz - dot * z) * iqn);
         if (rot16) {

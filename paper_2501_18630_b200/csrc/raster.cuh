@@ -23,6 +23,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Shared-memory loads through a 32-bit shared-window address computed once per kernel:
+// indexing the double-buffered record arrays inside the pair lambdas made the compiler
+// rebuild the shared window base (S2R SR_CgaCtaId + 6 uniform ops) on every pair.
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 struct Pair {
     float dx, dy, u, w, r2, x, om, k, alpha;
 };
@@ -352,9 +371,11 @@ __device__ __forceinline__ uint32_t entry_tile_mask(const float4 A, const float4
 // single threads walking up to 16 rows; the parts are OR-combined (K | 32: an entry's
 // parts sit in one warp) and regathered per chunk through s_mask.  Chunks >= ceil(nb / 32)
 // of s_col are left untouched (never read).
+// gmask (optional): the batch's slice of FrameView::emask, where each entry's mask is also
+// stored for the backward.
 template <int G, bool BBOX>
 __device__ __forceinline__ void batch_masks(const Record *sr, int nb, int X0, int Y0, float alpha_min,
-                                            uint32_t *s_mask, uint32_t (*s_col)[32]) {
+                                            uint32_t *s_mask, uint32_t (*s_col)[32], uint32_t *gmask = nullptr) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     int K = 1;
     while (K < 8 && nb * K * 2 <= BSR_BLOCK) K <<= 1;
@@ -363,6 +384,7 @@ __device__ __forceinline__ void batch_masks(const Record *sr, int nb, int X0, in
         if (t < nb) {
             const Record &r = sr[t];
             m = entry_tile_mask<G, BBOX>(r.a, r.b, r.c, r.d, X0, Y0, alpha_min);
+            if (gmask) gmask[t] = m;
         }
         s_col[warp][lane] = warp_transpose32(m, lane);
         return;
@@ -374,7 +396,10 @@ __device__ __forceinline__ void batch_masks(const Record *sr, int nb, int X0, in
         m = entry_tile_mask<G, BBOX>(r.a, r.b, r.c, r.d, X0, Y0, alpha_min, part, K);
     }
     for (int o = 1; o < K; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
-    if (part == 0 && e < nb) s_mask[e] = m;
+    if (part == 0 && e < nb) {
+        s_mask[e] = m;
+        if (gmask) gmask[e] = m;
+    }
     __syncthreads();
     if (warp < ((nb + 31) >> 5)) {
         const int ee = 32 * warp + lane;

@@ -39,6 +39,7 @@ struct RasterBwdArgs {
     const Record *rec;
     unsigned long long *stats;  // optional: [2] evaluated pairs
     int direct_max;
+    const uint32_t *emask;      // the forward's per-entry sub-block masks, or nullptr (computed here)
 };
 
 // fp64 pair evaluation for fp32-unsafe primitives; kept out of line so the common fp32
@@ -211,16 +212,21 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     // one (pixel, entry) pair of the back-to-front replay (_raster.pyx:197-241) plus the
     // accumulation of its 11 partials; GL = lanes reduced together (32: the whole warp
     // walks one entry, L: every group its own)
-    auto pair = [&](const Record *s_rec, const uint32_t *s_cidx, int lo, int j, bool act, auto gl_tag) {
+    const uint32_t srecb0 = (uint32_t)(__cvta_generic_to_shared(&s_recb[0][0]));
+    const uint32_t scidxb0 = (uint32_t)(__cvta_generic_to_shared(&s_cidxb[0][0]));
+    // rbase / cbase: shared-window addresses of the current batch's records / indices
+    auto pair = [&](uint32_t rbase, uint32_t cbase, int lo, int j, bool act, auto gl_tag) {
         constexpr int GL = decltype(gl_tag)::value;
         const int e = lo + j;  // local entry index
-        const int4 bd = s_rec[j].d;
-        const float4 A = s_rec[j].a, Bq = s_rec[j].b, C = s_rec[j].c;
+        const uint32_t ra = rbase + (uint32_t)j * (uint32_t)sizeof(Record);
+        const int4 bd = lds_i4(ra + 48);
+        const float4 A = lds_f4(ra), Bq = lds_f4(ra + 16), C = lds_f4(ra + 32);
+        const uint32_t cj = lds_u32(cbase + 4u * (uint32_t)j);
         if (STATS) pairs += (act && e < last && px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
         Pair p;
         bool geom64 = false;  // fp64-path record without a factor: xy-frame fp64 partials
         if (C.w < 0.f) {  // needle or fp64 primitive (uniform per entry)
-            const uint32_t c = s_cidx[j];
+            const uint32_t c = cj;
             const float4 N = f.needle[c];
             if (N.x == N.x) {  // needle: compensated fp32 (same bits as the forward)
                 p = eval_needle(A, Bq, N, px - bd.x, py - bd.z);
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                     constexpr uint32_t gm = GL >= 32 ? 0xffffffffu : ((1u << (GL & 31)) - 1u);
                     if (um & (gm << ((g * GL) & 31))) lead |= 1u << ((g * GL) & 31);
                 }
-                unsafe_geom_bwd<GL>(f.side64, f.rec64, f.det, s_cidx[j], d_x, px, py, geom64 && took, lead);
+                unsafe_geom_bwd<GL>(f.side64, f.rec64, f.det, cj, d_x, px, py, geom64 && took, lead);
             }
         }
         // geometry partials in the record's whitened frame (frame.cuh grad_acc, factor L of
@@ -289,7 +295,6 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         v[8] = w * g1;
         v[9] = w * g2;
         v[10] = w * gd;
-        const uint32_t cj = s_cidx[j];
         float *dst = f.grad_acc + (int64_t)cj * kGradStride;
         auto acc = [&](int k, float val) {
             if (DET == 0)
@@ -337,14 +342,20 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         if (more) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncthreads();
         const Record *s_rec = s_recb[buf];
-        const uint32_t *s_cidx = s_cidxb[buf];
+        const uint32_t rbase = srecb0 + (uint32_t)(buf * BSR_BLOCK) * (uint32_t)sizeof(Record);
+        const uint32_t cbase = scidxb0 + 4u * (uint32_t)(buf * BSR_BLOCK);
         // ---- one thread per entry: which sub-blocks of the tile can it reach (bit columns
-        //      per chunk of 32 entries, see raster_fwd.cu)
+        //      per chunk of 32 entries, see raster_fwd.cu) -- the forward's masks when it kept
+        //      them (the same entry_tile_mask; every entry before maxlast was reached by it)
         {
             uint32_t m = 0;
             if (t < nb) {
-                const Record &r = s_rec[t];
-                m = entry_tile_mask<G, STATS>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
+                if (!STATS && a.emask) {
+                    m = a.emask[start + lo + t];
+                } else {
+                    const Record &r = s_rec[t];
+                    m = entry_tile_mask<G, STATS>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
+                }
             }
             s_col[warp][lane] = warp_transpose32(m, lane);
         }
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                 if (!bits) break;
                 const int jb = 31 - __clz(bits);
                 bits &= ~(1u << jb);
-                pair(s_rec, s_cidx, lo, (c << 5) + jb, true, std::integral_constant<int, 32>());
+                pair(rbase, cbase, lo, (c << 5) + jb, true, std::integral_constant<int, 32>());
             }
         } else {
             int c = glim > 0 ? (glim - 1) >> 5 : -1;
@@ -401,7 +412,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                 const bool act = bits != 0;
                 const int jb = act ? 31 - __clz(bits) : 0;
                 bits &= ~(1u << jb);
-                pair(s_rec, s_cidx, lo, act ? (c << 5) + jb : 0, act, std::integral_constant<int, L>());
+                pair(rbase, cbase, lo, act ? (c << 5) + jb : 0, act, std::integral_constant<int, L>());
             }
         }
     }
@@ -445,6 +456,7 @@ int launch_raster_bwd(const FrameView &f, const float *d_color, bool use_mask, c
     a.ranges = ranges;
     a.rec = rec;
     a.stats = stats;
+    a.emask = (lists == nullptr && f.entry_cap > 0) ? f.emask : nullptr;
     // warps with at most this many contributing lanes add their partials with direct
     // atomics instead of the 16-shuffle reduction (BSR_BWD_DIRECT overrides, for A/B)
     static const int direct_max = [] {

@@ -40,6 +40,7 @@ struct RasterFwdArgs {
     const uint2 *ranges;     // tile -> [start, end)
     const Record *rec;
     unsigned long long *stats;  // optional: [0] evaluated pairs, [1] contributions
+    uint32_t *emask;            // optional: per-entry sub-block masks kept for the backward
 };
 
 // fp64 evaluation of an fp32-unsafe primitive, out of line so the common fp32 path is not
@@ -100,23 +101,27 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         cp_async_commit();
     };
 
+    const uint32_t srec0 = (uint32_t)(__cvta_generic_to_shared(&s_rec[0][0]));
+    const uint32_t scidx0 = (uint32_t)(__cvta_generic_to_shared(&s_cidx[0][0]));
     // one (pixel, entry) pair of the front-to-back composite (_raster.pyx:101-123)
     auto pair = [&](int b0, int buf, int j) -> bool {
         bool took = false;
-        const int4 bd = s_rec[buf][j].d;
+        const uint32_t ra = srec0 + (uint32_t)(buf * BSR_BLOCK + j) * (uint32_t)sizeof(Record);
+        const int4 bd = lds_i4(ra + 48);
         if (stats) pairs += (px >= bd.x && px <= bd.y && py >= bd.z && py <= bd.w);
-        const float4 A = s_rec[buf][j].a, B = s_rec[buf][j].b, C = s_rec[buf][j].c;
+        const float4 A = lds_f4(ra), B = lds_f4(ra + 16), C = lds_f4(ra + 32);
+        const uint32_t cj = lds_u32(scidx0 + 4u * (uint32_t)(buf * BSR_BLOCK + j));
         const bool unsafe = C.w < 0.f;  // needle or fp64 record (uniform per entry)
         const float Q = fabsf(C.w);
         bool fp64 = false;
         Pair p;
         if (unsafe) {
-            const float4 N = f.needle[s_cidx[buf][j]];
+            const float4 N = f.needle[cj];
             if (N.x == N.x) {  // needle: compensated fp32
                 p = eval_needle(A, B, N, px - bd.x, py - bd.z);
             } else {
                 fp64 = true;
-                const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)s_cidx[buf][j], B, px, py);
+                const float2 u = unsafe_pair_fwd(f.rec64 + kRec64 * (int64_t)cj, B, px, py);
                 p.alpha = u.x;
                 p.om = u.y;
             }
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         const int nch = (nb + 31) >> 5;
         // ---- one thread per entry: which sub-blocks of the tile can it reach; transposed
         //      per chunk of 32 entries into one bit column per sub-block
-        batch_masks<G, stats>(s_rec[buf], nb, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min, s_mask, s_col);
+        batch_masks<G, stats>(s_rec[buf], nb, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min, s_mask, s_col,
+                              a.emask ? a.emask + b0 : nullptr);
         __syncthreads();
         // ---- this warp's groups: open (some pixel not finished) and how much their entry
         //      sets overlap; groups that mostly share entries walk the union together
@@ -331,6 +337,8 @@ int launch_raster_fwd(const FrameView &f, const bsr_outputs &out, const float bg
     a.ranges = ranges;
     a.rec = rec;
     a.stats = stats;
+    // the frame's own lists (not the core seam's external ones): keep the entry masks
+    a.emask = (lists == nullptr && f.entry_cap > 0) ? f.emask : nullptr;
     const bool contrib = out.contributions != nullptr, st_on = stats != nullptr;
     int rc = BSR_OK;
     switch (raster_groups()) {
