@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     // one (pixel, entry) pair of the back-to-front replay (_raster.pyx:197-241) plus the
     // accumulation of its 11 partials; GL = lanes reduced together (32: the whole warp
     // walks one entry, L: every group its own)
+    bool batch_nf = false;  // the current batch holds an fp64-path record without a factor
     const uint32_t srecb0 = (uint32_t)(__cvta_generic_to_shared(&s_recb[0][0]));
     const uint32_t scidxb0 = (uint32_t)(__cvta_generic_to_shared(&s_cidxb[0][0]));
     // rbase / cbase: shared-window addresses of the current batch's records / indices
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         const float dk = dalpha * Bq.y;
         const float d_x = dk * fmaxf(-beta * pw, -kEdgeGradClamp);
         float v[16];
-        {
+        if (batch_nf) {  // rare: checked per batch so the common path has no extra vote
             const unsigned um = __ballot_sync(0xffffffffu, geom64 && took);
             if (um) {
                 // group-leader lanes whose group has a contributing lane
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         // ---- one thread per entry: which sub-blocks of the tile can it reach (bit columns
         //      per chunk of 32 entries, see raster_fwd.cu) -- the forward's masks when it kept
         //      them (the same entry_tile_mask; every entry before maxlast was reached by it)
+        bool nf = false;
         {
             uint32_t m = 0;
             if (t < nb) {
@@ -356,10 +358,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
                     const Record &r = s_rec[t];
                     m = entry_tile_mask<G, STATS>(r.a, r.b, r.c, r.d, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min);
                 }
+                if (s_rec[t].c.w < 0.f) {
+                    const float4 N = f.needle[s_cidxb[buf][t]];
+                    nf = N.x != N.x && N.y == 0.f;
+                }
             }
             s_col[warp][lane] = warp_transpose32(m, lane);
         }
-        __syncthreads();
+        batch_nf = __syncthreads_or(nf);
         if (wlast <= lo) continue;
         // entries [lo, lo + lim) precede the group's / warp's furthest last contributor
         const int glim = min(nb, glast - lo), wlim = min(nb, wlast - lo);
