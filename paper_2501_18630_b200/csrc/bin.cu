@@ -515,14 +515,18 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_kernel(FrameView f) {
     __shared__ SortSmem<kBuckets> sm;
     if (over_capacity(f)) return;
     const uint2 rg = f.tile_ranges[blockIdx.x];
-    if ((int)(rg.y - rg.x) > kSortSmem) return;
+    if ((int)(rg.y - rg.x) > kSortSmem) {  // queue it (tile_cur, the scatter cursors, is free now)
+        if (threadIdx.x == 0) f.tile_cur[atomicAdd(&f.ctr->big_tiles, 1u)] = blockIdx.x;
+        return;
+    }
     sort_tile<kBuckets>(f, blockIdx.x, s, sm);
 }
 
 // Crowded tiles (more than kSortSmem entries; config 4's dense cluster reaches ~4200):
 // the same bucket sort with kBigSortSmem entries in dynamic shared memory and 4x the fine
-// buckets, the tiles taken grid-stride by kBigSortCtas CTAs (the crowded tiles are known
-// on the device only); beyond kBigSortSmem the in-place bitonic network in global memory.
+// buckets; tile_sort_kernel queues the crowded tiles (their ids in tile_cur, the count in
+// Counters::big_tiles) and kBigSortCtas CTAs take them grid-stride; beyond kBigSortSmem the
+// in-place bitonic network in global memory.
 constexpr int kBigSortSmem = 20480;  // 160 KB of u64 keys
 constexpr int kBigBuckets = 4096;
 constexpr int kBigSortCtas = 148;
@@ -538,10 +542,11 @@ __global__ void __launch_bounds__(BSR_BLOCK) tile_sort_big_kernel(FrameView f) {
     extern __shared__ __align__(16) unsigned char big_smem[];
     BigSortSmem &b = *reinterpret_cast<BigSortSmem *>(big_smem);
     if (over_capacity(f)) return;
-    for (int tile = blockIdx.x; tile < f.n_tiles; tile += gridDim.x) {
+    const uint32_t nbig = f.ctr->big_tiles;
+    for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
+        const int tile = (int)f.tile_cur[k];
         const uint2 rg = f.tile_ranges[tile];
         const int n = (int)(rg.y - rg.x);
-        if (n <= kSortSmem) continue;
         if (n <= kBigSortSmem) {
             sort_tile<kBigBuckets>(f, tile, b.s, b.sm);
             continue;

@@ -30,7 +30,8 @@ struct Counters {
     uint32_t depth_ticket[kDepthPasses];   // global depth sort (parity export only)
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
     uint32_t depth_plan[kDepthPasses + 1];
-    uint32_t pad[5];
+    uint32_t big_tiles;      // crowded tiles queued by tile_sort for tile_sort_big (ids in tile_cur)
+    uint32_t pad[4];
 };
 
 // Deterministic accumulation of the backward's per-primitive partials
