@@ -108,9 +108,21 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- distributed
 def dist_setup(n_gpus):
+    """torch.distributed from the torchrun environment: NCCL, one GPU per rank.
+    BSR_DIST_BACKEND=gloo runs the same multi-rank code path over gloo (several ranks may
+    then share one GPU: a functional check of the launcher, the sharded exchange and the
+    JSON line on a one-GPU box; not a performance configuration)."""
     from paper_2501_18630_b200 import distributed as dd
 
-    return dd.init("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
+    if int(os.environ.get("WORLD_SIZE", "1")) <= 1:
+        return dd.init(None)
+    backend = os.environ.get("BSR_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        import torch
+
+        torch.cuda.set_device(0 if torch.cuda.device_count() == 1 else int(os.environ.get("LOCAL_RANK", "0")))
+        return dd.init("gloo")
+    return dd.init(backend)
 
 
 def barrier(world):
@@ -851,7 +863,9 @@ def nccl_info():
     except Exception:
         ver = None
     return {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "nccl_version": ver,
-            "collective": "all_reduce (sum, fp32) of the flat per-Gaussian gradient buffer per step"}
+            "collective": "per step: reduce_scatter (sum, fp32) of the flat per-Gaussian gradient buffer, "
+                          "Adam on the rank's shard, all_gather of the parameter shards "
+                          "(distributed.ShardedOptimizer); e2e: all_reduce + adam_step through the API"}
 
 
 # ----------------------------------------------------------------------------- launcher
