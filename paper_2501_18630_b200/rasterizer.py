@@ -39,13 +39,47 @@ _ENTRY_CAP: dict = {}  # (n, W, H) -> entry capacity to allocate (last that suff
 _VERIFIED: set = set()  # shapes whose capacity was verified by a synchronous check
 
 
+class PendingStatus:
+    """An asynchronous status check of one un-synchronised forward: the pinned counter
+    snapshot and the event after which it is valid, plus the frame's shape.  It does NOT
+    hold the frame's device buffer (a host running ahead of the device would otherwise keep
+    every in-flight frame alive and defeat the caching allocator)."""
+
+    __slots__ = ("snap", "ev", "key", "info", "done")
+
+    def __init__(self, snap, ev, key):
+        self.snap, self.ev, self.key, self.info, self.done = snap, ev, key, None, False
+
+    def ready(self) -> bool:
+        return self.done or self.ev.query()
+
+    def resolve(self) -> dict:
+        """Wait for the snapshot, decode it (once) and raise on a device-side error or
+        capacity overflow (the shape's capacity is then grown and re-verified next call)."""
+        if not self.done:
+            self.ev.synchronize()
+            self.done = True
+            info = _lib.FrameInfoC()
+            st = _lib.load().bsr_frame_snapshot_decode(ctypes.c_void_p(self.snap.data_ptr()), ctypes.byref(info))
+            _SNAP_POOL.append((self.snap, self.ev))
+            self.snap = self.ev = None
+            self.info = dict(visible=info.visible, entries=info.entries, entries_needed=info.entries_needed,
+                             flagged_pixels=info.flagged_pixels, status=info.status)
+            if st == _lib.BSR_ERR_CAPACITY:
+                _ENTRY_CAP[self.key] = int(min(2**31 - 1, info.entries_needed * 1.25 + 1024))
+                _VERIFIED.discard(self.key)  # the next call re-verifies synchronously
+                raise _lib.CapacityError(info.entries_needed)
+            _lib.check(st, "forward")
+        return self.info
+
+
 @dataclass(eq=False)
 class FrameState:
     """Saved forward state in a device buffer owned by torch's caching allocator.
 
-    ``pending`` holds an asynchronous status check (pinned counter snapshot + the event
-    after which it is valid) of a forward that was not synchronised; ``check()`` resolves
-    it (waiting for that event) and raises on a device-side error or capacity overflow."""
+    ``pending`` holds an asynchronous status check (PendingStatus) of a forward that was
+    not synchronised; ``check()`` resolves it (waiting for that forward) and raises on a
+    device-side error or capacity overflow."""
 
     buf: torch.Tensor
     nbytes: int
@@ -54,35 +88,24 @@ class FrameState:
     width: int
     height: int
     info: dict = field(default_factory=dict)
-    pending: tuple | None = None
+    pending: PendingStatus | None = None
 
     def ptr(self):
         return self.buf.data_ptr()
 
     def ready(self) -> bool:
-        return self.pending is None or self.pending[1].query()
+        return self.pending is None or self.pending.ready()
 
     def check(self) -> dict:
         """Resolve a pending asynchronous status (blocks until that forward finished)."""
         if self.pending is not None:
-            snap, ev = self.pending
-            ev.synchronize()
-            self.pending = None
-            info = _lib.FrameInfoC()
-            st = _lib.load().bsr_frame_snapshot_decode(ctypes.c_void_p(snap.data_ptr()), ctypes.byref(info))
-            self.info = dict(visible=info.visible, entries=info.entries, entries_needed=info.entries_needed,
-                             flagged_pixels=info.flagged_pixels, status=info.status)
-            if st == _lib.BSR_ERR_CAPACITY:
-                key = (self.n, self.width, self.height)
-                _ENTRY_CAP[key] = int(min(2**31 - 1, info.entries_needed * 1.25 + 1024))
-                _VERIFIED.discard(key)  # the next call re-verifies synchronously
-                raise _lib.CapacityError(info.entries_needed)
-            _lib.check(st, "forward")
+            p, self.pending = self.pending, None
+            self.info = p.resolve()
         return self.info
 
 
 _SNAPSHOT_BYTES = None
-_PENDING: list = []  # frames with unresolved asynchronous status checks (oldest first)
+_PENDING: list = []  # PendingStatus of un-synchronised forwards (oldest first)
 
 
 def _snapshot_bytes():
@@ -94,22 +117,26 @@ def _snapshot_bytes():
     return _SNAPSHOT_BYTES
 
 
+_SNAP_POOL: list = []  # (pinned snapshot, event) pairs of resolved checks, reused
+
+
 def _queue_status(frame: FrameState):
     """Enqueue the frame's status copy into pinned memory (no sync) and remember it."""
-    snap = torch.empty(_snapshot_bytes(), dtype=torch.uint8, pin_memory=True)
+    snap, ev = _SNAP_POOL.pop() if _SNAP_POOL else (
+        torch.empty(_snapshot_bytes(), dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
     _lib.check(_lib.load().bsr_frame_status_async(ctypes.c_void_p(frame.ptr()), ctypes.c_void_p(snap.data_ptr()),
                                                   _stream()), "frame_status_async")
-    ev = torch.cuda.Event()
     ev.record()
-    frame.pending = (snap, ev)
-    _PENDING.append(frame)
+    p = PendingStatus(snap, ev, (frame.n, frame.width, frame.height))
+    frame.pending = p
+    _PENDING.append(p)
 
 
 def check_pending(block: bool = False):
     """Resolve the asynchronous status checks of earlier un-synchronised forwards that have
     completed (all of them with ``block``); raises the first error found."""
     while _PENDING and (block or _PENDING[0].ready()):
-        _PENDING.pop(0).check()
+        _PENDING.pop(0).resolve()
 
 
 @dataclass
@@ -169,7 +196,31 @@ def scene_c(positions, rotations, log_scales, opacity_raw, shapes, sh=None, base
     return s
 
 
+def _camera_c(camera) -> _lib.CameraC:
+    """camera_c, cached on the camera object for as long as its values are unchanged."""
+    key = (camera.world_to_camera.tobytes(), camera.fx, camera.fy, camera.cx, camera.cy, camera.width, camera.height)
+    hit = getattr(camera, "_bsr_c", None)
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    c = _lib.camera_c(camera)
+    try:
+        camera._bsr_c = (key, c)
+    except AttributeError:  # slotted / frozen camera types: no cache
+        pass
+    return c
+
+
 def _prims_scene_c(prims: PrimitiveSet) -> _lib.SceneC:
+    """bsr_scene of a PrimitiveSet, cached while its flat buffer is the same tensor."""
+    hit = getattr(prims, "_bsr_scene", None)
+    if hit is not None and hit[0] is prims.flat and hit[1] == prims.flat.data_ptr():
+        return hit[2]
+    sc = _prims_scene_c_build(prims)
+    prims._bsr_scene = (prims.flat, prims.flat.data_ptr(), sc)
+    return sc
+
+
+def _prims_scene_c_build(prims: PrimitiveSet) -> _lib.SceneC:
     if prims.color_model == "sh":
         return scene_c(prims.positions, prims.rotations, prims.log_scales, prims.opacity_raw, prims.shapes,
                        sh=prims.sh)
@@ -191,9 +242,14 @@ def new_frame(n, width, height, entry_cap, device=None) -> FrameState:
 
 def frame_status(frame: FrameState, raise_on_error=True) -> dict:
     """Synchronous status of the frame's last forward (supersedes a pending async check)."""
-    frame.pending = None
-    if frame in _PENDING:
-        _PENDING.remove(frame)
+    if frame.pending is not None:  # superseded: drop the asynchronous check (recycle its buffers)
+        p, frame.pending = frame.pending, None
+        if p in _PENDING:
+            _PENDING.remove(p)
+        if not p.done:
+            p.ev.synchronize()
+            _SNAP_POOL.append((p.snap, p.ev))
+            p.done = True
     info = _lib.FrameInfoC()
     st = _lib.load().bsr_frame_status(ctypes.c_void_p(frame.ptr()), ctypes.byref(info), _stream())
     frame.info = dict(visible=info.visible, entries=info.entries, entries_needed=info.entries_needed,
@@ -226,7 +282,7 @@ def forward_raw(scene: _lib.SceneC, camera: Camera, background, outputs: _lib.Ou
     """
     _lib.require_cuda()
     lib = _lib.load()
-    cam = _lib.camera_c(camera)
+    cam = _camera_c(camera)
     bg = _bg_arr(background)
     n, w, h = int(scene.n), int(camera.width), int(camera.height)
     if check == "async" and (n, w, h) not in _VERIFIED:
@@ -283,7 +339,7 @@ def backward_raw(scene: _lib.SceneC, camera: Camera, background, frame: FrameSta
     ``det_ws`` (det_workspace) the deterministic backward (bsr_backward_deterministic):
     bitwise identical gradients run to run."""
     lib = _lib.load()
-    cam = _lib.camera_c(camera)
+    cam = _camera_c(camera)
     if d_color.dtype != torch.float32 or not d_color.is_contiguous() or not d_color.is_cuda:
         raise ValueError("d_color must be a contiguous float32 CUDA tensor")
     if tuple(d_color.shape) != (camera.height, camera.width, 3):
