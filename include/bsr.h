@@ -87,6 +87,11 @@ typedef struct bsr_scene {
 typedef struct bsr_grads {
     float *positions, *rotations, *log_scales, *opacity_raw, *shapes, *sh;
     float *base_colors, *lobe_axes, *lobe_colors;
+    /* 0: the gradients are ADDED into these buffers (multi-view accumulation); nonzero:
+     * they are WRITTEN -- every primitive's rows, culled ones zeroed, screen_grad_norm too --
+     * so the caller needs no memset and no buffer is read back (not with a deferred colour
+     * chain, bsr_backward_deferred_color / drgb). */
+    int32_t overwrite;
 } bsr_grads;
 
 /* Forward outputs (device; any pointer may be NULL to skip that output). */

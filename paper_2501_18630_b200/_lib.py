@@ -55,7 +55,8 @@ class SceneC(ctypes.Structure):
 class GradsC(ctypes.Structure):
     _fields_ = [("positions", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p),
                 ("opacity_raw", c_void_p), ("shapes", c_void_p), ("sh", c_void_p),
-                ("base_colors", c_void_p), ("lobe_axes", c_void_p), ("lobe_colors", c_void_p)]
+                ("base_colors", c_void_p), ("lobe_axes", c_void_p), ("lobe_colors", c_void_p),
+                ("overwrite", c_int32)]
 
 
 class OutputsC(ctypes.Structure):

@@ -344,7 +344,7 @@ static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const
                          const bsr_profile *prof, float *drgb, void *stream, void *det_ws = nullptr) {
     if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !d_color || bad_grads(scene, grads))
         return BSR_ERR_BAD_ARG;
-    if (drgb && scene->color_model != BSR_COLOR_SH) return BSR_ERR_BAD_ARG;
+    if (drgb && (scene->color_model != BSR_COLOR_SH || grads->overwrite)) return BSR_ERR_BAD_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
     if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;

@@ -80,6 +80,7 @@ template <int CM>
 __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grads &g, int64_t i, float vx,
                                              float vy, float vz, float dr, float dg, float dbl, float &ddx,
                                              float &ddy, float &ddz) {
+    const bool ovw = g.overwrite != 0;  // write instead of add (bsr_grads::overwrite)
     using Tr = AppTraits<CM>;
     if constexpr (Tr::sh) {
         constexpr int K = Tr::K;
@@ -95,7 +96,7 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
 #pragma unroll
             for (int q = 0; q < 3 * K / 4; ++q) {
                 const float4 x4 = __ldg(reinterpret_cast<const float4 *>(shp) + q);
-                const float4 g4 = reinterpret_cast<const float4 *>(gsh)[q];
+                const float4 g4 = ovw ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4 *>(gsh)[q];
                 shv[4 * q] = x4.x; shv[4 * q + 1] = x4.y; shv[4 * q + 2] = x4.z; shv[4 * q + 3] = x4.w;
                 gsv[4 * q] = g4.x; gsv[4 * q + 1] = g4.y; gsv[4 * q + 2] = g4.z; gsv[4 * q + 3] = g4.w;
             }
@@ -103,7 +104,7 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
 #pragma unroll
             for (int q = 0; q < 3 * K; ++q) {
                 shv[q] = __ldg(shp + q);
-                gsv[q] = gsh[q];
+                gsv[q] = ovw ? 0.f : gsh[q];
             }
         }
 #pragma unroll
@@ -127,9 +128,12 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
         }
     } else {
         constexpr int M = Tr::M;
-        g.base_colors[3 * i] += dr;  // d base = upstream
-        g.base_colors[3 * i + 1] += dg;
-        g.base_colors[3 * i + 2] += dbl;
+        auto put = [&](float *dst, float v) {
+            if (ovw) *dst = v; else *dst += v;
+        };
+        put(g.base_colors + 3 * i, dr);  // d base = upstream
+        put(g.base_colors + 3 * i + 1, dg);
+        put(g.base_colors + 3 * i + 2, dbl);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
             const int64_t o = (i * M + m) * 3;
@@ -146,21 +150,25 @@ __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grad
             const float w = fminf(fmaxf(ux * vx + uy * vy + uz * vz, 0.f), 1.f);
             const float expo = 4.0f * nrm;
             const float cr = sc.lobe_colors[o], cg = sc.lobe_colors[o + 1], cb = sc.lobe_colors[o + 2];
-            if (!(w > 1e-12f)) continue;  // outside the lobe's support: exactly zero gradients
+            if (!(w > 1e-12f)) {  // outside the lobe's support: exactly zero gradients
+                if (ovw)
+                    for (int q = 0; q < 3; ++q) g.lobe_colors[o + q] = g.lobe_axes[o + q] = 0.f;
+                continue;
+            }
             const float lw = __logf(w);
             const float resp = __expf(expo * lw);
             const float resp_dw = expo * __expf((expo - 1.0f) * lw);
-            g.lobe_colors[o] += resp * dr;
-            g.lobe_colors[o + 1] += resp * dg;
-            g.lobe_colors[o + 2] += resp * dbl;
+            put(g.lobe_colors + o, resp * dr);
+            put(g.lobe_colors + o + 1, resp * dg);
+            put(g.lobe_colors + o + 2, resp * dbl);
             const float d_resp = dr * cr + dg * cg + dbl * cb;
             const float d_w = d_resp * resp_dw;
             const float d_norm = d_resp * resp * lw * 4.0f;
             const float dux = d_w * vx, duy = d_w * vy, duz = d_w * vz;
             const float dot = dux * ux + duy * uy + duz * uz;
-            g.lobe_axes[o] += (dux - dot * ux) * inrm + d_norm * ux;
-            g.lobe_axes[o + 1] += (duy - dot * uy) * inrm + d_norm * uy;
-            g.lobe_axes[o + 2] += (duz - dot * uz) * inrm + d_norm * uz;
+            put(g.lobe_axes + o, (dux - dot * ux) * inrm + d_norm * ux);
+            put(g.lobe_axes + o + 1, (duy - dot * uy) * inrm + d_norm * uy);
+            put(g.lobe_axes + o + 2, (duz - dot * uz) * inrm + d_norm * uz);
             ddx += d_w * ux;
             ddy += d_w * uy;
             ddz += d_w * uz;
@@ -271,7 +279,8 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
         T v = 0;
         for (int j = 0; j < 3; ++j)
             for (int l = 0; l < 3; ++l) v += Q[3 * j + k] * gS[3 * j + l] * Q[3 * l + k];
-        a.g.log_scales[3 * i + k] += (float)(v * two * s2[k]);
+        const float gls = (float)(v * two * s2[k]);
+        if (a.g.overwrite) a.g.log_scales[3 * i + k] = gls; else a.g.log_scales[3 * i + k] += gls;
     }
     // _rotation_grad_to_quat (primitive.py:348-367)
     {
@@ -286,17 +295,19 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
         const float r2 = (float)((gy - dot * y) * iqn), r3 = (float)((gz - dot * z) * iqn);
         if (rot16) {
             float4 *gr = reinterpret_cast<float4 *>(a.g.rotations) + i;
-            float4 gq = *gr;
+            float4 gq = a.g.overwrite ? make_float4(0.f, 0.f, 0.f, 0.f) : *gr;
             gq.x += r0;
             gq.y += r1;
             gq.z += r2;
             gq.w += r3;
             *gr = gq;
         } else {
-            a.g.rotations[4 * i] += r0;
-            a.g.rotations[4 * i + 1] += r1;
-            a.g.rotations[4 * i + 2] += r2;
-            a.g.rotations[4 * i + 3] += r3;
+            const bool ow = a.g.overwrite != 0;
+            float *gr = a.g.rotations + 4 * i;
+            gr[0] = (ow ? 0.f : gr[0]) + r0;
+            gr[1] = (ow ? 0.f : gr[1]) + r1;
+            gr[2] = (ow ? 0.f : gr[2]) + r2;
+            gr[3] = (ow ? 0.f : gr[3]) + r3;
         }
     }
 }
@@ -315,10 +326,13 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
     // ---- opacity / shape chains
     const float oraw = sc.opacity_raw[i];
     const float o = oraw >= 0.f ? 1.f / (1.f + expf(-oraw)) : expf(oraw) / (1.f + expf(oraw));
-    a.g.opacity_raw[i] += d_o * o * (1.f - o);
+    const bool ovw = a.g.overwrite != 0;
+    const float gop = d_o * o * (1.f - o);
+    if (ovw) a.g.opacity_raw[i] = gop; else a.g.opacity_raw[i] += gop;
     const float bsh = sc.shapes[i];
     const float beta = 4.f * expf(fminf(fmaxf(bsh, -10.f), 10.f));
-    if (fabsf(bsh) <= 10.f) a.g.shapes[i] += d_beta * beta;
+    const float gsp = fabsf(bsh) <= 10.f ? d_beta * beta : 0.f;
+    if (ovw) a.g.shapes[i] = gsp; else a.g.shapes[i] += gsp;
 
     // ---- the geometric chain runs in fp64 in prebwd_geom_kernel (after this kernel)
     float dpx = 0.f, dpy = 0.f, dpz = 0.f;
@@ -342,10 +356,42 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
         dpz += (ddz - dd * vz) * ivn;
     }
     if (!a.drgb) {
-        a.g.positions[3 * i] += dpx;
-        a.g.positions[3 * i + 1] += dpy;
-        a.g.positions[3 * i + 2] += dpz;
+        if (ovw) {
+            a.g.positions[3 * i] = dpx;
+            a.g.positions[3 * i + 1] = dpy;
+            a.g.positions[3 * i + 2] = dpz;
+        } else {
+            a.g.positions[3 * i] += dpx;
+            a.g.positions[3 * i + 1] += dpy;
+            a.g.positions[3 * i + 2] += dpz;
+        }
     }
+}
+
+// bsr_grads::overwrite: the rows of a culled primitive (its gradients are zero,
+// rasterizer.py:262-320) -- written here since nothing else touches them
+template <int CM>
+__device__ __forceinline__ void zero_rows(const PreBwdArgs &a, int64_t i) {
+    using Tr = AppTraits<CM>;
+    const bsr_grads &g = a.g;
+    for (int q = 0; q < 3; ++q) g.positions[3 * i + q] = g.log_scales[3 * i + q] = 0.f;
+    if ((reinterpret_cast<uintptr_t>(g.rotations) & 15) == 0)
+        reinterpret_cast<float4 *>(g.rotations)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    else
+        for (int q = 0; q < 4; ++q) g.rotations[4 * i + q] = 0.f;
+    g.opacity_raw[i] = g.shapes[i] = 0.f;
+    if constexpr (Tr::sh) {
+        float *row = g.sh + 3 * Tr::K * i;
+        if ((3 * Tr::K) % 4 == 0 && (reinterpret_cast<uintptr_t>(g.sh) & 15) == 0) {
+            for (int q = 0; q < 3 * Tr::K / 4; ++q) reinterpret_cast<float4 *>(row)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (int q = 0; q < 3 * Tr::K; ++q) row[q] = 0.f;
+        }
+    } else {
+        for (int q = 0; q < 3; ++q) g.base_colors[3 * i + q] = 0.f;
+        for (int q = 0; q < 3 * Tr::M; ++q) g.lobe_axes[3 * Tr::M * i + q] = g.lobe_colors[3 * Tr::M * i + q] = 0.f;
+    }
+    if (a.screen_grad_norm) a.screen_grad_norm[i] = 0.f;
 }
 
 // Each warp takes 64 consecutive source indices and runs the visible ones densely (32
@@ -370,6 +416,7 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_c
         m[q] = __ballot_sync(0xffffffffu, vis);
         tot += __popc(m[q]);
         if (a.drgb && c < a.f.n && !vis) a.drgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.g.overwrite && c < a.f.n && !vis) zero_rows<K>(a, c);
     }
     for (int base = 0; base < tot; base += 32) {
         int r = base + lane;

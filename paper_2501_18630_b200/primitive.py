@@ -202,6 +202,21 @@ class GradientBuffer(FlatGroups):
     def zeros_for(cls, prims: PrimitiveSet) -> "GradientBuffer":
         return cls(prims.n, prims.k, device=prims.flat.device, lobes=prims.lobes)
 
+    @classmethod
+    def empty_for(cls, prims: PrimitiveSet) -> "GradientBuffer":
+        """Uninitialised group rows (for a backward in overwrite mode, which writes every
+        row); only the alignment padding between groups is zeroed."""
+        layout, total = group_layout(prims.n, prims.k, prims.lobes)
+        flat = torch.empty(total, dtype=torch.float32, device=prims.flat.device)
+        prev = 0
+        for _, a, b, _ in layout:
+            if a > prev:
+                flat[prev:a].zero_()
+            prev = b
+        if total > prev:
+            flat[prev:total].zero_()
+        return cls(prims.n, prims.k, flat=flat, lobes=prims.lobes)
+
     def zero_(self):
         self.flat.zero_()
         self.screen_grad_norm.zero_()

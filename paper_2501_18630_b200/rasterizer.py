@@ -368,8 +368,11 @@ def color_grad_views(scene: _lib.SceneC, drgb: torch.Tensor, cameras, grads: _li
     _lib.check(rc, "bsr_color_grad_views")
 
 
-def grads_c(g: GradientBuffer) -> _lib.GradsC:
+def grads_c(g: GradientBuffer, overwrite: bool = False) -> _lib.GradsC:
+    """bsr_grads of a GradientBuffer; ``overwrite``: the backward writes every row instead of
+    adding (no memset / read-back of the buffer; not with a deferred colour chain)."""
     c = _lib.GradsC()
+    c.overwrite = int(bool(overwrite))
     c.positions, c.rotations, c.log_scales = g.positions.data_ptr(), g.rotations.data_ptr(), g.log_scales.data_ptr()
     c.opacity_raw, c.shapes = g.opacity_raw.data_ptr(), g.shapes.data_ptr()
     if g.color_model == "sh":
@@ -428,8 +431,9 @@ def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, fo
     input) via fixed-point accumulation (bsr_backward_deterministic), at about
     twice the raster-backward cost."""
     _check_core(core)
-    if grads is None:
-        grads = GradientBuffer.zeros_for(prims)
+    fresh = grads is None
+    if fresh:  # written, not added: no memset of the (N x 60 floats at SH-3) buffer
+        grads = GradientBuffer.empty_for(prims) if len(prims) else GradientBuffer.zeros_for(prims)
     elif grads.flat.numel() != prims.flat.numel():
         raise ValueError("grads does not match prims")
     if len(prims) == 0:
@@ -441,7 +445,7 @@ def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, fo
     if d_depth is not None:
         d_depth = torch.as_tensor(d_depth, dtype=torch.float32, device=dev).contiguous()
     backward_raw(_prims_scene_c(prims), camera, background, forward_out.frame, d_color, d_depth,
-                 grads_c(grads), grads.screen_grad_norm,
+                 grads_c(grads, overwrite=fresh), grads.screen_grad_norm,
                  det_ws=det_workspace(len(prims), dev) if deterministic else None)
     return grads
 

@@ -375,6 +375,10 @@ class TrainStep:
             self.adam = AdamState(prims)
         self.scene = _prims_scene_c(prims)
         self.gc = grads_c(self.grads)
+        # one view without a deferred colour chain: its backward WRITES the gradient buffer
+        # (bsr_grads::overwrite), so the step needs no memset of it
+        self.gc_write = grads_c(self.grads, overwrite=True)
+        self.write_first = len(self.cameras) == 1 and self.sharded is None
         dev = prims.flat.device
         self.frames: dict = {}
         self.bufs = {}
@@ -402,7 +406,8 @@ class TrainStep:
 
     def step(self, check=False, adam=True):
         prof = self.profile
-        if not self._grads_clear:
+        write = self.write_first and self.drgb is None
+        if not self._grads_clear and not write:
             self.grads.flat.zero_()
         self._grads_clear = False
         for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
@@ -418,7 +423,8 @@ class TrainStep:
             loss_into(b["color"], target, b["d_image"], ws, self.lambda_ssim, values=self.loss_values[i])
             if prof is not None:
                 prof.mark_loss(i, end=True)
-            backward_raw(self.scene, cam, self.background, frame, b["d_image"], None, self.gc, None,
+            backward_raw(self.scene, cam, self.background, frame, b["d_image"], None,
+                         self.gc_write if (write and i == 0) else self.gc, None,
                          profile=None if prof is None else prof.bwd(i),
                          drgb=None if self.drgb is None else self.drgb[i], det_ws=self.det_ws)
         if self.drgb is not None:
