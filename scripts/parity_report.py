@@ -52,6 +52,9 @@ def main():
         try:
             if c == "needle":
                 rep = needle_case()
+            elif c == "sb":
+                rep, fok, gok = fullsize.run_sb_case()
+                rep["forward_ok"], rep["grads_ok"] = fok, gok
             else:
                 cfg, _, view = c.partition(":")
                 rep, fok, gok = fullsize.run_case(cfg, view=int(view or 0), bwd=cfg != "c2")

@@ -30,7 +30,8 @@ import numpy as np
 IMG_TOL = 1e-4
 RTOL, ATOL_REL = 1e-3, 1e-5
 KINK = 1e-5
-GROUPS = ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh")
+GROUPS = ("positions", "rotations", "log_scales", "opacity_raw", "shapes", "sh", "base_colors", "lobe_axes",
+          "lobe_colors")
 
 
 def grad_ratio(a, b):
@@ -202,5 +203,54 @@ def run_case(cfg, view=0, bwd=True, n=None, width=None, height=None, threads=Non
         gok = grads_ok(rep["grads"])
         del grads
     del out, prims
+    torch.cuda.empty_cache()
+    return rep, fok, gok
+
+
+def sb_scene_c2(seed=0, lobes=2):
+    """Config 2's geometry (1M Gaussians, the radius-8 hemisphere camera, 1920x1080) with the
+    reference's DEFAULT appearance model -- Spherical-Beta colour with two lobes -- and Beta
+    shapes spread over U(-1.5, 1.5) (exponents 0.9..18: the general (1 - r^2)^beta path)."""
+    from paper_2501_18630_b200.scenes import SbSplatScene, fibonacci_directions, make_workload
+
+    wl = make_workload("c2", seed=seed)
+    g = wl.scene
+    n = len(g.positions)
+    rng = np.random.default_rng([seed, 0x5B])
+    axes = fibonacci_directions(lobes)[None] * np.exp(rng.uniform(-0.3, 0.8, (n, lobes, 1)))
+    f = np.float32
+    scene = SbSplatScene(positions=g.positions, rotations=g.rotations, log_scales=g.log_scales,
+                         opacity_raw=g.opacity_raw, shapes=rng.uniform(-1.5, 1.5, n).astype(f),
+                         base_colors=rng.uniform(0.0, 1.0, (n, 3)).astype(f), lobe_axes=axes.astype(f),
+                         lobe_colors=(rng.uniform(-0.2, 1.0, (n, lobes, 3)) * 0.3).astype(f))
+    return scene, wl.cameras[0], wl.background
+
+
+def run_sb_case(threads=None):
+    """sb_scene_c2 forward + backward against the oracle (seeded upstream of the loss
+    gradient's scale); returns (report, forward ok, gradients ok)."""
+    import torch
+
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import PrimitiveSet, render_backward, render_tiled
+
+    threads = threads or os.cpu_count() or 1
+    scene, cam, bg = sb_scene_c2()
+    rep = {"case": f"c2 geometry, Spherical-Beta colour (2 lobes), N={len(scene.positions)} {cam.width}x{cam.height}"}
+    ref = orc.forward(scene, cam, bg, core="c", threads=threads)
+    prims = PrimitiveSet.from_reference(scene)
+    out = render_tiled(prims, cam, bg)
+    torch.cuda.synchronize()
+    rep["forward"] = compare_forward(out, ref)
+    fok = forward_ok(rep["forward"])
+    rng = np.random.default_rng(7)
+    up = (rng.standard_normal(ref["raw"].shape) / ref["raw"].size).astype(np.float32)
+    up[np.abs(ref["raw"]) < KINK] = 0.0
+    ref_g = orc.backward(scene, cam, bg, up.astype(np.float64), ref, core="c", threads=threads)
+    ref_g32 = orc.backward(scene, cam, bg, up.astype(np.float64), _fp32_records(ref), core="c", threads=threads)
+    grads = render_backward(prims, cam, bg, up, forward_out=out)
+    rep["grads"] = compare_grads(grads, ref_g, ref_g32=ref_g32)
+    gok = grads_ok(rep["grads"])
+    del grads, out, prims
     torch.cuda.empty_cache()
     return rep, fok, gok

@@ -51,3 +51,15 @@ def test_full_size_deterministic_backward_c1(cuda):
     ref_g = orc.backward(wl.scene, cam, bg, up.astype(np.float64), ref, core="c")
     rep = fullsize.compare_grads(g1, ref_g)
     assert fullsize.grads_ok(rep), rep
+
+
+def test_full_size_spherical_beta(cuda):
+    """The reference's default colour model at config-2 scale (1M Gaussians, 1080p, two
+    Spherical-Beta lobes, Beta shapes in U(-1.5, 1.5)): forward bit-exact / 1e-4, every
+    gradient group (incl. base colours, lobe axes, lobe colours) within the bar."""
+    import fullsize
+
+    rep, fok, gok = fullsize.run_sb_case()
+    msg = json.dumps(rep)[:4000]
+    assert fok, msg
+    assert gok, msg
