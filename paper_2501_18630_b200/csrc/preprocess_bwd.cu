@@ -439,8 +439,20 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_c
 // ill-conditioned conic is formed (the factor of each record class: raster.cuh
 // record_factor64).  fp64-path records without a factor carry xy-frame conic partials
 // summed in fp64 (side64, cleared here) and use the fp64 conic.
+template <bool DRGB>
 __device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) {
     const FrameView &f = a.f;
+    if (DRGB) {  // deferred colour chain: this kernel also does prebwd_one's non-colour part
+        const float *acc = f.grad_acc + i * kGradStride;
+        const float4 g1 = *reinterpret_cast<const float4 *>(acc + 4);
+        const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
+        const float oraw = a.sc.opacity_raw[i];
+        const float o = oraw >= 0.f ? 1.f / (1.f + expf(-oraw)) : expf(oraw) / (1.f + expf(oraw));
+        a.g.opacity_raw[i] += g1.y * o * (1.f - o);
+        const float bsh = a.sc.shapes[i];
+        if (fabsf(bsh) <= 10.f) a.g.shapes[i] += g1.z * (4.f * expf(fminf(fmaxf(bsh, -10.f), 10.f)));
+        a.drgb[i] = make_float4(g1.w, g2.x, g2.y, 0.f);
+    }
     double dmx, dmy, gm00, gs01, gm11;
     double l11, l21, l22;
     if (record_factor64(f, (uint32_t)i, l11, l21, l22)) {
@@ -476,6 +488,10 @@ __device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) 
     if (a.screen_grad_norm) a.screen_grad_norm[i] = (float)sqrt(dmx * dmx + dmy * dmy);
 }
 
+// DRGB: the multi-view deferred-colour mode, where the fp32 colour kernel has nothing
+// left but the opacity / shape chains and the d rgb store -- done here instead, so that
+// mode runs one kernel per view, not two.
+template <bool DRGB>
 __global__ void __launch_bounds__(kPreBwdThreads) prebwd_geom_kernel(__grid_constant__ const PreBwdArgs a) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
@@ -486,8 +502,10 @@ __global__ void __launch_bounds__(kPreBwdThreads) prebwd_geom_kernel(__grid_cons
 #pragma unroll
     for (int q = 0; q < kPreBwdChunk / 32; ++q) {
         const int64_t c = c0 + 32 * q + lane;
-        m[q] = __ballot_sync(0xffffffffu, c < a.f.n && a.f.tile_count[c] != 0);
+        const bool vis = c < a.f.n && a.f.tile_count[c] != 0;
+        m[q] = __ballot_sync(0xffffffffu, vis);
         tot += __popc(m[q]);
+        if (DRGB && c < a.f.n && !vis) a.drgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (int base = 0; base < tot; base += 32) {
         int r = base + lane;
@@ -499,7 +517,7 @@ __global__ void __launch_bounds__(kPreBwdThreads) prebwd_geom_kernel(__grid_cons
                 r -= __popc(m[k]);
                 q = k + 1;
             }
-        prebwd_geom_one(a, c0 + 32 * q + (int)__fns(m[q], 0, r + 1));
+        prebwd_geom_one<DRGB>(a, c0 + 32 * q + (int)__fns(m[q], 0, r + 1));
     }
 }
 
@@ -508,10 +526,15 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
     if (f.n == 0) return BSR_OK;
     PreBwdArgs a{sc, cam, f, g, screen_grad_norm, drgb};
     const unsigned blocks = (unsigned)div_up(f.n, (int64_t)kPreBwdChunk * (kPreBwdThreads / 32));
+    if (drgb) {  // deferred colour chain (SH, multi-view, accumulating): one fused kernel
+        BSR_CUDA_TRY((pdl_launch(prebwd_geom_kernel<true>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)));
+        BSR_LAUNCH_CHECK();
+        return BSR_OK;
+    }
 #define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)))
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
-    BSR_CUDA_TRY((pdl_launch(prebwd_geom_kernel, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)));
+    BSR_CUDA_TRY((pdl_launch(prebwd_geom_kernel<false>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)));
     BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
