@@ -80,6 +80,11 @@ typedef struct bsr_scene {
     const float *base_colors, *lobe_axes, *lobe_colors; /* SB arrays */
     int32_t lobes;       /* SB: M */
     int32_t reserved;
+    /* Optional: this view's fp32 colours precomputed by bsr_view_colors, (N, 4) float
+     * (rgb + pad).  bsr_forward then reads them instead of the appearance parameters (a
+     * multi-view step reads the SH coefficients once for all its views, not once per
+     * view); the colours are the same bits preprocess would compute.  NULL: evaluate. */
+    const float *view_rgb;
 } bsr_scene;
 
 /* Per-parameter gradient buffers (device fp32, same shapes); bsr_backward ADDS into them.
@@ -140,6 +145,10 @@ int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_cap,
 int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                 void *frame, uint64_t frame_bytes, int64_t entry_cap, const bsr_outputs *out,
                 const bsr_profile *profile, void *stream);
+/* fp32 colours of every primitive for each of `views` camera centres (world, double[3]
+ * each): rgb[v][i][0..2] (4 floats per primitive), exactly the values bsr_forward's
+ * preprocess computes for that view -- feed rgb + v*N*4 as bsr_scene.view_rgb. */
+int bsr_view_colors(const bsr_scene *scene, const double *centers, int32_t views, float *rgb, void *stream);
 /* Synchronises `stream`, then reports counters / device-side errors of the last forward. */
 int bsr_frame_status(const void *frame, bsr_frame_info *info, void *stream);
 /* Asynchronous status (no sync): enqueues on `stream` a copy of the frame's counters into

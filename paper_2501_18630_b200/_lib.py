@@ -49,7 +49,7 @@ class SceneC(ctypes.Structure):
                 ("opacity_raw", c_void_p), ("shapes", c_void_p), ("sh", c_void_p), ("n", c_int64),
                 ("sh_coeffs", c_int32), ("color_model", c_int32), ("base_colors", c_void_p),
                 ("lobe_axes", c_void_p), ("lobe_colors", c_void_p), ("lobes", c_int32),
-                ("reserved", c_int32)]
+                ("reserved", c_int32), ("view_rgb", c_void_p)]
 
 
 class GradsC(ctypes.Structure):
@@ -95,6 +95,7 @@ EXPORTS = {
     "bsr_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
                               c_void_p, c_void_p]),
     "bsr_frame_status": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "bsr_view_colors": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "bsr_frame_snapshot_bytes": (c_int32, [c_void_p]),
     "bsr_frame_status_async": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "bsr_frame_snapshot_decode": (c_int32, [c_void_p, c_void_p]),

@@ -199,6 +199,7 @@ static bool bad_camera(const bsr_camera *c) {
 
 static bool bad_scene(const bsr_scene *s) {
     if (!s || s->n < 0 || s->n >= (1ll << 31)) return true;
+    if (reinterpret_cast<uintptr_t>(s->view_rgb) & 15) return true;
     if (s->n > 0 && (!s->positions || !s->rotations || !s->log_scales || !s->opacity_raw || !s->shapes))
         return true;
     if (s->color_model == BSR_COLOR_SB) {
@@ -291,6 +292,18 @@ extern "C" int bsr_frame_status(const void *frame, bsr_frame_info *info, void *s
     info->status = c.status;
     info->reserved = 0;
     return c.status;
+}
+
+namespace bsr {
+int launch_view_colors(const bsr_scene &sc, const double *centers, int views, float *rgb, cudaStream_t st);
+}
+
+extern "C" int bsr_view_colors(const bsr_scene *scene, const double *centers, int32_t views, float *rgb,
+                               void *stream) {
+    if (bad_scene(scene) || views < 0 || (views > 0 && (!centers || !rgb)) ||
+        (reinterpret_cast<uintptr_t>(rgb) & 15))
+        return BSR_ERR_BAD_ARG;
+    return launch_view_colors(*scene, centers, views, rgb, (cudaStream_t)stream);
 }
 
 extern "C" int bsr_frame_snapshot_bytes(uint64_t *bytes) {

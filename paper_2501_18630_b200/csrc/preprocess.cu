@@ -57,6 +57,70 @@ struct PreSmem {
     float app[kPreThreads * AppTraits<CM>::floats];
 };
 
+// The fp32 colour of one primitive seen from `center` (appearance payload rows as staged):
+// shared by preprocess and bsr_view_colors so both produce the same bits.
+template <int CM>
+__device__ __forceinline__ void view_color(const float *pos, const double *center, const float *pa, const float *pb,
+                                           const float *pc, float rgb[3]) {
+    float vx = pos[0] - (float)center[0], vy = pos[1] - (float)center[1], vz = pos[2] - (float)center[2];
+    const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+    if constexpr (AppTraits<CM>::sh)
+        app_color32<CM>(pa, nullptr, nullptr, vx * inv, vy * inv, vz * inv, rgb);
+    else
+        app_color32<CM>(pa, pb, pc, vx * inv, vy * inv, vz * inv, rgb);
+}
+
+// bsr_view_colors: one thread per primitive reads its appearance row once and evaluates it
+// for every view (views <= kMaxColorViews per launch); rgb[v][i] as float4.
+constexpr int kMaxColorViews = 64;
+struct ViewColorArgs {
+    bsr_scene sc;
+    double center[kMaxColorViews][3];
+    int views;
+    float4 *rgb;
+};
+
+template <int CM>
+__global__ void __launch_bounds__(256) view_colors_kernel(__grid_constant__ const ViewColorArgs a) {
+    pdl_wait();
+    using Tr = AppTraits<CM>;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.sc.n) return;
+    float row[Tr::floats];
+    const float *src_a = Tr::sh ? a.sc.sh + 3 * Tr::K * i : a.sc.base_colors + 3 * i;
+    for (int q = 0; q < (Tr::sh ? 3 * Tr::K : 3); ++q) row[q] = __ldg(src_a + q);
+    if constexpr (!Tr::sh) {
+        for (int q = 0; q < 3 * Tr::M; ++q) {
+            row[3 + q] = __ldg(a.sc.lobe_axes + 3 * Tr::M * i + q);
+            row[3 + 3 * Tr::M + q] = __ldg(a.sc.lobe_colors + 3 * Tr::M * i + q);
+        }
+    }
+    const float pos[3] = {a.sc.positions[3 * i], a.sc.positions[3 * i + 1], a.sc.positions[3 * i + 2]};
+    for (int v = 0; v < a.views; ++v) {
+        float rgb[3];
+        view_color<CM>(pos, a.center[v], row, row + 3, row + 3 + 3 * Tr::M, rgb);
+        a.rgb[(int64_t)v * a.sc.n + i] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+    }
+}
+
+int launch_view_colors(const bsr_scene &sc, const double *centers, int views, float *rgb, cudaStream_t st) {
+    if (sc.n == 0 || views == 0) return BSR_OK;
+    for (int v0 = 0; v0 < views; v0 += kMaxColorViews) {
+        ViewColorArgs a;
+        a.sc = sc;
+        a.views = views - v0 < kMaxColorViews ? views - v0 : kMaxColorViews;
+        for (int v = 0; v < a.views; ++v)
+            for (int c = 0; c < 3; ++c) a.center[v][c] = centers[3 * (v0 + v) + c];
+        a.rgb = reinterpret_cast<float4 *>(rgb) + (int64_t)v0 * sc.n;
+        const unsigned blocks = (unsigned)div_up(sc.n, (int64_t)256);
+#define BSR_VC_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(view_colors_kernel<CM>, dim3(blocks), dim3(256), 0, st, a)))
+        BSR_DISPATCH_CM(sc, BSR_VC_LAUNCH);
+#undef BSR_VC_LAUNCH
+    }
+    BSR_LAUNCH_CHECK();
+    return BSR_OK;
+}
+
 template <int CM, int kPreThreads>
 __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) preprocess_fwd_kernel(PreArgs args) {
     pdl_wait();
@@ -111,7 +175,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
             bulk_g2s(sm.ls, sc.log_scales + 3 * base, b3, &s_bar[0]);
             bulk_g2s(sm.op, sc.opacity_raw + base, b1, &s_bar[0]);
             bulk_g2s(sm.shp, sc.shapes + base, b1, &s_bar[0]);
-            const bool eager = n <= kEagerAppMaxN && 2 * (int64_t)*f.vis_hint >= n;
+            const bool eager = !sc.view_rgb && n <= kEagerAppMaxN && 2 * (int64_t)*f.vis_hint >= n;
             s_eager = eager;
             if (eager) issue_app();
         }
@@ -131,7 +195,9 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
             sm.op[q] = sc.opacity_raw[base + q];
             sm.shp[q] = sc.shapes[base + q];
         }
-        if constexpr (Tr::sh) {
+        if (sc.view_rgb) {
+            // colours precomputed (bsr_view_colors): no appearance payload
+        } else if constexpr (Tr::sh) {
             for (int q = tid; q < cnt * 3 * Tr::K; q += kPreThreads) app_a[q] = app_src_a[q];
         } else {
             for (int q = tid; q < cnt * 3; q += kPreThreads) app_a[q] = app_src_a[q];
@@ -165,7 +231,9 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
     }
     // appearance payload of the visible primitives (the non-bulk path staged everything)
     bool app_bulk = false;
-    if (bulk && s_eager) {
+    if (sc.view_rgb) {
+        // colours precomputed (bsr_view_colors): nothing to stage
+    } else if (bulk && s_eager) {
         app_bulk = true;  // requested with the geometry
     } else if (bulk) {
         const int nvis = __syncthreads_count(vis);
@@ -191,17 +259,18 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
     // every thread waits for a requested bulk copy (a CTA must not retire with one in flight)
     if (app_bulk) mbar_wait(&s_bar[1], 0);
     if (vis) {
-        if (!app_bulk && bulk) cp_async_wait<0>();
-        const float *pos = sm.pos + 3 * tid;
         float rgb[3];
-        float vx = pos[0] - (float)args.cam.center[0], vy = pos[1] - (float)args.cam.center[1],
-              vz = pos[2] - (float)args.cam.center[2];
-        const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
-        if constexpr (Tr::sh)
-            app_color32<CM>(app_a + 3 * Tr::K * tid, nullptr, nullptr, vx * inv, vy * inv, vz * inv, rgb);
-        else
-            app_color32<CM>(app_a + 3 * tid, app_b + 3 * Tr::M * tid, app_c + 3 * Tr::M * tid, vx * inv,
-                            vy * inv, vz * inv, rgb);
+        if (sc.view_rgb) {
+            const float4 c4 = __ldg(reinterpret_cast<const float4 *>(sc.view_rgb) + i);
+            rgb[0] = c4.x;
+            rgb[1] = c4.y;
+            rgb[2] = c4.z;
+        } else {
+            if (!app_bulk && bulk) cp_async_wait<0>();
+            const float *pos = sm.pos + 3 * tid;
+            view_color<CM>(pos, args.cam.center, app_a + (Tr::sh ? 3 * Tr::K : 3) * tid, app_b + 3 * Tr::M * tid,
+                           app_c + 3 * Tr::M * tid, rgb);
+        }
         const double o = sigmoid64((double)sm.op[tid]);
         const double beta = shape_to_exponent64((double)sm.shp[tid]);
         double l11, l21, l22;

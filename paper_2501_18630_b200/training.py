@@ -334,7 +334,8 @@ class TrainStep:
 
     def __init__(self, prims: PrimitiveSet, cameras: list, targets: list, background, lrs=None,
                  lambda_ssim=0.2, process_group=None, cfg: TrainConfig | None = None, scene_scale=1.0,
-                 noise_rng=None, defer_color=True, deterministic=False, shard_optimizer=True):
+                 noise_rng=None, defer_color=True, deterministic=False, shard_optimizer=True,
+                 precompute_colors=True):
         """``cfg`` switches on the reference's full optimiser step (training.py:357-366):
         opacity / scale regularisers, the exponential position-lr schedule and the
         covariance-shaped position noise, all evaluated on the device from the device step
@@ -398,6 +399,18 @@ class TrainStep:
         if len(self.cameras) > 1 and prims.color_model == "sh" and defer_color:
             self.drgb = torch.empty((len(self.cameras), prims.n, 4), dtype=torch.float32, device=dev)
         self.det_ws = det_workspace(prims.n, dev) if deterministic else None
+        # several views: the colours of every view are evaluated in one pass over the
+        # appearance parameters (bsr_view_colors) at the start of the step, and each view's
+        # forward reads its (N, 4) slice instead of the SH coefficients (bsr_scene.view_rgb)
+        self.vrgb = None
+        if len(self.cameras) > 1 and precompute_colors:
+            self.vrgb = torch.empty((len(self.cameras), prims.n, 4), dtype=torch.float32, device=dev)
+            self.view_scenes = []
+            for v in range(len(self.cameras)):
+                sv = _lib.SceneC.from_buffer_copy(self.scene)
+                sv.view_rgb = self.vrgb[v].data_ptr()
+                self.view_scenes.append(sv)
+            self.centers = np.ascontiguousarray(np.stack([np.asarray(c.center, np.float64) for c in self.cameras]))
         self.profile = None  # optional rasterizer.StageProfiler-like object with .fwd/.bwd
         self._grads_clear = False  # the last step's Adam zeroed self.grads
 
@@ -410,10 +423,14 @@ class TrainStep:
         if not self._grads_clear and not write:
             self.grads.flat.zero_()
         self._grads_clear = False
+        if self.vrgb is not None:
+            _lib.check(_lib.load().bsr_view_colors(ctypes.byref(self.scene), self.centers.ctypes.data_as(ctypes.c_void_p),
+                                                   len(self.cameras), self.vrgb.data_ptr(), _stream()), "view_colors")
         for i, (cam, target) in enumerate(zip(self.cameras, self.targets)):
             key = (cam.width, cam.height)
             b = self.bufs[key]
-            frame = forward_raw(self.scene, cam, self.background, outputs_c(color=b["color"]),
+            frame = forward_raw(self.scene if self.vrgb is None else self.view_scenes[i], cam, self.background,
+                                outputs_c(color=b["color"]),
                                 frame=self._frame(cam), check=check,
                                 profile=None if prof is None else prof.fwd(i))
             self.frames[key] = frame
