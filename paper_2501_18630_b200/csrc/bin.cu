@@ -242,6 +242,28 @@ __global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
         }
         carry += s_chunk;
     }
+    // pass 3: the raster CTA -> tile map, tiles by decreasing entry count (log2 buckets, order
+    // inside a bucket arbitrary: every tile is independent), so the heaviest tiles of a
+    // crowded frame start first instead of forming the tail of the raster kernels
+    constexpr int kOrdBuckets = 33;
+    __shared__ uint32_t s_hist[kOrdBuckets], s_cur[kOrdBuckets];
+    if (t < kOrdBuckets) s_hist[t] = 0u;
+    __syncthreads();
+    auto bucket = [&](int i) {  // 0 = heaviest
+        const uint32_t c = over ? 0u : f.tile_cnt[i];
+        return c == 0u ? kOrdBuckets - 1 : __clz(c);
+    };
+    for (int i = t; i < T; i += kScanThreads) atomicAdd(&s_hist[bucket(i)], 1u);
+    __syncthreads();
+    if (t == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < kOrdBuckets; ++b) {
+            s_cur[b] = run;
+            run += s_hist[b];
+        }
+    }
+    __syncthreads();
+    for (int i = t; i < T; i += kScanThreads) f.tile_order[atomicAdd(&s_cur[bucket(i)], 1u)] = (uint32_t)i;
 }
 
 // Ascending bitonic sort of a[0, n) with virtual +inf padding to the next power of two

@@ -69,6 +69,8 @@ struct FrameView {
     uint2 *tile_ranges;      // [n_tiles] (start, end)
     uint32_t *tile_cnt;      // [n_tiles] entries per tile
     uint32_t *tile_cur;      // [n_tiles] scatter cursors
+    uint32_t *tile_order;    // [n_tiles] tiles by decreasing entry count (log2 buckets; bin_scan):
+                             // the raster kernels' CTA -> tile map, heavy tiles first
     // --- not zeroed ---
     uint32_t *depth_hist;    // [4][256]                  global depth sort: parity export only,
     uint32_t *depth_status;  // [4][ceil(N/4096)][256]     zeroed by bsr_debug_export
@@ -138,6 +140,7 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.tile_ranges = (uint2 *)take(8ull * f.n_tiles);
     f.tile_cnt = (uint32_t *)take(4ull * f.n_tiles);
     f.tile_cur = (uint32_t *)take(4ull * f.n_tiles);
+    f.tile_order = (uint32_t *)take(4ull * f.n_tiles);
     off = align_up(off, 256);
     f.zero_bytes = off;
     f.vis_hint = (uint32_t *)take(4);

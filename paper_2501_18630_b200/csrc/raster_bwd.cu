@@ -25,6 +25,10 @@
 #define BSR_DENSE_X10 30  // dense mode when groups share entries; backward: from 3 groups per entry (measured: config 4 raster bwd 4.27 -> 4.22 ms from 2.5; worse above 3.5)
 #endif
 
+#ifndef BSR_NATURAL_TILE_ORDER
+#define BSR_NATURAL_TILE_ORDER 0  // build knob for A/B runs: raster CTAs in tile-index order
+#endif
+
 namespace bsr {
 
 struct RasterBwdArgs {
@@ -146,7 +150,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
     __shared__ uint32_t s_col[BSR_BLOCK / 32][32];  // [chunk of 32 entries][tile sub-block]
     __shared__ int s_maxlast;
     const FrameView &f = a.f;
-    const int tile = blockIdx.x;
+    // the frame's own tiles go heavy first (bin_scan's tile_order); the core seam's external
+    // ranges keep the launch order
+    const int tile = (a.ranges == nullptr && !BSR_NATURAL_TILE_ORDER) ? (int)a.f.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;

@@ -28,6 +28,10 @@
 #define BSR_FWD_CTAS 4  // resident CTAs per SM the register budget targets
 #endif
 
+#ifndef BSR_NATURAL_TILE_ORDER
+#define BSR_NATURAL_TILE_ORDER 0  // build knob for A/B runs: raster CTAs in tile-index order
+#endif
+
 namespace bsr {
 
 struct RasterFwdArgs {
@@ -64,7 +68,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     __shared__ int s_flag[BSR_BLOCK];  // entry where the pixel was handed to the fp64 replay (-1: none);
                                        // written once, kept out of the pair loop's registers
     const FrameView &f = a.f;
-    const int tile = blockIdx.x;
+    // the frame's own tiles go heavy first (bin_scan's tile_order); the core seam's external
+    // ranges keep the launch order
+    const int tile = (a.ranges == nullptr && !BSR_NATURAL_TILE_ORDER) ? (int)a.f.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int wx0 = tx * BSR_TILE + (warp & 1) * 8, wy0 = ty * BSR_TILE + (warp >> 1) * 4;
