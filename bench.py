@@ -925,6 +925,13 @@ def main():
         line["secondary"]["c1"]["stage_ms"] = sec["extra"]["stage_ms"]
         line["secondary"]["c1"]["e2e_graph"] = sec["extra"].get("e2e_graph")
         line["gpu_launches_secondary"] = sec["gpu_launches"]
+        # config 3 at one GPU: the base of the multi-GPU series (the N > 1 default is config 3,
+        # N = 1 is config 4), so scaling efficiency can be read off the same config
+        base = measure("c3", args, rank, world, local, 5, W, False, False)
+        line["scaling_base"] = {"workload": "c3", "value": base["value"], "unit": base["unit"],
+                                "ms_per_step": base["ms_per_step"], "n_gpus": 1,
+                                "note": "config 3 (32 views, 3M Gaussians) on this one GPU; bench.py --gpus N (N > 1) "
+                                        "measures config 3 split 32/N across N GPUs"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

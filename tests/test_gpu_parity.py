@@ -662,7 +662,7 @@ def test_deterministic_training_steps_bitwise(cuda):
     assert torch.equal(runs[0][1], runs[1][1])
 
 
-@pytest.mark.parametrize("degree", [3, 1])
+@pytest.mark.parametrize("degree", [3, 1, "sb"])
 def test_precomputed_view_colours_are_bit_identical(cuda, degree):
     """bsr_view_colors + bsr_scene.view_rgb (multi-view steps read each view's colours from
     one pass over the SH coefficients) gives the same records as evaluating them in
@@ -673,13 +673,18 @@ def test_precomputed_view_colours_are_bit_identical(cuda, degree):
     from paper_2501_18630_b200 import PrimitiveSet
     from paper_2501_18630_b200.training import TrainStep, render_targets
 
+    from paper_2501_18630_b200.scenes import sb_random_scene
+
     rng = np.random.default_rng(96)
     cams = [toy_camera(80, 64, eye=(np.sin(a) * 4.0, 0.5, -np.cos(a) * 4.0)) for a in np.linspace(-0.6, 0.6, 5)]
-    tgt = render_targets(PrimitiveSet.from_scene(random_scene(rng, 400, degree=degree)), cams, np.ones(3))
-    scene = random_scene(np.random.default_rng(97), 500, degree=degree)
+    if degree == "sb":  # the reference's Spherical-Beta colour
+        mk = lambda r, n: PrimitiveSet.from_reference(sb_random_scene(r, n))  # noqa: E731
+    else:
+        mk = lambda r, n: PrimitiveSet.from_scene(random_scene(r, n, degree=degree))  # noqa: E731
+    tgt = render_targets(mk(rng, 400), cams, np.ones(3))
     runs = []
     for pre in (True, False):
-        p = PrimitiveSet.from_scene(scene)
+        p = mk(np.random.default_rng(97), 500)
         st = TrainStep(p, cams, tgt, np.ones(3), deterministic=True, precompute_colors=pre)
         assert (st.vrgb is not None) == pre
         st.step(check=True)
