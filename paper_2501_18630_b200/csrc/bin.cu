@@ -61,9 +61,9 @@ constexpr int kBigQueue = 64;
 template <bool COUNT>
 __device__ __forceinline__ void bin_one(const FrameView &f, uint32_t t, uint64_t key) {
     if (COUNT) {
-        atomicAdd(&f.tile_cnt[t], 1u);
+        atomicAdd(tile_cnt_at(f, t), 1u);
     } else {
-        const uint32_t slot = atomicAdd(&f.tile_cur[t], 1u);
+        const uint32_t slot = atomicAdd(tile_cur_at(f, t), 1u);
         f.tent[f.tile_ranges[t].x + slot] = key;
     }
 }
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
 // The counts stream through in chunks of 4096 (one uint4 per thread, coalesced), each
 // chunk is block-scanned (warp shuffles + one word per warp in shared memory) and its
 // ranges written back coalesced; a running total carries across chunks.
-constexpr int kScanThreads = 1024, kScanChunk = 4 * kScanThreads;
+constexpr int kScanThreads = 1024, kScanChunk = 4 * kScanThreads, kScanSmemTiles = 8192;
 __global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
     pdl_wait();
     __shared__ unsigned long long s_w[32];
@@ -163,10 +163,18 @@ __global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int T = f.n_tiles;
     const bool vec = (T & 3) == 0;  // uint4 / 2 x uint4 accesses stay aligned
+    // spread counters (small frames, FrameView::cnt_shift): read once, kept in shared memory
+    __shared__ uint32_t s_cnt[kScanSmemTiles];
+    const bool cached = f.cnt_shift > 0;  // implies T <= kScanSmemTiles
+    auto count = [&](int i) { return cached ? s_cnt[i] : *tile_cnt_at(f, i); };
     // pass 1: the total (capacity check before any range is written), 64-bit
     unsigned long long mine = 0;
     for (int i = 4 * t; i < T; i += kScanChunk)
-        for (int k = 0; k < 4; ++k) mine += i + k < T ? f.tile_cnt[i + k] : 0u;
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t c = i + k < T ? *tile_cnt_at(f, i + k) : 0u;
+            if (cached && i + k < T) s_cnt[i + k] = c;
+            mine += c;
+        }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if (lane == 0) s_w[warp] = mine;
@@ -194,14 +202,14 @@ __global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
     for (int base = 0; base < T; base += kScanChunk) {
         const int i = base + 4 * t;
         uint32_t c[4];
-        if (vec && i < T) {
+        if (f.cnt_shift == 0 && vec && i < T) {
             const uint4 c4 = *reinterpret_cast<const uint4 *>(f.tile_cnt + i);
             c[0] = c4.x;
             c[1] = c4.y;
             c[2] = c4.z;
             c[3] = c4.w;
         } else {
-            for (int k = 0; k < 4; ++k) c[k] = i + k < T ? f.tile_cnt[i + k] : 0u;
+            for (int k = 0; k < 4; ++k) c[k] = i + k < T ? count(i + k) : 0u;
         }
         const uint32_t sum = c[0] + c[1] + c[2] + c[3];
         uint32_t incl = sum;
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kScanThreads) bin_scan_kernel(FrameView f) {
     if (t < kOrdBuckets) s_hist[t] = 0u;
     __syncthreads();
     auto bucket = [&](int i) {  // 0 = heaviest
-        const uint32_t c = over ? 0u : f.tile_cnt[i];
+        const uint32_t c = over ? 0u : count(i);
         return c == 0u ? kOrdBuckets - 1 : __clz(c);
     };
     for (int i = t; i < T; i += kScanThreads) atomicAdd(&s_hist[bucket(i)], 1u);

@@ -67,8 +67,8 @@ struct FrameView {
     // --- zeroed every forward (one memset) ---
     Counters *ctr;
     uint2 *tile_ranges;      // [n_tiles] (start, end)
-    uint32_t *tile_cnt;      // [n_tiles] entries per tile
-    uint32_t *tile_cur;      // [n_tiles] scatter cursors
+    uint32_t *tile_cnt;      // [n_tiles << cnt_shift] entries per tile (tile_cnt_at)
+    uint32_t *tile_cur;      // [n_tiles << cnt_shift] scatter cursors (tile_cur_at)
     uint32_t *tile_order;    // [n_tiles] tiles by decreasing entry count (log2 buckets; bin_scan):
                              // the raster kernels' CTA -> tile map, heavy tiles first
     // --- not zeroed ---
@@ -86,10 +86,15 @@ struct FrameView {
     uint32_t *lists;         // [Ecap] source index per tile entry in depth order (tile_ranges)
     uint32_t *emask;         // [Ecap] sub-block occupancy mask of every tile entry the forward raster
                              // reached (raster.cuh entry_tile_mask), reused by the backward
+    uint32_t *mask_end;      // [n_tiles] emask holds the tile's entries [range.x, mask_end) (the
+                             // batches the forward raster processed before its pixels finished)
     float *t_final;          // [H*W]
     uint32_t *last;          // [H*W] local end index of last contributor (0: none / flagged)
     uint2 *flags;            // [H*W] (pixel, local entry index where fp32 became ambiguous)
-    double *replay_state;    // [H*W][6] raw(3), raw_depth, T, last  (fp64, flagged only)
+    double *replay_state;    // [H*W][6] by flag slot: raw(3), raw_depth, T, last  (fp64, flagged only)
+    double *split_state;     // [H*W][6] by flag slot, at the split point: T, prefix colour(3) + depth
+    float4 *bwd_init;        // [H*W] flagged pixels: the raster backward's starting "behind" state
+                             // (colour(3), depth) at the flag point, t_final holds -T there
     float4 *needle;          // [N] needle words of records with c.w < 0 (raster.cuh), NaN: fp64 path
     uint32_t *vis_hint;      // visible count of the previous forward on this frame (a
                              // scheduling hint for preprocess only: any value is safe)
@@ -107,10 +112,19 @@ struct FrameView {
     // --- sizes ---
     int64_t n, entry_cap;
     int W, H, tiles_x, tiles_y, n_tiles;
+    int cnt_shift;  // log2 of the word stride of tile_cnt / tile_cur (tile_cnt_at)
     int64_t depth_parts;
     int depth_items;  // sort_items() of the (parity-export) depth sort
     uint64_t zero_bytes, total_bytes;
 };
+
+// Per-tile counters (hot REDs / atomics), 2^cnt_shift words apart.
+__host__ __device__ __forceinline__ uint32_t *tile_cnt_at(const FrameView &f, uint32_t t) {
+    return f.tile_cnt + ((size_t)t << f.cnt_shift);
+}
+__host__ __device__ __forceinline__ uint32_t *tile_cur_at(const FrameView &f, uint32_t t) {
+    return f.tile_cur + ((size_t)t << f.cnt_shift);
+}
 
 // Carve the frame.  base == nullptr computes sizes only.
 inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_cap) {
@@ -138,8 +152,12 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     };
     f.ctr = (Counters *)take(sizeof(Counters));
     f.tile_ranges = (uint2 *)take(8ull * f.n_tiles);
-    f.tile_cnt = (uint32_t *)take(4ull * f.n_tiles);
-    f.tile_cur = (uint32_t *)take(4ull * f.n_tiles);
+    // small frames spread their tile counters (few tiles take millions of REDs: packed, they
+    // share a few L2 lines and the RED rate depends on how those lines hash to L2 slices)
+    // (bin_scan keeps spread counters in shared memory: at most 8192 tiles)
+    f.cnt_shift = f.n_tiles <= 4096 ? 5 : (f.n_tiles <= 8192 ? 3 : 0);
+    f.tile_cnt = (uint32_t *)take(4ull * f.n_tiles << f.cnt_shift);
+    f.tile_cur = (uint32_t *)take(4ull * f.n_tiles << f.cnt_shift);
     f.tile_order = (uint32_t *)take(4ull * f.n_tiles);
     off = align_up(off, 256);
     f.zero_bytes = off;
@@ -164,6 +182,9 @@ inline FrameView carve_frame(void *base, int64_t n, int W, int H, int64_t entry_
     f.grad_acc = (float *)take(4ull * kGradStride * n);
     f.needle = (float4 *)take(16ull * n);
     f.side64 = (double *)take(8ull * kSide64 * n);
+    f.mask_end = (uint32_t *)take(4ull * f.n_tiles);
+    f.split_state = (double *)take(8ull * 6 * npx);
+    f.bwd_init = (float4 *)take(16ull * npx);
     f.total_bytes = align_up(off, 256);
     return f;
 }

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
             const int osp = __shfl_sync(0xffffffffu, spanx, owner);
             if (e >= total) continue;
             const uint32_t local = e - (oin - ocnt), row = local / (uint32_t)osp;
-            atomicAdd(&f.tile_cnt[(uint32_t)(oty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)otx + (local - row * osp)], 1u);
+            atomicAdd(tile_cnt_at(f, (uint32_t)(oty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)otx + (local - row * osp)), 1u);
         }
         unsigned ob = __ballot_sync(0xffffffffu, own_big != 0);  // queue overflow: the warp itself
         while (ob) {
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
             const int bsp = __shfl_sync(0xffffffffu, spanx, src);
             for (uint32_t j = lane; j < bn; j += 32) {
                 const uint32_t row = j / (uint32_t)bsp;
-                atomicAdd(&f.tile_cnt[(uint32_t)(bty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)btx + (j - row * bsp)], 1u);
+                atomicAdd(tile_cnt_at(f, (uint32_t)(bty + (int)row) * (uint32_t)f.tiles_x + (uint32_t)btx + (j - row * bsp)), 1u);
             }
         }
         __syncthreads();
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreThreads == 128 ? 7 : 3) prepr
             const uint32_t t0 = s_big[q].x, bsp = s_big[q].y, bn = s_big[q].z;
             for (uint32_t j = tid; j < bn; j += kPreThreads) {
                 const uint32_t row = j / bsp;
-                atomicAdd(&f.tile_cnt[t0 + row * (uint32_t)f.tiles_x + (j - row * bsp)], 1u);
+                atomicAdd(tile_cnt_at(f, t0 + row * (uint32_t)f.tiles_x + (j - row * bsp)), 1u);
             }
         }
     }

@@ -173,6 +173,14 @@ __global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs 
         last = (int)(packed & 0x1FFFFFFFu);
         if (last > 0) {
             T = f.t_final[pix];
+            if (T < 0.f) {  // flagged pixel: the entries before the flag point (replay.cu)
+                T = -T;
+                const float4 b = f.bwd_init[pix];
+                B0 = b.x;
+                B1 = b.y;
+                B2 = b.z;
+                BD = b.w;
+            }
             g0 = a.d_color[3 * pix];
             g1 = a.d_color[3 * pix + 1];
             g2 = a.d_color[3 * pix + 2];

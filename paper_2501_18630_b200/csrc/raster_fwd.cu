@@ -34,6 +34,19 @@
 
 namespace bsr {
 
+#ifdef BSR_FLAG_REASONS
+// diagnostic build only: [alpha cutoff, alpha > 0.999, T stop, fp32 / needle / fp64 record]
+__device__ unsigned long long g_flag_reasons[6];
+extern "C" int bsr_debug_flag_reasons(unsigned long long *out, int reset) {
+    cudaMemcpyFromSymbol(out, g_flag_reasons, sizeof(g_flag_reasons));
+    if (reset) {
+        unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_flag_reasons, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
 struct RasterFwdArgs {
     FrameView f;
     bsr_outputs out;
@@ -170,6 +183,10 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
             }
         }
         if (ambiguous) {
+#ifdef BSR_FLAG_REASONS
+            atomicAdd(&g_flag_reasons[p.alpha > 0.999f ? 1 : (p.alpha >= a.alpha_min && fabsf(p.alpha - a.alpha_min) >= 0.05f * a.alpha_min) ? 2 : 0], 1ull);
+            atomicAdd(&g_flag_reasons[3 + (fp64 ? 2 : unsafe ? 1 : 0)], 1ull);
+#endif
             s_flag[t] = b0 + j - start;
             done = true;
         }
@@ -178,6 +195,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
 
     if (start < end) prefetch(start, 0);
     int buf = 0;
+    int reached = start;  // emask written for [start, reached)
     for (int b0 = start; b0 < end; b0 += BSR_BLOCK, buf ^= 1) {
         const bool more = b0 + BSR_BLOCK < end;
         if (more) prefetch(b0 + BSR_BLOCK, buf ^ 1);
@@ -189,6 +207,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         //      per chunk of 32 entries into one bit column per sub-block
         batch_masks<G, stats>(s_rec[buf], nb, tx * BSR_TILE, ty * BSR_TILE, a.alpha_min, s_mask, s_col,
                               a.emask ? a.emask + b0 : nullptr);
+        reached = b0 + nb;
         __syncthreads();
         // ---- this warp's groups: open (some pixel not finished) and how much their entry
         //      sets overlap; groups that mostly share entries walk the union together
@@ -259,6 +278,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         }
     }
     cp_async_wait<0>();
+    if (a.emask && t == 0) f.mask_end[tile] = (uint32_t)reached;  // the replay's entry pre-test
     if (stats) {
         unsigned long long p2 = pairs, c2s = (unsigned)cnt;
 #pragma unroll
@@ -277,8 +297,12 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
     if (flag_at >= 0) {
         const uint32_t slot = atomicAdd(&f.ctr->flagged, 1u);
         f.flags[slot] = make_uint2((uint32_t)pix, (uint32_t)flag_at);
-        f.last[pix] = 0;
-        return;  // every per-pixel output is written by the fp64 replay
+        // the certified entries before the flag stay with the fp32 backward: it walks
+        // [0, last) from this T (sign-marked; the replay adds the clamp bits and the state
+        // behind the flag point, bwd_init); every per-pixel output is written by the replay
+        f.t_final[pix] = -T;
+        f.last[pix] = (uint32_t)last;
+        return;
     }
     const float r0 = __fmaf_rn(a.bg[0], T, c0), r1 = __fmaf_rn(a.bg[1], T, c1),
                 r2 = __fmaf_rn(a.bg[2], T, c2);

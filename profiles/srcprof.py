@@ -1,7 +1,7 @@
 """Per-source-line instruction / stall summary of one kernel in an ncu report
 (`ncu -i REP --page source --csv --print-source cuda,sass`).
 
-    python profiles/srcprof.py REP KERNEL_REGEX [top]
+    python profiles/srcprof.py REP KERNEL_REGEX [top] [samp]   (samp: order by stall samples)
 """
 import csv
 import io
@@ -40,7 +40,8 @@ def main():
         tot_i += n_inst
         tot_s += samp
     print(f"total warp instructions {tot_i:.4g}, stall samples {tot_s}")
-    for (f, ln), (ni, ss, src) in sorted(lines.items(), key=lambda kv: -kv[1][0])[:top]:
+    col = 1 if len(sys.argv) > 4 and sys.argv[4] == "samp" else 0
+    for (f, ln), (ni, ss, src) in sorted(lines.items(), key=lambda kv: -kv[1][col])[:top]:
         print(f"{100 * ni / tot_i:5.1f}% inst {100 * ss / max(tot_s, 1):5.1f}% samp  {f}:{ln:<4} {src}")
 
 
