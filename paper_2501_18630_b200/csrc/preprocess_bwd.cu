@@ -79,13 +79,39 @@ __device__ __forceinline__ void sh_basis_and_grad(float x, float y, float z, flo
 template <int CM>
 __device__ __forceinline__ void app_backward(const bsr_scene &sc, const bsr_grads &g, int64_t i, float vx,
                                              float vy, float vz, float dr, float dg, float dbl, float &ddx,
-                                             float &ddy, float &ddz) {
+                                             float &ddy, float &ddz, float4 *srow = nullptr) {
     const bool ovw = g.overwrite != 0;  // write instead of add (bsr_grads::overwrite)
     using Tr = AppTraits<CM>;
     if constexpr (Tr::sh) {
         constexpr int K = Tr::K;
         float b[16], db[16][3];
         sh_basis_and_grad<K>(vx, vy, vz, b, db);
+        if ((3 * K) % 4 == 0 && srow) {
+            // the warp staged this row (preprocess_bwd_kernel): coefficients in, coefficient
+            // gradients out (overwrite mode; the warp stores the rows coalesced)
+            // four coefficients = three float4 at a time
+#pragma unroll
+            for (int g4 = 0; g4 < K / 4; ++g4) {
+                const float4 v0 = srow[3 * g4], v1 = srow[3 * g4 + 1], v2 = srow[3 * g4 + 2];
+                const float sv[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+                float gv[12];
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int k = 4 * g4 + kk;
+                    const float dbk = sv[3 * kk] * dr + sv[3 * kk + 1] * dg + sv[3 * kk + 2] * dbl;
+                    ddx += db[k][0] * dbk;
+                    ddy += db[k][1] * dbk;
+                    ddz += db[k][2] * dbk;
+                    gv[3 * kk] = 0.f + b[k] * dr;
+                    gv[3 * kk + 1] = 0.f + b[k] * dg;
+                    gv[3 * kk + 2] = 0.f + b[k] * dbl;
+                }
+                srow[3 * g4] = make_float4(gv[0], gv[1], gv[2], gv[3]);
+                srow[3 * g4 + 1] = make_float4(gv[4], gv[5], gv[6], gv[7]);
+                srow[3 * g4 + 2] = make_float4(gv[8], gv[9], gv[10], gv[11]);
+            }
+            return;
+        }
         // coefficients and their gradients move as float4 when a row of K*3 floats is
         // 16-byte aligned (K = 4, 16); coalescing-friendly vs 3K scalar accesses
         float shv[3 * K], gsv[3 * K];
@@ -313,7 +339,7 @@ __device__ __forceinline__ void geom_chain(const PreBwdArgs &a, int64_t i, T dmx
 }
 
 template <int K>
-__device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
+__device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c, float4 *srow = nullptr) {
     const float *acc = a.f.grad_acc + (int64_t)c * kGradStride;
     const float4 g1 = *reinterpret_cast<const float4 *>(acc + 4);
     const float4 g2 = *reinterpret_cast<const float4 *>(acc + 8);
@@ -349,7 +375,7 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
         vy *= ivn;
         vz *= ivn;
         float ddx = 0.f, ddy = 0.f, ddz = 0.f;
-        app_backward<K>(sc, a.g, i, vx, vy, vz, dr, dg, dbl, ddx, ddy, ddz);
+        app_backward<K>(sc, a.g, i, vx, vy, vz, dr, dg, dbl, ddx, ddy, ddz, srow);
         const float dd = ddx * vx + ddy * vy + ddz * vz;
         dpx += (ddx - dd * vx) * ivn;
         dpy += (ddy - dd * vy) * ivn;
@@ -371,7 +397,7 @@ __device__ __forceinline__ void prebwd_one(const PreBwdArgs &a, int64_t c) {
 // bsr_grads::overwrite: the rows of a culled primitive (its gradients are zero,
 // rasterizer.py:262-320) -- written here since nothing else touches them
 template <int CM>
-__device__ __forceinline__ void zero_rows(const PreBwdArgs &a, int64_t i) {
+__device__ __forceinline__ void zero_rows(const PreBwdArgs &a, int64_t i, bool sh_staged = false) {
     using Tr = AppTraits<CM>;
     const bsr_grads &g = a.g;
     for (int q = 0; q < 3; ++q) g.positions[3 * i + q] = g.log_scales[3 * i + q] = 0.f;
@@ -381,6 +407,10 @@ __device__ __forceinline__ void zero_rows(const PreBwdArgs &a, int64_t i) {
         for (int q = 0; q < 4; ++q) g.rotations[4 * i + q] = 0.f;
     g.opacity_raw[i] = g.shapes[i] = 0.f;
     if constexpr (Tr::sh) {
+        if (sh_staged) {  // the warp's coalesced row store writes it
+            if (a.screen_grad_norm) a.screen_grad_norm[i] = 0.f;
+            return;
+        }
         float *row = g.sh + 3 * Tr::K * i;
         if ((3 * Tr::K) % 4 == 0 && (reinterpret_cast<uintptr_t>(g.sh) & 15) == 0) {
             for (int q = 0; q < 3 * Tr::K / 4; ++q) reinterpret_cast<float4 *>(row)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -401,12 +431,30 @@ constexpr int kPreBwdChunk = 64;
 // 4-warp CTAs: small scenes (config 1: one wave) spread over more SMs
 constexpr int kPreBwdThreads = 128;
 
+// SH rows (3K floats, K = 4 / 16: whole float4s) of the warp's chunk are staged through
+// shared memory in overwrite mode: loaded and stored by the warp with lane-contiguous
+// 16-byte accesses (a thread per row would touch 32 rows 3K floats apart per access), the
+// culled rows' zeros included.
+static_assert(kPreBwdChunk == 64, "two visibility words per warp chunk");
+template <int CM>
+struct PreBwdStage {
+    static constexpr bool on = AppTraits<CM>::sh && (3 * AppTraits<CM>::K) % 4 == 0;
+    static constexpr int rw = on ? 3 * AppTraits<CM>::K / 4 : 0;  // float4 per row
+    static constexpr int rs = rw | 1;  // row stride: odd, so 8 lanes' float4 rows hit distinct banks
+    static constexpr size_t bytes = (size_t)(kPreBwdThreads / 32) * kPreBwdChunk * rs * 16;
+};
+
 template <int K>
 __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_constant__ const PreBwdArgs a) {
     pdl_wait();
+    using St = PreBwdStage<K>;
+    extern __shared__ float4 pbw_stage[];
     const int lane = threadIdx.x & 31;
     const int64_t c0 = ((blockIdx.x * (int64_t)kPreBwdThreads + threadIdx.x) >> 5) * kPreBwdChunk;
     if (c0 >= a.f.n) return;
+    const bool stage = St::on && a.g.overwrite && !a.drgb &&
+                       ((reinterpret_cast<uintptr_t>(a.sc.sh) | reinterpret_cast<uintptr_t>(a.g.sh)) & 15) == 0;
+    float4 *wbuf = pbw_stage + (threadIdx.x >> 5) * (kPreBwdChunk * St::rs);
     uint32_t m[kPreBwdChunk / 32];
     int tot = 0;
 #pragma unroll
@@ -416,7 +464,16 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_c
         m[q] = __ballot_sync(0xffffffffu, vis);
         tot += __popc(m[q]);
         if (a.drgb && c < a.f.n && !vis) a.drgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (a.g.overwrite && c < a.f.n && !vis) zero_rows<K>(a, c);
+        if (a.g.overwrite && c < a.f.n && !vis) zero_rows<K>(a, c, stage);
+    }
+    const int rows = (int)min((int64_t)kPreBwdChunk, a.f.n - c0);
+    if (St::on && stage) {
+        const float4 *src = reinterpret_cast<const float4 *>(a.sc.sh) + c0 * St::rw;
+        for (int u = lane; u < rows * St::rw; u += 32) {
+            const int row = u / St::rw;
+            if (((row < 32 ? m[0] : m[1]) >> (row & 31)) & 1u) wbuf[u + row * (St::rs - St::rw)] = __ldg(src + u);
+        }
+        __syncwarp();
     }
     for (int base = 0; base < tot; base += 32) {
         int r = base + lane;
@@ -428,7 +485,17 @@ __global__ void __launch_bounds__(kPreBwdThreads) preprocess_bwd_kernel(__grid_c
                 r -= __popc(m[k]);
                 q = k + 1;
             }
-        prebwd_one<K>(a, c0 + 32 * q + (int)__fns(m[q], 0, r + 1));
+        const int row = 32 * q + (int)__fns(m[q], 0, r + 1);
+        prebwd_one<K>(a, c0 + row, (St::on && stage) ? wbuf + row * St::rs : nullptr);
+    }
+    if (St::on && stage) {
+        __syncwarp();
+        float4 *dst = reinterpret_cast<float4 *>(a.g.sh) + c0 * St::rw;
+        for (int u = lane; u < rows * St::rw; u += 32) {
+            const int row = u / St::rw;
+            dst[u] = (((row < 32 ? m[0] : m[1]) >> (row & 31)) & 1u) ? wbuf[u + row * (St::rs - St::rw)]
+                                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
 }
 
@@ -531,7 +598,13 @@ int launch_preprocess_bwd(const bsr_scene &sc, const KCam &cam, const FrameView 
         BSR_LAUNCH_CHECK();
         return BSR_OK;
     }
-#define BSR_PREBWD_LAUNCH(CM) BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)))
+#define BSR_PREBWD_LAUNCH(CM)                                                                                   \
+    do {                                                                                                        \
+        static SmemAttrOnce attr;                                                                               \
+        BSR_CUDA_TRY(attr.ensure(preprocess_bwd_kernel<CM>, PreBwdStage<CM>::bytes));                           \
+        BSR_CUDA_TRY((pdl_launch(preprocess_bwd_kernel<CM>, dim3(blocks), dim3(kPreBwdThreads),                  \
+                                 PreBwdStage<CM>::bytes, st, a)));                                              \
+    } while (0)
     BSR_DISPATCH_CM(sc, BSR_PREBWD_LAUNCH);
 #undef BSR_PREBWD_LAUNCH
     BSR_CUDA_TRY((pdl_launch(prebwd_geom_kernel<false>, dim3(blocks), dim3(kPreBwdThreads), 0, st, a)));
