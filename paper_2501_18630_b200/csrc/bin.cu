@@ -68,14 +68,52 @@ __device__ __forceinline__ void bin_one(const FrameView &f, uint32_t t, uint64_t
     }
 }
 
+// Scatter of up to U entries per thread with every cursor atomic in flight before the first
+// store (the store needs the atomic's returned slot: one at a time, each warp would wait a
+// full L2 round trip per entry).
+template <int U>
+__device__ __forceinline__ void scatter_u(const FrameView &f, const uint32_t (&t)[U], const bool (&ok)[U],
+                                          const uint64_t (&key)[U]) {
+    uint32_t slot[U], at[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (ok[u]) slot[u] = atomicAdd(tile_cur_at(f, t[u]), 1u);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (ok[u]) at[u] = f.tile_ranges[t[u]].x;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (ok[u]) f.tent[at[u] + slot[u]] = key[u];
+}
+#ifndef BSR_SCATTER_U
+#define BSR_SCATTER_U 4
+#endif
+constexpr int kScatterU = BSR_SCATTER_U;
+
 template <bool COUNT>
 __device__ __forceinline__ void bin_rect(const FrameView &f, uint32_t c, uint32_t cnt, uint32_t j0, uint32_t step) {
     const RectInfo r = rect_of(f, c);
     const uint64_t key = COUNT ? 0ull : (((uint64_t)f.dkeys[0][c] << 32) | c);
-    for (uint32_t j = j0; j < cnt; j += step) {
+    auto tile_of = [&](uint32_t j) {
         const uint32_t row = j / (uint32_t)r.spanx;
-        bin_one<COUNT>(f, (uint32_t)(r.ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(r.tx0 + (int)(j - row * r.spanx)),
-                       key);
+        return (uint32_t)(r.ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(r.tx0 + (int)(j - row * r.spanx));
+    };
+    if (COUNT) {
+        for (uint32_t j = j0; j < cnt; j += step) bin_one<true>(f, tile_of(j), key);
+        return;
+    }
+    for (uint32_t j = j0; j < cnt; j += kScatterU * step) {
+        uint32_t t[kScatterU];
+        bool ok[kScatterU];
+        uint64_t k[kScatterU];
+#pragma unroll
+        for (int u = 0; u < kScatterU; ++u) {
+            const uint32_t ju = j + u * step;
+            ok[u] = ju < cnt;
+            t[u] = ok[u] ? tile_of(ju) : 0u;
+            k[u] = key;
+        }
+        scatter_u<kScatterU>(f, t, ok, k);
     }
 }
 
@@ -115,9 +153,9 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
             if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        for (uint32_t base = 0; base < total; base += 32) {
-            const uint32_t e = base + lane;
-            // owner = number of lanes whose inclusive prefix is <= e
+        // entry e of the warp: its owner lane (number of lanes whose inclusive prefix is <= e)
+        // and tile
+        auto entry = [&](uint32_t e, uint32_t &t, uint64_t &okey) {
             int lo = 0;
 #pragma unroll
             for (int s = 16; s; s >>= 1) {
@@ -130,12 +168,31 @@ __global__ void __launch_bounds__(BSR_BLOCK) bin_entries_kernel(FrameView f) {
             const int tx0 = __shfl_sync(0xffffffffu, r.tx0, owner);
             const int ty0 = __shfl_sync(0xffffffffu, r.ty0, owner);
             const int spanx = __shfl_sync(0xffffffffu, r.spanx, owner);
-            const uint64_t okey = __shfl_sync(0xffffffffu, key, owner);
-            if (e >= total) continue;
+            okey = __shfl_sync(0xffffffffu, key, owner);
             const uint32_t local = e - (oin - ocnt);
             const uint32_t row = local / (uint32_t)spanx;
-            const uint32_t t = (uint32_t)(ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(tx0 + (int)(local - row * spanx));
-            bin_one<COUNT>(f, t, okey);
+            t = (uint32_t)(ty0 + (int)row) * (uint32_t)f.tiles_x + (uint32_t)(tx0 + (int)(local - row * spanx));
+        };
+        if (COUNT) {
+            for (uint32_t base = 0; base < total; base += 32) {
+                uint32_t t;
+                uint64_t okey;
+                entry(base + lane, t, okey);
+                if (base + lane < total) bin_one<true>(f, t, okey);
+            }
+        } else {
+            for (uint32_t base = 0; base < total; base += 32 * kScatterU) {
+                uint32_t t[kScatterU];
+                bool ok[kScatterU];
+                uint64_t k[kScatterU];
+#pragma unroll
+                for (int u = 0; u < kScatterU; ++u) {
+                    const uint32_t e = base + 32 * u + lane;
+                    entry(e, t[u], k[u]);
+                    ok[u] = e < total;
+                }
+                scatter_u<kScatterU>(f, t, ok, k);
+            }
         }
         // queue overflow: the warp bins those rectangles itself
         unsigned ob = __ballot_sync(0xffffffffu, own_big != 0);
