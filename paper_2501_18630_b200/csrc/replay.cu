@@ -160,6 +160,26 @@ __device__ __forceinline__ int gather_entries(const ReplayArgs &a, const MaskTes
     return n;
 }
 
+// This thread's entry of the next round (-1: none), advancing base: when the rest of the
+// list fits in one round, the mask test is applied in place (no compaction barriers on
+// the short lists of small frames); otherwise the survivors are gathered.  surv aliases
+// round-local shared arrays, hence the barrier after reading it.
+template <int NT>
+__device__ __forceinline__ int next_entry(const ReplayArgs &a, int tile, int start, int px, int py, int &base, int end,
+                                          int *surv, int (*gwc)[NT / 32], int *next) {
+    const MaskTest mt = mask_test(a, tile, start, px, py);
+    if (end - base <= NT) {
+        const int e = base + (int)threadIdx.x;
+        base = end;
+        if (e >= end) return -1;
+        return (e >= mt.mend || ((__ldg(a.emask + e) >> mt.bit) & 1u)) ? e : -1;
+    }
+    const int n = gather_entries<NT>(a, mt, base, end, surv, gwc, next);
+    const int e = (int)threadIdx.x < n ? surv[threadIdx.x] : -1;
+    __syncthreads();
+    return e;
+}
+
 
 // Evaluate alpha exactly as _raster.pyx:107-113 (fp64, no contraction in this TU).
 __device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, double &dx, double &dy,
@@ -216,7 +236,8 @@ __device__ __forceinline__ int compact_slot(bool cand, S &sm) {
 // prefix at the split point) by slot; for the raster backward's part (raster_fwd.cu left
 // t_final = -T, last = its certified end) the normalised colour behind the split point,
 // (raw - prefix) / T, and the clamp bits of the fp64 raw (rasterizer.py:253).
-__device__ __forceinline__ void store_split(const ReplayArgs &a, uint32_t slot, int64_t pix, double r0, double r1,
+__device__ __forceinline__ void store_split(const ReplayArgs &a, uint32_t slot, int64_t pix, uint32_t last32,
+                                            double r0, double r1,
                                             double r2, double dd, double t_acc, int last, double t_flag,
                                             double p0, double p1, double p2, double pd) {
     const FrameView &f = a.f;
@@ -237,7 +258,7 @@ __device__ __forceinline__ void store_split(const ReplayArgs &a, uint32_t slot, 
     f.bwd_init[pix] = t_flag > 0.0 ? make_float4((float)((r0 - p0) * it), (float)((r1 - p1) * it),
                                                  (float)((r2 - p2) * it), (float)((dd - pd) * it))
                                    : make_float4((float)a.bg[0], (float)a.bg[1], (float)a.bg[2], 0.f);
-    f.last[pix] = (f.last[pix] & 0x1FFFFFFFu) | (!(r0 >= 0.0) ? 1u << 29 : 0u) | (!(r1 >= 0.0) ? 1u << 30 : 0u) |
+    f.last[pix] = (last32 & 0x1FFFFFFFu) | (!(r0 >= 0.0) ? 1u << 29 : 0u) | (!(r1 >= 0.0) ? 1u << 30 : 0u) |
                   (!(r2 >= 0.0) ? 1u << 31 : 0u);
 }
 
@@ -259,6 +280,7 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     const int tile = (py / BSR_TILE) * f.tiles_x + px / BSR_TILE;
     const int start = (int)ranges[tile].x, end = (int)ranges[tile].y;
     const int flag_at = (int)fl.y;
+    const uint32_t last32 = t == 0 ? f.last[pix] : 0u;  // the fp32 part's end (raster_fwd.cu), read early
 
     double t_acc = 1.0;  // thread 0: transmittance
     double sum = 0.0;    // lane c < 4 of warp 0: running r / g / b / depth sum
@@ -273,9 +295,7 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     int base = start;
     while (base < end) {
         if (sm.done) break;  // uniform (read after a barrier)
-        const int n = gather_entries<NT>(a, mask_test(a, tile, start, px, py), base, end, surv, sm.gwc, &sm.next);
-        const int e = t < n ? surv[t] : -1;
-        __syncthreads();  // surv aliases val
+        const int e = next_entry<NT>(a, tile, start, px, py, base, end, surv, sm.gwc, &sm.next);
         Entry64 en;
         bool cand = false;
         double alpha = 0.0;
@@ -386,7 +406,7 @@ __device__ void replay_fwd_one(const ReplayArgs &a, const P &prov, uint32_t slot
     if (a.out.transmittance) a.out.transmittance[pix] = (float)t_acc;
     if (a.out.depth) a.out.depth[pix] = (float)dd;
     if (a.out.pixel_count) a.out.pixel_count[pix] = count;
-    store_split(a, slot, pix, r0, r1, r2, dd, t_acc, last, t_flag, p0, p1, p2, pd);
+    store_split(a, slot, pix, last32, r0, r1, r2, dd, t_acc, last, t_flag, p0, p1, p2, pd);
 }
 
 // Gradients of one candidate (_raster.pyx:206-241 + depth) from its T and the colour /
@@ -477,9 +497,7 @@ __device__ void replay_bwd_cta(const ReplayArgs &a, const P &prov, uint32_t slot
     int *surv = reinterpret_cast<int *>(sm.r);
     int base = start + flag_at;
     while (base < end) {
-        const int n = gather_entries<BSR_BLOCK>(a, mask_test(a, tile, start, px, py), base, end, surv, sm.gwc, &sm.next);
-        const int e = t < n ? surv[t] : -1;
-        __syncthreads();  // surv aliases r
+        const int e = next_entry<BSR_BLOCK>(a, tile, start, px, py, base, end, surv, sm.gwc, &sm.next);
         Entry64 en;
         bool cand = false;
         double alpha = 0.0, dx = 0, dy = 0, x = 1, kernel = 0;
