@@ -330,6 +330,23 @@ def test_loss_matches_reference_golden(cuda):
     np.testing.assert_allclose(d, g["d_image"], rtol=1e-3, atol=1e-4 * scale)
 
 
+@pytest.mark.parametrize("w,h", [(1280, 720), (2304, 1856)])
+def test_loss_both_tilings_match_oracle(cuda, w, h):
+    """Both SSIM tilings (one channel per CTA up to 4 Mpixel, all three above) against the
+    oracle's fp64 loss (training.py:51-131) on random images."""
+    from oracle import pipeline as orc
+    from paper_2501_18630_b200 import training
+
+    rng = np.random.default_rng(w)
+    a = rng.uniform(0.0, 1.0, (h, w, 3)).astype(np.float32)
+    b = np.clip(a + rng.normal(0.0, 0.1, a.shape), 0.0, 1.0).astype(np.float32)
+    value, d_image = training.loss(a, b)
+    ref_value, ref_d = orc.loss(a.astype(np.float64), b.astype(np.float64))
+    assert value == pytest.approx(ref_value, rel=1e-5)
+    scale = np.abs(ref_d).max()
+    np.testing.assert_allclose(d_image.cpu().numpy(), ref_d, rtol=1e-3, atol=1e-4 * scale)
+
+
 def test_adam_matches_reference_golden(cuda):
     import torch
     from paper_2501_18630_b200 import training
