@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         } else {
             p = eval_pair(A, B, px - bd.x, py - bd.z);
         }
+        // most evaluated pairs are well below the cutoff: one compare leaves them (the
+        // tests below cannot pass for alpha below ~0.9 alpha_min; no extra live register)
+        if (!(p.alpha * 1.1111111f >= a.alpha_min)) return false;
         bool ambiguous = false;
         // rare path: alpha within 5% of the cutoff -> certify with the error bound
         if (fabsf(p.alpha - a.alpha_min) < 0.05f * a.alpha_min) {
