@@ -518,7 +518,6 @@ def e2e_api_loop(w, steps, world):
     import torch
 
     from paper_2501_18630_b200 import distributed as dd
-    from paper_2501_18630_b200.primitive import GradientBuffer
     from paper_2501_18630_b200.rasterizer import check_pending, render_backward, render_tiled
     from paper_2501_18630_b200.training import AdamState, LossWorkspace, adam_step, group_lrs, loss_into
 
@@ -574,12 +573,12 @@ def e2e_api_loop(w, steps, world):
             up_ev[b ^ 1].record(cs)
         main.wait_event(up_ev[b])
         tgt = tgt2[b]
-        grads = GradientBuffer.zeros_for(prims)
+        grads = None  # the first view's backward writes a fresh buffer, later views add into it
         for v, cam in enumerate(cams):
             out = render_tiled(prims, cam, bg)
             k = (cam.width, cam.height)
             loss_into(out.color, tgt[v], d_img[k], ws[k], values=vals[v])
-            render_backward(prims, cam, bg, d_img[k], forward_out=out, grads=grads)
+            grads = render_backward(prims, cam, bg, d_img[k], forward_out=out, grads=grads)
         if world > 1:
             dd.allreduce_grads(grads.flat)
         if state is not None:
