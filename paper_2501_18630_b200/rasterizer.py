@@ -143,12 +143,19 @@ def check_pending(block: bool = False):
 class RenderOutput:
     color: torch.Tensor  # (H, W, 3) max(raw, 0)
     alpha: torch.Tensor  # (H, W)
-    contributions: torch.Tensor  # (N,) int64
+    contributions: torch.Tensor  # (N,) int64 (counted in int32 on the device, widened on first access)
     raw_color: torch.Tensor  # (H, W, 3)
     transmittance: torch.Tensor  # (H, W)
     depth: torch.Tensor | None = None  # (H, W) extension
     pixel_count: torch.Tensor | None = None  # (H, W) int32 extension
     frame: FrameState | None = None
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if name == "contributions" and v is not None and v.dtype != torch.int64:
+            v = v.long()  # a step that never reads them skips the conversion kernel
+            object.__setattr__(self, "contributions", v)
+        return v
 
 
 def _stream():
@@ -417,7 +424,7 @@ def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, 
     out = outputs_c(color, raw, alpha, trans, depth, count, contrib)
     frame = forward_raw(_prims_scene_c(prims), camera, background, out, contrib=contrib,
                         check=True if sync else "async")
-    return RenderOutput(color, alpha, contrib.long(), raw, trans, depth, count, frame)
+    return RenderOutput(color, alpha, contrib, raw, trans, depth, count, frame)
 
 
 def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, forward_out=None,
