@@ -207,3 +207,12 @@ def require_cuda():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2501_18630_b200 needs a CUDA device (no CPU fallback)")
     load()
+
+
+def stream_ptr():
+    """Raw cudaStream_t of torch's current stream on the current device, as a ctypes
+    pointer.  Through the C++ accessor: torch.cuda.current_stream() re-runs Python device
+    availability checks on every call (~10 us, several times per rendered view)."""
+    import torch
+
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))

@@ -45,7 +45,7 @@ class CodecGroupC(ctypes.Structure):
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 # ----------------------------------------------------------------------------- PNG I/O

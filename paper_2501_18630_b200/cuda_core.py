@@ -52,7 +52,7 @@ def _scratch(v, width, height, e):
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 def forward_tiled(means, conics, opac, betas, colors, bounds, height, width, background, tile_size,

@@ -57,7 +57,7 @@ class DeviceRNG:
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 def _scratch(n: int, device):

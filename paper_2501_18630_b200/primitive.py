@@ -14,6 +14,8 @@ aligned for float4 loads.
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 import torch
 
@@ -37,8 +39,10 @@ def group_widths(k: int | None = None, lobes: int | None = None) -> dict:
     return w
 
 
+@functools.lru_cache(maxsize=256)
 def group_layout(n: int, k: int | None = None, lobes: int | None = None):
-    """[(name, start, stop, shape)] of the flat buffer for the SH (k) or SB (lobes) model."""
+    """((name, start, stop, shape), ...) of the flat buffer for the SH (k) or SB (lobes)
+    model, and its length (cached: every buffer of a set rebuilds its views from it)."""
     widths = {"positions": 3, "rotations": 4, "log_scales": 3, "opacity_raw": 1, "shapes": 1}
     shapes = {"positions": (n, 3), "rotations": (n, 4), "log_scales": (n, 3), "opacity_raw": (n,),
               "shapes": (n,)}
@@ -55,7 +59,7 @@ def group_layout(n: int, k: int | None = None, lobes: int | None = None):
         out.append((g, off, off + widths[g] * n, shapes[g]))
         off += widths[g] * n
         off = (off + 3) // 4 * 4  # every group starts 16-byte aligned (float4 access)
-    return out, off
+    return tuple(out), off
 
 
 class FlatGroups:

@@ -126,7 +126,7 @@ def _queue_status(frame: FrameState):
         torch.empty(_snapshot_bytes(), dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
     _lib.check(_lib.load().bsr_frame_status_async(ctypes.c_void_p(frame.ptr()), ctypes.c_void_p(snap.data_ptr()),
                                                   _stream()), "frame_status_async")
-    ev.record()
+    ev.record(torch.cuda.current_stream(torch._C._cuda_getDevice()))  # (int device: no availability checks)
     p = PendingStatus(snap, ev, (frame.n, frame.width, frame.height))
     frame.pending = p
     _PENDING.append(p)
@@ -159,7 +159,7 @@ class RenderOutput:
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 def _bg_arr(background):

@@ -64,7 +64,7 @@ def _tables(n, lobes, sh_coeffs):
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 def _parse_header(fh):

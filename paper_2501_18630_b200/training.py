@@ -34,7 +34,7 @@ ADAM_EPS = 1e-15  # training.py:33
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_ptr()
 
 
 class LossWorkspace:
