@@ -31,7 +31,8 @@ struct Counters {
     uint32_t depth_key_max_inv;  // max(~key) == ~min(key) over the 32-bit depth keys
     uint32_t depth_plan[kDepthPasses + 1];
     uint32_t big_tiles;      // crowded tiles queued by tile_sort for tile_sort_big (ids in tile_cur)
-    uint32_t pad[4];
+    uint32_t mid_tiles;      // tiles queued by tile_sort for tile_sort_mid (ids in tile_cnt)
+    uint32_t pad[3];
 };
 
 // Deterministic accumulation of the backward's per-primitive partials
