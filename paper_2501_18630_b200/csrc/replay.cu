@@ -196,9 +196,10 @@ __device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, doub
 // Forward rounds are wider (kReplayFwdThreads entries) and keep only what the recurrence
 // reads: alpha (overwritten by the weight alpha * T once T is known) and r, g, b, z.
 // Small frames (few flagged pixels, latency-bound) use one 1024-wide CTA per SM; large ones
-// (thousands of flagged pixels) eight 128-wide CTAs per SM for more pixels in flight
+// (thousands of flagged pixels) 32 one-warp CTAs per SM for more pixels in flight
 // (measured, scripts/ab_replay_nt.sh: config 3 1024 > 256 > 128, config 4 0.54 ms at
-// 1024 -> 0.20 at 256 -> 0.15 at 128).  BSR_REPLAY_NT overrides for A/B runs.
+// 1024 -> 0.20 at 256 -> 0.15 at 128; after the mask pre-test 0.172 at 128 -> 0.147 at
+// 64 -> 0.122 at 32).  BSR_REPLAY_NT overrides for A/B runs.
 constexpr int kRecBatch = 8;  // transmittance steps per batch (the stop test runs per batch)
 constexpr int64_t kReplayWideMaxPixels = 4 << 20;
 template <int NT>
@@ -656,13 +657,14 @@ static int launch_replay(bool fwd, const ReplayArgs &a, const P &prov, cudaStrea
             const char *e = getenv("BSR_REPLAY_NT");
             return e ? atoi(e) : 0;
         }();
-        const int nt = nt_env ? nt_env : ((int64_t)a.f.W * a.f.H <= kReplayWideMaxPixels ? 1024 : 128);
+        const int nt = nt_env ? nt_env : ((int64_t)a.f.W * a.f.H <= kReplayWideMaxPixels ? 1024 : 32);
         switch (nt) {
             case 1024: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 1024>, dim3(148), dim3(1024), 0, st, a, prov))); break;
             case 512: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 512>, dim3(2 * 148), dim3(512), 0, st, a, prov))); break;
             case 256: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 256>, dim3(4 * 148), dim3(256), 0, st, a, prov))); break;
             case 128: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 128>, dim3(8 * 148), dim3(128), 0, st, a, prov))); break;
-            default: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 64>, dim3(16 * 148), dim3(64), 0, st, a, prov))); break;
+            case 64: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 64>, dim3(16 * 148), dim3(64), 0, st, a, prov))); break;
+            default: BSR_CUDA_TRY((pdl_launch(replay_fwd_kernel<P, 32>, dim3(32 * 148), dim3(32), 0, st, a, prov))); break;
         }
     }
     else if ((int64_t)a.f.W * a.f.H <= kReplayWideMaxPixels)  // one CTA per flagged pixel
