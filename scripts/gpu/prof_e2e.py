@@ -18,7 +18,5 @@ ms, views, _, _ = bench.e2e_api_loop(w, 200, 1)
 pr.disable()
 print(cfg, "ms per step", ms / 200)
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(12)
-st.print_callers("copy_")
-st.print_callers("current_stream")
-st.print_callers("torch.zeros")
+st.sort_stats("tottime").print_stats(30)
+st.sort_stats("cumtime").print_stats(30)
