@@ -117,6 +117,10 @@ def dist_setup(n_gpus):
     if int(os.environ.get("WORLD_SIZE", "1")) <= 1:
         return dd.init(None)
     backend = os.environ.get("BSR_DIST_BACKEND", "nccl")
+    # the communicator's init lines (ranks, transports, NVLS) on stderr, also when the
+    # driver's torchrun launched the ranks instead of spawn_ranks
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if backend == "gloo":
         import torch
 
