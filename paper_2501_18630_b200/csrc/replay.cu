@@ -108,9 +108,10 @@ struct ReplayArgs {
 // (kept by the forward raster, raster.cuh entry_tile_mask: conservative for the fp64
 // alpha >= alpha_min decision, which the fp32 raster relies on for every pixel it
 // certifies) has the pixel's sub-block bit; entries past the tile's mask_end were not
-// reached by the forward and are all kept.  Collects, in list order, the next survivors
-// from `base` on into surv[] (at least min(NT, left), fewer than 2 NT) and advances base;
-// returns the count.  Uniform across the CTA (called by all threads).
+// reached by the forward and are all kept.  gather_entries collects, in list order, the
+// next survivors from `base` on into surv[] (NT of them, or all that are left) and advances
+// base past the last one taken; returns the count.  Uniform across the CTA (called by all
+// threads).
 struct MaskTest {
     int mend, bit;
 };
