@@ -137,10 +137,15 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // lane that does not take the pair (outside its last contributor, alpha < alpha_min, or
 // its group's list exhausted) runs it with alpha = 0 and dL/dalpha = 0, which leaves its
 // state (T, behind colour) exactly unchanged and all 11 partials exactly 0.
+// MINB: resident CTAs per SM the register budget targets.  4 (64 registers, some spills)
+// on frames of many tiles (config 4 raster bwd 4.42 -> 4.14 ms, config 3 0.771 -> 0.725 ms
+// per view); 3 on small ones, where the full register file would keep the concurrent fp64
+// replay's CTAs off the SMs until the raster's tail (config 1: 1.5-2% slower at 4)
+constexpr int kBwdWideMinTiles = 4096;
 // DET: 0 float atomics into grad_acc; 1 / 2 the deterministic bound / fixed-point passes
 // (frame.cuh DetAcc) -- the same values, added through det_add.
-template <bool STATS, int G, int DET>
-__global__ void __launch_bounds__(BSR_BLOCK, 3) raster_bwd_kernel(RasterBwdArgs a) {
+template <bool STATS, int G, int DET, int MINB>
+__global__ void __launch_bounds__(BSR_BLOCK, MINB) raster_bwd_kernel(RasterBwdArgs a) {
     pdl_wait();
     using SB = SubBlock<G>;
     using TG = TileGrid<G>;
@@ -449,13 +454,15 @@ int raster_groups();
 template <int G>
 static int launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
     if (stats)
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G, 0>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G, 0, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (a.f.det.mode == 1)
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 1>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 1, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (a.f.det.mode == 2)
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 2>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 2, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    else if (tiles >= kBwdWideMinTiles)
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 0, 4>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else
-        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 0>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 0, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     return BSR_OK;
 }
 
