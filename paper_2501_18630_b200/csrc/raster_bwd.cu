@@ -455,8 +455,12 @@ template <int G>
 static int launch_bwd_g(const RasterBwdArgs &a, int tiles, bool stats, cudaStream_t st) {
     if (stats)
         BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<true, G, 0, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    else if (a.f.det.mode == 1 && tiles >= kBwdWideMinTiles)
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 1, 4>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (a.f.det.mode == 1)
         BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 1, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    else if (a.f.det.mode == 2 && tiles >= kBwdWideMinTiles)
+        BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 2, 4>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (a.f.det.mode == 2)
         BSR_CUDA_TRY((pdl_launch(raster_bwd_kernel<false, G, 2, 3>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else if (tiles >= kBwdWideMinTiles)
