@@ -555,11 +555,17 @@ __device__ __forceinline__ void prebwd_geom_one(const PreBwdArgs &a, int64_t i) 
     if (a.screen_grad_norm) a.screen_grad_norm[i] = (float)sqrt(dmx * dmx + dmy * dmy);
 }
 
+// 6 resident CTAs per SM (80 registers; the fp64 chain then spills ~0.5 KB to L1, which the
+// extra warps hide: measured 4 / 5 / 6 / 7 / 8 per SM, config 3 0.281 / 0.264 / 0.260 /
+// 0.269 / 0.275 ms per view, config 4 preprocess_bwd 0.904 / 0.878 / 0.860 / 0.901 / 0.941 ms)
+#ifndef BSR_GEOM_MINB
+#define BSR_GEOM_MINB 6
+#endif
 // DRGB: the multi-view deferred-colour mode, where the fp32 colour kernel has nothing
 // left but the opacity / shape chains and the d rgb store -- done here instead, so that
 // mode runs one kernel per view, not two.
 template <bool DRGB>
-__global__ void __launch_bounds__(kPreBwdThreads) prebwd_geom_kernel(__grid_constant__ const PreBwdArgs a) {
+__global__ void __launch_bounds__(kPreBwdThreads, BSR_GEOM_MINB) prebwd_geom_kernel(__grid_constant__ const PreBwdArgs a) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t c0 = ((blockIdx.x * (int64_t)kPreBwdThreads + threadIdx.x) >> 5) * kPreBwdChunk;
