@@ -108,6 +108,11 @@ typedef struct bsr_outputs {
     float *depth;          /* (H,W)   sum_k w_k z_k (extension, no background term)          */
     int32_t *pixel_count;  /* (H,W)   contributors per pixel (extension)                     */
     int32_t *contributions;/* (N,)    pixels each primitive contributed to, ADDED into       */
+    int32_t defer_contributions; /* nonzero: bsr_forward adds only the fp64 replay's part of
+                            contributions (flagged pixels from their flag point on); the raster's
+                            part is added by bsr_contributions() on the same frame, when (if)
+                            the caller needs the counts -- counting inside the forward raster
+                            costs it ~18% (config 4) */
 } bsr_outputs;
 
 /* Optional profiling hooks (caller-owned; pass NULL to disable).
@@ -145,6 +150,12 @@ int bsr_frame_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_cap,
 int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
                 void *frame, uint64_t frame_bytes, int64_t entry_cap, const bsr_outputs *out,
                 const bsr_profile *profile, void *stream);
+/* The raster's part of the contributions of a forward run with defer_contributions, ADDED
+ * into contributions (N,): re-walks every pixel's certified entries on the unchanged frame
+ * (same decisions, no outputs written).  Call at most once per forward. */
+int bsr_contributions(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                      void *frame, uint64_t frame_bytes, int64_t entry_cap, int32_t *contributions,
+                      void *stream);
 /* fp32 colours of every primitive for each of `views` camera centres (world, double[3]
  * each): rgb[v][i][0..2] (4 floats per primitive), exactly the values bsr_forward's
  * preprocess computes for that view -- feed rgb + v*N*4 as bsr_scene.view_rgb. */

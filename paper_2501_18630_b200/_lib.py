@@ -62,7 +62,7 @@ class GradsC(ctypes.Structure):
 class OutputsC(ctypes.Structure):
     _fields_ = [("color", c_void_p), ("raw", c_void_p), ("alpha", c_void_p),
                 ("transmittance", c_void_p), ("depth", c_void_p), ("pixel_count", c_void_p),
-                ("contributions", c_void_p)]
+                ("contributions", c_void_p), ("defer_contributions", c_int32)]
 
 
 BSR_MAX_GROUPS = 16
@@ -95,6 +95,8 @@ EXPORTS = {
     "bsr_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
                               c_void_p, c_void_p]),
     "bsr_frame_status": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "bsr_contributions": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_uint64, c_int64, c_void_p,
+                                    c_void_p]),
     "bsr_view_colors": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "bsr_frame_snapshot_bytes": (c_int32, [c_void_p]),
     "bsr_frame_status_async": (c_int32, [c_void_p, c_void_p, c_void_p]),

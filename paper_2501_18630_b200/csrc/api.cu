@@ -12,6 +12,7 @@ namespace bsr {
 int launch_preprocess(const bsr_scene &, const KCam &, const FrameView &, cudaStream_t);
 int launch_depth_sort(const FrameView &, cudaStream_t);
 int launch_bin_count(const FrameView &, cudaStream_t);
+int launch_raster_count(const FrameView &, int32_t *, const float[3], float, float, cudaStream_t);
 int launch_bin_scatter(const FrameView &, cudaStream_t);
 int launch_tile_sort(const FrameView &, cudaStream_t);
 int launch_raster_fwd(const FrameView &, const bsr_outputs &, const float bg[3], float, float,
@@ -269,7 +270,9 @@ extern "C" int bsr_forward(const bsr_scene *scene, const bsr_camera *camera, con
     if ((rc = mark(prof, 3, st))) return rc;
     if ((rc = launch_tile_sort(f, st))) return rc;
     if ((rc = mark(prof, 4, st))) return rc;
-    if ((rc = launch_raster_fwd(f, *out, background, (float)kAlphaMin, (float)kTStop, nullptr, nullptr,
+    bsr_outputs out_raster = *out;  // deferred contributions: the replay counts its part now
+    if (out->defer_contributions) out_raster.contributions = nullptr;
+    if ((rc = launch_raster_fwd(f, out_raster, background, (float)kAlphaMin, (float)kTStop, nullptr, nullptr,
                                 nullptr, stats, st)))
         return rc;
     if ((rc = mark(prof, 5, st))) return rc;
@@ -415,6 +418,18 @@ static int backward_impl(const bsr_scene *scene, const bsr_camera *camera, const
     if ((rc = launch_preprocess_bwd(*scene, cam, f, *grads, screen_grad_norm, reinterpret_cast<float4 *>(drgb), st)))
         return rc;
     return mark(prof, 3, st);
+}
+
+extern "C" int bsr_contributions(const bsr_scene *scene, const bsr_camera *camera, const float background[3],
+                                 void *frame, uint64_t frame_bytes, int64_t entry_cap, int32_t *contributions,
+                                 void *stream) {
+    if (bad_scene(scene) || bad_camera(camera) || !background || !frame || !contributions || entry_cap < 0 ||
+        entry_cap >= (1ll << 31))
+        return BSR_ERR_BAD_ARG;
+    const FrameView f = carve_frame(frame, scene->n, camera->width, camera->height, entry_cap);
+    if (frame_bytes < f.total_bytes) return BSR_ERR_FRAME_TOO_SMALL;
+    if (scene->n == 0) return BSR_OK;
+    return launch_raster_count(f, contributions, background, (float)kAlphaMin, (float)kTStop, (cudaStream_t)stream);
 }
 
 extern "C" int bsr_det_workspace_bytes(int64_t n, uint64_t *bytes) {

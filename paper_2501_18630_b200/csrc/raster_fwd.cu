@@ -17,6 +17,7 @@
 //
 // Roofline: FP32 + XU pipes, per evaluated pair ~27 FP32 FLOP + 2 XU.
 #include <stdlib.h>
+#include <string.h>
 
 #include "raster.cuh"
 
@@ -68,7 +69,9 @@ __device__ __noinline__ float2 unsafe_pair_fwd(const double *m64, float4 B, int 
     return make_float2(p.alpha, p.om);
 }
 
-template <bool STATS, bool CONTRIB, int G>
+// COUNT: the deferred contributions pass (bsr_contributions): the same walk and decisions on
+// the unchanged frame, counting only (no frame state, no outputs, no masks written)
+template <bool STATS, bool CONTRIB, int G, bool COUNT = false>
 __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(RasterFwdArgs a) {
     pdl_wait();
     using SB = SubBlock<G>;
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(BSR_BLOCK, BSR_FWD_CTAS) raster_fwd_kernel(Ras
         }
     }
     cp_async_wait<0>();
+    if (COUNT) return;
     if (a.emask && t == 0) f.mask_end[tile] = (uint32_t)reached;  // the replay's entry pre-test
     if (stats) {
         unsigned long long p2 = pairs, c2s = (unsigned)cnt;
@@ -351,6 +355,29 @@ static int launch_fwd_g(const RasterFwdArgs &a, int tiles, bool stats, bool cont
         BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, true, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
     else
         BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, false, G>, dim3(tiles), dim3(BSR_BLOCK), 0, st, a)));
+    return BSR_OK;
+}
+
+// the deferred contributions pass: the frame's own lists, masks recomputed (not stored)
+int launch_raster_count(const FrameView &f, int32_t *contributions, const float bg[3], float alpha_min,
+                        float t_stop, cudaStream_t st) {
+    if (f.n_tiles == 0) return BSR_OK;
+    RasterFwdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.f = f;
+    a.out.contributions = contributions;
+    a.bg[0] = bg[0];
+    a.bg[1] = bg[1];
+    a.bg[2] = bg[2];
+    a.alpha_min = alpha_min;
+    a.t_stop = t_stop;
+    a.emask = nullptr;
+    switch (raster_groups()) {
+        case 1: BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, true, 1, true>, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, a))); break;
+        case 2: BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, true, 2, true>, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, a))); break;
+        default: BSR_CUDA_TRY((pdl_launch(raster_fwd_kernel<false, true, 4, true>, dim3(f.n_tiles), dim3(BSR_BLOCK), 0, st, a))); break;
+    }
+    BSR_LAUNCH_CHECK();
     return BSR_OK;
 }
 

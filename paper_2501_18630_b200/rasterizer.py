@@ -153,7 +153,17 @@ class RenderOutput:
     def __getattribute__(self, name):
         v = object.__getattribute__(self, name)
         if name == "contributions" and v is not None and v.dtype != torch.int64:
-            v = v.long()  # a step that never reads them skips the conversion kernel
+            # counted on first access: the forward left the raster's part to bsr_contributions
+            # (its frame is unchanged until then) and counted in int32; a step that never
+            # reads them skips both the count and the widening
+            pending = self.__dict__.pop("_pending_contrib", None)
+            if pending is not None:
+                scene, cam, bg, frame = pending
+                _lib.check(_lib.load().bsr_contributions(ctypes.byref(scene), ctypes.byref(cam), bg,
+                                                         ctypes.c_void_p(frame.ptr()), frame.nbytes,
+                                                         frame.entry_cap, ctypes.c_void_p(v.data_ptr()),
+                                                         _stream()), "contributions")
+            v = v.long()
             object.__setattr__(self, "contributions", v)
         return v
 
@@ -322,11 +332,12 @@ def forward_raw(scene: _lib.SceneC, camera: Camera, background, outputs: _lib.Ou
 
 
 def outputs_c(color=None, raw=None, alpha=None, trans=None, depth=None, pixel_count=None,
-              contributions=None) -> _lib.OutputsC:
+              contributions=None, defer_contributions=False) -> _lib.OutputsC:
     o = _lib.OutputsC()
     o.color, o.raw, o.alpha = _lib.ptr(color), _lib.ptr(raw), _lib.ptr(alpha)
     o.transmittance, o.depth = _lib.ptr(trans), _lib.ptr(depth)
     o.pixel_count, o.contributions = _lib.ptr(pixel_count), _lib.ptr(contributions)
+    o.defer_contributions = 1 if defer_contributions else 0
     return o
 
 
@@ -421,10 +432,12 @@ def render_tiled(prims: PrimitiveSet, camera: Camera, background, threads=None, 
         raw[:] = bgt
         return RenderOutput(torch.clamp_min(raw, 0.0), torch.zeros_like(alpha), contrib.long(), raw,
                             torch.ones_like(alpha), torch.zeros_like(alpha), torch.zeros_like(count), None)
-    out = outputs_c(color, raw, alpha, trans, depth, count, contrib)
-    frame = forward_raw(_prims_scene_c(prims), camera, background, out, contrib=contrib,
-                        check=True if sync else "async")
-    return RenderOutput(color, alpha, contrib, raw, trans, depth, count, frame)
+    out = outputs_c(color, raw, alpha, trans, depth, count, contrib, defer_contributions=True)
+    scene = _prims_scene_c(prims)
+    frame = forward_raw(scene, camera, background, out, contrib=contrib, check=True if sync else "async")
+    res = RenderOutput(color, alpha, contrib, raw, trans, depth, count, frame)
+    res._pending_contrib = (scene, _camera_c(camera), _bg_arr(background), frame)
+    return res
 
 
 def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, forward_out=None,

@@ -711,3 +711,35 @@ def test_precomputed_view_colours_are_bit_identical(cuda, degree):
         runs.append((p.flat.clone(), st.loss_values.clone()))
     assert torch.equal(runs[0][1], runs[1][1])
     assert torch.equal(runs[0][0].view(torch.int32), runs[1][0].view(torch.int32))
+
+def test_deferred_contributions_match_the_counting_forward(cuda):
+    """render_tiled leaves the raster's part of the contributions to a count pass run on
+    first access (bsr_contributions); it must equal the forward that counts inline, also
+    when read after the backward and a parameter update (config-1 scene, flagged pixels
+    included: their fp64 part is counted by the forward's replay either way)."""
+    import torch
+
+    from paper_2501_18630_b200 import PrimitiveSet, rasterizer as rz, training
+    from paper_2501_18630_b200.scenes import make_workload
+
+    wl = make_workload("c1", seed=3, n=100_000, views=1)
+    prims = PrimitiveSet.from_scene(wl.scene)
+    cam, bg = wl.cameras[0], wl.background
+    # inline counting (defer_contributions = 0)
+    h, w = cam.height, cam.width
+    color = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+    ref = torch.zeros(len(prims), dtype=torch.int32, device="cuda")
+    frame = rz.forward_raw(rz._prims_scene_c(prims), cam, bg, rz.outputs_c(color=color, contributions=ref),
+                           contrib=ref, check=True)
+    assert rz.frame_status(frame)["flagged_pixels"] > 0  # the replay's part is exercised
+    out = rz.render_tiled(prims, cam, bg)
+    assert torch.equal(out.color, color)
+    g = rz.render_backward(prims, cam, bg, torch.ones_like(out.color), forward_out=out)
+    state = training.AdamState(prims)
+    training.adam_step(prims, g, state, training.group_lrs())  # parameters move; the frame does not
+    got = out.contributions
+    assert got.dtype == torch.int64
+    np.testing.assert_array_equal(got.cpu().numpy(), ref.long().cpu().numpy())
+    assert int(ref.sum()) > 0
+    again = rz.render_tiled(prims, cam, bg)  # a second forward gets its own frame and count
+    assert again.contributions.shape == got.shape
