@@ -44,7 +44,7 @@ __device__ __forceinline__ double r2_error_bound(const Proj64 &p, double l11, do
 // half of the primitives (FrameView::vis_hint) the appearance block is requested together
 // with the geometry instead, so its latency overlaps the projection (measured with the
 // current CTA sizes: config 2 0.090 -> 0.080 ms, config 3 0.251 -> 0.237, config 4 0.616 ->
-// 0.605; scripts/ab_eager.sh).
+// 0.605; a build A/B with -DBSR_EAGER_APP_MAX_N=0, scripts/gpu/ab.sh).
 #ifndef BSR_EAGER_APP_MAX_N
 #define BSR_EAGER_APP_MAX_N (1ll << 40)  // no size limit (build knob for A/B runs)
 #endif

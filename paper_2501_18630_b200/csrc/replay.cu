@@ -198,7 +198,7 @@ __device__ __forceinline__ double alpha64(const Entry64 &e, int px, int py, doub
 // reads: alpha (overwritten by the weight alpha * T once T is known) and r, g, b, z.
 // Small frames (few flagged pixels, latency-bound) use one 1024-wide CTA per SM; large ones
 // (thousands of flagged pixels) 32 one-warp CTAs per SM for more pixels in flight
-// (measured, scripts/ab_replay_nt.sh: config 3 1024 > 256 > 128, config 4 0.54 ms at
+// (measured, scripts/gpu/ab_env.sh with BSR_REPLAY_NT: config 3 1024 > 256 > 128, config 4 0.54 ms at
 // 1024 -> 0.20 at 256 -> 0.15 at 128; after the mask pre-test 0.172 at 128 -> 0.147 at
 // 64 -> 0.122 at 32).  BSR_REPLAY_NT overrides for A/B runs.
 constexpr int kRecBatch = 8;  // transmittance steps per batch (the stop test runs per batch)
