@@ -1,7 +1,7 @@
 // fp64 projection + SH colour of one primitive.  Included ONLY by translation units
 // compiled with -fmad=false (preprocess.cu, replay.cu) so that every caller produces the
-// same bits, and so the operation order matches the reference's numpy/-ffp-contract=off
-// arithmetic as closely as a restatement can.
+// same bits, and so the operation order matches the reference's numpy arithmetic (ufuncs
+// unfused, matmuls as OpenBLAS's FMA chains: dot3) as closely as a restatement can.
 #pragma once
 
 #include "common.cuh"
@@ -41,6 +41,16 @@ __device__ __forceinline__ bool quat_to_rot64(const float *q4, double R[9]) {
     return true;
 }
 
+// One entry of a numpy float64 matmul with inner dimension 3: OpenBLAS's dgemm kernels
+// (this image's numpy, scipy-openblas 0.3.30) accumulate along k with FMAs,
+// fma(x2, y2, fma(x1, y1, x0 y0)); measured bit-identical on every entry of the oracle's
+// four projection matmuls (scripts/matmul_order.py), while the unfused sum differs in
+// ~40% of entries -- enough, on near-singular covariances, to move an alpha across the
+// 1/255 cutoff.
+__device__ __forceinline__ double dot3(double x0, double x1, double x2, double y0, double y1, double y2) {
+    return fma(x2, y2, fma(x1, y1, x0 * y0));
+}
+
 // numpy's float64 -> int32 cast on x86 (cvttsd2si): out-of-range / NaN -> INT32_MIN,
 // followed by wrapping int32 arithmetic (primitive.py:254-261).
 __device__ __forceinline__ int np_i32(double v) {
@@ -59,9 +69,9 @@ __device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat
     const double px = pos3[0], py = pos3[1], pz = pos3[2];
     const double *R = cam.R;
     // cam_pts = positions @ R^T + t
-    p.tx = ((px * R[0] + py * R[1]) + pz * R[2]) + cam.t[0];
-    p.ty = ((px * R[3] + py * R[4]) + pz * R[5]) + cam.t[1];
-    p.tz = ((px * R[6] + py * R[7]) + pz * R[8]) + cam.t[2];
+    p.tx = dot3(px, py, pz, R[0], R[1], R[2]) + cam.t[0];
+    p.ty = dot3(px, py, pz, R[3], R[4], R[5]) + cam.t[1];
+    p.tz = dot3(px, py, pz, R[6], R[7], R[8]) + cam.t[2];
     if (!(p.tz > kNearPlane)) return p;
     const double tx = p.tx, ty = p.ty, tz = p.tz;
     p.mx = cam.fx * tx / tz + cam.cx;
@@ -80,8 +90,7 @@ __device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            S[3 * i + j] = (rs[3 * i] * rs[3 * j] + rs[3 * i + 1] * rs[3 * j + 1]) +
-                           rs[3 * i + 2] * rs[3 * j + 2];
+            S[3 * i + j] = dot3(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], rs[3 * j], rs[3 * j + 1], rs[3 * j + 2]);
     // J (2x3), a = J @ R_cam (2x3)
     const double tz2 = tz * tz;
     const double j00 = cam.fx / tz, j02 = -cam.fx * tx / tz2;
@@ -89,8 +98,8 @@ __device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat
     double A[6];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        A[j] = (j00 * R[j] + 0.0 * R[3 + j]) + j02 * R[6 + j];
-        A[3 + j] = (0.0 * R[j] + j11 * R[3 + j]) + j12 * R[6 + j];
+        A[j] = dot3(j00, 0.0, j02, R[j], R[3 + j], R[6 + j]);
+        A[3 + j] = dot3(0.0, j11, j12, R[j], R[3 + j], R[6 + j]);
     }
     // cov = (A @ S) @ A^T
     double AS[6];
@@ -98,10 +107,10 @@ __device__ __forceinline__ Proj64 project64(const float *pos3, const float *quat
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            AS[3 * i + j] = (A[3 * i] * S[j] + A[3 * i + 1] * S[3 + j]) + A[3 * i + 2] * S[6 + j];
-    double c00 = (AS[0] * A[0] + AS[1] * A[1]) + AS[2] * A[2];
-    double c01 = (AS[0] * A[3] + AS[1] * A[4]) + AS[2] * A[5];
-    double c11 = (AS[3] * A[3] + AS[4] * A[4]) + AS[5] * A[5];
+            AS[3 * i + j] = dot3(A[3 * i], A[3 * i + 1], A[3 * i + 2], S[j], S[3 + j], S[6 + j]);
+    double c00 = dot3(AS[0], AS[1], AS[2], A[0], A[1], A[2]);
+    double c01 = dot3(AS[0], AS[1], AS[2], A[3], A[4], A[5]);
+    double c11 = dot3(AS[3], AS[4], AS[5], A[3], A[4], A[5]);
     c00 += kCovConditioning;
     c11 += kCovConditioning;
     p.c00 = c00;

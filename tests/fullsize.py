@@ -100,11 +100,14 @@ def _rows(r):
     return r.reshape(r.shape[0], -1).max(axis=1) if r.ndim > 1 else r
 
 
-def compare_grads(grads, ref_g, detail=True, ref_g32=None):
+def compare_grads(grads, ref_g, detail=True, ref_g32=None, ref_ulp=None):
     """Per group: max ratio (<= 1 passes).  With ``ref_g32`` (the oracle's gradients with
     the raster records' colour and opacity rounded to fp32) rows whose reference gradient
     itself moves by more than half the tolerance under that rounding are ILL-POSED at
-    fp32: they must stay within 1 + 4 x their own sensitivity instead of within 1."""
+    fp32: they must stay within 1 + 4 x their own sensitivity instead of within 1.
+    ``ref_ulp`` (records' fp64 mean / conic moved one ulp, _ulp_geometry) adds the
+    sensitivity of the reference to its own fp64 geometry rounding; a row's sensitivity is
+    the larger of the two."""
     rep = {}
     for k in GROUPS:
         if k not in ref_g:
@@ -116,6 +119,8 @@ def compare_grads(grads, ref_g, detail=True, ref_g32=None):
         n_ill = 0
         if ref_g32 is not None:
             sens = _rows(grad_ratio(ref_g32[k], b))
+            if ref_ulp is not None:
+                sens = np.maximum(sens, _rows(grad_ratio(ref_ulp[k], b)))
             ill = sens > 0.5
             n_ill = int(ill.sum())
             rows = np.where(ill, rows / (1.0 + 4.0 * sens), rows)
@@ -146,6 +151,23 @@ def _fp32_records(ref):
     return f2
 
 
+def _ulp_geometry(ref):
+    """The oracle's forward state with every raster record's 2D mean and conic moved by one
+    fp64 ulp -- the other conditioning probe: two IEEE-valid evaluations of the reference's
+    projection (e.g. numpy's FMA-chained matmuls vs an unfused sum) differ by about this
+    much, so a gradient that moves under it is not determined by the reference either
+    (measured at c4 seed 0: row 4892568's position gradient moves 3.5 %, row 4863872's 14 %,
+    conic kappa ~ 3e9 near the near plane)."""
+    f2 = dict(ref)
+    sh = dict(ref["shaded"])
+    s = dict(sh["sorted"])
+    for k in ("means", "conics"):
+        s[k] = np.nextafter(s[k], np.inf)
+    sh["sorted"] = s
+    f2["shaded"] = sh
+    return f2
+
+
 def _row_geometry(ref, grep):
     """Depth, 2D extent and conic condition number of the worst rows (diagnostics)."""
     b = ref["batch"]
@@ -166,7 +188,7 @@ def _row_geometry(ref, grep):
     return out
 
 
-def run_case(cfg, view=0, bwd=True, n=None, width=None, height=None, threads=None, bins=True):
+def run_case(cfg, view=0, bwd=True, n=None, width=None, height=None, threads=None, bins=True, seed=0):
     """One full-size case; returns (report dict, forward ok, gradients ok or None)."""
     import torch
 
@@ -177,10 +199,10 @@ def run_case(cfg, view=0, bwd=True, n=None, width=None, height=None, threads=Non
     threads = threads or os.cpu_count() or 1
     default_n = {"c0": 10_000, "c1": 100_000, "c2": 1_000_000, "c3": 3_000_000, "c4": 6_000_000}[cfg]
     n = n or default_n
-    wl = make_workload(cfg, seed=0, n=n, width=width, height=height,
+    wl = make_workload(cfg, seed=seed, n=n, width=width, height=height,
                        views=(view + 1) if cfg == "c3" else None)
     scene, cam, bg = wl.scene, wl.cameras[view], wl.background
-    rep = {"case": f"{cfg} view {view} N={n} {cam.width}x{cam.height}", "threads": threads}
+    rep = {"case": f"{cfg} seed {seed} view {view} N={n} {cam.width}x{cam.height}", "threads": threads}
     t0 = time.perf_counter()
     ref = orc.forward(scene, cam, bg, core="c", threads=threads)
     rep["oracle_fwd_s"] = round(time.perf_counter() - t0, 2)
@@ -197,8 +219,10 @@ def run_case(cfg, view=0, bwd=True, n=None, width=None, height=None, threads=Non
         rep["oracle_bwd_s"] = round(time.perf_counter() - t0, 2)
         ref_g32 = orc.backward(scene, cam, bg, up.astype(np.float64), _fp32_records(ref), core="c",
                                threads=threads)
+        ref_ulp = orc.backward(scene, cam, bg, up.astype(np.float64), _ulp_geometry(ref), core="c",
+                               threads=threads)
         grads = render_backward(prims, cam, bg, up, forward_out=out)
-        rep["grads"] = compare_grads(grads, ref_g, ref_g32=ref_g32)
+        rep["grads"] = compare_grads(grads, ref_g, ref_g32=ref_g32, ref_ulp=ref_ulp)
         rep["worst_geometry"] = _row_geometry(ref, rep["grads"])
         gok = grads_ok(rep["grads"])
         del grads
@@ -248,8 +272,9 @@ def run_sb_case(threads=None):
     up[np.abs(ref["raw"]) < KINK] = 0.0
     ref_g = orc.backward(scene, cam, bg, up.astype(np.float64), ref, core="c", threads=threads)
     ref_g32 = orc.backward(scene, cam, bg, up.astype(np.float64), _fp32_records(ref), core="c", threads=threads)
+    ref_ulp = orc.backward(scene, cam, bg, up.astype(np.float64), _ulp_geometry(ref), core="c", threads=threads)
     grads = render_backward(prims, cam, bg, up, forward_out=out)
-    rep["grads"] = compare_grads(grads, ref_g, ref_g32=ref_g32)
+    rep["grads"] = compare_grads(grads, ref_g, ref_g32=ref_g32, ref_ulp=ref_ulp)
     gok = grads_ok(rep["grads"])
     del grads, out, prims
     torch.cuda.empty_cache()
