@@ -192,8 +192,36 @@ class PrimitiveSet(FlatGroups):
         return {g: getattr(self, g).detach().cpu().numpy() for g in self.groups}
 
 
+# GradientBuffer attributes that never depend on pending colour chains
+_GRAD_META = frozenset(("n", "k", "lobes", "color_model", "layout", "groups", "param_names", "sh_coeffs",
+                        "group_ends", "layout_c", "flush_pending"))
+
+
 class GradientBuffer(FlatGroups):
-    """Per-parameter gradients aligned with the primitive set (rasterizer.py:49-80)."""
+    """Per-parameter gradients aligned with the primitive set (rasterizer.py:49-80).
+
+    A buffer that rasterizer.render_backward accumulates several views of an SH set into
+    may hold those views' colour chains deferred (``_pending``: their d rgb rows, applied
+    by one bsr_color_grad_views); reading any gradient attribute applies them first, so
+    the values seen are always the complete sums."""
+
+    def __getattribute__(self, name):
+        if name[:1] != "_" and name not in _GRAD_META:
+            d = object.__getattribute__(self, "__dict__")
+            p = d.get("_pending")
+            if p is not None:
+                d["_pending"] = None
+                p.apply(self)
+        return object.__getattribute__(self, name)
+
+    def flush_pending(self):
+        """Apply deferred colour chains now (otherwise done on the next attribute read)."""
+        d = self.__dict__
+        p = d.get("_pending")
+        if p is not None:
+            d["_pending"] = None
+            p.apply(self)
+        return self
 
     def __init__(self, n, k, flat=None, device="cuda", lobes=None):
         _, total = group_layout(n, k, lobes)

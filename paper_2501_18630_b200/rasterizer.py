@@ -452,6 +452,15 @@ def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, fo
     twice the raster-backward cost."""
     _check_core(core)
     fresh = grads is None
+    # accumulating into a buffer (a further view of a multi-view step) of an SH set: this
+    # view's colour chain is deferred into the buffer's pending d rgb rows and applied for
+    # all pending views at once when the gradients are next read (_ColorPending)
+    pend = None
+    if not fresh:
+        pend = grads.__dict__.pop("_pending", None)
+        if pend is not None and (pend.prims is not prims or pend.count == pend.cap or deterministic):
+            pend.apply(grads)
+            pend = None
     if fresh:  # written, not added: no memset of the (N x 60 floats at SH-3) buffer
         grads = GradientBuffer.empty_for(prims) if len(prims) else GradientBuffer.zeros_for(prims)
     elif grads.flat.numel() != prims.flat.numel():
@@ -464,10 +473,51 @@ def render_backward(prims: PrimitiveSet, camera: Camera, background, d_color, fo
     d_color = torch.as_tensor(d_color, dtype=torch.float32, device=dev).contiguous()
     if d_depth is not None:
         d_depth = torch.as_tensor(d_depth, dtype=torch.float32, device=dev).contiguous()
-    backward_raw(_prims_scene_c(prims), camera, background, forward_out.frame, d_color, d_depth,
+    defer = not fresh and not deterministic and prims.color_model == "sh"
+    if defer and pend is None:
+        pend = _ColorPending.reuse(grads, prims)
+    scene = pend.scene if defer else _prims_scene_c(prims)
+    backward_raw(scene, camera, background, forward_out.frame, d_color, d_depth,
                  grads_c(grads, overwrite=fresh), grads.screen_grad_norm,
-                 det_ws=det_workspace(len(prims), dev) if deterministic else None)
+                 det_ws=det_workspace(len(prims), dev) if deterministic else None,
+                 drgb=pend.drgb[pend.count] if defer else None)
+    if defer:
+        pend.cams.append(camera)
+        pend.count += 1
+        grads.__dict__["_pending"] = pend
     return grads
+
+
+class _ColorPending:
+    """Deferred colour chains of the views render_backward accumulated into one
+    GradientBuffer (bsr_backward_deferred_color rows, applied by bsr_color_grad_views:
+    the coefficient gradients are read and written once for all of them instead of once
+    per view -- the public-API form of TrainStep's multi-view path)."""
+
+    kMaxBytes = 2 << 30  # d rgb rows kept per buffer (up to 32 views)
+
+    def __init__(self, prims: PrimitiveSet):
+        self.prims = prims
+        self.scene = _prims_scene_c(prims)
+        self.cap = int(max(1, min(32, self.kMaxBytes // max(1, 16 * prims.n))))
+        self.drgb = torch.empty((self.cap, prims.n, 4), dtype=torch.float32, device=prims.flat.device)
+        self.cams = []
+        self.count = 0
+
+    @classmethod
+    def reuse(cls, grads: GradientBuffer, prims: PrimitiveSet) -> "_ColorPending":
+        p = grads.__dict__.get("_color_pool")
+        if p is None or p.prims is not prims:
+            p = cls(prims)
+            grads.__dict__["_color_pool"] = p
+        p.scene = _prims_scene_c(prims)  # the parameter pointers / sizes as of this call
+        p.cams, p.count = [], 0
+        return p
+
+    def apply(self, grads: GradientBuffer):
+        if self.count:
+            color_grad_views(self.scene, self.drgb[:self.count], self.cams, grads_c(grads))
+        self.cams, self.count = [], 0
 
 
 def render_masked(prims: PrimitiveSet, camera: Camera, background, predicate, threads=None) -> RenderOutput:

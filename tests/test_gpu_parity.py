@@ -498,6 +498,40 @@ def test_multiview_deferred_colour_chain_matches_per_view(cuda, degree, views, n
     np.testing.assert_allclose(a.loss_values.cpu().numpy(), b.loss_values.cpu().numpy(), rtol=1e-12)
 
 
+@pytest.mark.parametrize("degree,views", [(3, 5), (1, 40)])
+def test_public_api_multiview_accumulation_defers_colour_chain(cuda, degree, views):
+    """render_backward(grads=g) over several views of an SH set defers each further view's
+    colour chain into g (rasterizer._ColorPending) and applies them on the next read of
+    g: the sums equal per-view fresh backwards added up (fp32 summation order), the 40-view
+    case crosses the 32-view pending capacity, and a read between views flushes."""
+    import torch
+
+    from paper_2501_18630_b200 import PrimitiveSet, render_backward, render_tiled
+
+    rng = np.random.default_rng(91)
+    prims = PrimitiveSet.from_scene(random_scene(rng, 300, degree=degree))
+    angles = np.linspace(-0.6, 0.6, views)
+    cams = [toy_camera(64, 48, eye=(np.sin(a) * 4.0, 0.3 * np.cos(2 * a), -np.cos(a) * 4.0)) for a in angles]
+    ups = [torch.as_tensor(rng.standard_normal((48, 64, 3)), dtype=torch.float32, device="cuda") for _ in cams]
+    bg = np.ones(3)
+    g = None
+    for v, (cam, up) in enumerate(zip(cams, ups)):
+        g = render_backward(prims, cam, bg, up, forward_out=render_tiled(prims, cam, bg), grads=g)
+        if v == 2:
+            assert g.__dict__.get("_pending") is not None and g.__dict__["_pending"].count == 2
+            _ = g.positions  # a read applies the pending chains
+            assert g.__dict__.get("_pending") is None
+    ref = {name: torch.zeros_like(getattr(g, name)) for name in g.groups}
+    for cam, up in zip(cams, ups):
+        r = render_backward(prims, cam, bg, up, forward_out=render_tiled(prims, cam, bg))
+        for name in ref:
+            ref[name] += getattr(r, name)
+    torch.cuda.synchronize()
+    for name in g.groups:
+        scale = max(float(ref[name].abs().max()), 1e-30)
+        torch.testing.assert_close(getattr(g, name), ref[name], rtol=1e-4, atol=1e-6 * scale, msg=name)
+
+
 def test_entry_capacity_overflow_retries(cuda):
     """A frame whose tile-entry capacity is too small reports BSR_ERR_CAPACITY with the
     entries needed; forward_raw grows the frame and the result is unchanged."""
